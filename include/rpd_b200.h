@@ -1,0 +1,259 @@
+/*
+ * rpd_b200.h — C-ABI of the B200-native road-pothole-detection hot path.
+ *
+ * This is the drop-in boundary.  Every entry point replaces one free function of
+ * the reference C++ library `namespace rpd` (arxiv 2012.10802 re-implementation
+ * under /root/reference/proj); the replaced declaration is cited as file:line
+ * relative to /root/reference/proj.  Buffers are row-major rasters, index
+ * v*W+u (types.hpp:9-10); disparities are float32 with invalid = -1.0f
+ * (types.hpp:16,21); labels are int32 with 0 = background (types.hpp:19).
+ * Cost volumes use the reference layout (v*W+u)*(d_max+1)+d (sgm.hpp:19).
+ *
+ * All host pointers are caller-owned.  The library owns only the device
+ * workspaces inside an rpd_ctx.  A context is single-threaded: one per
+ * (host thread, device); concurrent contexts are fine (sgm/pipeline are
+ * reentrant in the reference, rpd_cli.cpp:293-302).
+ *
+ * Errors: every call returns an rpd_status.  RPD_EINVAL mirrors
+ * std::invalid_argument, RPD_EDEGENERATE mirrors std::runtime_error /
+ * DegenerateFitError (pipeline.hpp:17-19).  rpd_last_error(ctx) holds the
+ * reference-style message ("census_cost_volume: d_max >= width", ...).
+ *
+ * Two shared libraries export this exact symbol set:
+ *   paper_2012_10802_b200/_lib/librpd_b200.so   — the product (sm_100a CUDA)
+ *   oracle/_build/librpd_oracle.so               — CPU restatement, TEST ONLY
+ */
+#ifndef RPD_B200_H
+#define RPD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RPD_ABI_VERSION 1
+
+typedef enum rpd_status {
+  RPD_OK = 0,
+  RPD_EINVAL = 1,       /* std::invalid_argument */
+  RPD_EDEGENERATE = 2,  /* std::runtime_error (degenerate data) / DegenerateFitError */
+  RPD_ECUDA = 3,        /* CUDA runtime failure (product library only) */
+  RPD_ENOMEM = 4,       /* device or host allocation failed */
+  RPD_ECAPACITY = 5     /* a caller-provided output buffer is too small */
+} rpd_status;
+
+typedef struct rpd_ctx rpd_ctx;
+
+/* RoadModel, types.hpp:33-37: d(u,v) = a0 + a1 (v cos(phi) - u sin(phi)). */
+typedef struct rpd_road_model {
+  double a0;
+  double a1;
+  double phi;
+} rpd_road_model;
+
+/* PipelineConfig, config.hpp:10-36 (same field names and defaults), plus
+ * `sgm_paths` (4 or 8): the first `sgm_paths` entries of kEightDirections
+ * (sgm.hpp:41-43).  The reference always uses 8 (sgm.cpp:183-186). */
+typedef struct rpd_config {
+  double delta_pt;
+  double delta_dt;
+  double delta_pd;
+  int32_t d_max;
+  int32_t d_max_pt;
+  double lambda1;
+  double lambda2;
+  int32_t census_window;
+  double lr_threshold;
+  int32_t superpixels;
+  double compactness;
+  int32_t slic_iterations;
+  double hist_bin_width;
+  double tau_diag;
+  int32_t border_margin;
+  int32_t min_superpixels;
+  int32_t connectivity;
+  double roll_bracket;
+  double roll_tol;
+  double focal;
+  double baseline;
+  double cu;
+  double cv;
+  int32_t sgm_paths;
+} rpd_config;
+
+/* SuperpixelMap::Center, segmentation.hpp:11-15. */
+typedef struct rpd_center {
+  double cu;
+  double cv;
+  double value;
+} rpd_center;
+
+/* LineFit, road_geometry.hpp:20-23. */
+typedef struct rpd_line_fit {
+  rpd_road_model model;
+  double e0min;
+} rpd_line_fit;
+
+/* RoadFit, road_geometry.hpp:34-38. */
+typedef struct rpd_road_fit {
+  rpd_road_model model;
+  double e0min;
+  int64_t used;
+} rpd_road_fit;
+
+/* RectRoi, road_geometry.hpp:45-47. */
+typedef struct rpd_rect_roi {
+  int32_t u0, v0, width, height;
+} rpd_rect_roi;
+
+/* ThresholdResult, segmentation.hpp:48-55. */
+typedef struct rpd_threshold {
+  double t_r;
+  double t_s;
+  double mu1;
+  double mu2;
+  double excluded_fraction;
+  int32_t degenerate;
+} rpd_threshold;
+
+/* Stage names of StageClock laps (pipeline.cpp:64-104). */
+#define RPD_NUM_STAGES 7
+/* 0 sgm_bootstrap, 1 road_fit, 2 sgm_pt, 3 road_refit,
+ * 4 disparity_transform, 5 slic, 6 detect */
+
+/* DetectResult, pipeline.hpp:26-38.  Every pointer may be NULL (not copied
+ * back).  Raster outputs are H*W. */
+typedef struct rpd_detect_out {
+  float* d0;
+  float* d1;
+  float* d2;
+  float* d3;
+  int32_t* labels;        /* final pothole labels */
+  int32_t* sp_labels;     /* SuperpixelMap::labels */
+  rpd_center* centers;    /* SuperpixelMap::centers, up to centers_cap */
+  int32_t centers_cap;
+  /* scalar results, always written */
+  int32_t sp_count;
+  double sp_spacing;
+  rpd_road_fit coarse_fit; /* bootstrap fit after a0 *= 2 (pipeline.cpp:73) */
+  rpd_road_fit fit;
+  rpd_threshold threshold;
+  int64_t clamped;
+  int32_t n_potholes;
+  double stage_ms[RPD_NUM_STAGES];
+  double total_ms;
+} rpd_detect_out;
+
+/* ---- context / config ------------------------------------------------- */
+int rpd_abi_version(void);
+/* Creates a context on `device`.  max_h/max_w/max_levels are sizing hints
+ * (workspaces grow on demand). */
+rpd_status rpd_ctx_create(int device, int max_h, int max_w, int max_levels, rpd_ctx** out);
+void rpd_ctx_destroy(rpd_ctx* ctx);
+const char* rpd_last_error(const rpd_ctx* ctx);
+/* The cudaStream_t all work of this context is ordered on (NULL for the oracle). */
+void* rpd_ctx_stream(rpd_ctx* ctx);
+
+void rpd_config_default(rpd_config* cfg);                               /* config.hpp:11-33 */
+rpd_status rpd_config_validate(rpd_ctx* ctx, const rpd_config* cfg);     /* config.cpp:9-22 */
+rpd_status rpd_config_set(rpd_ctx* ctx, rpd_config* cfg, const char* key,
+                          const char* value);                            /* config.cpp:24-51 */
+
+/* ---- pipeline ----------------------------------------------------------- */
+/* detect_potholes_pipeline, pipeline.hpp:43-44 / pipeline.cpp:47-109.
+ * left/right: H*W float32 gray images in [0,255]. */
+rpd_status rpd_detect(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                      const rpd_config* cfg, rpd_detect_out* out);
+/* Same, uint8 images (exact: intensities are only compared / averaged). */
+rpd_status rpd_detect_u8(rpd_ctx* ctx, const uint8_t* left, const uint8_t* right, int h,
+                         int w, const rpd_config* cfg, rpd_detect_out* out);
+
+/* ---- perspective transformation (perspective.hpp) ----------------------- */
+/* compute_row_shifts, perspective.hpp:23-35; shifts: H doubles. */
+rpd_status rpd_compute_row_shifts(rpd_ctx* ctx, const rpd_road_model* model, int w, int h,
+                                  double delta_pt, double* shifts);
+/* warp_right_image, perspective.hpp:45-66; image H*W float, in_view H*W u8. */
+rpd_status rpd_warp_right_image(rpd_ctx* ctx, const float* right, int h, int w,
+                                const double* shifts, float* image, uint8_t* in_view);
+/* restore_disparity, perspective.hpp:69-80. */
+rpd_status rpd_restore_disparity(rpd_ctx* ctx, const float* d0, int h, int w,
+                                 const double* shifts, float* d1);
+
+/* ---- SGM (sgm.hpp) ------------------------------------------------------ */
+/* census_cost_volume, sgm.hpp:49-51; costs: H*W*(d_max+1) floats.
+ * right_in_view may be NULL. */
+rpd_status rpd_census_cost_volume(rpd_ctx* ctx, const float* left, const float* right_warped,
+                                  int h, int w, int d_max, int window,
+                                  const uint8_t* right_in_view, float* costs);
+/* aggregate_costs, sgm.hpp:56; dirs: ndirs (du,dv) pairs. */
+rpd_status rpd_aggregate_costs(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
+                               const int32_t* dirs, int ndirs, float lambda1, float lambda2,
+                               float* aggregated);
+/* swap_reference, sgm.hpp:59. */
+rpd_status rpd_swap_reference(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
+                              float* right_costs);
+/* select_disparity, sgm.hpp:63. */
+rpd_status rpd_select_disparity(rpd_ctx* ctx, const float* aggregated, int h, int w,
+                                int d_max, float* disparity);
+/* consistency_filter, sgm.hpp:66-67 (in place on left_disp). */
+rpd_status rpd_consistency_filter(rpd_ctx* ctx, float* left_disp, const float* right_disp,
+                                  int h, int w, double threshold);
+/* match_pair, sgm.hpp:77-79.  shifts (H doubles) may be NULL. */
+rpd_status rpd_match_pair(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                          const rpd_road_model* model, const rpd_config* cfg, int d_max,
+                          float* d0, float* d1, double* shifts);
+
+/* ---- road geometry (road_geometry.hpp) ---------------------------------- */
+/* sample_observations, road_geometry.hpp:51-53.  roi may be NULL (whole map).
+ * d/u/v must hold min(#valid, cap) doubles; *count receives that number. */
+rpd_status rpd_sample_observations(rpd_ctx* ctx, const float* d1, int h, int w,
+                                   const rpd_rect_roi* roi, int64_t cap, double* d, double* u,
+                                   double* v, int64_t* count);
+/* fit_line, road_geometry.hpp:28. */
+rpd_status rpd_fit_line(rpd_ctx* ctx, const double* d, const double* u, const double* v,
+                        int64_t k, double phi, rpd_line_fit* out);
+/* estimate_roll, road_geometry.hpp:31-32. */
+rpd_status rpd_estimate_roll(rpd_ctx* ctx, const double* d, const double* u, const double* v,
+                             int64_t k, double bracket_lo, double bracket_hi, double tol,
+                             rpd_road_model* out);
+/* fit_road, road_geometry.hpp:43. */
+rpd_status rpd_fit_road(rpd_ctx* ctx, const double* d, const double* u, const double* v,
+                        int64_t k, double bracket, double tol, rpd_road_fit* out);
+/* transform_disparity, road_geometry.hpp:61-62. */
+rpd_status rpd_transform_disparity(rpd_ctx* ctx, const float* d1, int h, int w,
+                                   const rpd_road_model* model, double delta_dt, float* d2,
+                                   int64_t* clamped);
+
+/* ---- segmentation (segmentation.hpp) ------------------------------------ */
+/* slic, segmentation.hpp:28.  labels H*W; centers up to centers_cap. */
+rpd_status rpd_slic(rpd_ctx* ctx, const float* d2, int h, int w, int p, double compactness,
+                    int iterations, int32_t* labels, rpd_center* centers, int centers_cap,
+                    int32_t* count, double* spacing);
+/* pool_superpixels, segmentation.hpp:32. */
+rpd_status rpd_pool_superpixels(rpd_ctx* ctx, const float* d2, const int32_t* sp_labels,
+                                int sp_count, int h, int w, float* d3);
+/* build_histogram, segmentation.hpp:46.  counts: n*n int64 row-major, n <= cap_n.
+ * When cap_n is too small, *n is still written and RPD_ECAPACITY returned. */
+rpd_status rpd_build_histogram(rpd_ctx* ctx, const float* d2, int h, int w, double bin_width,
+                               int64_t* counts, int64_t cap_n, int64_t* n, double* origin,
+                               int64_t* total);
+/* find_road_threshold, segmentation.hpp:60-61. */
+rpd_status rpd_find_road_threshold(rpd_ctx* ctx, const int64_t* counts, int64_t n,
+                                   double bin_width, double origin, int64_t total,
+                                   double delta_pd, double tau, rpd_threshold* out);
+/* connected_components, segmentation.hpp:65. */
+rpd_status rpd_connected_components(rpd_ctx* ctx, const int32_t* mask, int h, int w,
+                                    int connectivity, int32_t* out);
+/* detect_potholes, segmentation.hpp:69-71. */
+rpd_status rpd_detect_potholes(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels,
+                               double sp_spacing, int h, int w, const rpd_threshold* thr,
+                               int border_margin, int min_superpixels, int connectivity,
+                               int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RPD_B200_H */

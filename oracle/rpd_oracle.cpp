@@ -1,0 +1,1330 @@
+// rpd_oracle.cpp — CPU ORACLE (test infrastructure, NOT the product).
+//
+// A scalar, sequential C++20 restatement of the reference hot path
+// (/root/reference/proj, cited file:line below).  It exports the same C-ABI as
+// the CUDA library (include/rpd_b200.h) so the parity tests can run one set of
+// ctypes bindings against both libraries.  Only tests/, __graft_entry__.smoke()
+// and bench.py's CPU-baseline leg may load it.
+//
+// Parity pins: the known answers of the reference's own unit tests and
+// acceptance oracles are ported in tests/test_oracle_*.py.
+// The reference itself cannot be compiled here (Eigen3, libpng, doctest absent;
+// SURVEY.md §8c) so there is no literal-reference cross-check.
+//
+// Deliberate, documented choices where the reference is unpinned:
+//  * fit_line reductions (road_geometry.cpp:20-24, 37) are Eigen reductions
+//    whose SIMD order cannot be reproduced without Eigen.  The oracle fixes one
+//    order — kFitLanes strided lanes, then an adjacent-pairwise tree — which is
+//    also the device kernel's order (DESIGN.md §road fit).
+//  * `sgm_paths` (4 or 8) selects the first entries of kEightDirections
+//    (sgm.hpp:41-43); the reference always uses 8 (sgm.cpp:183-186).
+//
+// Build: g++ -O2 -std=c++20 -ffp-contract=off (no -march=native): x86-64 SSE2
+// arithmetic without contraction, like the reference build.
+
+#include <algorithm>
+#include <array>
+#include <bit>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rpd_b200.h"
+
+namespace oracle {
+
+// ---------------------------------------------------------------- rasters --
+template <typename T>
+struct Raster {  // row-major (v, u), types.hpp:9-10
+  int h = 0, w = 0;
+  std::vector<T> a;
+  Raster() = default;
+  Raster(int h_, int w_, T fill = T{}) : h(h_), w(w_), a(size_t(h_) * w_, fill) {}
+  T& operator()(int v, int u) { return a[size_t(v) * w + u]; }
+  const T& operator()(int v, int u) const { return a[size_t(v) * w + u]; }
+};
+using Gray = Raster<float>;
+using Disp = Raster<float>;
+using Labels = Raster<int>;
+constexpr float kInvalid = -1.0f;  // types.hpp:21
+inline bool valid(float d) { return d != kInvalid; }
+
+struct Model {
+  double a0 = 0, a1 = 0, phi = 0;
+};
+// types.hpp:39-41
+inline double road_at(const Model& m, double u, double v) {
+  return m.a0 + m.a1 * (v * std::cos(m.phi) - u * std::sin(m.phi));
+}
+
+struct Degenerate : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ------------------------------------------------------------- config ----
+void config_default(rpd_config* c) {  // config.hpp:11-33
+  c->delta_pt = 5.0;
+  c->delta_dt = 30.0;
+  c->delta_pd = 2.36;
+  c->d_max = 64;
+  c->d_max_pt = 16;
+  c->lambda1 = 8.0;
+  c->lambda2 = 32.0;
+  c->census_window = 5;
+  c->lr_threshold = 1.0;
+  c->superpixels = 1365;
+  c->compactness = 8.0;
+  c->slic_iterations = 10;
+  c->hist_bin_width = 0.25;
+  c->tau_diag = 3.0;
+  c->border_margin = 5;
+  c->min_superpixels = 2;
+  c->connectivity = 8;
+  c->roll_bracket = 0.261799;
+  c->roll_tol = 1e-4;
+  c->focal = 700.0;
+  c->baseline = 0.12;
+  c->cu = -1.0;
+  c->cv = -1.0;
+  c->sgm_paths = 8;
+}
+
+void config_validate(const rpd_config& c) {  // config.cpp:9-22
+  auto fail = [](const char* m) { throw std::invalid_argument(std::string("config: ") + m); };
+  if (c.delta_pt < 0) fail("delta_pt must be >= 0");
+  if (c.delta_dt <= 0) fail("delta_dt must be > 0");
+  if (c.delta_pd <= 0) fail("delta_pd must be > 0");
+  if (c.d_max < 1 || c.d_max_pt < 1) fail("d_max must be >= 1");
+  if (!(c.lambda1 > 0 && c.lambda1 <= c.lambda2)) fail("need 0 < lambda1 <= lambda2");
+  if (c.census_window != 3 && c.census_window != 5 && c.census_window != 7)
+    fail("census_window must be 3, 5 or 7");
+  if (c.superpixels < 4) fail("superpixels must be >= 4");
+  if (c.compactness <= 0) fail("compactness must be > 0");
+  if (c.connectivity != 4 && c.connectivity != 8) fail("connectivity must be 4 or 8");
+  if (c.roll_bracket <= 0 || c.roll_tol <= 0) fail("roll bracket/tol must be > 0");
+  if (c.focal <= 0 || c.baseline <= 0) fail("focal and baseline must be > 0");
+  if (c.sgm_paths != 4 && c.sgm_paths != 8) fail("sgm_paths must be 4 or 8");
+}
+
+// --------------------------------------------------------- perspective ----
+struct Shifts {
+  std::vector<double> s;
+  double delta_pt = 0;
+};
+
+// perspective.hpp:23-35
+Shifts row_shifts(const Model& m, int w, int h, double delta_pt) {
+  if (w < 2) throw std::invalid_argument("compute_row_shifts: width must be >= 2");
+  Shifts t;
+  t.delta_pt = delta_pt;
+  t.s.resize(size_t(h));
+  for (int v = 0; v < h; ++v) {
+    const double left = road_at(m, 0.0, v);
+    const double right = road_at(m, double(w), v);
+    t.s[size_t(v)] = std::max(0.0, std::min(left, right) - delta_pt);
+  }
+  return t;
+}
+
+struct Warped {
+  Gray img;
+  Raster<uint8_t> in_view;
+};
+
+// perspective.hpp:45-66
+Warped warp(const Gray& right, const Shifts& t) {
+  const int h = right.h, w = right.w;
+  if (int(t.s.size()) != h)
+    throw std::invalid_argument("warp_right_image: table length != image height");
+  Warped out{Gray(h, w, 0.0f), Raster<uint8_t>(h, w, 0)};
+  for (int v = 0; v < h; ++v) {
+    const double shift = t.s[size_t(v)];
+    for (int u = 0; u < w; ++u) {
+      const double s = u - shift;
+      if (s < 0.0 || s > w - 1) continue;
+      const int s0 = int(std::floor(s));
+      const int s1 = std::min(s0 + 1, w - 1);
+      const double frac = s - s0;
+      out.img(v, u) = float((1.0 - frac) * right(v, s0) + frac * right(v, s1));
+      out.in_view(v, u) = 1;
+    }
+  }
+  return out;
+}
+
+// perspective.hpp:69-80
+Disp restore(const Disp& d0, const Shifts& t) {
+  if (int(t.s.size()) != d0.h)
+    throw std::invalid_argument("restore_disparity: table length != map height");
+  Disp d1 = d0;
+  for (int v = 0; v < d0.h; ++v) {
+    const float add = float(t.s[size_t(v)]);
+    for (int u = 0; u < d0.w; ++u)
+      if (valid(d0(v, u))) d1(v, u) = d0(v, u) + add;
+  }
+  return d1;
+}
+
+// ----------------------------------------------------------------- SGM ----
+struct Volume {  // sgm.hpp:15-33
+  int w = 0, h = 0, d_max = 0;
+  std::vector<float> c;
+  Volume() = default;
+  Volume(int w_, int h_, int dm) : w(w_), h(h_), d_max(dm), c(size_t(w_) * h_ * (dm + 1), 0.f) {}
+  int levels() const { return d_max + 1; }
+  float& at(int v, int u, int d) { return c[(size_t(v) * w + u) * levels() + d]; }
+  float at(int v, int u, int d) const { return c[(size_t(v) * w + u) * levels() + d]; }
+};
+
+using Dirs = std::vector<std::array<int, 2>>;
+Dirs eight_directions() {  // sgm.hpp:41-43
+  return {{{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {1, 1}, {-1, 1}, {1, -1}, {-1, -1}}};
+}
+
+// sgm.cpp:13-34: bit per window sample, MSB first in row-major window order,
+// centre skipped, coordinates clamped at the border.
+Raster<uint64_t> census(const Gray& img, int window) {
+  const int h = img.h, w = img.w, r = window / 2;
+  Raster<uint64_t> out(h, w, 0);
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      const float c = img(v, u);
+      uint64_t bits = 0;
+      for (int dv = -r; dv <= r; ++dv) {
+        const int vv = std::clamp(v + dv, 0, h - 1);
+        for (int du = -r; du <= r; ++du) {
+          if (dv == 0 && du == 0) continue;
+          const int uu = std::clamp(u + du, 0, w - 1);
+          bits = (bits << 1) | (img(vv, uu) < c ? 1u : 0u);
+        }
+      }
+      out(v, u) = bits;
+    }
+  return out;
+}
+
+// sgm.cpp:38-68
+Volume cost_volume(const Gray& left, const Gray& right, int d_max, int window,
+                   const Raster<uint8_t>* in_view) {
+  const int h = left.h, w = left.w;
+  if (right.h != h || right.w != w)
+    throw std::invalid_argument("census_cost_volume: dimension mismatch");
+  if (window % 2 == 0) throw std::invalid_argument("census_cost_volume: window must be odd");
+  if (d_max >= w) throw std::invalid_argument("census_cost_volume: d_max >= width");
+  const float worst = float(window * window - 1);
+  const auto cl = census(left, window), cr = census(right, window);
+  Volume vol(w, h, d_max);
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u)
+      for (int d = 0; d <= d_max; ++d) {
+        const int ur = u - d;
+        vol.at(v, u, d) = (ur < 0 || (in_view && !(*in_view)(v, ur)))
+                              ? worst
+                              : float(std::popcount(cl(v, u) ^ cr(v, ur)));
+      }
+  return vol;
+}
+
+// sgm.cpp:70-110 — scan-line recursion per direction, summed over directions
+// in direction order.
+Volume aggregate(const Volume& raw, const Dirs& dirs, float l1, float l2) {
+  const int w = raw.w, h = raw.h, n = raw.levels();
+  Volume total(w, h, raw.d_max);
+  std::vector<float> line(size_t(w) * h * n);
+  for (const auto& dir : dirs) {
+    const int du = dir[0], dv = dir[1];
+    const int v0 = dv >= 0 ? 0 : h - 1, v1 = dv >= 0 ? h : -1, vs = dv >= 0 ? 1 : -1;
+    const int u0 = du >= 0 ? 0 : w - 1, u1 = du >= 0 ? w : -1, us = du >= 0 ? 1 : -1;
+    for (int v = v0; v != v1; v += vs)
+      for (int u = u0; u != u1; u += us) {
+        const size_t base = (size_t(v) * w + u) * n;
+        float* cur = &line[base];
+        const float* c = &raw.c[base];
+        const int pv = v - dv, pu = u - du;
+        if (pv < 0 || pv >= h || pu < 0 || pu >= w) {
+          std::copy(c, c + n, cur);
+          continue;
+        }
+        const float* prev = &line[(size_t(pv) * w + pu) * n];
+        float mn = prev[0];
+        for (int d = 1; d < n; ++d) mn = std::min(mn, prev[d]);
+        const float cap = mn + l2;
+        for (int d = 0; d < n; ++d) {
+          float b = prev[d];
+          if (d > 0) b = std::min(b, prev[d - 1] + l1);
+          if (d + 1 < n) b = std::min(b, prev[d + 1] + l1);
+          b = std::min(b, cap);
+          cur[d] = c[d] + b - mn;
+        }
+      }
+    for (size_t i = 0; i < total.c.size(); ++i) total.c[i] += line[i];
+  }
+  return total;
+}
+
+// sgm.cpp:112-121
+Volume swap_ref(const Volume& left) {
+  const float worst = *std::max_element(left.c.begin(), left.c.end());
+  Volume right(left.w, left.h, left.d_max);
+  for (int v = 0; v < left.h; ++v)
+    for (int u = 0; u < left.w; ++u)
+      for (int d = 0; d <= left.d_max; ++d)
+        right.at(v, u, d) = (u + d < left.w) ? left.at(v, u + d, d) : worst;
+  return right;
+}
+
+// sgm.cpp:123-153
+Disp wta(const Volume& agg) {
+  const int w = agg.w, h = agg.h, n = agg.levels();
+  Disp out(h, w);
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      const float* c = &agg.c[(size_t(v) * w + u) * n];
+      int best = 0;
+      for (int d = 1; d < n; ++d)
+        if (c[d] < c[best]) best = d;
+      bool ambiguous = false;
+      for (int d = 0; d < n; ++d)
+        if (std::abs(d - best) > 1 && c[d] <= c[best]) ambiguous = true;
+      if (ambiguous) {
+        out(v, u) = kInvalid;
+        continue;
+      }
+      float r = float(best);
+      if (best > 0 && best < n - 1) {
+        const float denom = c[best - 1] + c[best + 1] - 2.0f * c[best];
+        if (denom > 0.0f) r += (c[best - 1] - c[best + 1]) / (2.0f * denom);
+      }
+      out(v, u) = r;
+    }
+  return out;
+}
+
+// sgm.cpp:155-170
+void lr_check(Disp& left, const Disp& right, double thr) {
+  for (int v = 0; v < left.h; ++v)
+    for (int u = 0; u < left.w; ++u) {
+      const float dl = left(v, u);
+      if (!valid(dl)) continue;
+      const int ur = u - int(std::lround(dl));
+      if (ur < 0 || ur >= left.w || !valid(right(v, ur)) || std::abs(dl - right(v, ur)) > thr)
+        left(v, u) = kInvalid;
+    }
+}
+
+struct Match {
+  Disp d0, d1;
+  Shifts shifts;
+};
+
+Dirs config_dirs(const rpd_config& cfg) {
+  Dirs all = eight_directions();
+  all.resize(size_t(cfg.sgm_paths == 4 ? 4 : 8));
+  return all;
+}
+
+// sgm.cpp:172-226
+Match match_pair(const Gray& left, const Gray& right, const Model& m, const rpd_config& cfg,
+                 int d_max) {
+  if (left.h != right.h || left.w != right.w)
+    throw std::invalid_argument("match_pair: dimension mismatch");
+  Match res;
+  res.shifts = row_shifts(m, left.w, left.h, cfg.delta_pt);
+  Warped wr = warp(right, res.shifts);
+  const float l1 = float(cfg.lambda1), l2 = float(cfg.lambda2);
+  const Dirs dirs = config_dirs(cfg);
+  Volume raw = cost_volume(left, wr.img, d_max, cfg.census_window, &wr.in_view);
+  res.d0 = wta(aggregate(raw, dirs, l1, l2));
+  Disp right_disp = wta(aggregate(swap_ref(raw), dirs, l1, l2));
+  lr_check(res.d0, right_disp, cfg.lr_threshold);
+  // flat raw cost curve (sgm.cpp:200-212)
+  for (int v = 0; v < left.h; ++v)
+    for (int u = 0; u < left.w; ++u) {
+      if (!valid(res.d0(v, u))) continue;
+      float lo = std::numeric_limits<float>::max(), hi = std::numeric_limits<float>::lowest();
+      for (int d = 0; d <= d_max; ++d) {
+        const int ur = u - d;
+        if (ur < 0 || !wr.in_view(v, ur)) continue;
+        lo = std::min(lo, raw.at(v, u, d));
+        hi = std::max(hi, raw.at(v, u, d));
+      }
+      if (hi <= lo) res.d0(v, u) = kInvalid;
+    }
+  // best sample past the warped border (sgm.cpp:216-222)
+  for (int v = 0; v < left.h; ++v)
+    for (int u = 0; u < left.w; ++u) {
+      const float d = res.d0(v, u);
+      if (!valid(d)) continue;
+      const int ur = u - int(std::lround(d));
+      if (ur < 0 || !wr.in_view(v, ur)) res.d0(v, u) = kInvalid;
+    }
+  res.d1 = restore(res.d0, res.shifts);
+  return res;
+}
+
+// ------------------------------------------------------- road geometry ----
+struct Obs {
+  std::vector<double> d, u, v;
+  size_t count() const { return d.size(); }
+};
+
+// Fixed reduction order shared with the device kernel: element i goes to lane
+// i mod kFitLanes (sequential within a lane, starting from +0.0), then lanes
+// are combined by an adjacent-pairwise tree.
+constexpr int kFitLanes = 8192;
+template <typename F>
+double lane_tree_sum(size_t k, F term) {
+  std::vector<double> lane(kFitLanes, 0.0);
+  for (size_t i = 0; i < k; ++i) lane[i % kFitLanes] += term(i);
+  for (int width = 1; width < kFitLanes; width *= 2)
+    for (int j = 0; j < kFitLanes; j += 2 * width) lane[size_t(j)] += lane[size_t(j + width)];
+  return lane[0];
+}
+
+struct LineFit {
+  Model model;
+  double e0min = 0;
+};
+
+// road_geometry.cpp:12-39
+LineFit fit_line(const Obs& o, double phi) {
+  const size_t k = o.count();
+  if (k < 3) throw std::invalid_argument("fit_line: need at least 3 observations");
+  const double c = std::cos(phi), s = std::sin(phi);
+  auto t = [&](size_t i) { return c * o.v[i] - s * o.u[i]; };
+  const double kk = double(k);
+  const double st = lane_tree_sum(k, [&](size_t i) { return t(i); });
+  const double stt = lane_tree_sum(k, [&](size_t i) { const double x = t(i); return x * x; });
+  const double sd = lane_tree_sum(k, [&](size_t i) { return o.d[i]; });
+  const double sdt = lane_tree_sum(k, [&](size_t i) { return o.d[i] * t(i); });
+  const double det = kk * stt - st * st;
+  const double scale = std::max(kk * stt, 1.0);
+  if (std::abs(det) < 1e-12 * scale)
+    throw Degenerate("fit_line: degenerate observations (singular normal matrix)");
+  LineFit f;
+  f.model.phi = phi;
+  f.model.a0 = (stt * sd - st * sdt) / det;
+  f.model.a1 = (kk * sdt - st * sd) / det;
+  f.e0min = lane_tree_sum(k, [&](size_t i) {
+    const double r = o.d[i] - f.model.a0 - f.model.a1 * t(i);
+    return r * r;
+  });
+  return f;
+}
+
+// road_geometry.cpp:41-68 — golden-section search on e0min(phi).
+Model estimate_roll(const Obs& o, double lo, double hi, double tol) {
+  if (tol <= 0) throw std::invalid_argument("estimate_roll: tol must be > 0");
+  constexpr double g = 0.6180339887498949;
+  double a = lo, b = hi;
+  double x1 = b - g * (b - a), x2 = a + g * (b - a);
+  double f1 = fit_line(o, x1).e0min, f2 = fit_line(o, x2).e0min;
+  while (b - a > tol) {
+    if (f1 < f2) {
+      b = x2;
+      x2 = x1;
+      f2 = f1;
+      x1 = b - g * (b - a);
+      f1 = fit_line(o, x1).e0min;
+    } else {
+      a = x1;
+      x1 = x2;
+      f1 = f2;
+      x2 = a + g * (b - a);
+      f2 = fit_line(o, x2).e0min;
+    }
+  }
+  return fit_line(o, 0.5 * (a + b)).model;
+}
+
+struct RoadFit {
+  Model model;
+  double e0min = 0;
+  int64_t used = 0;
+};
+
+// road_geometry.cpp:70-101
+RoadFit fit_road(const Obs& o, double bracket, double tol) {
+  const Model m = estimate_roll(o, -bracket, bracket, tol);
+  const LineFit first = fit_line(o, m.phi);
+  const size_t k = o.count();
+  const double rms = std::sqrt(first.e0min / double(k));
+  RoadFit out{first.model, first.e0min, int64_t(k)};
+  if (rms <= 0) return out;
+  Obs kept;
+  for (size_t i = 0; i < k; ++i) {
+    const double r = o.d[i] - road_at(first.model, o.u[i], o.v[i]);
+    if (std::abs(r) <= 3.0 * rms) {
+      kept.d.push_back(o.d[i]);
+      kept.u.push_back(o.u[i]);
+      kept.v.push_back(o.v[i]);
+    }
+  }
+  if (kept.count() < 3 || kept.count() == k) return out;
+  const Model m2 = estimate_roll(kept, -bracket, bracket, tol);
+  const LineFit second = fit_line(kept, m2.phi);
+  return RoadFit{second.model, second.e0min, int64_t(kept.count())};
+}
+
+// road_geometry.cpp:103-134
+Obs sample(const Disp& d1, const rpd_rect_roi* roi, int64_t cap) {
+  const int h = d1.h, w = d1.w;
+  rpd_rect_roi r = roi ? *roi : rpd_rect_roi{0, 0, w, h};
+  r.u0 = std::clamp(r.u0, 0, w);
+  r.v0 = std::clamp(r.v0, 0, h);
+  r.width = std::clamp(r.width, 0, w - r.u0);
+  r.height = std::clamp(r.height, 0, h - r.v0);
+  std::vector<std::array<int, 2>> pts;
+  for (int v = r.v0; v < r.v0 + r.height; ++v)
+    for (int u = r.u0; u < r.u0 + r.width; ++u)
+      if (valid(d1(v, u))) pts.push_back({u, v});
+  const int64_t n = int64_t(pts.size());
+  if (n < 3) throw Degenerate("sample_observations: fewer than 3 valid pixels");
+  const int64_t k = std::min(n, cap);
+  Obs o;
+  o.d.resize(size_t(k));
+  o.u.resize(size_t(k));
+  o.v.resize(size_t(k));
+  for (int64_t i = 0; i < k; ++i) {
+    const auto& p = pts[size_t(i * n / k)];
+    o.u[size_t(i)] = p[0];
+    o.v[size_t(i)] = p[1];
+    o.d[size_t(i)] = d1(p[1], p[0]);
+  }
+  return o;
+}
+
+// road_geometry.cpp:136-151
+Disp transform(const Disp& d1, const Model& m, double delta_dt, int64_t* clamped) {
+  Disp d2 = d1;
+  int64_t n = 0;
+  for (int v = 0; v < d1.h; ++v)
+    for (int u = 0; u < d1.w; ++u) {
+      if (!valid(d1(v, u))) continue;
+      double x = d1(v, u) - road_at(m, u, v) + delta_dt;
+      if (x < 0) {
+        x = 0;
+        ++n;
+      }
+      d2(v, u) = float(x);
+    }
+  if (clamped) *clamped = n;
+  return d2;
+}
+
+// -------------------------------------------------------- segmentation ----
+struct Center {
+  double cu = 0, cv = 0, value = 0;
+};
+struct Superpixels {
+  Labels labels;
+  std::vector<Center> centers;
+  int count = 0;
+  double spacing = 0;
+};
+
+constexpr int kDU[8] = {1, -1, 0, 0, 1, 1, -1, -1};  // segmentation.cpp:104-105
+constexpr int kDV[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+
+// segmentation.cpp:22-28 (float difference, then squared in double)
+double gradient_at(const Gray& vals, int u, int v) {
+  const double gu = vals(v, std::min(u + 1, vals.w - 1)) - vals(v, u);
+  const double gv = vals(std::min(v + 1, vals.h - 1), u) - vals(v, u);
+  return gu * gu + gv * gv;
+}
+
+// segmentation.cpp:30-72
+void assign(const Gray& vals, const std::vector<Center>& cs, double S, double m, Labels& lab) {
+  const int h = vals.h, w = vals.w;
+  Raster<double> best(h, w, std::numeric_limits<double>::infinity());
+  std::fill(lab.a.begin(), lab.a.end(), 0);
+  const int win = int(std::ceil(S));
+  const double sw = m * m / (S * S);
+  for (size_t k = 0; k < cs.size(); ++k) {
+    const Center& c = cs[k];
+    const int cu = int(std::lround(c.cu)), cv = int(std::lround(c.cv));
+    const int va = std::max(0, cv - win), vb = std::min(h - 1, cv + win);
+    const int ua = std::max(0, cu - win), ub = std::min(w - 1, cu + win);
+    for (int v = va; v <= vb; ++v)
+      for (int u = ua; u <= ub; ++u) {
+        const double dval = vals(v, u) - c.value;
+        const double du = u - c.cu, dv = v - c.cv;
+        const double dist = dval * dval + (du * du + dv * dv) * sw;
+        if (dist < best(v, u)) {
+          best(v, u) = dist;
+          lab(v, u) = int(k) + 1;
+        }
+      }
+  }
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      if (lab(v, u) != 0) continue;
+      double nearest = std::numeric_limits<double>::infinity();
+      for (size_t k = 0; k < cs.size(); ++k) {
+        const double du = u - cs[k].cu, dv = v - cs[k].cv;
+        const double dd = du * du + dv * dv;
+        if (dd < nearest) {
+          nearest = dd;
+          lab(v, u) = int(k) + 1;
+        }
+      }
+    }
+}
+
+// segmentation.cpp:74-93 (sums accumulate in scan order)
+void update(const Gray& vals, const Labels& lab, std::vector<Center>& cs) {
+  const size_t K = cs.size();
+  std::vector<double> su(K, 0), sv(K, 0), sx(K, 0);
+  std::vector<int64_t> n(K, 0);
+  for (int v = 0; v < lab.h; ++v)
+    for (int u = 0; u < lab.w; ++u) {
+      const int k = lab(v, u) - 1;
+      if (k < 0) continue;
+      su[size_t(k)] += u;
+      sv[size_t(k)] += v;
+      sx[size_t(k)] += vals(v, u);
+      ++n[size_t(k)];
+    }
+  for (size_t k = 0; k < K; ++k) {
+    if (n[k] == 0) continue;
+    cs[k].cu = su[k] / double(n[k]);
+    cs[k].cv = sv[k] / double(n[k]);
+    cs[k].value = sx[k] / double(n[k]);
+  }
+}
+
+// segmentation.cpp:98-166
+void connectivity(Labels& lab) {
+  const int h = lab.h, w = lab.w;
+  Labels piece(h, w, 0);
+  std::vector<int64_t> size;
+  std::vector<int> plabel;
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      if (piece(v, u) != 0) continue;
+      const int id = int(size.size()) + 1;
+      const int l = lab(v, u);
+      int64_t sz = 0;
+      std::deque<std::array<int, 2>> q{{u, v}};
+      piece(v, u) = id;
+      while (!q.empty()) {
+        const auto [pu, pv] = q.front();
+        q.pop_front();
+        ++sz;
+        for (int i = 0; i < 8; ++i) {
+          const int nu = pu + kDU[i], nv = pv + kDV[i];
+          if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+          if (piece(nv, nu) == 0 && lab(nv, nu) == l) {
+            piece(nv, nu) = id;
+            q.push_back({nu, nv});
+          }
+        }
+      }
+      size.push_back(sz);
+      plabel.push_back(l);
+    }
+  std::map<int, int> main_piece;
+  for (size_t i = 0; i < size.size(); ++i) {
+    auto it = main_piece.find(plabel[i]);
+    if (it == main_piece.end() || size[i] > size[size_t(it->second - 1)])
+      main_piece[plabel[i]] = int(i) + 1;
+  }
+  std::vector<char> kept(size.size(), 0);
+  for (const auto& kv : main_piece) kept[size_t(kv.second - 1)] = 1;
+  std::deque<std::array<int, 2>> front;
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      if (kept[size_t(piece(v, u) - 1)])
+        front.push_back({u, v});
+      else
+        lab(v, u) = 0;
+    }
+  while (!front.empty()) {
+    const auto [pu, pv] = front.front();
+    front.pop_front();
+    for (int i = 0; i < 8; ++i) {
+      const int nu = pu + kDU[i], nv = pv + kDV[i];
+      if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+      if (lab(nv, nu) == 0) {
+        lab(nv, nu) = lab(pv, pu);
+        front.push_back({nu, nv});
+      }
+    }
+  }
+}
+
+// segmentation.cpp:170-229
+Superpixels slic(const Disp& d2, int p, double m, int iters) {
+  const int h = d2.h, w = d2.w;
+  if (p < 4) throw std::invalid_argument("slic: p must be >= 4");
+  if (p > w * h) throw std::invalid_argument("slic: p exceeds pixel count");
+  Gray vals = d2;
+  for (auto& x : vals.a)
+    if (!valid(x)) x = 0.0f;
+  Superpixels sp;
+  sp.spacing = std::sqrt(double(w) * h / p);
+  const int nu = std::max(1, int(std::lround(std::sqrt(double(p) * w / h))));
+  const int nv = std::max(1, int(std::lround(double(p) / nu)));
+  const double su = double(w) / nu, sv = double(h) / nv;
+  for (int j = 0; j < nv; ++j)
+    for (int i = 0; i < nu; ++i) {
+      const int cu = int((i + 0.5) * su), cv = int((j + 0.5) * sv);
+      double best = std::numeric_limits<double>::infinity();
+      int bu = cu, bv = cv;
+      for (int dv = -1; dv <= 1; ++dv)
+        for (int du = -1; du <= 1; ++du) {
+          const int uu = std::clamp(cu + du, 0, w - 1), vv = std::clamp(cv + dv, 0, h - 1);
+          const double g = gradient_at(vals, uu, vv);
+          if (g < best) {
+            best = g;
+            bu = uu;
+            bv = vv;
+          }
+        }
+      sp.centers.push_back({double(bu), double(bv), double(vals(bv, bu))});
+    }
+  sp.labels = Labels(h, w, 0);
+  assign(vals, sp.centers, sp.spacing, m, sp.labels);
+  for (int it = 0; it < iters; ++it) {
+    update(vals, sp.labels, sp.centers);
+    assign(vals, sp.centers, sp.spacing, m, sp.labels);
+  }
+  connectivity(sp.labels);
+  std::map<int, int> remap;
+  for (auto& l : sp.labels.a) {
+    auto [it, fresh] = remap.try_emplace(l, int(remap.size()) + 1);
+    (void)fresh;
+    l = it->second;
+  }
+  sp.count = int(remap.size());
+  sp.centers.assign(size_t(sp.count), Center{});
+  update(vals, sp.labels, sp.centers);
+  return sp;
+}
+
+// segmentation.cpp:231-249
+Disp pool(const Disp& d2, const Labels& lab, int count) {
+  if (d2.h != lab.h || d2.w != lab.w)
+    throw std::invalid_argument("pool_superpixels: dimension mismatch");
+  std::vector<double> sum(size_t(count) + 1, 0.0);
+  std::vector<int64_t> n(size_t(count) + 1, 0);
+  for (size_t i = 0; i < d2.a.size(); ++i) {
+    if (!valid(d2.a[i])) continue;
+    sum[size_t(lab.a[i])] += d2.a[i];
+    ++n[size_t(lab.a[i])];
+  }
+  Disp d3(d2.h, d2.w);
+  for (size_t i = 0; i < d2.a.size(); ++i) {
+    const size_t k = size_t(lab.a[i]);
+    d3.a[i] = n[k] > 0 ? float(sum[k] / double(n[k])) : kInvalid;
+  }
+  return d3;
+}
+
+struct Hist {
+  double bw = 0.25, origin = 0;
+  int64_t n = 0;
+  std::vector<int64_t> counts;  // n*n row-major, rows = g1 bins
+  int64_t total = 0;
+  double center(int64_t b) const { return origin + (b + 0.5) * bw; }
+};
+
+// segmentation.cpp:251-296
+Hist histogram(const Disp& d2, double bw) {
+  if (bw <= 0) throw std::invalid_argument("build_histogram: bin_width must be > 0");
+  const int h = d2.h, w = d2.w;
+  std::vector<std::array<double, 2>> g;
+  for (int v = 1; v + 1 < h; ++v)
+    for (int u = 1; u + 1 < w; ++u) {
+      if (!valid(d2(v, u))) continue;
+      double sum = 0.0;
+      bool ok = true;
+      for (int dv = -1; dv <= 1 && ok; ++dv)
+        for (int du = -1; du <= 1; ++du) {
+          if (du == 0 && dv == 0) continue;
+          const float x = d2(v + dv, u + du);
+          if (!valid(x)) {
+            ok = false;
+            break;
+          }
+          sum += x;
+        }
+      if (ok) g.push_back({double(d2(v, u)), sum / 8.0});
+    }
+  Hist hist;
+  hist.bw = bw;
+  if (g.empty()) return hist;
+  double lo = g[0][0], hi = g[0][0];
+  for (const auto& x : g) {
+    lo = std::min({lo, x[0], x[1]});
+    hi = std::max({hi, x[0], x[1]});
+  }
+  hist.origin = std::floor(lo / bw) * bw;
+  auto bin = [&](double x) { return int64_t(std::floor((x - hist.origin) / bw)); };
+  hist.n = bin(hi) + 1;
+  hist.counts.assign(size_t(hist.n * hist.n), 0);
+  for (const auto& x : g) {
+    const int64_t i = std::min(bin(x[0]), hist.n - 1), j = std::min(bin(x[1]), hist.n - 1);
+    ++hist.counts[size_t(i * hist.n + j)];
+    ++hist.total;
+  }
+  return hist;
+}
+
+// segmentation.cpp:298-359
+rpd_threshold threshold(const Hist& hist, double delta_pd, double tau) {
+  std::map<double, int64_t> diag;
+  int64_t excluded = 0;
+  for (int64_t i = 0; i < hist.n; ++i)
+    for (int64_t j = 0; j < hist.n; ++j) {
+      const int64_t c = hist.counts[size_t(i * hist.n + j)];
+      if (c == 0) continue;
+      const double g1 = hist.center(i), g2 = hist.center(j);
+      if (std::abs(g1 - g2) > tau) {
+        excluded += c;
+        continue;
+      }
+      diag[(g1 + g2) / 2.0] += c;
+    }
+  if (diag.empty()) throw Degenerate("find_road_threshold: all vectors excluded");
+  rpd_threshold res{};
+  res.excluded_fraction = hist.total > 0 ? double(excluded) / double(hist.total) : 0.0;
+  std::vector<double> x;
+  std::vector<int64_t> wt;
+  for (const auto& kv : diag) {
+    x.push_back(kv.first);
+    wt.push_back(kv.second);
+  }
+  const size_t m = x.size();
+  if (m < 2) {
+    res.degenerate = 1;
+    res.mu1 = res.mu2 = res.t_r = x[0];
+    res.t_s = res.t_r - delta_pd;
+    return res;
+  }
+  std::vector<double> pw(m + 1, 0), pwx(m + 1, 0), pwxx(m + 1, 0);
+  for (size_t i = 0; i < m; ++i) {
+    pw[i + 1] = pw[i] + double(wt[i]);
+    pwx[i + 1] = pwx[i] + double(wt[i]) * x[i];
+    pwxx[i + 1] = pwxx[i] + double(wt[i]) * x[i] * x[i];
+  }
+  auto sse = [&](size_t a, size_t b) {
+    const double n = pw[b] - pw[a], s = pwx[b] - pwx[a], ss = pwxx[b] - pwxx[a];
+    return ss - s * s / n;
+  };
+  size_t split = 1;
+  double best = std::numeric_limits<double>::infinity();
+  for (size_t s = 1; s < m; ++s) {
+    const double e = sse(0, s) + sse(s, m);
+    if (e < best) {
+      best = e;
+      split = s;
+    }
+  }
+  res.mu1 = (pwx[split] - pwx[0]) / (pw[split] - pw[0]);
+  res.mu2 = (pwx[m] - pwx[split]) / (pw[m] - pw[split]);
+  res.t_r = res.mu2;
+  res.t_s = res.t_r - delta_pd;
+  return res;
+}
+
+// segmentation.cpp:361-390
+Labels ccl(const Labels& mask, int conn) {
+  const int h = mask.h, w = mask.w, nd = conn == 4 ? 4 : 8;
+  Labels out(h, w, 0);
+  int next = 0;
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      if (mask(v, u) == 0 || out(v, u) != 0) continue;
+      ++next;
+      std::deque<std::array<int, 2>> q{{u, v}};
+      out(v, u) = next;
+      while (!q.empty()) {
+        const auto [pu, pv] = q.front();
+        q.pop_front();
+        for (int i = 0; i < nd; ++i) {
+          const int nu = pu + kDU[i], nv = pv + kDV[i];
+          if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+          if (mask(nv, nu) != 0 && out(nv, nu) == 0) {
+            out(nv, nu) = next;
+            q.push_back({nu, nv});
+          }
+        }
+      }
+    }
+  return out;
+}
+
+// segmentation.cpp:392-434
+Labels detect(const Disp& d3, const Labels& sp_labels, double spacing, const rpd_threshold& thr,
+              int margin, int min_sp, int conn) {
+  const int h = d3.h, w = d3.w;
+  Labels mask(h, w, 0);
+  for (size_t i = 0; i < d3.a.size(); ++i)
+    if (valid(d3.a[i]) && d3.a[i] < thr.t_s) mask.a[i] = 1;
+  const Labels comp = ccl(mask, conn);
+  const int nc = comp.a.empty() ? 0 : *std::max_element(comp.a.begin(), comp.a.end());
+  std::vector<char> border(size_t(nc) + 1, 0);
+  std::vector<int64_t> area(size_t(nc) + 1, 0);
+  std::vector<std::map<int, char>> sps(size_t(nc) + 1);
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      const int c = comp(v, u);
+      if (c == 0) continue;
+      ++area[size_t(c)];
+      sps[size_t(c)][sp_labels(v, u)] = 1;
+      if (u < margin || u >= w - margin || v < margin || v >= h - margin) border[size_t(c)] = 1;
+    }
+  const int64_t min_area = int64_t(spacing * spacing);
+  std::vector<int> relabel(size_t(nc) + 1, 0);
+  Labels out(h, w, 0);
+  int next = 0;
+  for (size_t i = 0; i < comp.a.size(); ++i) {
+    const int c = comp.a[i];
+    if (c == 0) continue;
+    if (border[size_t(c)] || area[size_t(c)] < min_area || int(sps[size_t(c)].size()) < min_sp)
+      continue;
+    if (relabel[size_t(c)] == 0) relabel[size_t(c)] = ++next;
+    out.a[i] = relabel[size_t(c)];
+  }
+  return out;
+}
+
+// ------------------------------------------------------------ pipeline ----
+// pipeline.cpp:25-34
+Gray half(const Gray& img) {
+  const int h = img.h / 2, w = img.w / 2;
+  Gray out(h, w);
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u)
+      out(v, u) = 0.25f * (img(2 * v, 2 * u) + img(2 * v, 2 * u + 1) + img(2 * v + 1, 2 * u) +
+                           img(2 * v + 1, 2 * u + 1));
+  return out;
+}
+
+}  // namespace oracle
+
+// ===================================================================== ABI ==
+using namespace oracle;
+
+struct rpd_ctx {
+  std::string err;
+};
+
+namespace {
+
+Gray to_gray(const float* p, int h, int w) {
+  Gray g(h, w);
+  std::memcpy(g.a.data(), p, sizeof(float) * g.a.size());
+  return g;
+}
+void put(float* dst, const Raster<float>& r) {
+  if (dst) std::memcpy(dst, r.a.data(), sizeof(float) * r.a.size());
+}
+void put(int32_t* dst, const Raster<int>& r) {
+  if (dst) std::memcpy(dst, r.a.data(), sizeof(int32_t) * r.a.size());
+}
+Obs to_obs(const double* d, const double* u, const double* v, int64_t k) {
+  Obs o;
+  o.d.assign(d, d + k);
+  o.u.assign(u, u + k);
+  o.v.assign(v, v + k);
+  return o;
+}
+
+template <typename F>
+rpd_status guard(rpd_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->err.clear();
+    return RPD_OK;
+  } catch (const std::invalid_argument& e) {
+    if (ctx) ctx->err = e.what();
+    return RPD_EINVAL;
+  } catch (const std::runtime_error& e) {
+    if (ctx) ctx->err = e.what();
+    return RPD_EDEGENERATE;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "out of memory";
+    return RPD_ENOMEM;
+  }
+}
+
+void check_dims(int h, int w) {
+  if (h <= 0 || w <= 0) throw std::invalid_argument("image dimensions must be positive");
+}
+
+rpd_status detect_impl(rpd_ctx* ctx, const Gray& left, const Gray& right, const rpd_config* cfg,
+                       rpd_detect_out* out) {
+  return guard(ctx, [&] {
+    const rpd_config& c = *cfg;
+    config_validate(c);
+    if (left.h != right.h || left.w != right.w)
+      throw std::invalid_argument("match_pair: dimension mismatch");
+    // pipeline.cpp:57-63 bootstrap at half resolution with a flat model
+    const bool halve = left.h >= 64 && left.w >= 64;
+    rpd_config boot = c;
+    if (halve) boot.d_max = (c.d_max + 1) / 2;
+    Match bootm = halve ? match_pair(half(left), half(right), Model{}, boot, boot.d_max)
+                        : match_pair(left, right, Model{}, c, c.d_max);
+    RoadFit coarse;
+    try {
+      coarse = fit_road(sample(bootm.d1, nullptr, 100000), c.roll_bracket, c.roll_tol);
+    } catch (const std::runtime_error& e) {
+      throw Degenerate(std::string("road fit failed: ") + e.what());
+    }
+    if (halve) coarse.model.a0 *= 2.0;
+    Match pt = match_pair(left, right, coarse.model, c, c.d_max_pt);
+    RoadFit fit;
+    try {
+      fit = fit_road(sample(pt.d1, nullptr, 100000), c.roll_bracket, c.roll_tol);
+    } catch (const std::runtime_error& e) {
+      throw Degenerate(std::string("road refit failed: ") + e.what());
+    }
+    int64_t clamped = 0;
+    Disp d2 = transform(pt.d1, fit.model, c.delta_dt, &clamped);
+    Superpixels sp = slic(d2, c.superpixels, c.compactness, c.slic_iterations);
+    Disp d3 = pool(d2, sp.labels, sp.count);
+    Hist hist = histogram(d2, c.hist_bin_width);
+    rpd_threshold thr = threshold(hist, c.delta_pd, c.tau_diag);
+    Labels lab = detect(d3, sp.labels, sp.spacing, thr, c.border_margin, c.min_superpixels,
+                        c.connectivity);
+    put(out->d0, pt.d0);
+    put(out->d1, pt.d1);
+    put(out->d2, d2);
+    put(out->d3, d3);
+    put(out->labels, lab);
+    put(out->sp_labels, sp.labels);
+    if (out->centers)
+      for (int k = 0; k < std::min(out->centers_cap, sp.count); ++k)
+        out->centers[k] = {sp.centers[size_t(k)].cu, sp.centers[size_t(k)].cv,
+                           sp.centers[size_t(k)].value};
+    out->sp_count = sp.count;
+    out->sp_spacing = sp.spacing;
+    out->coarse_fit = {{coarse.model.a0, coarse.model.a1, coarse.model.phi}, coarse.e0min,
+                       coarse.used};
+    out->fit = {{fit.model.a0, fit.model.a1, fit.model.phi}, fit.e0min, fit.used};
+    out->threshold = thr;
+    out->clamped = clamped;
+    out->n_potholes = lab.a.empty() ? 0 : *std::max_element(lab.a.begin(), lab.a.end());
+    for (double& s : out->stage_ms) s = 0.0;
+    out->total_ms = 0.0;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int rpd_abi_version(void) { return RPD_ABI_VERSION; }
+
+rpd_status rpd_ctx_create(int, int, int, int, rpd_ctx** out) {
+  if (!out) return RPD_EINVAL;
+  *out = new rpd_ctx();
+  return RPD_OK;
+}
+void rpd_ctx_destroy(rpd_ctx* ctx) { delete ctx; }
+const char* rpd_last_error(const rpd_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+void* rpd_ctx_stream(rpd_ctx*) { return nullptr; }
+
+void rpd_config_default(rpd_config* cfg) { config_default(cfg); }
+
+rpd_status rpd_config_validate(rpd_ctx* ctx, const rpd_config* cfg) {
+  return guard(ctx, [&] { config_validate(*cfg); });
+}
+
+rpd_status rpd_config_set(rpd_ctx* ctx, rpd_config* c, const char* key_c, const char* val_c) {
+  return guard(ctx, [&] {  // config.cpp:24-51
+    const std::string key = key_c, value = val_c;
+    auto d = [&] { return std::stod(value); };
+    auto i = [&] { return std::stoi(value); };
+    if (key == "delta_pt") c->delta_pt = d();
+    else if (key == "delta_dt") c->delta_dt = d();
+    else if (key == "delta_pd") c->delta_pd = d();
+    else if (key == "d_max") c->d_max = i();
+    else if (key == "d_max_pt") c->d_max_pt = i();
+    else if (key == "lambda1") c->lambda1 = d();
+    else if (key == "lambda2") c->lambda2 = d();
+    else if (key == "census_window") c->census_window = i();
+    else if (key == "lr_threshold") c->lr_threshold = d();
+    else if (key == "superpixels") c->superpixels = i();
+    else if (key == "compactness") c->compactness = d();
+    else if (key == "slic_iterations") c->slic_iterations = i();
+    else if (key == "hist_bin_width") c->hist_bin_width = d();
+    else if (key == "tau_diag") c->tau_diag = d();
+    else if (key == "border_margin") c->border_margin = i();
+    else if (key == "min_superpixels") c->min_superpixels = i();
+    else if (key == "connectivity") c->connectivity = i();
+    else if (key == "roll_bracket") c->roll_bracket = d();
+    else if (key == "roll_tol") c->roll_tol = d();
+    else if (key == "focal") c->focal = d();
+    else if (key == "baseline") c->baseline = d();
+    else if (key == "cu") c->cu = d();
+    else if (key == "cv") c->cv = d();
+    else if (key == "sgm_paths") c->sgm_paths = i();
+    else throw std::invalid_argument("config: unknown key '" + key + "'");
+  });
+}
+
+rpd_status rpd_detect(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                      const rpd_config* cfg, rpd_detect_out* out) {
+  if (h <= 0 || w <= 0) {
+    if (ctx) ctx->err = "image dimensions must be positive";
+    return RPD_EINVAL;
+  }
+  return detect_impl(ctx, to_gray(left, h, w), to_gray(right, h, w), cfg, out);
+}
+
+rpd_status rpd_detect_u8(rpd_ctx* ctx, const uint8_t* left, const uint8_t* right, int h, int w,
+                         const rpd_config* cfg, rpd_detect_out* out) {
+  if (h <= 0 || w <= 0) {
+    if (ctx) ctx->err = "image dimensions must be positive";
+    return RPD_EINVAL;
+  }
+  Gray l(h, w), r(h, w);
+  for (size_t i = 0; i < l.a.size(); ++i) {
+    l.a[i] = float(left[i]);
+    r.a[i] = float(right[i]);
+  }
+  return detect_impl(ctx, l, r, cfg, out);
+}
+
+rpd_status rpd_compute_row_shifts(rpd_ctx* ctx, const rpd_road_model* m, int w, int h,
+                                  double delta_pt, double* shifts) {
+  return guard(ctx, [&] {
+    const Shifts t = row_shifts({m->a0, m->a1, m->phi}, w, h, delta_pt);
+    std::copy(t.s.begin(), t.s.end(), shifts);
+  });
+}
+
+rpd_status rpd_warp_right_image(rpd_ctx* ctx, const float* right, int h, int w,
+                                const double* shifts, float* image, uint8_t* in_view) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    Shifts t;
+    t.s.assign(shifts, shifts + h);
+    const Warped wr = warp(to_gray(right, h, w), t);
+    put(image, wr.img);
+    if (in_view) std::memcpy(in_view, wr.in_view.a.data(), wr.in_view.a.size());
+  });
+}
+
+rpd_status rpd_restore_disparity(rpd_ctx* ctx, const float* d0, int h, int w,
+                                 const double* shifts, float* d1) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    Shifts t;
+    t.s.assign(shifts, shifts + h);
+    put(d1, restore(to_gray(d0, h, w), t));
+  });
+}
+
+rpd_status rpd_census_cost_volume(rpd_ctx* ctx, const float* left, const float* right, int h,
+                                  int w, int d_max, int window, const uint8_t* in_view,
+                                  float* costs) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (d_max < 0) throw std::invalid_argument("census_cost_volume: d_max must be >= 0");
+    Raster<uint8_t> iv;
+    if (in_view) {
+      iv = Raster<uint8_t>(h, w);
+      std::memcpy(iv.a.data(), in_view, iv.a.size());
+    }
+    const Volume vol =
+        cost_volume(to_gray(left, h, w), to_gray(right, h, w), d_max, window, in_view ? &iv : nullptr);
+    std::memcpy(costs, vol.c.data(), sizeof(float) * vol.c.size());
+  });
+}
+
+static Volume to_volume(const float* costs, int h, int w, int d_max) {
+  if (h <= 0 || w <= 0 || d_max < 0) throw std::invalid_argument("cost volume: bad dimensions");
+  Volume v(w, h, d_max);
+  std::memcpy(v.c.data(), costs, sizeof(float) * v.c.size());
+  return v;
+}
+
+rpd_status rpd_aggregate_costs(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
+                               const int32_t* dirs, int ndirs, float l1, float l2, float* agg) {
+  return guard(ctx, [&] {
+    Dirs ds;
+    for (int i = 0; i < ndirs; ++i) ds.push_back({dirs[2 * i], dirs[2 * i + 1]});
+    const Volume out = aggregate(to_volume(costs, h, w, d_max), ds, l1, l2);
+    std::memcpy(agg, out.c.data(), sizeof(float) * out.c.size());
+  });
+}
+
+rpd_status rpd_swap_reference(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
+                              float* right_costs) {
+  return guard(ctx, [&] {
+    const Volume out = swap_ref(to_volume(costs, h, w, d_max));
+    std::memcpy(right_costs, out.c.data(), sizeof(float) * out.c.size());
+  });
+}
+
+rpd_status rpd_select_disparity(rpd_ctx* ctx, const float* agg, int h, int w, int d_max,
+                                float* disp) {
+  return guard(ctx, [&] { put(disp, wta(to_volume(agg, h, w, d_max))); });
+}
+
+rpd_status rpd_consistency_filter(rpd_ctx* ctx, float* left, const float* right, int h, int w,
+                                  double thr) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    Disp l = to_gray(left, h, w);
+    lr_check(l, to_gray(right, h, w), thr);
+    put(left, l);
+  });
+}
+
+rpd_status rpd_match_pair(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                          const rpd_road_model* m, const rpd_config* cfg, int d_max, float* d0,
+                          float* d1, double* shifts) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (cfg->sgm_paths != 4 && cfg->sgm_paths != 8)
+      throw std::invalid_argument("config: sgm_paths must be 4 or 8");
+    const Match r = match_pair(to_gray(left, h, w), to_gray(right, h, w), {m->a0, m->a1, m->phi},
+                               *cfg, d_max);
+    put(d0, r.d0);
+    put(d1, r.d1);
+    if (shifts) std::copy(r.shifts.s.begin(), r.shifts.s.end(), shifts);
+  });
+}
+
+rpd_status rpd_sample_observations(rpd_ctx* ctx, const float* d1, int h, int w,
+                                   const rpd_rect_roi* roi, int64_t cap, double* d, double* u,
+                                   double* v, int64_t* count) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    const Obs o = sample(to_gray(d1, h, w), roi, cap);
+    std::copy(o.d.begin(), o.d.end(), d);
+    std::copy(o.u.begin(), o.u.end(), u);
+    std::copy(o.v.begin(), o.v.end(), v);
+    *count = int64_t(o.count());
+  });
+}
+
+rpd_status rpd_fit_line(rpd_ctx* ctx, const double* d, const double* u, const double* v,
+                        int64_t k, double phi, rpd_line_fit* out) {
+  return guard(ctx, [&] {
+    const LineFit f = fit_line(to_obs(d, u, v, k), phi);
+    *out = {{f.model.a0, f.model.a1, f.model.phi}, f.e0min};
+  });
+}
+
+rpd_status rpd_estimate_roll(rpd_ctx* ctx, const double* d, const double* u, const double* v,
+                             int64_t k, double lo, double hi, double tol, rpd_road_model* out) {
+  return guard(ctx, [&] {
+    const Model m = estimate_roll(to_obs(d, u, v, k), lo, hi, tol);
+    *out = {m.a0, m.a1, m.phi};
+  });
+}
+
+rpd_status rpd_fit_road(rpd_ctx* ctx, const double* d, const double* u, const double* v,
+                        int64_t k, double bracket, double tol, rpd_road_fit* out) {
+  return guard(ctx, [&] {
+    const RoadFit f = fit_road(to_obs(d, u, v, k), bracket, tol);
+    *out = {{f.model.a0, f.model.a1, f.model.phi}, f.e0min, f.used};
+  });
+}
+
+rpd_status rpd_transform_disparity(rpd_ctx* ctx, const float* d1, int h, int w,
+                                   const rpd_road_model* m, double delta_dt, float* d2,
+                                   int64_t* clamped) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    put(d2, transform(to_gray(d1, h, w), {m->a0, m->a1, m->phi}, delta_dt, clamped));
+  });
+}
+
+rpd_status rpd_slic(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, int iters,
+                    int32_t* labels, rpd_center* centers, int cap, int32_t* count,
+                    double* spacing) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    const Superpixels sp = slic(to_gray(d2, h, w), p, m, iters);
+    put(labels, sp.labels);
+    if (centers)
+      for (int k = 0; k < std::min(cap, sp.count); ++k)
+        centers[k] = {sp.centers[size_t(k)].cu, sp.centers[size_t(k)].cv,
+                      sp.centers[size_t(k)].value};
+    if (count) *count = sp.count;
+    if (spacing) *spacing = sp.spacing;
+  });
+}
+
+rpd_status rpd_pool_superpixels(rpd_ctx* ctx, const float* d2, const int32_t* lab, int count,
+                                int h, int w, float* d3) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    Labels l(h, w);
+    std::memcpy(l.a.data(), lab, sizeof(int32_t) * l.a.size());
+    for (int x : l.a)
+      if (x < 0 || x > count) throw std::invalid_argument("pool_superpixels: label out of range");
+    put(d3, pool(to_gray(d2, h, w), l, count));
+  });
+}
+
+rpd_status rpd_build_histogram(rpd_ctx* ctx, const float* d2, int h, int w, double bw,
+                               int64_t* counts, int64_t cap_n, int64_t* n, double* origin,
+                               int64_t* total) {
+  rpd_status st = RPD_OK;
+  const rpd_status g = guard(ctx, [&] {
+    check_dims(h, w);
+    const Hist hist = histogram(to_gray(d2, h, w), bw);
+    *n = hist.n;
+    *origin = hist.origin;
+    *total = hist.total;
+    if (hist.n > cap_n) {
+      st = RPD_ECAPACITY;
+      if (ctx) ctx->err = "build_histogram: counts buffer too small";
+      return;
+    }
+    if (counts) std::copy(hist.counts.begin(), hist.counts.end(), counts);
+  });
+  return g != RPD_OK ? g : st;
+}
+
+rpd_status rpd_find_road_threshold(rpd_ctx* ctx, const int64_t* counts, int64_t n, double bw,
+                                   double origin, int64_t total, double delta_pd, double tau,
+                                   rpd_threshold* out) {
+  return guard(ctx, [&] {
+    Hist hist;
+    hist.bw = bw;
+    hist.origin = origin;
+    hist.n = n;
+    hist.total = total;
+    hist.counts.assign(counts, counts + n * n);
+    *out = threshold(hist, delta_pd, tau);
+  });
+}
+
+rpd_status rpd_connected_components(rpd_ctx* ctx, const int32_t* mask, int h, int w, int conn,
+                                    int32_t* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    Labels m(h, w);
+    std::memcpy(m.a.data(), mask, sizeof(int32_t) * m.a.size());
+    put(out, ccl(m, conn));
+  });
+}
+
+rpd_status rpd_detect_potholes(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels,
+                               double spacing, int h, int w, const rpd_threshold* thr,
+                               int margin, int min_sp, int conn, int32_t* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    Labels l(h, w);
+    std::memcpy(l.a.data(), sp_labels, sizeof(int32_t) * l.a.size());
+    put(out, detect(to_gray(d3, h, w), l, spacing, *thr, margin, min_sp, conn));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,576 @@
+"""ctypes mirror of the C-ABI in include/rpd_b200.h.
+
+The functions follow the reference C++ API of `namespace rpd`
+(/root/reference/proj/include/rpd/*.hpp): same names, argument meaning,
+buffer layouts and error behaviour.  Exceptions map the ABI status codes back
+onto the reference's exception types:
+
+  RPD_EINVAL       -> InvalidArgument   (std::invalid_argument, a ValueError)
+  RPD_EDEGENERATE  -> DegenerateError   (std::runtime_error / DegenerateFitError)
+
+`Context` binds one shared library.  The product library is the sm_100a CUDA
+build (`paper_2012_10802_b200.load_library()`); the parity tests bind the same
+class to the CPU oracle (oracle/_build/librpd_oracle.so) as the checker.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+RPD_OK, RPD_EINVAL, RPD_EDEGENERATE, RPD_ECUDA, RPD_ENOMEM, RPD_ECAPACITY = range(6)
+STAGE_NAMES = ("sgm_bootstrap", "road_fit", "sgm_pt", "road_refit",
+               "disparity_transform", "slic", "detect")  # pipeline.cpp:64-104
+EIGHT_DIRECTIONS = ((1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, 1), (1, -1), (-1, -1))
+INVALID = -1.0  # kInvalidDisparity, types.hpp:21
+
+
+class RpdError(Exception):
+    pass
+
+
+class InvalidArgument(RpdError, ValueError):
+    """std::invalid_argument."""
+
+
+class DegenerateError(RpdError, RuntimeError):
+    """std::runtime_error on degenerate data (DegenerateFitError in the pipeline)."""
+
+
+class CudaError(RpdError, RuntimeError):
+    pass
+
+
+class CapacityError(RpdError):
+    pass
+
+
+# ------------------------------------------------------------------ structs --
+class RoadModel(C.Structure):
+    _fields_ = [("a0", C.c_double), ("a1", C.c_double), ("phi", C.c_double)]
+
+    def __repr__(self):
+        return f"RoadModel(a0={self.a0!r}, a1={self.a1!r}, phi={self.phi!r})"
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("delta_pt", C.c_double), ("delta_dt", C.c_double), ("delta_pd", C.c_double),
+        ("d_max", C.c_int32), ("d_max_pt", C.c_int32),
+        ("lambda1", C.c_double), ("lambda2", C.c_double),
+        ("census_window", C.c_int32), ("lr_threshold", C.c_double),
+        ("superpixels", C.c_int32), ("compactness", C.c_double),
+        ("slic_iterations", C.c_int32), ("hist_bin_width", C.c_double),
+        ("tau_diag", C.c_double), ("border_margin", C.c_int32),
+        ("min_superpixels", C.c_int32), ("connectivity", C.c_int32),
+        ("roll_bracket", C.c_double), ("roll_tol", C.c_double),
+        ("focal", C.c_double), ("baseline", C.c_double), ("cu", C.c_double),
+        ("cv", C.c_double), ("sgm_paths", C.c_int32),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+    def copy(self):
+        c = Config()
+        C.pointer(c)[0] = self
+        return c
+
+
+class Center(C.Structure):
+    _fields_ = [("cu", C.c_double), ("cv", C.c_double), ("value", C.c_double)]
+
+
+class LineFit(C.Structure):
+    _fields_ = [("model", RoadModel), ("e0min", C.c_double)]
+
+
+class RoadFit(C.Structure):
+    _fields_ = [("model", RoadModel), ("e0min", C.c_double), ("used", C.c_int64)]
+
+
+class RectRoi(C.Structure):
+    _fields_ = [("u0", C.c_int32), ("v0", C.c_int32), ("width", C.c_int32),
+                ("height", C.c_int32)]
+
+
+class Threshold(C.Structure):
+    _fields_ = [("t_r", C.c_double), ("t_s", C.c_double), ("mu1", C.c_double),
+                ("mu2", C.c_double), ("excluded_fraction", C.c_double),
+                ("degenerate", C.c_int32)]
+
+
+class DetectOut(C.Structure):
+    _fields_ = [
+        ("d0", C.POINTER(C.c_float)), ("d1", C.POINTER(C.c_float)),
+        ("d2", C.POINTER(C.c_float)), ("d3", C.POINTER(C.c_float)),
+        ("labels", C.POINTER(C.c_int32)), ("sp_labels", C.POINTER(C.c_int32)),
+        ("centers", C.POINTER(Center)), ("centers_cap", C.c_int32),
+        ("sp_count", C.c_int32), ("sp_spacing", C.c_double),
+        ("coarse_fit", RoadFit), ("fit", RoadFit), ("threshold", Threshold),
+        ("clamped", C.c_int64), ("n_potholes", C.c_int32),
+        ("stage_ms", C.c_double * 7), ("total_ms", C.c_double),
+    ]
+
+
+@dataclass
+class DetectResult:
+    """DetectResult, pipeline.hpp:26-38."""
+    d0: Optional[np.ndarray]
+    d1: Optional[np.ndarray]
+    d2: Optional[np.ndarray]
+    d3: Optional[np.ndarray]
+    labels: Optional[np.ndarray]
+    sp_labels: Optional[np.ndarray]
+    centers: Optional[np.ndarray]
+    sp_count: int
+    sp_spacing: float
+    coarse_fit: RoadFit
+    fit: RoadFit
+    threshold: Threshold
+    clamped: int
+    n_potholes: int
+    stage_ms: dict = field(default_factory=dict)
+    total_ms: float = 0.0
+
+
+@dataclass
+class Histogram2D:
+    """Histogram2D, segmentation.hpp:34-41."""
+    bin_width: float
+    origin: float
+    counts: np.ndarray
+    total: int
+
+    def center(self, b):
+        return self.origin + (b + 0.5) * self.bin_width
+
+
+# ------------------------------------------------------------------ helpers --
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _fp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _ip(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+_SIGS = {
+    "rpd_abi_version": (C.c_int, []),
+    "rpd_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "rpd_ctx_destroy": (None, [_vp]),
+    "rpd_last_error": (C.c_char_p, [_vp]),
+    "rpd_ctx_stream": (_vp, [_vp]),
+    "rpd_config_default": (None, [C.POINTER(Config)]),
+    "rpd_config_validate": (C.c_int, [_vp, C.POINTER(Config)]),
+    "rpd_config_set": (C.c_int, [_vp, C.POINTER(Config), C.c_char_p, C.c_char_p]),
+    "rpd_detect": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config),
+                             C.POINTER(DetectOut)]),
+    "rpd_detect_u8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config),
+                                C.POINTER(DetectOut)]),
+    "rpd_compute_row_shifts": (C.c_int, [_vp, C.POINTER(RoadModel), C.c_int, C.c_int,
+                                         C.c_double, _vp]),
+    "rpd_warp_right_image": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp]),
+    "rpd_restore_disparity": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
+    "rpd_census_cost_volume": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         _vp, _vp]),
+    "rpd_aggregate_costs": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int,
+                                      C.c_float, C.c_float, _vp]),
+    "rpd_swap_reference": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
+    "rpd_select_disparity": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
+    "rpd_consistency_filter": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_double]),
+    "rpd_match_pair": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
+                                 C.POINTER(Config), C.c_int, _vp, _vp, _vp]),
+    "rpd_sample_observations": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.POINTER(RectRoi),
+                                          C.c_int64, _vp, _vp, _vp, C.POINTER(C.c_int64)]),
+    "rpd_fit_line": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, C.c_double,
+                               C.POINTER(LineFit)]),
+    "rpd_estimate_roll": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, C.c_double, C.c_double,
+                                    C.c_double, C.POINTER(RoadModel)]),
+    "rpd_fit_road": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, C.c_double, C.c_double,
+                               C.POINTER(RoadFit)]),
+    "rpd_transform_disparity": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
+                                          C.c_double, _vp, C.POINTER(C.c_int64)]),
+    "rpd_slic": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _vp,
+                           _vp, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+    "rpd_pool_superpixels": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
+    "rpd_build_histogram": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, _vp,
+                                      C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64)]),
+    "rpd_find_road_threshold": (C.c_int, [_vp, _vp, C.c_int64, C.c_double, C.c_double,
+                                          C.c_int64, C.c_double, C.c_double,
+                                          C.POINTER(Threshold)]),
+    "rpd_connected_components": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
+    "rpd_detect_potholes": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, C.c_int,
+                                      C.POINTER(Threshold), C.c_int, C.c_int, C.c_int, _vp]),
+}
+
+ABI_SYMBOLS = tuple(_SIGS)
+
+
+class Library:
+    """One loaded shared library exporting the rpd_* C-ABI."""
+
+    def __init__(self, path: str):
+        self.path = str(path)
+        self.dll = C.CDLL(self.path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(self.dll, name)
+            fn.restype = res
+            fn.argtypes = args
+        if self.dll.rpd_abi_version() != 1:
+            raise RpdError(f"{path}: unexpected ABI version")
+
+    def default_config(self, **overrides) -> Config:
+        cfg = Config()
+        self.dll.rpd_config_default(C.byref(cfg))
+        for k, v in overrides.items():
+            if not hasattr(cfg, k):
+                raise InvalidArgument(f"config: unknown key '{k}'")
+            setattr(cfg, k, v)
+        return cfg
+
+    def context(self, device: int = 0, max_h: int = 0, max_w: int = 0, max_levels: int = 0):
+        return Context(self, device, max_h, max_w, max_levels)
+
+
+class Context:
+    """rpd_ctx: per (host thread, device) state.  Methods mirror namespace rpd."""
+
+    def __init__(self, lib: Library, device=0, max_h=0, max_w=0, max_levels=0):
+        self.lib = lib
+        self.dll = lib.dll
+        h = _vp()
+        self._check(self.dll.rpd_ctx_create(device, max_h, max_w, max_levels, C.byref(h)),
+                    ctx=None)
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.dll.rpd_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def stream(self):
+        return self.dll.rpd_ctx_stream(self.handle)
+
+    def _check(self, st, ctx="self"):
+        if st == RPD_OK:
+            return
+        msg = ""
+        if ctx is not None and getattr(self, "handle", None):
+            raw = self.dll.rpd_last_error(self.handle)
+            msg = raw.decode() if raw else ""
+        exc = {RPD_EINVAL: InvalidArgument, RPD_EDEGENERATE: DegenerateError,
+               RPD_ECUDA: CudaError, RPD_ECAPACITY: CapacityError}.get(st, RpdError)
+        raise exc(msg or f"rpd status {st}")
+
+    # -------------------------------------------------------------- config --
+    def validate(self, cfg: Config):
+        self._check(self.dll.rpd_config_validate(self.handle, C.byref(cfg)))
+
+    def config_set(self, cfg: Config, key: str, value):
+        self._check(self.dll.rpd_config_set(self.handle, C.byref(cfg), key.encode(),
+                                            str(value).encode()))
+
+    # ------------------------------------------------------------ pipeline --
+    def detect(self, left, right, cfg: Config, want=("d0", "d1", "d2", "d3", "labels",
+                                                      "sp_labels", "centers")) -> DetectResult:
+        """detect_potholes_pipeline (pipeline.hpp:43-44).  uint8 inputs use the
+        exact uint8 entry point, anything else is passed as float32."""
+        u8 = isinstance(left, np.ndarray) and left.dtype == np.uint8
+        if u8:
+            left = np.ascontiguousarray(left)
+            right = np.ascontiguousarray(right)
+        else:
+            left = _f32(left)
+            right = _f32(right)
+        if left.shape != right.shape or left.ndim != 2:
+            raise InvalidArgument("match_pair: dimension mismatch")
+        h, w = left.shape
+        bufs = {k: (np.empty((h, w), np.float32) if k in want else None)
+                for k in ("d0", "d1", "d2", "d3")}
+        bufs["labels"] = np.empty((h, w), np.int32) if "labels" in want else None
+        bufs["sp_labels"] = np.empty((h, w), np.int32) if "sp_labels" in want else None
+        cap = h * w if "centers" in want else 0
+        centers = (Center * max(cap, 1))() if cap else None
+        out = DetectOut()
+        for k in ("d0", "d1", "d2", "d3"):
+            setattr(out, k, _fp(bufs[k]))
+        out.labels = _ip(bufs["labels"])
+        out.sp_labels = _ip(bufs["sp_labels"])
+        out.centers = C.cast(centers, C.POINTER(Center)) if centers is not None else None
+        out.centers_cap = cap
+        fn = self.dll.rpd_detect_u8 if u8 else self.dll.rpd_detect
+        self._check(fn(self.handle, _ptr(left), _ptr(right), h, w, C.byref(cfg), C.byref(out)))
+        cent = None
+        if centers is not None:
+            cent = np.array([(c.cu, c.cv, c.value) for c in centers[:out.sp_count]],
+                            dtype=np.float64).reshape(-1, 3)
+        return DetectResult(
+            d0=bufs["d0"], d1=bufs["d1"], d2=bufs["d2"], d3=bufs["d3"],
+            labels=bufs["labels"], sp_labels=bufs["sp_labels"], centers=cent,
+            sp_count=out.sp_count, sp_spacing=out.sp_spacing, coarse_fit=out.coarse_fit,
+            fit=out.fit, threshold=out.threshold, clamped=out.clamped,
+            n_potholes=out.n_potholes,
+            stage_ms={n: out.stage_ms[i] for i, n in enumerate(STAGE_NAMES)},
+            total_ms=out.total_ms)
+
+    # --------------------------------------------------------- perspective --
+    def compute_row_shifts(self, model: RoadModel, width: int, height: int, delta_pt: float):
+        out = np.empty(height, np.float64)
+        self._check(self.dll.rpd_compute_row_shifts(self.handle, C.byref(model), width, height,
+                                                    delta_pt, _ptr(out)))
+        return out
+
+    def warp_right_image(self, right, shifts):
+        right = _f32(right)
+        shifts = _f64(shifts)
+        h, w = right.shape
+        if shifts.shape[0] != h:
+            raise InvalidArgument("warp_right_image: table length != image height")
+        img = np.empty((h, w), np.float32)
+        iv = np.empty((h, w), np.uint8)
+        self._check(self.dll.rpd_warp_right_image(self.handle, _ptr(right), h, w, _ptr(shifts),
+                                                  _ptr(img), _ptr(iv)))
+        return img, iv
+
+    def restore_disparity(self, d0, shifts):
+        d0 = _f32(d0)
+        shifts = _f64(shifts)
+        h, w = d0.shape
+        if shifts.shape[0] != h:
+            raise InvalidArgument("restore_disparity: table length != map height")
+        d1 = np.empty((h, w), np.float32)
+        self._check(self.dll.rpd_restore_disparity(self.handle, _ptr(d0), h, w, _ptr(shifts),
+                                                   _ptr(d1)))
+        return d1
+
+    # ----------------------------------------------------------------- SGM --
+    def census_cost_volume(self, left, right_warped, d_max: int, window: int, in_view=None):
+        left = _f32(left)
+        right_warped = _f32(right_warped)
+        if left.shape != right_warped.shape:
+            raise InvalidArgument("census_cost_volume: dimension mismatch")
+        h, w = left.shape
+        iv = None if in_view is None else np.ascontiguousarray(in_view, dtype=np.uint8)
+        out = np.empty((h, w, max(d_max, 0) + 1), np.float32)
+        self._check(self.dll.rpd_census_cost_volume(self.handle, _ptr(left), _ptr(right_warped),
+                                                    h, w, d_max, window, _ptr(iv), _ptr(out)))
+        return out
+
+    def aggregate_costs(self, costs, lambda1=8.0, lambda2=32.0,
+                        directions: Sequence = EIGHT_DIRECTIONS):
+        costs = _f32(costs)
+        h, w, n = costs.shape
+        dirs = np.ascontiguousarray(np.array(directions, dtype=np.int32).reshape(-1, 2))
+        out = np.empty_like(costs)
+        self._check(self.dll.rpd_aggregate_costs(self.handle, _ptr(costs), h, w, n - 1,
+                                                 _ptr(dirs), dirs.shape[0], lambda1, lambda2,
+                                                 _ptr(out)))
+        return out
+
+    def swap_reference(self, costs):
+        costs = _f32(costs)
+        h, w, n = costs.shape
+        out = np.empty_like(costs)
+        self._check(self.dll.rpd_swap_reference(self.handle, _ptr(costs), h, w, n - 1,
+                                                _ptr(out)))
+        return out
+
+    def select_disparity(self, aggregated):
+        agg = _f32(aggregated)
+        h, w, n = agg.shape
+        out = np.empty((h, w), np.float32)
+        self._check(self.dll.rpd_select_disparity(self.handle, _ptr(agg), h, w, n - 1,
+                                                  _ptr(out)))
+        return out
+
+    def consistency_filter(self, left_disp, right_disp, threshold: float):
+        """Returns the filtered copy (the reference mutates in place)."""
+        left = _f32(left_disp).copy()
+        right = _f32(right_disp)
+        h, w = left.shape
+        self._check(self.dll.rpd_consistency_filter(self.handle, _ptr(left), _ptr(right), h, w,
+                                                    threshold))
+        return left
+
+    def match_pair(self, left, right, model: RoadModel, cfg: Config, d_max: int):
+        left = _f32(left)
+        right = _f32(right)
+        if left.shape != right.shape:
+            raise InvalidArgument("match_pair: dimension mismatch")
+        h, w = left.shape
+        d0 = np.empty((h, w), np.float32)
+        d1 = np.empty((h, w), np.float32)
+        sh = np.empty(h, np.float64)
+        self._check(self.dll.rpd_match_pair(self.handle, _ptr(left), _ptr(right), h, w,
+                                            C.byref(model), C.byref(cfg), d_max, _ptr(d0),
+                                            _ptr(d1), _ptr(sh)))
+        return d0, d1, sh
+
+    # ------------------------------------------------------- road geometry --
+    def sample_observations(self, d1, roi: Optional[RectRoi] = None, cap: int = 100000):
+        d1 = _f32(d1)
+        h, w = d1.shape
+        n = min(h * w, cap)
+        d = np.empty(max(n, 1), np.float64)
+        u = np.empty_like(d)
+        v = np.empty_like(d)
+        k = C.c_int64(0)
+        self._check(self.dll.rpd_sample_observations(
+            self.handle, _ptr(d1), h, w, C.byref(roi) if roi is not None else None, cap,
+            _ptr(d), _ptr(u), _ptr(v), C.byref(k)))
+        k = k.value
+        return d[:k].copy(), u[:k].copy(), v[:k].copy()
+
+    def fit_line(self, d, u, v, phi: float) -> LineFit:
+        d, u, v = _f64(d), _f64(u), _f64(v)
+        out = LineFit()
+        self._check(self.dll.rpd_fit_line(self.handle, _ptr(d), _ptr(u), _ptr(v), d.shape[0],
+                                          phi, C.byref(out)))
+        return out
+
+    def estimate_roll(self, d, u, v, lo: float, hi: float, tol: float) -> RoadModel:
+        d, u, v = _f64(d), _f64(u), _f64(v)
+        out = RoadModel()
+        self._check(self.dll.rpd_estimate_roll(self.handle, _ptr(d), _ptr(u), _ptr(v),
+                                               d.shape[0], lo, hi, tol, C.byref(out)))
+        return out
+
+    def fit_road(self, d, u, v, bracket: float, tol: float) -> RoadFit:
+        d, u, v = _f64(d), _f64(u), _f64(v)
+        out = RoadFit()
+        self._check(self.dll.rpd_fit_road(self.handle, _ptr(d), _ptr(u), _ptr(v), d.shape[0],
+                                          bracket, tol, C.byref(out)))
+        return out
+
+    def transform_disparity(self, d1, model: RoadModel, delta_dt: float):
+        d1 = _f32(d1)
+        h, w = d1.shape
+        d2 = np.empty_like(d1)
+        clamped = C.c_int64(0)
+        self._check(self.dll.rpd_transform_disparity(self.handle, _ptr(d1), h, w,
+                                                     C.byref(model), delta_dt, _ptr(d2),
+                                                     C.byref(clamped)))
+        return d2, clamped.value
+
+    # -------------------------------------------------------- segmentation --
+    def slic(self, d2, p: int, compactness: float, iterations: int):
+        d2 = _f32(d2)
+        h, w = d2.shape
+        labels = np.empty((h, w), np.int32)
+        cap = max(1, min(h * w, 4 * max(p, 1) + 64))
+        centers = (Center * cap)()
+        count = C.c_int32(0)
+        spacing = C.c_double(0)
+        self._check(self.dll.rpd_slic(self.handle, _ptr(d2), h, w, p, compactness, iterations,
+                                      _ptr(labels), centers, cap, C.byref(count),
+                                      C.byref(spacing)))
+        cent = np.array([(c.cu, c.cv, c.value) for c in centers[:min(count.value, cap)]],
+                        dtype=np.float64).reshape(-1, 3)
+        return labels, cent, count.value, spacing.value
+
+    def pool_superpixels(self, d2, sp_labels, sp_count: int):
+        d2 = _f32(d2)
+        lab = _i32(sp_labels)
+        h, w = d2.shape
+        if lab.shape != d2.shape:
+            raise InvalidArgument("pool_superpixels: dimension mismatch")
+        d3 = np.empty_like(d2)
+        self._check(self.dll.rpd_pool_superpixels(self.handle, _ptr(d2), _ptr(lab), sp_count,
+                                                  h, w, _ptr(d3)))
+        return d3
+
+    def build_histogram(self, d2, bin_width: float) -> Histogram2D:
+        d2 = _f32(d2)
+        h, w = d2.shape
+        n = C.c_int64(0)
+        origin = C.c_double(0)
+        total = C.c_int64(0)
+        st = self.dll.rpd_build_histogram(self.handle, _ptr(d2), h, w, bin_width, None, 0,
+                                          C.byref(n), C.byref(origin), C.byref(total))
+        if st not in (RPD_OK, RPD_ECAPACITY):
+            self._check(st)
+        nn = n.value
+        counts = np.zeros((nn, nn), np.int64)
+        if nn > 0:
+            self._check(self.dll.rpd_build_histogram(self.handle, _ptr(d2), h, w, bin_width,
+                                                     _ptr(counts), nn, C.byref(n),
+                                                     C.byref(origin), C.byref(total)))
+        return Histogram2D(bin_width, origin.value, counts, total.value)
+
+    def find_road_threshold(self, hist: Histogram2D, delta_pd: float, tau: float = 3.0):
+        counts = np.ascontiguousarray(hist.counts, dtype=np.int64)
+        n = counts.shape[0] if counts.ndim == 2 else 0
+        out = Threshold()
+        self._check(self.dll.rpd_find_road_threshold(self.handle, _ptr(counts), n,
+                                                     hist.bin_width, hist.origin, hist.total,
+                                                     delta_pd, tau, C.byref(out)))
+        return out
+
+    def connected_components(self, mask, connectivity: int = 8):
+        mask = _i32(mask)
+        h, w = mask.shape
+        out = np.empty_like(mask)
+        self._check(self.dll.rpd_connected_components(self.handle, _ptr(mask), h, w,
+                                                      connectivity, _ptr(out)))
+        return out
+
+    def detect_potholes(self, d3, sp_labels, sp_spacing: float, thr: Threshold,
+                        border_margin: int, min_superpixels: int, connectivity: int = 8):
+        d3 = _f32(d3)
+        lab = _i32(sp_labels)
+        h, w = d3.shape
+        out = np.empty((h, w), np.int32)
+        self._check(self.dll.rpd_detect_potholes(self.handle, _ptr(d3), _ptr(lab), sp_spacing,
+                                                 h, w, C.byref(thr), border_margin,
+                                                 min_superpixels, connectivity, _ptr(out)))
+        return out
+
+
+def model(a0=0.0, a1=0.0, phi=0.0) -> RoadModel:
+    return RoadModel(a0, a1, phi)
+
+
+def threshold(t_r=0.0, t_s=0.0, mu1=0.0, mu2=0.0, excluded_fraction=0.0, degenerate=0):
+    return Threshold(t_r, t_s, mu1, mu2, excluded_fraction, degenerate)

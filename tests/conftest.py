@@ -1,0 +1,74 @@
+"""Shared fixtures.
+
+`ctx` is parametrized over two implementations of the same C-ABI:
+  * "oracle" — oracle/_build/librpd_oracle.so, the CPU restatement (runs here);
+  * "cuda"   — paper_2012_10802_b200/_lib/librpd_b200.so on cuda:0 (marked gpu).
+Known-answer tests ported from the reference suites therefore pin both the
+oracle and the product.  Parity tests (test_parity_*.py) take both contexts and
+compare them on the same seeded inputs.
+"""
+from __future__ import annotations
+
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+ORACLE_LIB = ROOT / "oracle" / "_build" / "librpd_oracle.so"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+def _ensure_oracle():
+    if not ORACLE_LIB.exists():
+        subprocess.run(["make", "-C", str(ROOT / "oracle")], check=True,
+                       stdout=subprocess.DEVNULL)
+    return ORACLE_LIB
+
+
+@pytest.fixture(scope="session")
+def oracle_lib():
+    from paper_2012_10802_b200.api import Library
+    return Library(str(_ensure_oracle()))
+
+
+@pytest.fixture(scope="session")
+def oracle(oracle_lib):
+    return oracle_lib.context()
+
+
+@pytest.fixture(scope="session")
+def cuda_lib():
+    import paper_2012_10802_b200 as pkg
+    return pkg.load_library()  # raises loudly if the CUDA library is missing
+
+
+@pytest.fixture(scope="session")
+def gpu(cuda_lib):
+    return cuda_lib.context(0)
+
+
+@pytest.fixture(params=["oracle", pytest.param("cuda", marks=pytest.mark.gpu)])
+def ctx(request):
+    if request.param == "oracle":
+        return request.getfixturevalue("oracle")
+    return request.getfixturevalue("gpu")
+
+
+@pytest.fixture
+def lib(ctx):
+    return ctx.lib
+
+
+def mt_textured(w, h, seed):
+    """Seeded uniform [0,255] integer texture (stand-in for test_sgm.cpp:68-75)."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, 256, size=(h, w)).astype(np.float32)

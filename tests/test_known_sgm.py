@@ -1,0 +1,176 @@
+"""Known answers of the reference SGM suite, run against both implementations.
+
+Ports /root/reference/proj/tests/test_sgm.cpp and acceptance.cpp check 1
+(:47-102).  Random inputs are our own seeded numpy draws (the reference's
+std::mt19937 distributions are implementation-defined); every fixed value
+(24, 1, 3.0, 3.1667, ...) is the reference's.
+"""
+from __future__ import annotations
+
+import functools
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2012_10802_b200.api import EIGHT_DIRECTIONS, InvalidArgument, model
+from conftest import mt_textured
+
+
+def dp_oracle_aggregate(raw, l1, l2, directions):
+    """Memoised top-down DP, independent of the scan-order implementation
+    (test_sgm.cpp:15-58).  Accumulates each direction in float32, like the
+    reference (`total.at(...) += static_cast<float>(...)`)."""
+    h, w, n = raw.shape
+    total = np.zeros_like(raw, dtype=np.float32)
+    sys.setrecursionlimit(100000)
+    for du, dv in directions:
+        @functools.lru_cache(maxsize=None)
+        def agg(v, u, d):
+            pv, pu = v - dv, u - du
+            if pv < 0 or pv >= h or pu < 0 or pu >= w:
+                return float(raw[v, u, d])
+            prev_min = min(agg(pv, pu, k) for k in range(n))
+            best = agg(pv, pu, d)
+            if d > 0:
+                best = min(best, agg(pv, pu, d - 1) + l1)
+            if d + 1 < n:
+                best = min(best, agg(pv, pu, d + 1) + l1)
+            best = min(best, prev_min + l2)
+            return float(raw[v, u, d]) + best - prev_min
+        for v in range(h):
+            for u in range(w):
+                for d in range(n):
+                    total[v, u, d] = np.float32(total[v, u, d] + np.float32(agg(v, u, d)))
+    return total
+
+
+def random_volume(w, h, d_max, seed, cost_max=40):
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, cost_max + 1, size=(h, w, d_max + 1)).astype(np.float32)
+
+
+def argmin_d(vol):
+    return np.argmin(vol, axis=2)  # first minimum, like the strict `<` scan
+
+
+def test_census_constant_images_zero_in_range(ctx):
+    img = np.full((8, 8), 100.0, np.float32)
+    vol = ctx.census_cost_volume(img, img, 3, 5)
+    for d in range(4):
+        assert np.all(vol[:, d:, d] == 0.0) if d else np.all(vol[:, :, 0] == 0.0)
+    assert np.all(vol[:, 3:, :] == 0.0)
+    assert vol[0, 0, 1] == 24.0  # out-of-range sample carries the maximum cost
+
+
+def test_census_integer_shift_recovered(ctx):
+    right = mt_textured(32, 16, 3)
+    left = np.empty_like(right)
+    for u in range(32):
+        left[:, u] = right[:, max(0, u - 2)]
+    vol = ctx.census_cost_volume(left, right, 6, 5)
+    am = argmin_d(vol)
+    assert np.all(am[2:14, 6:30] == 2)
+
+
+def test_census_one_flipped_bit_costs_one(ctx):
+    left = np.full((9, 9), 10.0, np.float32)
+    right = left.copy()
+    right[4, 3] = 5.0
+    vol = ctx.census_cost_volume(left, right, 0, 5)
+    assert vol[4, 4, 0] == 1.0
+
+
+def test_aggregation_single_direction_large_penalties(ctx):
+    row = random_volume(12, 1, 5, 11)
+    agg = ctx.aggregate_costs(row, 1e6, 1e6, [(1, 0)])
+    exp = dp_oracle_aggregate(row, np.float32(1e6), np.float32(1e6), [(1, 0)])
+    assert np.array_equal(agg, exp)
+
+
+def test_aggregation_4x4x4_eight_directions(ctx):
+    vol = random_volume(4, 4, 3, 21)
+    agg = ctx.aggregate_costs(vol, 7.0, 20.0)
+    exp = dp_oracle_aggregate(vol, 7.0, 20.0, EIGHT_DIRECTIONS)
+    assert np.array_equal(agg, exp)
+
+
+def test_acceptance_check1_random_volumes_equal_dp_oracle(ctx):
+    """acceptance.cpp:78-102: 50 random volumes up to 16x16x8, costs 0..60,
+    lambda1=7, lambda2=21, exact equality."""
+    rng = np.random.default_rng(1001)
+    for _ in range(50):
+        w, h, dm = int(rng.integers(2, 17)), int(rng.integers(2, 17)), int(rng.integers(1, 9))
+        vol = rng.integers(0, 61, size=(h, w, dm + 1)).astype(np.float32)
+        agg = ctx.aggregate_costs(vol, 7.0, 21.0)
+        exp = dp_oracle_aggregate(vol, 7.0, 21.0, EIGHT_DIRECTIONS)
+        assert np.array_equal(agg, exp)
+
+
+def test_zero_penalties_preserve_argmin(ctx):
+    vol = random_volume(10, 6, 7, 31)
+    idx = np.arange(vol.size, dtype=np.int64).reshape(vol.shape)
+    vol = (vol * 64.0 + (idx % 61)).astype(np.float32)
+    agg = ctx.aggregate_costs(vol, 0.0, 0.0)
+    assert np.array_equal(argmin_d(agg), argmin_d(vol))
+
+
+def test_constant_offset_preserves_argmin(ctx):
+    vol = random_volume(8, 5, 6, 41)
+    idx = np.arange(vol.size, dtype=np.int64).reshape(vol.shape)
+    vol = (vol * 64.0 + (idx % 53)).astype(np.float32)
+    a = ctx.aggregate_costs(vol)
+    b = ctx.aggregate_costs(vol + np.float32(9.0))
+    assert np.array_equal(argmin_d(a), argmin_d(b))
+
+
+def _parabola_volume(c234):
+    vol = np.zeros((1, 1, 7), np.float32)
+    vol[0, 0, :] = [40, 30, 0, 0, 0, 31, 41]
+    vol[0, 0, 2:5] = c234
+    return vol
+
+
+def test_parabola_refinement(ctx):
+    assert ctx.select_disparity(_parabola_volume([4, 2, 4]))[0, 0] == pytest.approx(3.0)
+    assert ctx.select_disparity(_parabola_volume([4, 2, 3]))[0, 0] == pytest.approx(3.1667,
+                                                                                  rel=1e-4)
+    edge = np.array([[[1, 5, 6, 7]]], np.float32)
+    assert ctx.select_disparity(edge)[0, 0] == 0.0  # boundary: no refinement
+
+
+def test_refinement_within_half_pixel(ctx):
+    for seed in range(20):
+        vol = random_volume(6, 4, 8, 100 + seed, 1000)
+        disp = ctx.select_disparity(vol)
+        am = argmin_d(vol)
+        ok = disp != -1.0
+        assert np.all(np.abs(disp[ok] - np.round(disp[ok])) <= 0.5)
+        assert np.all(np.abs(disp[ok] - am[ok]) <= 0.5)
+
+
+def test_match_pair_self_match_zero_disparity(ctx, lib):
+    img = mt_textured(64, 32, 77)
+    cfg = lib.default_config(delta_pt=0.0)
+    d0, _, _ = ctx.match_pair(img, img, model(), cfg, 8)
+    valid = d0 != -1.0
+    assert valid.sum() > 32 * 64 // 2
+    assert np.all(np.abs(d0[valid]) <= 0.5)
+
+
+def test_match_pair_textureless_mostly_invalid(ctx, lib):
+    flat = np.full((48, 64), 128.0, np.float32)
+    cfg = lib.default_config(delta_pt=0.0)
+    d0, _, _ = ctx.match_pair(flat, flat, model(), cfg, 8)
+    assert (d0 == -1.0).sum() >= int(0.9 * 48 * 64)
+
+
+def test_dimension_and_range_errors(ctx):
+    a = np.zeros((4, 8), np.float32)
+    b = np.zeros((4, 9), np.float32)
+    with pytest.raises(InvalidArgument):
+        ctx.census_cost_volume(a, b, 2, 5)
+    with pytest.raises(InvalidArgument):
+        ctx.census_cost_volume(a, a, 8, 5)
+    with pytest.raises(InvalidArgument):
+        ctx.census_cost_volume(a, a, 2, 4)
