@@ -1,0 +1,247 @@
+// abi_core.cu — context lifecycle, config and the SGM / perspective entry
+// points of the C-ABI (include/rpd_b200.h).  Host buffers are copied to
+// context-owned device workspaces; all device work is ordered on ctx->stream.
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "abi_util.hpp"
+#include "sgm.cuh"
+
+namespace rpdg {
+
+void reset_status(rpd_ctx* ctx) {
+  RPD_CK(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
+}
+
+static const char* status_message(int where) {
+  switch (where) {
+    case kWhereSampleBoot: return "road fit failed: sample_observations: fewer than 3 valid pixels";
+    case kWhereFitBoot:
+      return "road fit failed: fit_line: degenerate observations (singular normal matrix)";
+    case kWhereSamplePt:
+      return "road refit failed: sample_observations: fewer than 3 valid pixels";
+    case kWhereFitPt:
+      return "road refit failed: fit_line: degenerate observations (singular normal matrix)";
+    case kWhereThresholdEmpty: return "find_road_threshold: all vectors excluded";
+    case kWhereHistTooLarge: return "build_histogram: histogram too large for the device band";
+    case kWhereSample: return "sample_observations: fewer than 3 valid pixels";
+    case kWhereFit: return "fit_line: degenerate observations (singular normal matrix)";
+    default: return "device failure";
+  }
+}
+
+void sync_and_check(rpd_ctx* ctx) {
+  DevStatus h{};
+  RPD_CK(cudaMemcpyAsync(&h, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  RPD_CK(cudaStreamSynchronize(ctx->stream));
+  if (h.code == RPD_EDEGENERATE) throw Degenerate(status_message(h.where));
+  if (h.code == RPD_EINVAL) throw InvalidArg(status_message(h.where));
+  if (h.code == RPD_ENOMEM) throw CudaFail(status_message(h.where));
+  if (h.code != 0) throw CudaFail(status_message(h.where));
+}
+
+}  // namespace rpdg
+
+using namespace rpdg;
+
+extern "C" {
+
+int rpd_abi_version(void) { return RPD_ABI_VERSION; }
+
+rpd_status rpd_ctx_create(int device, int, int, int, rpd_ctx** out) {
+  if (!out) return RPD_EINVAL;
+  *out = nullptr;
+  rpd_ctx* ctx = new (std::nothrow) rpd_ctx();
+  if (!ctx) return RPD_ENOMEM;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->status, sizeof(DevStatus));
+  if (e == cudaSuccess) e = cudaMemset(ctx->status, 0, sizeof(DevStatus));
+  for (int i = 0; e == cudaSuccess && i <= RPD_NUM_STAGES; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount,
+                                                   device);
+  int major = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    rpd_ctx_destroy(ctx);
+    return RPD_ECUDA;
+  }
+  if (major < 10) {  // built for sm_100a only
+    rpd_ctx_destroy(ctx);
+    return RPD_ECUDA;
+  }
+  *out = ctx;
+  return RPD_OK;
+}
+
+void rpd_ctx_destroy(rpd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->ws.release();
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->status) cudaFree(ctx->status);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* rpd_last_error(const rpd_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+void* rpd_ctx_stream(rpd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+void rpd_config_default(rpd_config* cfg) {
+  if (cfg) config_default(cfg);
+}
+
+rpd_status rpd_config_validate(rpd_ctx* ctx, const rpd_config* cfg) {
+  return guard(ctx, [&] { config_validate(*cfg); });
+}
+
+rpd_status rpd_config_set(rpd_ctx* ctx, rpd_config* cfg, const char* key, const char* value) {
+  return guard(ctx, [&] { config_set(cfg, key, value); });
+}
+
+// ------------------------------------------------------------ perspective --
+rpd_status rpd_compute_row_shifts(rpd_ctx* ctx, const rpd_road_model* model, int w, int h,
+                                  double delta_pt, double* shifts) {
+  return guard(ctx, [&] {
+    if (w < 2) throw InvalidArg("compute_row_shifts: width must be >= 2");
+    if (h <= 0) return;
+    DevModel* m = upload_model(ctx, *model);
+    double* s = ctx->ws.get<double>("abi_shifts", h);
+    launch_row_shifts(m, h, w, delta_pt, s, ctx->stream);
+    download(ctx, shifts, s, sizeof(double) * h);
+  });
+}
+
+rpd_status rpd_warp_right_image(rpd_ctx* ctx, const float* right, int h, int w,
+                                const double* shifts, float* image, uint8_t* in_view) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    const size_t n = size_t(h) * w;
+    const float* r = upload(ctx, "abi_in0", right, n);
+    const double* s = upload(ctx, "abi_shifts", shifts, size_t(h));
+    float* o = ctx->ws.get<float>("abi_out0", n);
+    uint8_t* iv = ctx->ws.get<uint8_t>("abi_out1", n);
+    launch_warp_right(r, s, h, w, o, iv, ctx->stream);
+    if (image) download(ctx, image, o, sizeof(float) * n);
+    if (in_view) download(ctx, in_view, iv, n);
+  });
+}
+
+rpd_status rpd_restore_disparity(rpd_ctx* ctx, const float* d0, int h, int w,
+                                 const double* shifts, float* d1) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    const size_t n = size_t(h) * w;
+    const float* a = upload(ctx, "abi_in0", d0, n);
+    const double* s = upload(ctx, "abi_shifts", shifts, size_t(h));
+    float* o = ctx->ws.get<float>("abi_out0", n);
+    launch_restore(a, s, h, w, o, ctx->stream);
+    download(ctx, d1, o, sizeof(float) * n);
+  });
+}
+
+// -------------------------------------------------------------------- SGM --
+rpd_status rpd_census_cost_volume(rpd_ctx* ctx, const float* left, const float* right, int h,
+                                  int w, int d_max, int window, const uint8_t* in_view,
+                                  float* costs) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (window % 2 == 0) throw InvalidArg("census_cost_volume: window must be odd");
+    if (window < 3 || window > 7) throw InvalidArg("census_cost_volume: window must be 3, 5 or 7");
+    if (d_max >= w) throw InvalidArg("census_cost_volume: d_max >= width");
+    if (d_max < 0) throw InvalidArg("census_cost_volume: d_max must be >= 0");
+    const size_t n = size_t(h) * w;
+    const float* l = upload(ctx, "abi_in0", left, n);
+    const float* r = upload(ctx, "abi_in1", right, n);
+    const uint8_t* iv = in_view ? upload(ctx, "abi_in2", in_view, n) : nullptr;
+    uint64_t* cl = ctx->ws.get<uint64_t>("abi_cl", n);
+    uint64_t* cr = ctx->ws.get<uint64_t>("abi_cr", n);
+    launch_census(l, h, w, window, cl, ctx->stream);
+    launch_census(r, h, w, window, cr, ctx->stream);
+    const size_t cells = n * size_t(d_max + 1);
+    float* c = ctx->ws.get<float>("abi_vol0", cells);
+    launch_cost_f32(cl, cr, iv, h, w, d_max + 1, window, c, ctx->stream);
+    download(ctx, costs, c, sizeof(float) * cells);
+  });
+}
+
+rpd_status rpd_aggregate_costs(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
+                               const int32_t* dirs, int ndirs, float l1, float l2, float* agg) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (d_max < 0 || ndirs < 0) throw InvalidArg("aggregate_costs: bad dimensions");
+    const size_t cells = size_t(h) * w * size_t(d_max + 1);
+    const float* c = upload(ctx, "abi_vol0", costs, cells);
+    float* o = ctx->ws.get<float>("abi_vol1", cells);
+    aggregate_f32(ctx, c, h, w, d_max + 1, dirs, ndirs, l1, l2, o);
+    download(ctx, agg, o, sizeof(float) * cells);
+  });
+}
+
+rpd_status rpd_swap_reference(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
+                              float* right_costs) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (d_max < 0) throw InvalidArg("swap_reference: bad dimensions");
+    const size_t cells = size_t(h) * w * size_t(d_max + 1);
+    const float* c = upload(ctx, "abi_vol0", costs, cells);
+    float* o = ctx->ws.get<float>("abi_vol1", cells);
+    swap_reference_f32(ctx, c, h, w, d_max + 1, o);
+    download(ctx, right_costs, o, sizeof(float) * cells);
+  });
+}
+
+rpd_status rpd_select_disparity(rpd_ctx* ctx, const float* agg, int h, int w, int d_max,
+                                float* disp) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (d_max < 0) throw InvalidArg("select_disparity: bad dimensions");
+    const size_t n = size_t(h) * w;
+    const float* a = upload(ctx, "abi_vol0", agg, n * size_t(d_max + 1));
+    float* o = ctx->ws.get<float>("abi_out0", n);
+    select_disparity_f32(a, h, w, d_max + 1, o, ctx->stream);
+    download(ctx, disp, o, sizeof(float) * n);
+  });
+}
+
+rpd_status rpd_consistency_filter(rpd_ctx* ctx, float* left, const float* right, int h, int w,
+                                  double thr) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    const size_t n = size_t(h) * w;
+    float* l = upload(ctx, "abi_in0", left, n);
+    const float* r = upload(ctx, "abi_in1", right, n);
+    consistency_filter_dev(l, r, h, w, thr, ctx->stream);
+    download(ctx, left, l, sizeof(float) * n);
+  });
+}
+
+rpd_status rpd_match_pair(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                          const rpd_road_model* model, const rpd_config* cfg, int d_max,
+                          float* d0, float* d1, double* shifts) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (cfg->sgm_paths != 4 && cfg->sgm_paths != 8)
+      throw InvalidArg("config: sgm_paths must be 4 or 8");
+    const size_t n = size_t(h) * w;
+    const float* l = upload(ctx, "abi_in0", left, n);
+    const float* r = upload(ctx, "abi_in1", right, n);
+    DevModel* m = upload_model(ctx, *model);
+    float* o0 = ctx->ws.get<float>("abi_out0", n);
+    float* o1 = ctx->ws.get<float>("abi_out1", n);
+    double* s = ctx->ws.get<double>("abi_shifts", h);
+    match_pair_dev(ctx, l, r, h, w, m, *cfg, d_max, o0, o1, s);
+    if (d0) download(ctx, d0, o0, sizeof(float) * n);
+    if (d1) download(ctx, d1, o1, sizeof(float) * n);
+    if (shifts) download(ctx, shifts, s, sizeof(double) * h);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// common.cuh — shared infrastructure of librpd_b200.so (sm_100a only).
+//
+// Conventions
+//  * Every translation unit is compiled with --fmad=false: no a*b+c
+//    contraction anywhere, so double/float expressions round exactly like the
+//    reference's x86-64 SSE2 build (SURVEY.md §7 hard part 1).
+//  * Errors inside the library are C++ exceptions (InvalidArg / Degenerate /
+//    CudaFail) that the extern "C" layer (abi.cu) maps onto rpd_status.
+//  * All device work of a context is ordered on ctx->stream.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rpd_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "librpd_b200 targets sm_100a only"
+#endif
+
+namespace rpdg {
+
+struct InvalidArg : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct Degenerate : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Capacity : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define RPD_CK(x)                                                                    \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      throw ::rpdg::CudaFail(std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define RPD_LAUNCH_CHECK() RPD_CK(cudaGetLastError())
+
+constexpr float kInvalid = -1.0f;  // types.hpp:21
+
+inline int cdiv(long long a, long long b) { return int((a + b - 1) / b); }
+__host__ __device__ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// Device-side status word shared by the pipeline kernels: the first kernel
+// that hits a reference exception condition records it; the host checks it
+// once at the end of the call (no mid-pipeline synchronisation).
+struct DevStatus {
+  int code;    // 0 ok, else rpd_status
+  int where;   // kind of failure, see status_message()
+  long long aux;
+};
+enum StatusWhere : int {
+  kWhereNone = 0,
+  kWhereSampleBoot = 1,      // sample_observations n<3 in bootstrap fit
+  kWhereFitBoot = 2,         // fit_line singular in bootstrap fit
+  kWhereSamplePt = 3,
+  kWhereFitPt = 4,
+  kWhereThresholdEmpty = 5,  // find_road_threshold: all vectors excluded
+  kWhereHistTooLarge = 6,
+  kWhereSample = 7,          // standalone sample_observations
+  kWhereFit = 8,             // standalone fit_line / estimate_roll / fit_road
+};
+
+__device__ inline void set_status(DevStatus* st, int code, int where, long long aux = 0) {
+  if (atomicCAS(&st->code, 0, code) == 0) {
+    st->where = where;
+    st->aux = aux;
+  }
+}
+
+// Road model as the device sees it: cos/sin travel with phi so every kernel
+// evaluates road_disparity_at (types.hpp:39-41) with the same two values.
+struct DevModel {
+  double a0, a1, phi, c, s;
+};
+
+// road_disparity_at, types.hpp:39-41 — a0 + a1*(v*cos - u*sin), no FMA.
+__host__ __device__ inline double road_at(const DevModel& m, double u, double v) {
+  return m.a0 + m.a1 * (v * m.c - u * m.s);
+}
+
+// ----------------------------------------------------------- workspace ----
+// Grow-only named device buffers.  Pointers stay stable until a request
+// exceeds the current capacity, so captured CUDA graphs stay valid for a
+// fixed problem shape.
+class Workspace {
+ public:
+  ~Workspace() { release(); }
+  void release() {
+    for (auto& kv : bufs_)
+      if (kv.second.p) cudaFree(kv.second.p);
+    bufs_.clear();
+  }
+  template <typename T>
+  T* get(const std::string& name, size_t count) {
+    Buf& b = bufs_[name];
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (b.bytes < bytes) {
+      if (b.p) RPD_CK(cudaFree(b.p));
+      b.p = nullptr;
+      b.bytes = 0;
+      const size_t want = bytes + bytes / 8;  // headroom for small shape drift
+      if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        throw CudaFail("device allocation of " + std::to_string(want) + " bytes failed (" +
+                       name + ")");
+      }
+      b.bytes = want;
+      ++generation_;
+    }
+    return static_cast<T*>(b.p);
+  }
+  unsigned generation() const { return generation_; }
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs_;
+  unsigned generation_ = 0;
+};
+
+// Pinned host staging area (grow-only).
+class PinnedHost {
+ public:
+  ~PinnedHost() {
+    if (p_) cudaFreeHost(p_);
+  }
+  void* get(size_t bytes) {
+    if (bytes > bytes_) {
+      if (p_) RPD_CK(cudaFreeHost(p_));
+      p_ = nullptr;
+      RPD_CK(cudaMallocHost(&p_, bytes));
+      bytes_ = bytes;
+    }
+    return p_;
+  }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+}  // namespace rpdg
+
+struct rpd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  rpdg::Workspace ws;
+  rpdg::PinnedHost pinned;
+  rpdg::DevStatus* status = nullptr;  // device
+  cudaEvent_t ev[RPD_NUM_STAGES + 1] = {};
+  int sm_count = 148;
+};
+
+namespace rpdg {
+
+// Host-side helpers shared by the translation units ---------------------
+void reset_status(rpd_ctx* ctx);
+// Synchronises the stream and throws the recorded device status, if any.
+void sync_and_check(rpd_ctx* ctx);
+DevModel host_model(const rpd_road_model& m);  // cos/sin on the host (glibc)
+
+}  // namespace rpdg

@@ -1,0 +1,824 @@
+// sgm.cu — semi-global matching for sm_100a.
+//
+// Reference: /root/reference/proj/src/sgm.cpp (census :13-34, cost :38-68,
+// aggregation :70-110, swap :112-121, WTA :123-153, LR :155-170,
+// match_pair :172-226) and include/rpd/perspective.hpp (warp :45-66,
+// restore :69-80, shifts :23-35).
+//
+// Fast integer path.  With integral penalties every value the
+// reference's float recursion produces is a small integer, so the recursion is
+// evaluated on packed u16x2 lanes with the native sm_100 DPX instructions
+// (VIADDMNMX.U16x2 = fused add+min, VIMNMX.U16x2) and stored as u8:
+//   0 <= L_r(p,d) <= (window^2-1) + lambda2 <= 255.
+// One thread (or a G-lane group) owns one scan chain and holds every disparity
+// level of the chain's current pixel in registers; raw costs are prefetched D
+// steps ahead.  All 2P (direction x {left,right}-reference) chains of a pass run
+// in ONE launch and write per-path u8 volumes; a WTA kernel sums them (exact
+// u16) and applies select_disparity's rules.  The right-reference cost volume
+// C_R(v,u,d) = C_L(v,u+d,d) is generated directly from the census words.
+
+#include <cfloat>
+
+#include <cub/cub.cuh>
+
+#include "sgm.cuh"
+
+namespace rpdg {
+
+// --------------------------------------------------------------- layout ----
+namespace {
+constexpr int kMaxFastLevels = 576;
+}
+
+SgmLayout sgm_layout(int h, int w, int levels, int paths) {
+  SgmLayout L;
+  L.h = h;
+  L.w = w;
+  L.levels = levels;
+  L.paths = paths;
+  if (levels <= 36) {
+    L.G = 1;
+    L.wpl = (levels + 3) / 4;
+  } else {
+    int G = 2;
+    while (4 * 9 * G < levels) G *= 2;
+    L.G = G;
+    L.wpl = std::max(5, (levels + 4 * G - 1) / (4 * G));
+  }
+  L.lw = 4 * L.wpl * L.G;
+  return L;
+}
+
+bool sgm_fast_path_ok(float l1, float l2, int window) {
+  const float maxc = float(window * window - 1);
+  return l1 >= 1.0f && l2 >= l1 && l1 == std::floor(l1) && l2 == std::floor(l2) &&
+         maxc + l2 <= 255.0f;
+}
+
+// ------------------------------------------------------- image kernels ----
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ out,
+                            long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = float(in[i]);
+}
+
+void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st) {
+  const int blocks = std::min<long long>((n + 255) / 256, 148 * 16);
+  k_u8_to_f32<<<std::max(blocks, 1), 256, 0, st>>>(in, out, n);
+  RPD_LAUNCH_CHECK();
+}
+
+// half_image, pipeline.cpp:25-34: 0.25f * (((a + b) + c) + d)
+__global__ void k_half(const float* __restrict__ in, int h, int w, float* __restrict__ out) {
+  const int hh = h / 2, hw = w / 2;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= hw || v >= hh) return;
+  const float* r0 = in + size_t(2 * v) * w + 2 * u;
+  const float* r1 = r0 + w;
+  out[size_t(v) * hw + u] = 0.25f * (r0[0] + r0[1] + r1[0] + r1[1]);
+}
+
+void launch_half_image(const float* in, int h, int w, float* out, cudaStream_t st) {
+  if (h / 2 == 0 || w / 2 == 0) return;
+  k_half<<<dim3(cdiv(w / 2, 128), h / 2), 128, 0, st>>>(in, h, w, out);
+  RPD_LAUNCH_CHECK();
+}
+
+// compute_row_shifts, perspective.hpp:23-35.  std::min / std::max semantics
+// spelled out so signed zeros match.
+__global__ void k_row_shifts(const DevModel* __restrict__ m, int h, int w, double delta,
+                             double* __restrict__ shifts) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= h) return;
+  const DevModel md = *m;
+  const double g0 = road_at(md, 0.0, double(v));
+  const double gw = road_at(md, double(w), double(v));
+  const double lo = (gw < g0) ? gw : g0;
+  const double x = lo - delta;
+  shifts[v] = (0.0 < x) ? x : 0.0;
+}
+
+void launch_row_shifts(const DevModel* model, int h, int w, double delta_pt, double* shifts,
+                       cudaStream_t st) {
+  k_row_shifts<<<cdiv(h, 128), 128, 0, st>>>(model, h, w, delta_pt, shifts);
+  RPD_LAUNCH_CHECK();
+}
+
+// warp_right_image, perspective.hpp:45-66
+__global__ void k_warp(const float* __restrict__ right, const double* __restrict__ shifts, int h,
+                       int w, float* __restrict__ out, uint8_t* __restrict__ iv) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const size_t i = size_t(v) * w + u;
+  const double s = double(u) - shifts[v];
+  if (s < 0.0 || s > double(w - 1)) {
+    out[i] = 0.0f;
+    iv[i] = 0;
+    return;
+  }
+  const int s0 = int(floor(s));
+  const int s1 = min(s0 + 1, w - 1);
+  const double t = s - double(s0);
+  const float* row = right + size_t(v) * w;
+  out[i] = float((1.0 - t) * double(row[s0]) + t * double(row[s1]));
+  iv[i] = 1;
+}
+
+void launch_warp_right(const float* right, const double* shifts, int h, int w, float* out,
+                       uint8_t* in_view, cudaStream_t st) {
+  k_warp<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(right, shifts, h, w, out, in_view);
+  RPD_LAUNCH_CHECK();
+}
+
+// restore_disparity, perspective.hpp:69-80
+__global__ void k_restore(const float* __restrict__ d0, const double* __restrict__ shifts, int h,
+                          int w, float* __restrict__ d1) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const size_t i = size_t(v) * w + u;
+  const float d = d0[i];
+  d1[i] = (d != kInvalid) ? d + float(shifts[v]) : d;
+}
+
+void launch_restore(const float* d0, const double* shifts, int h, int w, float* d1,
+                    cudaStream_t st) {
+  k_restore<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(d0, shifts, h, w, d1);
+  RPD_LAUNCH_CHECK();
+}
+
+// census_transform, sgm.cpp:13-34: MSB-first bits over the row-major window,
+// centre skipped, coordinates clamped.
+template <int R>
+__global__ void k_census(const float* __restrict__ img, int h, int w, uint64_t* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const float c = img[size_t(v) * w + u];
+  uint64_t bits = 0;
+#pragma unroll
+  for (int dv = -R; dv <= R; ++dv) {
+    const float* row = img + size_t(min(max(v + dv, 0), h - 1)) * w;
+#pragma unroll
+    for (int du = -R; du <= R; ++du) {
+      if (dv == 0 && du == 0) continue;
+      bits = (bits << 1) | (row[min(max(u + du, 0), w - 1)] < c ? 1ull : 0ull);
+    }
+  }
+  out[size_t(v) * w + u] = bits;
+}
+
+void launch_census(const float* img, int h, int w, int window, uint64_t* out, cudaStream_t st) {
+  const dim3 grid(cdiv(w, 128), h);
+  switch (window) {
+    case 3: k_census<1><<<grid, 128, 0, st>>>(img, h, w, out); break;
+    case 5: k_census<2><<<grid, 128, 0, st>>>(img, h, w, out); break;
+    case 7: k_census<3><<<grid, 128, 0, st>>>(img, h, w, out); break;
+    default: throw InvalidArg("census_cost_volume: window must be odd");
+  }
+  RPD_LAUNCH_CHECK();
+}
+
+// census_cost_volume, sgm.cpp:38-68, float output in the reference layout.
+__global__ void k_cost_f32(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
+                           const uint8_t* __restrict__ iv, int h, int w, int levels, float maxc,
+                           float* __restrict__ costs) {
+  const long long n = (long long)h * w * levels;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = int(i % levels);
+    const long long p = i / levels;
+    const int u = int(p % w);
+    const int ur = u - d;
+    float c;
+    if (ur < 0 || (iv && !iv[p - d]))
+      c = maxc;
+    else
+      c = float(__popcll(cl[p] ^ cr[p - d]));
+    costs[i] = c;
+  }
+}
+
+void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_view, int h, int w,
+                     int levels, int window, float* costs, cudaStream_t st) {
+  const long long n = (long long)h * w * levels;
+  const int blocks = int(std::min<long long>((n + 255) / 256, 148 * 32));
+  k_cost_f32<<<std::max(blocks, 1), 256, 0, st>>>(cl, cr, in_view, h, w, levels,
+                                                  float(window * window - 1), costs);
+  RPD_LAUNCH_CHECK();
+}
+
+// --------------------------------------------------- fast u8 cost volumes --
+// One thread per (pixel, 4-level word).  Levels >= L are padded with 0xFF.
+// C_L(v,u,d) = popc(cl(u) ^ cr(u-d))  if u-d >= 0 and in_view(u-d), else maxc
+// C_R(v,u,d) = popc(cl(u+d) ^ cr(u))  if u+d <  W and in_view(u),   else maxc
+__global__ void k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
+                          const uint8_t* __restrict__ iv, int h, int w, int levels, int nw,
+                          uint32_t maxc, uint32_t* __restrict__ vol_l,
+                          uint32_t* __restrict__ vol_r) {
+  const long long n = (long long)h * w * nw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = int(i % nw);
+    const long long p = i / nw;
+    const int u = int(p % w);
+    const uint64_t a = cl[p];
+    const uint64_t b = cr[p];
+    const bool ivu = iv[p] != 0;
+    uint32_t wl = 0, wr = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int d = 4 * j + q;
+      uint32_t cL = 0xFF, cR = 0xFF;
+      if (d < levels) {
+        cL = (u - d < 0 || !iv[p - d]) ? maxc : uint32_t(__popcll(a ^ cr[p - d]));
+        cR = (u + d >= w || !ivu) ? maxc : uint32_t(__popcll(cl[p + d] ^ b));
+      }
+      wl |= cL << (8 * q);
+      wr |= cR << (8 * q);
+    }
+    vol_l[i] = wl;
+    vol_r[i] = wr;
+  }
+}
+
+// u8 volume (stride lw) -> float reference layout (parity dumps only).
+__global__ void k_u8vol_to_f32(const uint8_t* __restrict__ vol, long long npix, int lw, int levels,
+                               float* __restrict__ out) {
+  const long long n = npix * levels;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / levels;
+    const int d = int(i % levels);
+    out[i] = float(vol[p * lw + d]);
+  }
+}
+
+// ------------------------------------------------------ path aggregation --
+struct AggJob {
+  const uint8_t* cost;
+  uint8_t* out;
+  int du, dv;
+  int nchains;
+  int block0;
+};
+struct AggArgs {
+  AggJob job[16];
+  int njobs;
+  int h, w, lw;
+  uint32_t p1x2, p2x2;
+};
+
+constexpr uint32_t kInf2 = 0x7FFF7FFFu;
+constexpr int kAggThreads = 64;
+
+template <int NPL>
+__device__ __forceinline__ uint32_t min_pairs(const uint32_t (&x)[NPL]) {
+  uint32_t t[NPL];
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) t[k] = x[k];
+#pragma unroll
+  for (int width = 1; width < NPL; width *= 2)
+#pragma unroll
+    for (int i = 0; i + width < NPL; i += 2 * width) t[i] = __vminu2(t[i], t[i + width]);
+  return t[0];
+}
+
+// Scan-chain cursor.  Horizontal chains are rows; vertical chains columns;
+// diagonal chains start at column `chain` of the first row and wrap around the
+// image width — a wrap starts a new reference chain (no predecessor).
+struct Cursor {
+  int v, u;
+};
+
+template <int WPL, int G, int D>
+__global__ void __launch_bounds__(kAggThreads)
+    k_aggregate(const __grid_constant__ AggArgs a) {
+  constexpr int NPL = 2 * WPL;
+  constexpr int CPB = kAggThreads / G;
+  int j = 0;
+#pragma unroll 1
+  while (j + 1 < a.njobs && int(blockIdx.x) >= a.job[j + 1].block0) ++j;
+  const AggJob& J = a.job[j];
+  const int g = threadIdx.x % G;
+  const int chain = (int(blockIdx.x) - J.block0) * CPB + int(threadIdx.x) / G;
+  if (chain >= J.nchains) return;  // whole group leaves together
+  const unsigned gmask =
+      G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+
+  const int h = a.h, w = a.w, lw = a.lw;
+  const int du = J.du, dv = J.dv;
+  const bool horiz = dv == 0;
+  const int nsteps = horiz ? w : h;
+  auto start = [&]() {
+    Cursor c;
+    if (horiz) {
+      c.v = chain;
+      c.u = du > 0 ? 0 : w - 1;
+    } else {
+      c.v = dv > 0 ? 0 : h - 1;
+      c.u = chain;
+    }
+    return c;
+  };
+  auto advance = [&](Cursor& c) {
+    if (horiz) {
+      c.u += du;
+    } else {
+      c.v += dv;
+      c.u += du;
+      if (c.u >= w) c.u -= w;
+      if (c.u < 0) c.u += w;
+    }
+  };
+  const uint8_t* __restrict__ cost = J.cost + g * WPL * 4;
+  uint8_t* __restrict__ out = J.out + g * WPL * 4;
+  auto offset = [&](const Cursor& c) { return (size_t(c.v) * w + c.u) * lw; };
+
+  uint32_t buf[D][WPL];
+  Cursor pc = start();
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < nsteps) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(cost + offset(pc));
+#pragma unroll
+      for (int q = 0; q < WPL; ++q) buf[k][q] = __ldg(src + q);
+      advance(pc);
+    }
+  }
+
+  Cursor cc = start();
+  uint32_t prev[NPL];
+  uint32_t mnx2 = 0;
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) prev[k] = kInf2;
+
+  for (int s0 = 0; s0 < nsteps; s0 += D) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int s = s0 + k;
+      if (s >= nsteps) break;
+      uint32_t raw[NPL];
+#pragma unroll
+      for (int q = 0; q < WPL; ++q) {
+        raw[2 * q] = __byte_perm(buf[k][q], 0u, 0x4140);
+        raw[2 * q + 1] = __byte_perm(buf[k][q], 0u, 0x4342);
+      }
+      if (s + D < nsteps) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(cost + offset(pc));
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) buf[k][q] = __ldg(src + q);
+        advance(pc);
+      }
+      const bool has_pred =
+          s > 0 && (horiz || du == 0 || unsigned(cc.u - du) < unsigned(w));
+      uint32_t cur[NPL];
+      if (!has_pred) {
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) cur[q] = raw[q];
+      } else {
+        uint32_t lo_nb = kInf2, hi_nb = kInf2;
+        if (G > 1) {
+          const uint32_t up = __shfl_up_sync(gmask, prev[NPL - 1], 1, G);
+          const uint32_t dn = __shfl_down_sync(gmask, prev[0], 1, G);
+          if (g > 0) lo_nb = up;
+          if (g < G - 1) hi_nb = dn;
+        }
+        const uint32_t ceil2 = mnx2 + a.p2x2;
+        uint32_t qprev = __byte_perm(lo_nb, prev[0], 0x5432);  // (prev[d-1], prev[d]) of pair 0
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+          const uint32_t nxt = (q + 1 < NPL) ? prev[q + 1] : hi_nb;
+          const uint32_t qn = __byte_perm(prev[q], nxt, 0x5432);  // (prev[2q+1], prev[2q+2])
+          uint32_t t = __viaddmin_u16x2(qprev, a.p1x2, prev[q]);
+          t = __viaddmin_u16x2(qn, a.p1x2, t);
+          t = __vminu2(t, ceil2);
+          cur[q] = raw[q] + t - mnx2;  // per-half exact: t >= mn, no carry
+          qprev = qn;
+        }
+      }
+      {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(out + offset(cc));
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) dst[q] = __byte_perm(cur[2 * q], cur[2 * q + 1], 0x6420);
+      }
+      const uint32_t m2 = min_pairs<NPL>(cur);
+      uint32_t m = min(m2 & 0xFFFFu, m2 >> 16);
+      if (G > 1) {
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1)
+          m = min(m, __shfl_xor_sync(gmask, m, off, G));
+      }
+      mnx2 = m * 0x10001u;
+#pragma unroll
+      for (int q = 0; q < NPL; ++q) prev[q] = cur[q];
+      advance(cc);
+    }
+  }
+}
+
+using AggKernel = void (*)(AggArgs);
+
+template <int WPL, int G>
+AggKernel pick_depth() {
+  if constexpr (WPL <= 5)
+    return k_aggregate<WPL, G, 8>;
+  else
+    return k_aggregate<WPL, G, 4>;
+}
+
+AggKernel agg_kernel(int wpl, int G) {
+#define RPD_AGG_CASE(W_, G_) \
+  if (wpl == W_ && G == G_) return pick_depth<W_, G_>();
+  RPD_AGG_CASE(1, 1) RPD_AGG_CASE(2, 1) RPD_AGG_CASE(3, 1) RPD_AGG_CASE(4, 1)
+  RPD_AGG_CASE(5, 1) RPD_AGG_CASE(6, 1) RPD_AGG_CASE(7, 1) RPD_AGG_CASE(8, 1)
+  RPD_AGG_CASE(9, 1)
+  RPD_AGG_CASE(5, 2) RPD_AGG_CASE(6, 2) RPD_AGG_CASE(7, 2) RPD_AGG_CASE(8, 2) RPD_AGG_CASE(9, 2)
+  RPD_AGG_CASE(5, 4) RPD_AGG_CASE(6, 4) RPD_AGG_CASE(7, 4) RPD_AGG_CASE(8, 4) RPD_AGG_CASE(9, 4)
+  RPD_AGG_CASE(5, 8) RPD_AGG_CASE(6, 8) RPD_AGG_CASE(7, 8) RPD_AGG_CASE(8, 8) RPD_AGG_CASE(9, 8)
+  RPD_AGG_CASE(5, 16) RPD_AGG_CASE(6, 16) RPD_AGG_CASE(7, 16) RPD_AGG_CASE(8, 16)
+  RPD_AGG_CASE(9, 16)
+#undef RPD_AGG_CASE
+  throw InvalidArg("sgm: unsupported level layout");
+}
+
+// ----------------------------------------------------- WTA (select_disparity)
+// Sums the P per-path u8 volumes into exact u16 costs S(d) and applies
+// sgm.cpp:123-153: first argmin; invalid if S(d) <= S(best) for |d-best| > 1;
+// parabola with float arithmetic in the reference's order.
+struct WtaArgs {
+  const uint8_t* path[8];
+  int paths;
+  long long npix;
+  int lw, levels;
+  float* disp;
+  float* dump;  // optional S(d) in the reference float layout
+};
+
+__device__ __forceinline__ void wta_visit(uint32_t s, int d, uint32_t& minv, int& best,
+                                          int& cnt, uint32_t& last, uint32_t& sbm1,
+                                          uint32_t& sbp1) {
+  if (d == best + 1) sbp1 = s;
+  if (s < minv) {
+    minv = s;
+    best = d;
+    cnt = 1;
+    sbm1 = last;
+  } else if (s == minv) {
+    ++cnt;
+  }
+  last = s;
+}
+
+__global__ void k_wta(const __grid_constant__ WtaArgs a) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= a.npix) return;
+  const int nw = a.lw / 4;
+  uint32_t minv = 0xFFFFFFFFu, last = 0, sbm1 = 0, sbp1 = 0;
+  int best = -2, cnt = 0;
+  for (int j = 0; j < nw; ++j) {
+    if (4 * j >= a.levels) break;
+    uint32_t s01 = 0, s23 = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < a.paths) {
+        const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a.path[r] + p * a.lw) + j);
+        s01 += __byte_perm(x, 0u, 0x4140);
+        s23 += __byte_perm(x, 0u, 0x4342);
+      }
+    }
+    const uint32_t sv[4] = {s01 & 0xFFFFu, s01 >> 16, s23 & 0xFFFFu, s23 >> 16};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int d = 4 * j + q;
+      if (d < a.levels) {
+        wta_visit(sv[q], d, minv, best, cnt, last, sbm1, sbp1);
+        if (a.dump) a.dump[p * a.levels + d] = float(sv[q]);
+      }
+    }
+  }
+  // occurrences of the minimum other than best and best+1 make it ambiguous
+  const int near = (best + 1 < a.levels && sbp1 == minv) ? 1 : 0;
+  float r;
+  if (cnt - 1 - near > 0) {
+    r = kInvalid;
+  } else {
+    r = float(best);
+    if (best > 0 && best < a.levels - 1) {
+      const float cm = float(sbm1), cb = float(minv), cp = float(sbp1);
+      const float denom = cm + cp - 2.0f * cb;
+      if (denom > 0.0f) r += (cm - cp) / (2.0f * denom);
+    }
+  }
+  a.disp[p] = r;
+}
+
+// ------------------------------------------- LR check + post filters ----
+// consistency_filter (sgm.cpp:155-170), flat raw cost curve (:200-212),
+// best sample out of view (:216-222), restore_disparity (perspective.hpp:69-80).
+template <typename CostT>
+__global__ void k_post(const float* __restrict__ dl, const float* __restrict__ dr,
+                       const CostT* __restrict__ cost, int cstride,
+                       const uint8_t* __restrict__ iv, const double* __restrict__ shifts, int h,
+                       int w, int levels, double thr, float* __restrict__ d0,
+                       float* __restrict__ d1) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const size_t i = size_t(v) * w + u;
+  const size_t row = size_t(v) * w;
+  float d = dl[i];
+  if (d != kInvalid) {
+    const int ur = u - int(lroundf(d));
+    if (ur < 0 || ur >= w) {
+      d = kInvalid;
+    } else {
+      const float x = dr[row + ur];
+      if (x == kInvalid || double(fabsf(d - x)) > thr) d = kInvalid;
+    }
+  }
+  if (d != kInvalid) {
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    const CostT* c = cost + i * size_t(cstride);
+    for (int k = 0; k < levels; ++k) {
+      const int ur = u - k;
+      if (ur < 0) break;
+      if (!iv[row + ur]) continue;
+      const float x = float(c[k]);
+      lo = (x < lo) ? x : lo;
+      hi = (hi < x) ? x : hi;
+      if (lo < hi) break;
+    }
+    if (hi <= lo) d = kInvalid;
+  }
+  if (d != kInvalid) {
+    const int ur = u - int(lroundf(d));
+    if (ur < 0 || !iv[row + ur]) d = kInvalid;
+  }
+  d0[i] = d;
+  d1[i] = (d != kInvalid) ? d + float(shifts[v]) : d;
+}
+
+// ------------------------------------------------------ generic float path --
+// One thread per chain start (pixel whose predecessor is outside the image)
+// walking the chain; prev values are read back from `line`, as sgm.cpp:84-105.
+__global__ void k_agg_f32_dir(const float* __restrict__ raw, float* __restrict__ line,
+                              float* __restrict__ total, int h, int w, int n, int du, int dv,
+                              float l1, float l2, int first) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= (long long)h * w) return;
+  int v = int(p / w), u = int(p % w);
+  if (!(v - dv < 0 || v - dv >= h || u - du < 0 || u - du >= w)) return;
+  bool head = true;
+  while (v >= 0 && v < h && u >= 0 && u < w) {
+    const size_t base = (size_t(v) * w + u) * n;
+    const float* c = raw + base;
+    float* cur = line + base;
+    float* tot = total + base;
+    if (head) {
+      for (int d = 0; d < n; ++d) {
+        cur[d] = c[d];
+        tot[d] = first ? cur[d] : tot[d] + cur[d];
+      }
+      head = false;
+    } else {
+      const float* prev = line + (size_t(v - dv) * w + (u - du)) * n;
+      float mn = prev[0];
+      for (int d = 1; d < n; ++d) mn = (prev[d] < mn) ? prev[d] : mn;
+      const float cap = mn + l2;
+      for (int d = 0; d < n; ++d) {
+        float b = prev[d];
+        if (d > 0) { const float x = prev[d - 1] + l1; b = (x < b) ? x : b; }
+        if (d + 1 < n) { const float x = prev[d + 1] + l1; b = (x < b) ? x : b; }
+        b = (cap < b) ? cap : b;
+        cur[d] = c[d] + b - mn;
+        tot[d] = first ? cur[d] : tot[d] + cur[d];
+      }
+    }
+    v += dv;
+    u += du;
+  }
+}
+
+void aggregate_f32(rpd_ctx* ctx, const float* costs, int h, int w, int levels,
+                   const int32_t* dirs, int ndirs, float l1, float l2, float* out) {
+  const long long npix = (long long)h * w;
+  float* line = ctx->ws.get<float>("agg_f32_line", size_t(npix) * levels);
+  if (ndirs == 0) {
+    RPD_CK(cudaMemsetAsync(out, 0, sizeof(float) * size_t(npix) * levels, ctx->stream));
+    return;
+  }
+  for (int r = 0; r < ndirs; ++r) {
+    const int du = dirs[2 * r], dv = dirs[2 * r + 1];
+    if (du == 0 && dv == 0) throw InvalidArg("aggregate_costs: zero direction");
+    k_agg_f32_dir<<<cdiv(npix, 128), 128, 0, ctx->stream>>>(costs, line, out, h, w, levels, du,
+                                                            dv, l1, l2, r == 0);
+    RPD_LAUNCH_CHECK();
+  }
+}
+
+__global__ void k_select_f32(const float* __restrict__ agg, long long npix, int n,
+                             float* __restrict__ disp) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  const float* c = agg + p * n;
+  int best = 0;
+  for (int d = 1; d < n; ++d)
+    if (c[d] < c[best]) best = d;
+  bool amb = false;
+  for (int d = 0; d < n; ++d)
+    if (abs(d - best) > 1 && c[d] <= c[best]) amb = true;
+  if (amb) {
+    disp[p] = kInvalid;
+    return;
+  }
+  float r = float(best);
+  if (best > 0 && best < n - 1) {
+    const float denom = c[best - 1] + c[best + 1] - 2.0f * c[best];
+    if (denom > 0.0f) r += (c[best - 1] - c[best + 1]) / (2.0f * denom);
+  }
+  disp[p] = r;
+}
+
+void select_disparity_f32(const float* agg, int h, int w, int levels, float* disp,
+                          cudaStream_t st) {
+  const long long npix = (long long)h * w;
+  k_select_f32<<<cdiv(npix, 128), 128, 0, st>>>(agg, npix, levels, disp);
+  RPD_LAUNCH_CHECK();
+}
+
+__global__ void k_swap_f32(const float* __restrict__ in, const float* __restrict__ maxv, int h,
+                           int w, int n, float* __restrict__ out) {
+  const long long total = (long long)h * w * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = int(i % n);
+    const long long p = i / n;
+    const int u = int(p % w);
+    out[i] = (u + d < w) ? in[(p + d) * n + d] : *maxv;
+  }
+}
+
+void swap_reference_f32(rpd_ctx* ctx, const float* costs, int h, int w, int levels, float* out) {
+  const long long total = (long long)h * w * levels;
+  float* maxv = ctx->ws.get<float>("swap_max", 1);
+  size_t tmp_bytes = 0;
+  cub::DeviceReduce::Max(nullptr, tmp_bytes, costs, maxv, total, ctx->stream);
+  void* tmp = ctx->ws.get<uint8_t>("cub_tmp_swap", tmp_bytes);
+  cub::DeviceReduce::Max(tmp, tmp_bytes, costs, maxv, total, ctx->stream);
+  RPD_LAUNCH_CHECK();
+  const int blocks = int(std::min<long long>((total + 255) / 256, 148 * 32));
+  k_swap_f32<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(costs, maxv, h, w, levels, out);
+  RPD_LAUNCH_CHECK();
+}
+
+__global__ void k_lr_only(float* __restrict__ left, const float* __restrict__ right, int h, int w,
+                          double thr) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const size_t i = size_t(v) * w + u;
+  const float d = left[i];
+  if (d == kInvalid) return;
+  const int ur = u - int(lroundf(d));
+  if (ur < 0 || ur >= w) {
+    left[i] = kInvalid;
+    return;
+  }
+  const float x = right[size_t(v) * w + ur];
+  if (x == kInvalid || double(fabsf(d - x)) > thr) left[i] = kInvalid;
+}
+
+void consistency_filter_dev(float* left, const float* right, int h, int w, double thr,
+                            cudaStream_t st) {
+  k_lr_only<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(left, right, h, w, thr);
+  RPD_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ match_pair ---
+void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                    const DevModel* model, const rpd_config& cfg, int d_max, float* d0,
+                    float* d1, double* shifts, const MatchDump* dump) {
+  if (w < 2) throw InvalidArg("compute_row_shifts: width must be >= 2");
+  if (cfg.census_window % 2 == 0 || cfg.census_window < 3 || cfg.census_window > 7)
+    throw InvalidArg("census_cost_volume: window must be odd");
+  if (d_max >= w) throw InvalidArg("census_cost_volume: d_max >= width");
+  if (d_max < 0) throw InvalidArg("census_cost_volume: d_max must be >= 0");
+  cudaStream_t st = ctx->stream;
+  const long long npix = (long long)h * w;
+  const int levels = d_max + 1;
+  const int window = cfg.census_window;
+  const float l1 = float(cfg.lambda1), l2 = float(cfg.lambda2);
+
+  launch_row_shifts(model, h, w, cfg.delta_pt, shifts, st);
+  float* warped = ctx->ws.get<float>("mp_warped", npix);
+  uint8_t* iv = ctx->ws.get<uint8_t>("mp_inview", npix);
+  launch_warp_right(right, shifts, h, w, warped, iv, st);
+  uint64_t* cl = ctx->ws.get<uint64_t>("mp_census_l", npix);
+  uint64_t* cr = ctx->ws.get<uint64_t>("mp_census_r", npix);
+  launch_census(left, h, w, window, cl, st);
+  launch_census(warped, h, w, window, cr, st);
+  float* dl = ctx->ws.get<float>("mp_disp_l", npix);
+  float* dr = ctx->ws.get<float>("mp_disp_r", npix);
+  const dim3 rowgrid(cdiv(w, 128), h);
+  int32_t dirs[16];
+  const int paths = cfg.sgm_paths == 4 ? 4 : 8;
+  const int eight[16] = {1, 0, -1, 0, 0, 1, 0, -1, 1, 1, -1, 1, 1, -1, -1, -1};
+  for (int i = 0; i < 2 * paths; ++i) dirs[i] = eight[i];
+
+  if (!sgm_fast_path_ok(l1, l2, window) || levels > kMaxFastLevels) {
+    // generic float path (non-integral or very large penalties)
+    float* cost = ctx->ws.get<float>("mp_cost_f32", size_t(npix) * levels);
+    float* costr = ctx->ws.get<float>("mp_costr_f32", size_t(npix) * levels);
+    float* agg = ctx->ws.get<float>("mp_agg_f32", size_t(npix) * levels);
+    launch_cost_f32(cl, cr, iv, h, w, levels, window, cost, st);
+    aggregate_f32(ctx, cost, h, w, levels, dirs, paths, l1, l2, agg);
+    if (dump && dump->agg_left)
+      RPD_CK(cudaMemcpyAsync(dump->agg_left, agg, sizeof(float) * npix * levels,
+                             cudaMemcpyDeviceToDevice, st));
+    select_disparity_f32(agg, h, w, levels, dl, st);
+    swap_reference_f32(ctx, cost, h, w, levels, costr);
+    aggregate_f32(ctx, costr, h, w, levels, dirs, paths, l1, l2, agg);
+    if (dump && dump->agg_right)
+      RPD_CK(cudaMemcpyAsync(dump->agg_right, agg, sizeof(float) * npix * levels,
+                             cudaMemcpyDeviceToDevice, st));
+    select_disparity_f32(agg, h, w, levels, dr, st);
+    if (dump && dump->cost)
+      RPD_CK(cudaMemcpyAsync(dump->cost, cost, sizeof(float) * npix * levels,
+                             cudaMemcpyDeviceToDevice, st));
+    k_post<float><<<rowgrid, 128, 0, st>>>(dl, dr, cost, levels, iv, shifts, h, w, levels,
+                                           cfg.lr_threshold, d0, d1);
+    RPD_LAUNCH_CHECK();
+  } else {
+    const SgmLayout L = sgm_layout(h, w, levels, paths);
+    const int nw = L.lw / 4;
+    uint8_t* vol_l = ctx->ws.get<uint8_t>("mp_vol_l", size_t(npix) * L.lw);
+    uint8_t* vol_r = ctx->ws.get<uint8_t>("mp_vol_r", size_t(npix) * L.lw);
+    uint8_t* pathbuf = ctx->ws.get<uint8_t>("mp_paths", size_t(npix) * L.lw * 2 * paths);
+    {
+      const long long n = npix * nw;
+      const int blocks = int(std::min<long long>((n + 255) / 256, 148 * 32));
+      k_cost_u8<<<std::max(blocks, 1), 256, 0, st>>>(
+          cl, cr, iv, h, w, levels, nw, uint32_t(window * window - 1),
+          reinterpret_cast<uint32_t*>(vol_l), reinterpret_cast<uint32_t*>(vol_r));
+      RPD_LAUNCH_CHECK();
+    }
+    AggArgs args{};
+    args.h = h;
+    args.w = w;
+    args.lw = L.lw;
+    const uint32_t p1 = uint32_t(l1), p2 = uint32_t(l2);
+    args.p1x2 = p1 | (p1 << 16);
+    args.p2x2 = p2 | (p2 << 16);
+    const int cpb = kAggThreads / L.G;
+    int blocks = 0;
+    for (int vol = 0; vol < 2; ++vol)
+      for (int r = 0; r < paths; ++r) {
+        AggJob& J = args.job[args.njobs];
+        J.cost = vol == 0 ? vol_l : vol_r;
+        J.out = pathbuf + size_t(vol * paths + r) * npix * L.lw;
+        J.du = dirs[2 * r];
+        J.dv = dirs[2 * r + 1];
+        J.nchains = (J.dv == 0) ? h : w;
+        J.block0 = blocks;
+        blocks += cdiv(J.nchains, cpb);
+        ++args.njobs;
+      }
+    // launch horizontal (longest) chains first: jobs are ordered as listed,
+    // blocks are scheduled in index order.
+    agg_kernel(L.wpl, L.G)<<<blocks, kAggThreads, 0, st>>>(args);
+    RPD_LAUNCH_CHECK();
+    for (int vol = 0; vol < 2; ++vol) {
+      WtaArgs wa{};
+      for (int r = 0; r < paths; ++r) wa.path[r] = pathbuf + size_t(vol * paths + r) * npix * L.lw;
+      wa.paths = paths;
+      wa.npix = npix;
+      wa.lw = L.lw;
+      wa.levels = levels;
+      wa.disp = vol == 0 ? dl : dr;
+      wa.dump = dump ? (vol == 0 ? dump->agg_left : dump->agg_right) : nullptr;
+      k_wta<<<cdiv(npix, 128), 128, 0, st>>>(wa);
+      RPD_LAUNCH_CHECK();
+    }
+    if (dump && dump->cost) {
+      const long long n = npix * levels;
+      k_u8vol_to_f32<<<int(std::min<long long>((n + 255) / 256, 148 * 32)), 256, 0, st>>>(
+          vol_l, npix, L.lw, levels, dump->cost);
+      RPD_LAUNCH_CHECK();
+    }
+    k_post<uint8_t><<<rowgrid, 128, 0, st>>>(dl, dr, vol_l, L.lw, iv, shifts, h, w, levels,
+                                             cfg.lr_threshold, d0, d1);
+    RPD_LAUNCH_CHECK();
+  }
+  if (dump && dump->disp_left)
+    RPD_CK(cudaMemcpyAsync(dump->disp_left, dl, sizeof(float) * npix, cudaMemcpyDeviceToDevice,
+                           st));
+  if (dump && dump->disp_right)
+    RPD_CK(cudaMemcpyAsync(dump->disp_right, dr, sizeof(float) * npix, cudaMemcpyDeviceToDevice,
+                           st));
+}
+
+}  // namespace rpdg

@@ -1,0 +1,66 @@
+// sgm.cuh — semi-global matching on the device (sgm.cpp:13-226 of the reference).
+#pragma once
+
+#include "common.cuh"
+
+namespace rpdg {
+
+// Geometry of the fast integer path for one pass.
+struct SgmLayout {
+  int h = 0, w = 0;
+  int levels = 0;   // L = d_max + 1
+  int G = 1;        // lanes per scan chain
+  int wpl = 1;      // u8 cost words per lane (4 levels per word)
+  int lw = 4;       // bytes per pixel in the u8 volumes = 4*wpl*G >= L
+  int paths = 8;    // P
+};
+SgmLayout sgm_layout(int h, int w, int levels, int paths);
+
+// Whether the integer u8/u16x2 path reproduces the reference's float
+// arithmetic bit-exactly for these penalties (integral lambdas and
+// (window^2-1) + lambda2 <= 255); otherwise the generic float path runs.
+bool sgm_fast_path_ok(float lambda1, float lambda2, int window);
+
+// Optional materialisation of the fast path's intermediate volumes in the
+// reference float layout (v*W+u)*L+d, for parity dumps.
+struct MatchDump {
+  float* cost = nullptr;       // census_cost_volume
+  float* agg_left = nullptr;   // aggregate_costs(cost)
+  float* agg_right = nullptr;  // aggregate_costs(swap_reference(cost))
+  float* disp_left = nullptr;  // select_disparity(agg_left)
+  float* disp_right = nullptr; // select_disparity(agg_right)
+};
+
+// ---------------------------------------------------------------- kernels --
+void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st);
+void launch_half_image(const float* in, int h, int w, float* out, cudaStream_t st);
+void launch_row_shifts(const DevModel* model, int h, int w, double delta_pt, double* shifts,
+                       cudaStream_t st);
+void launch_warp_right(const float* right, const double* shifts, int h, int w, float* out,
+                       uint8_t* in_view, cudaStream_t st);
+void launch_restore(const float* d0, const double* shifts, int h, int w, float* d1,
+                    cudaStream_t st);
+void launch_census(const float* img, int h, int w, int window, uint64_t* out, cudaStream_t st);
+// Float cost volume in the reference layout (census_cost_volume ABI).
+void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_view, int h, int w,
+                     int levels, int window, float* costs, cudaStream_t st);
+
+// Generic float path (any direction list, any penalties), used by the
+// aggregate_costs / select_disparity / swap_reference ABI and as the
+// match_pair path for non-integral penalties.
+void aggregate_f32(rpd_ctx* ctx, const float* costs, int h, int w, int levels,
+                   const int32_t* dirs_host, int ndirs, float l1, float l2, float* out);
+void swap_reference_f32(rpd_ctx* ctx, const float* costs, int h, int w, int levels, float* out);
+void select_disparity_f32(const float* agg, int h, int w, int levels, float* disp,
+                          cudaStream_t st);
+void consistency_filter_dev(float* left, const float* right, int h, int w, double thr,
+                            cudaStream_t st);
+
+// Full matching pass on device buffers (match_pair, sgm.cpp:172-226).
+// model: device pointer.  left/right: float images.  Outputs d0, d1 (H*W)
+// and shifts (H doubles) are device pointers.
+void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                    const DevModel* model, const rpd_config& cfg, int d_max, float* d0,
+                    float* d1, double* shifts, const MatchDump* dump = nullptr);
+
+}  // namespace rpdg
