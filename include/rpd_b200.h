@@ -170,6 +170,26 @@ rpd_status rpd_detect(rpd_ctx* ctx, const float* left, const float* right, int h
 rpd_status rpd_detect_u8(rpd_ctx* ctx, const uint8_t* left, const uint8_t* right, int h,
                          int w, const rpd_config* cfg, rpd_detect_out* out);
 
+/* Streaming extension (no reference counterpart): device-resident uint8
+ * inputs.  rpd_input_buffers_u8 returns the context's device input buffers
+ * (fill them with cudaMemcpyAsync on rpd_ctx_stream(ctx)); rpd_detect_async_u8
+ * enqueues one frame on the context stream and returns without waiting;
+ * rpd_detect_fetch waits, checks the device status and copies the requested
+ * outputs (same fields as rpd_detect). */
+rpd_status rpd_input_buffers_u8(rpd_ctx* ctx, int h, int w, uint8_t** d_left, uint8_t** d_right);
+rpd_status rpd_detect_async_u8(rpd_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right,
+                               int h, int w, const rpd_config* cfg);
+rpd_status rpd_detect_fetch(rpd_ctx* ctx, rpd_detect_out* out);
+
+/* Parity extension: runs the production match_pair SGM path and materialises
+ * its intermediates in the reference float layout (v*W+u)*(d_max+1)+d:
+ * census_cost_volume, aggregate_costs of it and of swap_reference(it), and the
+ * two select_disparity maps before the consistency filter.  NULL skips. */
+rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                               const rpd_road_model* model, const rpd_config* cfg, int d_max,
+                               float* cost, float* agg_left, float* agg_right, float* disp_left,
+                               float* disp_right);
+
 /* ---- perspective transformation (perspective.hpp) ----------------------- */
 /* compute_row_shifts, perspective.hpp:23-35; shifts: H doubles. */
 rpd_status rpd_compute_row_shifts(rpd_ctx* ctx, const rpd_road_model* model, int w, int h,

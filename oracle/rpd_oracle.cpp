@@ -1198,6 +1198,28 @@ rpd_status rpd_match_pair(rpd_ctx* ctx, const float* left, const float* right, i
   });
 }
 
+rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                               const rpd_road_model* m, const rpd_config* cfg, int d_max,
+                               float* cost, float* agg_left, float* agg_right, float* disp_left,
+                               float* disp_right) {
+  return guard(ctx, [&] {  // the intermediates of sgm.cpp:179-194
+    check_dims(h, w);
+    const Shifts t = row_shifts({m->a0, m->a1, m->phi}, w, h, cfg->delta_pt);
+    const Warped wr = warp(to_gray(right, h, w), t);
+    const Dirs dirs = config_dirs(*cfg);
+    const float l1 = float(cfg->lambda1), l2 = float(cfg->lambda2);
+    const Volume raw =
+        cost_volume(to_gray(left, h, w), wr.img, d_max, cfg->census_window, &wr.in_view);
+    const Volume al = aggregate(raw, dirs, l1, l2);
+    const Volume ar = aggregate(swap_ref(raw), dirs, l1, l2);
+    if (cost) std::memcpy(cost, raw.c.data(), sizeof(float) * raw.c.size());
+    if (agg_left) std::memcpy(agg_left, al.c.data(), sizeof(float) * al.c.size());
+    if (agg_right) std::memcpy(agg_right, ar.c.data(), sizeof(float) * ar.c.size());
+    put(disp_left, wta(al));
+    put(disp_right, wta(ar));
+  });
+}
+
 rpd_status rpd_sample_observations(rpd_ctx* ctx, const float* d1, int h, int w,
                                    const rpd_rect_roi* roi, int64_t cap, double* d, double* u,
                                    double* v, int64_t* count) {

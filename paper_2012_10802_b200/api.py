@@ -232,7 +232,16 @@ _SIGS = {
                                       C.POINTER(Threshold), C.c_int, C.c_int, C.c_int, _vp]),
 }
 
+_EXT_SIGS = {  # extensions of the product library (streaming)
+    "rpd_input_buffers_u8": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp), C.POINTER(_vp)]),
+    "rpd_detect_async_u8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config)]),
+    "rpd_detect_fetch": (C.c_int, [_vp, C.POINTER(DetectOut)]),
+}
+_SIGS["rpd_match_pair_dump"] = (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
+                                          C.POINTER(Config), C.c_int, _vp, _vp, _vp, _vp, _vp])
+
 ABI_SYMBOLS = tuple(_SIGS)
+EXTENSION_SYMBOLS = tuple(_EXT_SIGS)
 
 
 class Library:
@@ -245,6 +254,12 @@ class Library:
             fn = getattr(self.dll, name)
             fn.restype = res
             fn.argtypes = args
+        self.has_streaming = all(hasattr(self.dll, n) for n in _EXT_SIGS)
+        if self.has_streaming:
+            for name, (res, args) in _EXT_SIGS.items():
+                fn = getattr(self.dll, name)
+                fn.restype = res
+                fn.argtypes = args
         if self.dll.rpd_abi_version() != 1:
             raise RpdError(f"{path}: unexpected ABI version")
 
@@ -447,6 +462,19 @@ class Context:
                                             C.byref(model), C.byref(cfg), d_max, _ptr(d0),
                                             _ptr(d1), _ptr(sh)))
         return d0, d1, sh
+
+    def match_pair_dump(self, left, right, model: RoadModel, cfg: Config, d_max: int):
+        """Intermediates of match_pair: (cost, agg_left, agg_right, disp_left, disp_right)."""
+        left = _f32(left)
+        right = _f32(right)
+        h, w = left.shape
+        vols = [np.empty((h, w, d_max + 1), np.float32) for _ in range(3)]
+        maps = [np.empty((h, w), np.float32) for _ in range(2)]
+        self._check(self.dll.rpd_match_pair_dump(self.handle, _ptr(left), _ptr(right), h, w,
+                                                 C.byref(model), C.byref(cfg), d_max,
+                                                 *[_ptr(v) for v in vols],
+                                                 *[_ptr(m) for m in maps]))
+        return (*vols, *maps)
 
     # ------------------------------------------------------- road geometry --
     def sample_observations(self, d1, roi: Optional[RectRoi] = None, cap: int = 100000):

@@ -82,6 +82,7 @@ void rpd_ctx_destroy(rpd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  pipeline_forget(ctx);
   ctx->ws.release();
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -241,6 +242,39 @@ rpd_status rpd_match_pair(rpd_ctx* ctx, const float* left, const float* right, i
     if (d0) download(ctx, d0, o0, sizeof(float) * n);
     if (d1) download(ctx, d1, o1, sizeof(float) * n);
     if (shifts) download(ctx, shifts, s, sizeof(double) * h);
+  });
+}
+
+rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* right, int h, int w,
+                               const rpd_road_model* model, const rpd_config* cfg, int d_max,
+                               float* cost, float* agg_left, float* agg_right, float* disp_left,
+                               float* disp_right) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (cfg->sgm_paths != 4 && cfg->sgm_paths != 8)
+      throw InvalidArg("config: sgm_paths must be 4 or 8");
+    if (d_max < 0) throw InvalidArg("census_cost_volume: d_max must be >= 0");
+    const size_t n = size_t(h) * w;
+    const size_t cells = n * size_t(d_max + 1);
+    const float* l = upload(ctx, "abi_in0", left, n);
+    const float* r = upload(ctx, "abi_in1", right, n);
+    DevModel* m = upload_model(ctx, *model);
+    float* o0 = ctx->ws.get<float>("abi_out0", n);
+    float* o1 = ctx->ws.get<float>("abi_out1", n);
+    double* s = ctx->ws.get<double>("abi_shifts", h);
+    MatchDump dump;
+    dump.cost = cost ? ctx->ws.get<float>("abi_dump_cost", cells) : nullptr;
+    dump.agg_left = agg_left ? ctx->ws.get<float>("abi_dump_aggl", cells) : nullptr;
+    dump.agg_right = agg_right ? ctx->ws.get<float>("abi_dump_aggr", cells) : nullptr;
+    dump.disp_left = disp_left ? ctx->ws.get<float>("abi_dump_dl", n) : nullptr;
+    dump.disp_right = disp_right ? ctx->ws.get<float>("abi_dump_dr", n) : nullptr;
+    match_pair_dev(ctx, l, r, h, w, m, *cfg, d_max, o0, o1, s, &dump);
+    if (cost) download(ctx, cost, dump.cost, sizeof(float) * cells);
+    if (agg_left) download(ctx, agg_left, dump.agg_left, sizeof(float) * cells);
+    if (agg_right) download(ctx, agg_right, dump.agg_right, sizeof(float) * cells);
+    if (disp_left) download(ctx, disp_left, dump.disp_left, sizeof(float) * n);
+    if (disp_right) download(ctx, disp_right, dump.disp_right, sizeof(float) * n);
+    RPD_CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -1,0 +1,213 @@
+// ccl.cuh — union-find connected-component labelling and warp run
+// reductions shared by SLIC connectivity and pothole labelling.
+//
+// Components are rooted at their MINIMUM raster index (union links the larger
+// root under the smaller), so "first encounter in scan order"
+// (segmentation.cpp:104-124, 370-388) is a rank of roots by index.
+#pragma once
+
+#include "seg.cuh"
+
+namespace rpdg {
+
+__device__ __forceinline__ int uf_find(const int* __restrict__ parent, int p) {
+  int q = parent[p];
+  while (q != p) {
+    p = q;
+    q = parent[p];
+  }
+  return p;
+}
+
+__device__ __forceinline__ void uf_union(int* parent, int a, int b) {
+  while (true) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    if (a < b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(&parent[a], b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
+// Same-class predicate for the CCL kernels.
+struct SameLabel {  // SLIC pieces: equal superpixel label (all pixels foreground)
+  const int32_t* lab;
+  __device__ bool fg(int) const { return true; }
+  __device__ bool same(int p, int q) const { return lab[p] == lab[q]; }
+};
+struct SameMask {  // binary mask components
+  const int32_t* mask;
+  __device__ bool fg(int p) const { return mask[p] != 0; }
+  __device__ bool same(int p, int q) const { return mask[q] != 0; }
+};
+
+template <typename Pred>
+__global__ void k_uf_init(Pred pr, int h, int w, int* __restrict__ parent) {
+  const long long n = (long long)h * w;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x)
+    parent[p] = pr.fg(int(p)) ? int(p) : -1;
+}
+
+// Merge with the already-visited neighbours (left, up-left, up, up-right).
+template <typename Pred>
+__global__ void k_uf_merge(Pred pr, int h, int w, int conn8, int* parent) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const int p = v * w + u;
+  if (!pr.fg(p)) return;
+  if (u > 0 && pr.same(p, p - 1)) uf_union(parent, p, p - 1);
+  if (v > 0) {
+    const int up = p - w;
+    if (pr.same(p, up)) uf_union(parent, p, up);
+    if (conn8) {
+      if (u > 0 && pr.same(p, up - 1)) uf_union(parent, p, up - 1);
+      if (u + 1 < w && pr.same(p, up + 1)) uf_union(parent, p, up + 1);
+    }
+  }
+}
+
+__global__ void k_uf_flatten(int h, int w, int* parent);
+
+template <typename Pred>
+void uf_label(Pred pr, int h, int w, int conn8, int* parent, int sm_count, cudaStream_t st) {
+  const long long n = (long long)h * w;
+  const int blocks = int(std::min<long long>((n + 255) / 256, sm_count * 16));
+  k_uf_init<<<std::max(blocks, 1), 256, 0, st>>>(pr, h, w, parent);
+  RPD_LAUNCH_CHECK();
+  k_uf_merge<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(pr, h, w, conn8, parent);
+  RPD_LAUNCH_CHECK();
+  k_uf_flatten<<<std::max(blocks, 1), 256, 0, st>>>(h, w, parent);
+  RPD_LAUNCH_CHECK();
+}
+
+// Segmented (contiguous-run) warp sum: lanes with equal `key` in a contiguous
+// run are summed into the run's first lane; returns true on that lane.
+// key < 0 lanes are skipped.
+template <typename T>
+__device__ __forceinline__ T shfl_down_any(T x, int off) {
+  return __shfl_down_sync(0xFFFFFFFFu, x, off);
+}
+__device__ __forceinline__ Acc128 shfl_down_any(Acc128 x, int off) {
+  Acc128 r;
+  r.lo = __shfl_down_sync(0xFFFFFFFFu, x.lo, off);
+  r.hi = __shfl_down_sync(0xFFFFFFFFu, x.hi, off);
+  return r;
+}
+__device__ __forceinline__ Acc128 acc_add(Acc128 a, Acc128 b) {
+  Acc128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1 : 0);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T plus_(T a, T b) {
+  return a + b;
+}
+__device__ __forceinline__ Acc128 plus_(Acc128 a, Acc128 b) { return acc_add(a, b); }
+
+struct RunInfo {
+  int end;    // last lane of this lane's run
+  bool head;  // first lane of its run (and key >= 0)
+};
+
+__device__ __forceinline__ RunInfo run_info(int key) {
+  const int lane = threadIdx.x & 31;
+  const int nxt = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+  const int prv = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+  const bool tail = lane == 31 || nxt != key;
+  const unsigned tails = __ballot_sync(0xFFFFFFFFu, tail);
+  RunInfo r;
+  r.end = lane + __ffs(tails >> lane) - 1;
+  r.head = key >= 0 && (lane == 0 || prv != key);
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T run_sum(T x, const RunInfo& ri) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const T o = shfl_down_any(x, off);
+    if (lane + off <= ri.end) x = plus_(x, o);
+  }
+  return x;
+}
+
+__device__ __forceinline__ void atomic_add_acc(Acc128* a, Acc128 x) {
+  const unsigned long long old = atomicAdd(&a->lo, x.lo);
+  const unsigned long long carry = (old + x.lo) < old ? 1ull : 0ull;
+  const unsigned long long hi = (unsigned long long)x.hi + carry;
+  if (hi) atomicAdd(reinterpret_cast<unsigned long long*>(&a->hi), hi);
+}
+
+// Exact fixed-point image of a float: x * 2^100 as a signed 128-bit integer.
+// Exact for 2^-77 <= |x| < 2^27 (and 0); anything else sets *inexact.
+__device__ __forceinline__ Acc128 to_fixed(float x, int* inexact) {
+  Acc128 r{0ull, 0ll};
+  if (x == 0.0f) return r;
+  const uint32_t b = __float_as_uint(x);
+  const int e = int((b >> 23) & 0xFFu);
+  unsigned long long m = b & 0x7FFFFFu;
+  int ex;
+  if (e == 0) {
+    ex = -149;
+  } else {
+    m |= 0x800000u;
+    ex = e - 150;
+  }
+  int s = ex + 100;
+  if (s < 0) {
+    *inexact = 1;
+    m = (-s >= 64) ? 0 : (m >> (-s));
+    s = 0;
+  }
+  if (s > 103) {
+    *inexact = 1;
+    s = 103;
+  }
+  if (s < 64) {
+    r.lo = m << s;
+    r.hi = (s > 40) ? (long long)(m >> (64 - s)) : 0;
+  } else {
+    r.lo = 0;
+    r.hi = (long long)(m << (s - 64));
+  }
+  if (b >> 31) {
+    r.lo = ~r.lo + 1ull;
+    r.hi = ~r.hi + (r.lo == 0 ? 1 : 0);
+  }
+  return r;
+}
+
+// Correctly rounded double of (a * 2^-100).
+__device__ __forceinline__ double fixed_to_double(Acc128 a) {
+  const bool neg = a.hi < 0;
+  unsigned __int128 x = (unsigned __int128)(unsigned long long)a.hi << 64 | a.lo;
+  if (neg) x = ~x + 1;
+  if (x == 0) return 0.0;
+  const unsigned long long hi = (unsigned long long)(x >> 64);
+  const int top = hi ? 127 - __clzll(hi) : 63 - __clzll((unsigned long long)x);
+  double mag;
+  if (top <= 52) {
+    mag = double((unsigned long long)x);
+    mag = ldexp(mag, -100);
+  } else {
+    const int shift = top - 52;
+    unsigned long long mant = (unsigned long long)(x >> shift);
+    const unsigned __int128 rem = x & ((((unsigned __int128)1) << shift) - 1);
+    const unsigned __int128 half = ((unsigned __int128)1) << (shift - 1);
+    if (rem > half || (rem == half && (mant & 1ull))) ++mant;
+    mag = ldexp(double(mant), shift - 100);
+  }
+  return neg ? -mag : mag;
+}
+
+}  // namespace rpdg

@@ -164,6 +164,7 @@ struct rpd_ctx {
   rpdg::DevStatus* status = nullptr;  // device
   cudaEvent_t ev[RPD_NUM_STAGES + 1] = {};
   int sm_count = 148;
+  void* pipeline = nullptr;  // rpdg::PipelineState (pipeline.cu)
 };
 
 namespace rpdg {
@@ -173,5 +174,6 @@ void reset_status(rpd_ctx* ctx);
 // Synchronises the stream and throws the recorded device status, if any.
 void sync_and_check(rpd_ctx* ctx);
 DevModel host_model(const rpd_road_model& m);  // cos/sin on the host (glibc)
+void pipeline_forget(rpd_ctx* ctx);           // releases captured graphs
 
 }  // namespace rpdg

@@ -17,6 +17,8 @@
 // Eigen's own SIMD order (road_geometry.cpp:20-24, 37) is not reproducible
 // without Eigen; the reference tests pin these sums to 1e-9 relative.
 
+#include <algorithm>
+
 #include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
@@ -559,18 +561,14 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ 
 }
 
 void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitDynSmem));
-    attr_done = true;
-  }
-  const long long kmax = req.compact ? 100000LL * 0 + (1LL << 22) : req.k_host;
+  RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitDynSmem));
+  RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
   if (!req.compact && req.k_host > (long long)kMaxRowsTrim * kFitLanes)
     throw InvalidArg("fit: too many observations for the device fit (max 524288)");
   FitKParams P{};
   P.r = req;
   P.status = ctx->status;
-  const long long scratch = req.compact ? std::min<long long>(kmax, (long long)kMaxRowsTrim * kFitLanes)
+  const long long scratch = req.compact ? (long long)kMaxRowsTrim * kFitLanes
                                         : std::max<long long>(req.k_host, 1);
   if (req.mode == kFitRoad) {
     if (req.compact) {

@@ -35,12 +35,11 @@ void pool_superpixels_dev(rpd_ctx* ctx, const float* d2, const int32_t* labels, 
 // find_road_threshold (298-359).  Only |i-j| <= band is stored; everything
 // else is provably excluded by the |g1-g2| > tau test and is counted.
 struct HistDev {
-  long long* band;        // rows x (2*band+1)
-  int band;               // half width
+  long long* bins;   // rows x (2*half+1), row = g1 bin, column = g2 bin - g1 bin + half
+  int half;
   long long cap_rows;
-  double* lohi;           // [lo, hi] (device)
-  long long* meta;        // [n, total, excluded_outside_band, inexact]
-  double* origin;         // device double
+  long long* meta;   // [n, total, excluded outside the band, lo key, hi key]
+  double* origin;    // device double
 };
 HistDev build_histogram_dev(rpd_ctx* ctx, const float* d2, int h, int w, double bin_width,
                             double tau);
@@ -52,6 +51,11 @@ void build_histogram_full_dev(rpd_ctx* ctx, const float* d2, int h, int w, doubl
 // band == n-1).  Result written to *out (device rpd_threshold).
 void find_threshold_dev(rpd_ctx* ctx, const HistDev& hd, double bin_width, double delta_pd,
                         double tau, rpd_threshold* out, int where);
+
+// find_road_threshold on a caller-provided dense n x n histogram (device).
+void threshold_from_full_dev(rpd_ctx* ctx, const long long* counts_dev, long long n, double bw,
+                             double origin, long long total, double delta_pd, double tau,
+                             rpd_threshold* out);
 
 // connected_components, segmentation.cpp:361-390 (mask: nonzero = foreground).
 void connected_components_dev(rpd_ctx* ctx, const int32_t* mask, int h, int w, int connectivity,

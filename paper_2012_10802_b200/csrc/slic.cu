@@ -1,0 +1,637 @@
+// slic.cu — SLIC superpixels + pooling for sm_100a.
+//
+// Reference: /root/reference/proj/src/segmentation.cpp:13-249.
+//
+//  * assign_pixels (:30-72) is pixel-centric: each pixel scans the centre
+//    bucket grid for every centre whose window [lround(c) +- ceil(S)] contains
+//    it and keeps the lexicographic minimum (dist, k) — identical to the
+//    reference's ascending-k scan with strict `<`.  Pixels covered by no window
+//    go to a warp-per-pixel nearest-centre fallback.
+//  * update_centers (:74-93) and pool_superpixels (:231-249) sum per label;
+//    coordinate sums are exact int64, value sums are exact signed 128-bit
+//    fixed point (x * 2^100), so the atomics' order cannot change the result.
+//  * enforce_connectivity (:98-166): union-find pieces, largest piece per label
+//    (ties -> first piece in scan order), then a level-synchronous BFS that
+//    reproduces the reference's FIFO claim order exactly: the level-(k+1) queue
+//    is ordered by (claimer's queue rank, neighbour index), and an orphan is
+//    claimed by its adjacent level-k pixel of lowest queue rank.
+//  * compaction to 1..count by first appearance in scan order (:218-224).
+
+#include <cub/cub.cuh>
+
+#include "ccl.cuh"
+
+namespace rpdg {
+
+__global__ void k_uf_flatten(int h, int w, int* parent) {
+  const long long n = (long long)h * w;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    if (parent[p] >= 0) parent[p] = uf_find(parent, int(p));
+  }
+}
+
+namespace {
+
+constexpr int kDU[8] = {1, -1, 0, 0, 1, 1, -1, -1};  // segmentation.cpp:104-105
+constexpr int kDV[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+__constant__ int c_du[8] = {1, -1, 0, 0, 1, 1, -1, -1};
+__constant__ int c_dv[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+
+struct Centers {
+  double* cu;
+  double* cv;
+  double* val;
+  int* icu;
+  int* icv;
+};
+
+struct CenterSums {
+  int* n;
+  long long* su;
+  long long* sv;
+  Acc128* sx;
+};
+
+// values_or_zero, segmentation.cpp:13-19
+__global__ void k_values_or_zero(const float* __restrict__ d2, long long n, float* __restrict__ vals) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float x = d2[i];
+    vals[i] = x != kInvalid ? x : 0.0f;
+  }
+}
+
+// gradient_at, segmentation.cpp:22-28 (float difference, squared in double)
+__device__ __forceinline__ double gradient_at(const float* vals, int h, int w, int u, int v) {
+  const float c = vals[size_t(v) * w + u];
+  const double gu = double(vals[size_t(v) * w + min(u + 1, w - 1)] - c);
+  const double gv = double(vals[size_t(min(v + 1, h - 1)) * w + u] - c);
+  return gu * gu + gv * gv;
+}
+
+// Seeds on the nu x nv grid nudged to the lowest gradient (:182-206).
+__global__ void k_seeds(const float* __restrict__ vals, int h, int w, int nu, int nv, double su,
+                        double sv, Centers c) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nu * nv) return;
+  const int i = k % nu, j = k / nu;
+  const int cu = int((i + 0.5) * su), cv = int((j + 0.5) * sv);
+  double best = __longlong_as_double(0x7FF0000000000000ll);
+  int bu = cu, bv = cv;
+  for (int dv = -1; dv <= 1; ++dv)
+    for (int du = -1; du <= 1; ++du) {
+      const int uu = min(max(cu + du, 0), w - 1), vv = min(max(cv + dv, 0), h - 1);
+      const double g = gradient_at(vals, h, w, uu, vv);
+      if (g < best) {
+        best = g;
+        bu = uu;
+        bv = vv;
+      }
+    }
+  c.cu[k] = double(bu);
+  c.cv[k] = double(bv);
+  c.val[k] = double(vals[size_t(bv) * w + bu]);
+}
+
+// Single-CTA counting sort of the centres into the bucket grid.
+constexpr int kBucketThreads = 1024;
+constexpr int kBucketItems = 8;  // supports up to 8192 buckets (32 KB smem)
+constexpr int kMaxBuckets = kBucketThreads * kBucketItems;
+
+__global__ void __launch_bounds__(kBucketThreads)
+    k_buckets(Centers c, int K, int w, int h, int B, int nbx, int nby, int* __restrict__ cell_start,
+              int* __restrict__ cell_items) {
+  using Scan = cub::BlockScan<int, kBucketThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int cnt[kMaxBuckets];
+  const int nb = nbx * nby;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const int iu = int(lround(c.cu[k])), iv = int(lround(c.cv[k]));
+    c.icu[k] = iu;
+    c.icv[k] = iv;
+    const int bx = min(max(iu, 0) / B, nbx - 1), by = min(max(iv, 0) / B, nby - 1);
+    atomicAdd(&cnt[by * nbx + bx], 1);
+  }
+  __syncthreads();
+  int items[kBucketItems];
+#pragma unroll
+  for (int q = 0; q < kBucketItems; ++q) {
+    const int b = threadIdx.x * kBucketItems + q;
+    items[q] = b < nb ? cnt[b] : 0;
+  }
+  int total;
+  Scan(tmp).ExclusiveSum(items, items, total);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kBucketItems; ++q) {
+    const int b = threadIdx.x * kBucketItems + q;
+    if (b < nb) {
+      cell_start[b] = items[q];
+      cnt[b] = items[q];  // becomes the scatter cursor
+    }
+  }
+  if (threadIdx.x == 0) cell_start[nb] = total;
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const int iu = c.icu[k], iv = c.icv[k];
+    const int bx = min(max(iu, 0) / B, nbx - 1), by = min(max(iv, 0) / B, nby - 1);
+    const int pos = atomicAdd(&cnt[by * nbx + bx], 1);
+    cell_items[pos] = k;
+  }
+}
+
+struct AssignArgs {
+  const float* vals;
+  int h, w;
+  Centers c;
+  const int* cell_start;
+  const int* cell_items;
+  int B, nbx, nby, win;
+  double sw;
+  int32_t* labels;
+  int* orphan_list;
+  int* orphan_count;
+};
+
+// assign_pixels, segmentation.cpp:30-57 (windowed part).
+__global__ void k_assign(const __grid_constant__ AssignArgs a) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= a.w) return;
+  const size_t p = size_t(v) * a.w + u;
+  const double x = double(a.vals[p]);
+  const int bx0 = u - a.win < 0 ? 0 : (u - a.win) / a.B;
+  const int bx1 = min(a.nbx - 1, (u + a.win) / a.B);
+  const int by0 = v - a.win < 0 ? 0 : (v - a.win) / a.B;
+  const int by1 = min(a.nby - 1, (v + a.win) / a.B);
+  double best = __longlong_as_double(0x7FF0000000000000ll);
+  int bk = -1;
+  for (int by = by0; by <= by1; ++by)
+    for (int bx = bx0; bx <= bx1; ++bx) {
+      const int b = by * a.nbx + bx;
+      const int e = a.cell_start[b + 1];
+      for (int idx = a.cell_start[b]; idx < e; ++idx) {
+        const int k = a.cell_items[idx];
+        if (abs(u - a.c.icu[k]) > a.win || abs(v - a.c.icv[k]) > a.win) continue;
+        const double dval = x - a.c.val[k];
+        const double du = double(u) - a.c.cu[k], dv = double(v) - a.c.cv[k];
+        const double dist = dval * dval + (du * du + dv * dv) * a.sw;
+        if (dist < best || (dist == best && k < bk)) {
+          best = dist;
+          bk = k;
+        }
+      }
+    }
+  if (bk < 0) {
+    a.labels[p] = 0;
+    const int slot = atomicAdd(a.orphan_count, 1);
+    a.orphan_list[slot] = int(p);
+  } else {
+    a.labels[p] = bk + 1;
+  }
+}
+
+// Nearest-centre fallback, segmentation.cpp:59-71 (one warp per pixel).
+__global__ void k_assign_fallback(int w, Centers c, int K, int32_t* __restrict__ labels,
+                                  const int* __restrict__ list, const int* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int n = *count;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
+    const int p = list[i];
+    const int u = p % w, v = p / w;
+    double best = __longlong_as_double(0x7FF0000000000000ll);
+    int bk = -1;
+    for (int k = lane; k < K; k += 32) {
+      const double du = double(u) - c.cu[k], dv = double(v) - c.cv[k];
+      const double d = du * du + dv * dv;
+      if (d < best) {
+        best = d;
+        bk = k;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+      const int ok = __shfl_xor_sync(0xFFFFFFFFu, bk, off);
+      if (ok >= 0 && (bk < 0 || ob < best || (ob == best && ok < bk))) {
+        best = ob;
+        bk = ok;
+      }
+    }
+    if (lane == 0 && bk >= 0) labels[p] = bk + 1;
+  }
+}
+
+// Per-label sums of (u, v, value, n) with warp run pre-aggregation.  `valid`
+// restricts to valid pixels (pooling); vals may be the raw d2 then.
+__global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __restrict__ labels,
+                             int h, int w, int max_label, bool valid_only, bool coords,
+                             CenterSums s, int* __restrict__ inexact) {
+  const long long n = (long long)h * w;
+  const long long base = (long long)blockIdx.x * blockDim.x;
+  for (long long p0 = base; p0 < n; p0 += (long long)gridDim.x * blockDim.x) {
+    const long long p = p0 + threadIdx.x;
+    int key = -1;
+    float x = 0.0f;
+    if (p < n) {
+      const int l = labels[p];
+      x = vals[p];
+      if (l >= 0 && l <= max_label && (!valid_only || x != kInvalid)) key = l;
+    }
+    const RunInfo ri = run_info(key);
+    int bad = 0;
+    Acc128 ax = key >= 0 ? to_fixed(x, &bad) : Acc128{0ull, 0ll};
+    if (bad) atomicOr(inexact, 1);
+    const int cnt = run_sum(key >= 0 ? 1 : 0, ri);
+    ax = run_sum(ax, ri);
+    long long su = 0, sv = 0;
+    if (coords) {
+      su = run_sum(key >= 0 ? (long long)(p % w) : 0ll, ri);
+      sv = run_sum(key >= 0 ? (long long)(p / w) : 0ll, ri);
+    }
+    if (ri.head) {
+      atomicAdd(&s.n[key], cnt);
+      atomic_add_acc(&s.sx[key], ax);
+      if (coords) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
+      }
+    }
+  }
+}
+
+// update_centers tail (:88-92), then zero the sums for the next round.
+// Label k+1 belongs to centre k.
+__global__ void k_center_finalize(CenterSums s, Centers c, int K) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int l = k + 1;
+  const int n = s.n[l];
+  if (n > 0) {
+    const double dn = double(n);
+    c.cu[k] = double(s.su[l]) / dn;
+    c.cv[k] = double(s.sv[l]) / dn;
+    c.val[k] = fixed_to_double(s.sx[l]) / dn;
+  }
+  s.n[l] = 0;
+  s.su[l] = 0;
+  s.sv[l] = 0;
+  s.sx[l] = Acc128{0ull, 0ll};
+}
+
+__global__ void k_zero_sums(CenterSums s, int nlabels) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlabels) return;
+  s.n[l] = 0;
+  s.su[l] = 0;
+  s.sv[l] = 0;
+  s.sx[l] = Acc128{0ull, 0ll};
+}
+
+// ------------------------------------------------ enforce_connectivity ----
+__global__ void k_piece_sizes(const int* __restrict__ parent, long long n, int* __restrict__ size) {
+  for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < n;
+       p0 += (long long)gridDim.x * blockDim.x) {
+    const long long p = p0 + threadIdx.x;
+    const int key = p < n ? parent[p] : -1;
+    const RunInfo ri = run_info(key);
+    const int c = run_sum(key >= 0 ? 1 : 0, ri);
+    if (ri.head) atomicAdd(&size[key], c);
+  }
+}
+
+// Largest piece per label; ties go to the earlier piece (smaller root index).
+__global__ void k_main_piece(const int* __restrict__ parent, const int32_t* __restrict__ labels,
+                             const int* __restrict__ size, long long n,
+                             unsigned long long* __restrict__ best) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    if (parent[p] != p) continue;
+    const unsigned long long key =
+        ((unsigned long long)(unsigned)size[p] << 32) | (0xFFFFFFFFull - (unsigned long long)p);
+    atomicMax(&best[labels[p]], key);
+  }
+}
+
+__global__ void k_orphans(const int* __restrict__ parent, int32_t* __restrict__ labels,
+                          const unsigned long long* __restrict__ best, long long n,
+                          int* __restrict__ claim) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int l = labels[p];
+    const long long root = (long long)(0xFFFFFFFFull - (best[l] & 0xFFFFFFFFull));
+    if (parent[p] != root) labels[p] = 0;
+    claim[p] = 0x7FFFFFFF;
+  }
+}
+
+// Level-0 frontier: kept pixels with an orphan neighbour, in scan order.
+__global__ void k_frontier_flags(const int32_t* __restrict__ labels, int h, int w,
+                                 int* __restrict__ flags) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (u >= w) return;
+  const size_t p = size_t(v) * w + u;
+  int f = 0;
+  if (labels[p] != 0) {
+    for (int i = 0; i < 8; ++i) {
+      const int nu = u + c_du[i], nv = v + c_dv[i];
+      if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+      if (labels[size_t(nv) * w + nu] == 0) {
+        f = 1;
+        break;
+      }
+    }
+  }
+  flags[p] = f;
+}
+
+__global__ void k_scatter_flagged(const int* __restrict__ flags, const int* __restrict__ pos,
+                                  long long n, int* __restrict__ list, int* __restrict__ total) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    if (flags[p]) list[pos[p]] = int(p);
+    if (p == n - 1) *total = pos[p] + flags[p];
+  }
+}
+
+// Ordered multi-source BFS (single CTA), segmentation.cpp:145-165.
+constexpr int kBfsThreads = 1024;
+__global__ void __launch_bounds__(kBfsThreads)
+    k_bfs(int32_t* labels, int h, int w, int* claim, int* qa, int* qb, const int* n0) {
+  using Scan = cub::BlockScan<int, kBfsThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  int na = *n0;
+  int* A = qa;
+  int* B = qb;
+  while (na > 0) {
+    for (int i = threadIdx.x; i < na; i += blockDim.x) {
+      const int p = A[i];
+      const int u = p % w, v = p / w;
+      for (int j = 0; j < 8; ++j) {
+        const int nu = u + c_du[j], nv = v + c_dv[j];
+        if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+        const int q = nv * w + nu;
+        if (labels[q] == 0) atomicMin(&claim[q], i * 8 + j);
+      }
+    }
+    __syncthreads();
+    int nb = 0;
+    for (int c0 = 0; c0 < na; c0 += blockDim.x) {
+      const int i = c0 + threadIdx.x;
+      int mine = 0;
+      unsigned won = 0;
+      int p = 0;
+      if (i < na) {
+        p = A[i];
+        const int u = p % w, v = p / w;
+        for (int j = 0; j < 8; ++j) {
+          const int nu = u + c_du[j], nv = v + c_dv[j];
+          if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+          const int q = nv * w + nu;
+          if (claim[q] == i * 8 + j) {
+            won |= 1u << j;
+            ++mine;
+          }
+        }
+      }
+      int off, tot;
+      Scan(tmp).ExclusiveSum(mine, off, tot);
+      if (won) {
+        const int lab = labels[p];
+        const int u = p % w, v = p / w;
+        int o = nb + off;
+        for (int j = 0; j < 8; ++j) {
+          if (!(won >> j & 1u)) continue;
+          const int q = (v + c_dv[j]) * w + (u + c_du[j]);
+          labels[q] = lab;
+          B[o++] = q;
+        }
+      }
+      nb += tot;
+      __syncthreads();
+    }
+    na = nb;
+    int* t = A;
+    A = B;
+    B = t;
+    __syncthreads();
+  }
+}
+
+// First appearance of each label in scan order (:218-224).
+__global__ void k_label_minidx(const int32_t* __restrict__ labels, long long n,
+                               int* __restrict__ minidx) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x)
+    atomicMin(&minidx[labels[p]], int(p));
+}
+
+__global__ void k_first_flags(const int32_t* __restrict__ labels, const int* __restrict__ minidx,
+                              long long n, int* __restrict__ flags) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x)
+    flags[p] = minidx[labels[p]] == int(p) ? 1 : 0;
+}
+
+__global__ void k_relabel(int32_t* __restrict__ labels, const int* __restrict__ minidx,
+                          const int* __restrict__ rank, long long n) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x)
+    labels[p] = rank[minidx[labels[p]]] + 1;
+}
+
+__global__ void k_count_from_scan(const int* __restrict__ flags, const int* __restrict__ pos,
+                                  long long n, int* __restrict__ count) {
+  *count = pos[n - 1] + flags[n - 1];
+}
+
+__global__ void k_fill_int(int* p, int v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_centers_out(Centers c, const CenterSums s, const int* __restrict__ count,
+                              int K, double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  if (k < *count) {
+    out[3 * k] = c.cu[k];
+    out[3 * k + 1] = c.cv[k];
+    out[3 * k + 2] = c.val[k];
+  }
+}
+
+// pool_superpixels tail: D3(p) = float(sum / n) of its label or invalid.
+__global__ void k_pool_write(const int32_t* __restrict__ labels, CenterSums s, long long n,
+                             int max_label, float* __restrict__ d3) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int l = labels[p];
+    float r = kInvalid;
+    if (l >= 0 && l <= max_label) {
+      const int c = s.n[l];
+      if (c > 0) r = float(fixed_to_double(s.sx[l]) / double(c));
+    }
+    d3[p] = r;
+  }
+}
+
+}  // namespace
+
+static void scan_flags(rpd_ctx* ctx, const int* flags, int* pos, long long n, const char* tag) {
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flags, pos, int(n), ctx->stream);
+  void* tmp = ctx->ws.get<uint8_t>(std::string("cub_scan_") + tag, tmp_bytes);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flags, pos, int(n), ctx->stream);
+  RPD_LAUNCH_CHECK();
+}
+
+SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, int iterations) {
+  if (p < 4) throw InvalidArg("slic: p must be >= 4");
+  if ((long long)p > (long long)w * h) throw InvalidArg("slic: p exceeds pixel count");
+  cudaStream_t st = ctx->stream;
+  const long long n = (long long)h * w;
+  const int gblocks = int(std::max<long long>(1, std::min<long long>((n + 255) / 256,
+                                                                      ctx->sm_count * 16)));
+  const dim3 rowgrid(cdiv(w, 128), h);
+  // host-side scalars exactly as segmentation.cpp:178-186 (glibc on the host)
+  const double S = std::sqrt(double(w) * h / p);
+  const int nu = std::max(1, int(std::lround(std::sqrt(double(p) * w / h))));
+  const int nv = std::max(1, int(std::lround(double(p) / nu)));
+  const int K = nu * nv;
+  const double su = double(w) / nu, sv = double(h) / nv;
+  const int win = int(std::ceil(S));
+  const double sw = m * m / (S * S);
+  int B = std::max(win, 1);
+  while ((long long)cdiv(w, B) * cdiv(h, B) > kMaxBuckets) B *= 2;
+  const int nbx = cdiv(w, B), nby = cdiv(h, B);
+
+  float* vals = ctx->ws.get<float>("slic_vals", n);
+  int32_t* labels = ctx->ws.get<int32_t>("slic_labels", n);
+  Centers c{ctx->ws.get<double>("slic_cu", K), ctx->ws.get<double>("slic_cv", K),
+            ctx->ws.get<double>("slic_val", K), ctx->ws.get<int>("slic_icu", K),
+            ctx->ws.get<int>("slic_icv", K)};
+  CenterSums s{ctx->ws.get<int>("slic_n", K + 1), ctx->ws.get<long long>("slic_su", K + 1),
+               ctx->ws.get<long long>("slic_sv", K + 1), ctx->ws.get<Acc128>("slic_sx", K + 1)};
+  int* cell_start = ctx->ws.get<int>("slic_cell_start", nbx * nby + 1);
+  int* cell_items = ctx->ws.get<int>("slic_cell_items", K);
+  int* orphan_list = ctx->ws.get<int>("slic_orphans", n);
+  int* orphan_count = ctx->ws.get<int>("slic_orphan_count", 2);
+  int* inexact = orphan_count + 1;
+
+  k_values_or_zero<<<gblocks, 256, 0, st>>>(d2, n, vals);
+  RPD_LAUNCH_CHECK();
+  k_seeds<<<cdiv(K, 128), 128, 0, st>>>(vals, h, w, nu, nv, su, sv, c);
+  RPD_LAUNCH_CHECK();
+  k_zero_sums<<<cdiv(K + 1, 256), 256, 0, st>>>(s, K + 1);
+  RPD_LAUNCH_CHECK();
+  RPD_CK(cudaMemsetAsync(orphan_count, 0, 2 * sizeof(int), st));
+
+  AssignArgs aa{vals, h, w, c, cell_start, cell_items, B, nbx, nby, win, sw, labels,
+                orphan_list, orphan_count};
+  auto assign = [&]() {
+    k_buckets<<<1, kBucketThreads, 0, st>>>(c, K, w, h, B, nbx, nby, cell_start, cell_items);
+    RPD_LAUNCH_CHECK();
+    RPD_CK(cudaMemsetAsync(orphan_count, 0, sizeof(int), st));
+    k_assign<<<rowgrid, 128, 0, st>>>(aa);
+    RPD_LAUNCH_CHECK();
+    k_assign_fallback<<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
+                                                         orphan_count);
+    RPD_LAUNCH_CHECK();
+  };
+  auto update = [&]() {
+    k_label_sums<<<gblocks, 256, 0, st>>>(vals, labels, h, w, K, false, true, s, inexact);
+    RPD_LAUNCH_CHECK();
+    k_center_finalize<<<cdiv(K, 256), 256, 0, st>>>(s, c, K);
+    RPD_LAUNCH_CHECK();
+  };
+  assign();
+  for (int it = 0; it < iterations; ++it) {
+    update();
+    assign();
+  }
+
+  // enforce_connectivity
+  int* parent = ctx->ws.get<int>("slic_parent", n);
+  int* psize = ctx->ws.get<int>("slic_psize", n);
+  unsigned long long* best = ctx->ws.get<unsigned long long>("slic_best", K + 1);
+  int* claim = ctx->ws.get<int>("slic_claim", n);
+  int* flags = ctx->ws.get<int>("slic_flags", n);
+  int* pos = ctx->ws.get<int>("slic_pos", n);
+  int* qa = ctx->ws.get<int>("slic_qa", n);
+  int* qb = ctx->ws.get<int>("slic_qb", n);
+  int* n0 = ctx->ws.get<int>("slic_n0", 1);
+  uf_label(SameLabel{labels}, h, w, 1, parent, ctx->sm_count, st);
+  RPD_CK(cudaMemsetAsync(psize, 0, sizeof(int) * n, st));
+  RPD_CK(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * (K + 1), st));
+  k_piece_sizes<<<gblocks, 256, 0, st>>>(parent, n, psize);
+  RPD_LAUNCH_CHECK();
+  k_main_piece<<<gblocks, 256, 0, st>>>(parent, labels, psize, n, best);
+  RPD_LAUNCH_CHECK();
+  k_orphans<<<gblocks, 256, 0, st>>>(parent, labels, best, n, claim);
+  RPD_LAUNCH_CHECK();
+  k_frontier_flags<<<rowgrid, 128, 0, st>>>(labels, h, w, flags);
+  RPD_LAUNCH_CHECK();
+  scan_flags(ctx, flags, pos, n, "front");
+  k_scatter_flagged<<<gblocks, 256, 0, st>>>(flags, pos, n, qa, n0);
+  RPD_LAUNCH_CHECK();
+  k_bfs<<<1, kBfsThreads, 0, st>>>(labels, h, w, claim, qa, qb, n0);
+  RPD_LAUNCH_CHECK();
+
+  // compaction by first appearance
+  int* minidx = ctx->ws.get<int>("slic_minidx", K + 1);
+  int* count = ctx->ws.get<int>("slic_count", 1);
+  k_fill_int<<<cdiv(K + 1, 256), 256, 0, st>>>(minidx, 0x7FFFFFFF, K + 1);
+  RPD_LAUNCH_CHECK();
+  k_label_minidx<<<gblocks, 256, 0, st>>>(labels, n, minidx);
+  RPD_LAUNCH_CHECK();
+  k_first_flags<<<gblocks, 256, 0, st>>>(labels, minidx, n, flags);
+  RPD_LAUNCH_CHECK();
+  scan_flags(ctx, flags, pos, n, "first");
+  k_count_from_scan<<<1, 1, 0, st>>>(flags, pos, n, count);
+  RPD_LAUNCH_CHECK();
+  k_relabel<<<gblocks, 256, 0, st>>>(labels, minidx, pos, n);
+  RPD_LAUNCH_CHECK();
+  // final update_centers over the compacted labels (centres start at zero)
+  RPD_CK(cudaMemsetAsync(c.cu, 0, sizeof(double) * K, st));
+  RPD_CK(cudaMemsetAsync(c.cv, 0, sizeof(double) * K, st));
+  RPD_CK(cudaMemsetAsync(c.val, 0, sizeof(double) * K, st));
+  update();
+  double* cout = ctx->ws.get<double>("slic_centers_out", 3 * size_t(K));
+  k_centers_out<<<cdiv(K, 128), 128, 0, st>>>(c, s, count, K, cout);
+  RPD_LAUNCH_CHECK();
+  SlicOut out;
+  out.labels = labels;
+  out.centers = cout;
+  out.count = count;
+  out.spacing = S;
+  out.k_seeds = K;
+  (void)kDU;
+  (void)kDV;
+  return out;
+}
+
+void pool_superpixels_dev(rpd_ctx* ctx, const float* d2, const int32_t* labels, int h, int w,
+                          int max_count, float* d3) {
+  cudaStream_t st = ctx->stream;
+  const long long n = (long long)h * w;
+  const int gblocks = int(std::max<long long>(1, std::min<long long>((n + 255) / 256,
+                                                                      ctx->sm_count * 16)));
+  CenterSums s{ctx->ws.get<int>("pool_n", max_count + 1), nullptr, nullptr,
+               ctx->ws.get<Acc128>("pool_sx", max_count + 1)};
+  int* inexact = ctx->ws.get<int>("pool_inexact", 1);
+  RPD_CK(cudaMemsetAsync(s.n, 0, sizeof(int) * (max_count + 1), st));
+  RPD_CK(cudaMemsetAsync(s.sx, 0, sizeof(Acc128) * (max_count + 1), st));
+  k_label_sums<<<gblocks, 256, 0, st>>>(d2, labels, h, w, max_count, true, false, s, inexact);
+  RPD_LAUNCH_CHECK();
+  k_pool_write<<<gblocks, 256, 0, st>>>(labels, s, n, max_count, d3);
+  RPD_LAUNCH_CHECK();
+}
+
+}  // namespace rpdg
