@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""bench.py — stereo pothole detection (arxiv 2012.10802 pipeline) on B200.
+
+Workload: BASELINE.json configs[1] ("cfg2"): one 800x1312 uint8 stereo pair,
+D=128 (d_max=127, bootstrap L=65 at half resolution, PT pass L=17), 8 SGM
+paths, P1=10, P2=120, SLIC p=2000.  Seeded synthetic scene (the paper's
+datasets are not available; paper_2012_10802_b200/synth.py).
+
+A step = one full detect_potholes_pipeline (pipeline.cpp:47-109) on one pair:
+bootstrap SGM, road fit, PT SGM, road refit, DT, SLIC + pooling, threshold,
+labelling.  N GPUs = N independent ranks (frames are independent; weak
+scaling, no collective on the data path).
+
+  value  frames/s with the pair resident in HBM; device time per step from
+         CUDA events on the library's stream; L2 flushed (256 MiB write)
+         between steps outside the timed events; max over ranks.
+  e2e    frames/s through the C-ABI call rpd_detect_u8 with pinned HOST
+         buffers: H2D of the pair, the pipeline, D2H of labels + d1 + d2.
+  roofline  the SGM path-aggregation kernel (dominant): SURVEY.md §8(d)
+         algorithmic bytes 2*(5P-2)*cells per launch / its CUDA-event time.
+  cpu_baseline  the CPU oracle (scalar restatement of the reference) on all
+         host cores, one frame per thread.
+
+`--impl reference` times that CPU path alone and prints the same JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "stereo frames/s end-to-end and SGM GDE/s at 1/2/4/8 B200 vs CPU oracle"
+ORACLE_LIB = ROOT / "oracle" / "_build" / "librpd_oracle.so"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, help="BASELINE config index (1-5)")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="0 = all host cores")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def gde_per_frame(h, w, cfg):
+    """Sum over passes of H_p * W_p * L_p."""
+    if h >= 64 and w >= 64:
+        boot = (h // 2) * (w // 2) * ((cfg.d_max + 1) // 2 + 1)
+    else:
+        boot = h * w * (cfg.d_max + 1)
+    return boot + h * w * (cfg.d_max_pt + 1)
+
+
+# ----------------------------------------------------------- clock sampling --
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU oracle --
+def cpu_oracle_run(scene, cfg_fields, threads, frames_per_thread=1):
+    """Oracle detect on `threads` host threads, one frame each; returns
+    (frames/s, wall s, frames)."""
+    from paper_2012_10802_b200.api import Library
+    lib = Library(str(ORACLE_LIB))
+    ctxs = [lib.context() for _ in range(threads)]
+    cfg = lib.default_config(**cfg_fields)
+    errors = []
+
+    def work(c):
+        try:
+            for _ in range(frames_per_thread):
+                c.detect(scene.left, scene.right, cfg, want=("labels",))
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    ts = [threading.Thread(target=work, args=(c,)) for c in ctxs]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    if errors:
+        raise errors[0]
+    frames = threads * frames_per_thread
+    return frames / dt, dt, frames
+
+
+def cpu_threads(args):
+    return args.cpu_threads or (os.cpu_count() or 1)
+
+
+# ---------------------------------------------------------------- GPU arm ---
+def gpu_arm(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_2012_10802_b200 as pkg
+    from paper_2012_10802_b200.api import Center, DetectOut
+    from paper_2012_10802_b200.synth import PIPELINE, SHAPES, make_scene, pipeline_config
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    lib = pkg.load_library()
+    ctx = lib.context(local)
+    c = args.config
+    h, w = SHAPES[c]
+    scene = make_scene(c, 0)  # replicas of the config's pair on every rank
+    cfg = pipeline_config(lib, c)
+    gde = gde_per_frame(h, w, cfg)
+
+    # ---- device-resident value
+    left_d = torch.from_numpy(scene.left).cuda()
+    right_d = torch.from_numpy(scene.right).cuda()
+    ctx.set_profiling(True)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        ctx.detect_async_u8(left_d.data_ptr(), right_d.data_ptr(), h, w, cfg)
+        ctx.fetch()
+    kernels = ctx.stats().kernels_last_frame
+    clocks = Clocks(local)
+    barrier()
+    clocks.start()
+    step_ms, agg_ms, agg_bytes, sgm_ms, npot = [], [], [], [], []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush, ordered before the step, outside the events
+        e0.record(stream)
+        ctx.detect_async_u8(left_d.data_ptr(), right_d.data_ptr(), h, w, cfg)
+        e1.record(stream)
+        out = ctx.fetch()  # waits + checks the device status (not timed)
+        step_ms.append(e0.elapsed_time(e1))
+        st = ctx.stats()
+        agg_ms.append(sum(st.sgm_agg_ms[i] for i in range(st.sgm_passes)))
+        agg_bytes.append(sum(st.sgm_agg_alg_bytes[i] for i in range(st.sgm_passes)))
+        sgm_ms.append(out.stage_ms[0] + out.stage_ms[2])
+        npot.append(out.n_potholes)
+    barrier()
+    clk = clocks.stop()
+    total_ms = allmax(sum(step_ms))
+    value = world * args.steps / (total_ms / 1e3)
+    sgm_total_ms = allmax(sum(sgm_ms))
+    sgm_gdes = world * args.steps * gde / (sgm_total_ms / 1e3) / 1e9
+
+    # ---- e2e through the C-ABI with pinned host buffers
+    n = h * w
+    lh = torch.from_numpy(scene.left).pin_memory()
+    rh = torch.from_numpy(scene.right).pin_memory()
+    labels_h = torch.empty(n, dtype=torch.int32).pin_memory()
+    d1_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    d2_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    o = DetectOut()
+    o.labels = C.cast(labels_h.data_ptr(), C.POINTER(C.c_int32))
+    o.d1 = C.cast(d1_h.data_ptr(), C.POINTER(C.c_float))
+    o.d2 = C.cast(d2_h.data_ptr(), C.POINTER(C.c_float))
+    ctx.set_profiling(False)
+    for _ in range(max(1, args.warmup)):
+        ctx.detect_raw(lh.data_ptr(), rh.data_ptr(), h, w, cfg, o)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.detect_raw(lh.data_ptr(), rh.data_ptr(), h, w, cfg, o)
+    e2e_s = allmax(time.perf_counter() - t0)
+    barrier()
+    e2e = world * args.steps / e2e_s
+
+    # ---- roofline of the aggregation kernel
+    pk = peaks()
+    peak = pk.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    achieved = (sum(agg_bytes) / 1e9) / (sum(agg_ms) / 1e3)
+    traffic = None
+    tf = ROOT / "profiles" / "agg_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    result = {
+        "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8/u16 (SGM), f32/f64 (fit, SLIC)",
+        "data": "synthetic (seeded BASELINE cfg%d scene, synth.py; paper datasets unavailable)" % c,
+        "config": {"workload": "cfg%d: %dx%d uint8 pair, D=%d, P=%d, P1=%g, P2=%g, SLIC p=%d" % (
+            c, h, w, cfg.d_max + 1, cfg.sgm_paths, cfg.lambda1, cfg.lambda2, cfg.superpixels),
+            "frames_per_step_per_gpu": 1, "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": "frame replicas per GPU, no collective"},
+        "sgm_gdes": round(sgm_gdes, 3),
+        "gde_per_frame": gde,
+        "stage_ms": {k: round(v, 4) for k, v in zip(
+            ("sgm_bootstrap", "road_fit", "sgm_pt", "road_refit", "disparity_transform",
+             "slic", "detect"), list(out.stage_ms))},
+        "n_potholes": npot[-1] if npot else None,
+        "e2e": {"value": round(e2e, 3), "unit": "frames/s", "h2d_bytes_per_step": 2 * n,
+                "d2h_bytes_per_step": 12 * n},
+        "gpu_launches": kernels * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_aggregate (SGM path aggregation, 2P paths)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": peak_src,
+                     "agg_ms_per_frame": round(sum(agg_ms) / len(agg_ms), 4),
+                     "alg_bytes_per_frame": agg_bytes[0] if agg_bytes else None,
+                     "note": "achieved = SURVEY §8(d) algorithmic bytes / event time; the "
+                             "kernel moves ~1/3 of them (u8 per-path outputs, no u16 sums)"},
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        thr = cpu_threads(args)
+        fps, dt, frames = cpu_oracle_run(scene, PIPELINE[c] | {}, thr)
+        result["cpu_baseline"] = {"value": round(fps, 4), "unit": "frames/s", "cores": thr,
+                                  "kind": "port",
+                                  "sample": f"{frames} cfg{c} frames, one per thread "
+                                            f"({dt:.1f} s wall)"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------- reference arm ---
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2012_10802_b200.synth import PIPELINE, SHAPES, make_scene
+    c = args.config
+    h, w = SHAPES[c]
+    scene = make_scene(c, 0)
+    thr = cpu_threads(args)
+    for _ in range(args.warmup):
+        cpu_oracle_run(scene, PIPELINE[c], thr)
+    tot_frames, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        _, dt, frames = cpu_oracle_run(scene, PIPELINE[c], thr)
+        tot_frames += frames
+        tot_s += dt
+    fps = tot_frames / tot_s
+
+    class _Cfg:
+        pass
+    cfg = _Cfg()
+    cfg.d_max = PIPELINE[c]["d_max"]
+    cfg.d_max_pt = PIPELINE[c].get("d_max_pt", 16)
+    result = {
+        "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot_s / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (reference arithmetic)",
+        "data": "synthetic (seeded BASELINE cfg%d scene)" % c,
+        "config": {"workload": "cfg%d: %dx%d uint8 pair, D=%d, P=%d" % (
+            c, h, w, PIPELINE[c]["d_max"] + 1, PIPELINE[c]["sgm_paths"]),
+            "implementation": "CPU oracle restatement of the reference (reference build "
+                              "impossible: Eigen3/libpng absent)"},
+        "sgm_gdes": None,
+        "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": thr, "kind": "port",
+                         "sample": f"per step {thr} cfg{c} frames, one per host thread"},
+        "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(result), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = env_rank()
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        gpu_arm(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -181,6 +181,22 @@ rpd_status rpd_detect_async_u8(rpd_ctx* ctx, const uint8_t* d_left, const uint8_
                                int h, int w, const rpd_config* cfg);
 rpd_status rpd_detect_fetch(rpd_ctx* ctx, rpd_detect_out* out);
 
+/* Measurement extension.  With profiling enabled, CUDA events are recorded on
+ * the context stream around every SGM path-aggregation launch (the dominant
+ * kernel); rpd_ctx_stats reports them for the last frame together with the
+ * SURVEY §8(d) algorithmic bytes of each launch and the kernel count of the
+ * last frame's captured graph. */
+typedef struct rpd_stats {
+  int32_t kernels_last_frame;   /* kernel launches of one rpd_detect* frame */
+  int32_t graph_replayed;       /* 1 if the last frame replayed a captured graph */
+  int32_t sgm_passes;           /* aggregation launches recorded (<= 2) */
+  double sgm_agg_ms[2];         /* device duration of each aggregation launch */
+  double sgm_agg_alg_bytes[2];  /* 2*(5P-2)*cells: u8 cost read + u16 sum read/write */
+  double sgm_cells[2];          /* H*W*L of the pass */
+} rpd_stats;
+rpd_status rpd_ctx_set_profiling(rpd_ctx* ctx, int enable);
+rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out);
+
 /* Parity extension: runs the production match_pair SGM path and materialises
  * its intermediates in the reference float layout (v*W+u)*(d_max+1)+d:
  * census_cost_volume, aggregate_costs of it and of swap_reference(it), and the

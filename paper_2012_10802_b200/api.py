@@ -232,10 +232,18 @@ _SIGS = {
                                       C.POINTER(Threshold), C.c_int, C.c_int, C.c_int, _vp]),
 }
 
-_EXT_SIGS = {  # extensions of the product library (streaming)
+class Stats(C.Structure):
+    _fields_ = [("kernels_last_frame", C.c_int32), ("graph_replayed", C.c_int32),
+                ("sgm_passes", C.c_int32), ("sgm_agg_ms", C.c_double * 2),
+                ("sgm_agg_alg_bytes", C.c_double * 2), ("sgm_cells", C.c_double * 2)]
+
+
+_EXT_SIGS = {  # extensions of the product library (streaming, measurement)
     "rpd_input_buffers_u8": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp), C.POINTER(_vp)]),
     "rpd_detect_async_u8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config)]),
     "rpd_detect_fetch": (C.c_int, [_vp, C.POINTER(DetectOut)]),
+    "rpd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "rpd_ctx_stats": (C.c_int, [_vp, C.POINTER(Stats)]),
 }
 _SIGS["rpd_match_pair_dump"] = (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
                                           C.POINTER(Config), C.c_int, _vp, _vp, _vp, _vp, _vp])
@@ -369,6 +377,37 @@ class Context:
             n_potholes=out.n_potholes,
             stage_ms={n: out.stage_ms[i] for i, n in enumerate(STAGE_NAMES)},
             total_ms=out.total_ms)
+
+    # ------------------------------------------- streaming / measurement --
+    def input_buffers_u8(self, h: int, w: int):
+        """Device pointers (ints) of the context's uint8 input buffers."""
+        l, r = _vp(), _vp()
+        self._check(self.dll.rpd_input_buffers_u8(self.handle, h, w, C.byref(l), C.byref(r)))
+        return l.value, r.value
+
+    def detect_async_u8(self, d_left: int, d_right: int, h: int, w: int, cfg: Config):
+        self._check(self.dll.rpd_detect_async_u8(self.handle, d_left, d_right, h, w,
+                                                 C.byref(cfg)))
+
+    def fetch(self, out: Optional[DetectOut] = None) -> DetectOut:
+        out = out if out is not None else DetectOut()
+        self._check(self.dll.rpd_detect_fetch(self.handle, C.byref(out)))
+        return out
+
+    def set_profiling(self, enable: bool):
+        self._check(self.dll.rpd_ctx_set_profiling(self.handle, 1 if enable else 0))
+
+    def stats(self) -> Stats:
+        s = Stats()
+        self._check(self.dll.rpd_ctx_stats(self.handle, C.byref(s)))
+        return s
+
+    def detect_raw(self, left_ptr: int, right_ptr: int, h: int, w: int, cfg: Config,
+                   out: DetectOut, u8: bool = True):
+        """rpd_detect(_u8) on raw host pointers (e.g. pinned buffers)."""
+        fn = self.dll.rpd_detect_u8 if u8 else self.dll.rpd_detect
+        self._check(fn(self.handle, left_ptr, right_ptr, h, w, C.byref(cfg), C.byref(out)))
+        return out
 
     # --------------------------------------------------------- perspective --
     def compute_row_shifts(self, model: RoadModel, width: int, height: int, delta_pt: float):

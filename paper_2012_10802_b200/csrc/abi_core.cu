@@ -31,6 +31,15 @@ static const char* status_message(int where) {
   }
 }
 
+void record_event(rpd_ctx* ctx, cudaEvent_t ev) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  RPD_CK(cudaStreamIsCapturing(ctx->stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    RPD_CK(cudaEventRecordWithFlags(ev, ctx->stream, cudaEventRecordExternal));
+  else
+    RPD_CK(cudaEventRecord(ev, ctx->stream));
+}
+
 void sync_and_check(rpd_ctx* ctx) {
   DevStatus h{};
   RPD_CK(cudaMemcpyAsync(&h, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
@@ -61,6 +70,7 @@ rpd_status rpd_ctx_create(int device, int, int, int, rpd_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&ctx->status, sizeof(DevStatus));
   if (e == cudaSuccess) e = cudaMemset(ctx->status, 0, sizeof(DevStatus));
   for (int i = 0; e == cudaSuccess && i <= RPD_NUM_STAGES; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreate(&ctx->agg_ev[i / 2][i % 2]);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount,
                                                    device);
   int major = 0;
@@ -86,6 +96,9 @@ void rpd_ctx_destroy(rpd_ctx* ctx) {
   ctx->ws.release();
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& pr : ctx->agg_ev)
+    for (auto& e : pr)
+      if (e) cudaEventDestroy(e);
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -94,6 +107,28 @@ void rpd_ctx_destroy(rpd_ctx* ctx) {
 const char* rpd_last_error(const rpd_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 void* rpd_ctx_stream(rpd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+rpd_status rpd_ctx_set_profiling(rpd_ctx* ctx, int enable) {
+  return guard(ctx, [&] { ctx->profile = enable != 0; });
+}
+
+rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out) {
+  return guard(ctx, [&] {
+    RPD_CK(cudaStreamSynchronize(ctx->stream));
+    rpd_stats s{};
+    s.kernels_last_frame = ctx->kernels_last_frame;
+    s.graph_replayed = ctx->graph_replayed;
+    s.sgm_passes = ctx->profile ? ctx->agg_pass : 0;
+    for (int i = 0; i < s.sgm_passes; ++i) {
+      float ms = 0;
+      RPD_CK(cudaEventElapsedTime(&ms, ctx->agg_ev[i][0], ctx->agg_ev[i][1]));
+      s.sgm_agg_ms[i] = ms;
+      s.sgm_agg_alg_bytes[i] = ctx->agg_alg_bytes[i];
+      s.sgm_cells[i] = ctx->agg_cells[i];
+    }
+    *out = s;
+  });
+}
 
 void rpd_config_default(rpd_config* cfg) {
   if (cfg) config_default(cfg);

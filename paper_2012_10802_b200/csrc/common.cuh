@@ -165,6 +165,14 @@ struct rpd_ctx {
   cudaEvent_t ev[RPD_NUM_STAGES + 1] = {};
   int sm_count = 148;
   void* pipeline = nullptr;  // rpdg::PipelineState (pipeline.cu)
+  // measurement (rpd_ctx_set_profiling / rpd_ctx_stats)
+  bool profile = false;
+  int agg_pass = 0;                       // aggregation launches recorded this frame
+  cudaEvent_t agg_ev[2][2] = {};          // [pass][start/end]
+  double agg_alg_bytes[2] = {0, 0};
+  double agg_cells[2] = {0, 0};
+  int kernels_last_frame = 0;
+  int graph_replayed = 0;
 };
 
 namespace rpdg {
@@ -175,5 +183,8 @@ void reset_status(rpd_ctx* ctx);
 void sync_and_check(rpd_ctx* ctx);
 DevModel host_model(const rpd_road_model& m);  // cos/sin on the host (glibc)
 void pipeline_forget(rpd_ctx* ctx);           // releases captured graphs
+// Records `ev` on ctx->stream; inside a stream capture it becomes an external
+// event-record node so the event is really recorded on every graph replay.
+void record_event(rpd_ctx* ctx, cudaEvent_t ev);
 
 }  // namespace rpdg

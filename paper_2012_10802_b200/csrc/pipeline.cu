@@ -50,7 +50,7 @@ struct FrameBuffers {
 };
 
 struct GraphKey {
-  int h, w, u8;
+  int h, w, u8, profile;
   rpd_config cfg;
   bool operator<(const GraphKey& o) const {
     return std::memcmp(this, &o, sizeof(GraphKey)) < 0;
@@ -60,6 +60,7 @@ struct GraphKey {
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   unsigned generation = 0;
+  int kernels = 0;
   FrameBuffers fb{};
 };
 
@@ -79,13 +80,20 @@ __global__ void k_flat_model(DevModel* m) { *m = DevModel{0.0, 0.0, 0.0, 1.0, 0.
 
 // Stage event: inside a stream capture it must become an external event-record
 // node (a plain record would only act as a capture-internal dependency).
-void record_stage(rpd_ctx* ctx, int i) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  RPD_CK(cudaStreamIsCapturing(ctx->stream, &cs));
-  if (cs == cudaStreamCaptureStatusActive)
-    RPD_CK(cudaEventRecordWithFlags(ctx->ev[i], ctx->stream, cudaEventRecordExternal));
-  else
-    RPD_CK(cudaEventRecord(ctx->ev[i], ctx->stream));
+void record_stage(rpd_ctx* ctx, int i) { record_event(ctx, ctx->ev[i]); }
+
+int count_kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  RPD_CK(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) RPD_CK(cudaGraphGetNodes(g, nodes.data(), &n));
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    RPD_CK(cudaGraphNodeGetType(nd, &t));
+    if (t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
 }
 
 FrameBuffers alloc_frame(rpd_ctx* ctx, int h, int w, int K) {
@@ -126,6 +134,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   cudaStream_t st = ctx->stream;
   const long long n = (long long)h * w;
   reset_status(ctx);
+  ctx->agg_pass = 0;
   record_stage(ctx, 0);
   if (u8) {
     launch_u8_to_f32(f.left8, f.left, n, st);
@@ -198,11 +207,14 @@ void run_frame(rpd_ctx* ctx, int h, int w, bool u8, const rpd_config& c, FrameBu
   key.h = h;
   key.w = w;
   key.u8 = u8 ? 1 : 0;
+  key.profile = ctx->profile ? 1 : 0;
   key.cfg = c;
   auto it = ps.graphs.find(key);
   if (it != ps.graphs.end() && it->second.exec && it->second.generation == ctx->ws.generation()) {
     RPD_CK(cudaGraphLaunch(it->second.exec, ctx->stream));
     out = it->second.fb;
+    ctx->graph_replayed = 1;
+    ctx->kernels_last_frame = it->second.kernels;
     return;
   }
   // eager run (allocates every workspace buffer)
@@ -210,6 +222,7 @@ void run_frame(rpd_ctx* ctx, int h, int w, bool u8, const rpd_config& c, FrameBu
   FrameBuffers f = alloc_frame(ctx, h, w, 0);
   enqueue_frame(ctx, f, h, w, u8, c);
   out = f;
+  ctx->graph_replayed = 0;
   if (ctx->ws.generation() != gen0) return;  // buffers moved: capture next time
   // capture for the next call with the same key
   cudaGraph_t g = nullptr;
@@ -227,6 +240,8 @@ void run_frame(rpd_ctx* ctx, int h, int w, bool u8, const rpd_config& c, FrameBu
     if (g) cudaGraphDestroy(g);
     return;
   }
+  const int kernels = count_kernel_nodes(g);
+  ctx->kernels_last_frame = kernels;
   cudaGraphExec_t exec = nullptr;
   if (cudaGraphInstantiate(&exec, g, 0) != cudaSuccess) {
     cudaGetLastError();
@@ -237,6 +252,7 @@ void run_frame(rpd_ctx* ctx, int h, int w, bool u8, const rpd_config& c, FrameBu
   GraphEntry& e = ps.graphs[key];
   if (e.exec) cudaGraphExecDestroy(e.exec);
   e.exec = exec;
+  e.kernels = kernels;
   e.generation = ctx->ws.generation();
   e.fb = fg;
 }

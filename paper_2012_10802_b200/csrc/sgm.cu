@@ -789,8 +789,18 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
       }
     // launch horizontal (longest) chains first: jobs are ordered as listed,
     // blocks are scheduled in index order.
+    const int pass = ctx->agg_pass;
+    const bool prof = ctx->profile && pass < 2;
+    if (prof) record_event(ctx, ctx->agg_ev[pass][0]);
     agg_kernel(L.wpl, L.G)<<<blocks, kAggThreads, 0, st>>>(args);
     RPD_LAUNCH_CHECK();
+    if (prof) {
+      record_event(ctx, ctx->agg_ev[pass][1]);
+      const double cells = double(npix) * levels;
+      ctx->agg_alg_bytes[pass] = 2.0 * (5.0 * paths - 2.0) * cells;
+      ctx->agg_cells[pass] = cells;
+      ctx->agg_pass = pass + 1;
+    }
     for (int vol = 0; vol < 2; ++vol) {
       WtaArgs wa{};
       for (int r = 0; r < paths; ++r) wa.path[r] = pathbuf + size_t(vol * paths + r) * npix * L.lw;
