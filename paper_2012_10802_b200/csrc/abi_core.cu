@@ -1,6 +1,7 @@
 // abi_core.cu — context lifecycle, config and the SGM / perspective entry
 // points of the C-ABI (include/rpd_b200.h).  Host buffers are copied to
 // context-owned device workspaces; all device work is ordered on ctx->stream.
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -9,6 +10,14 @@
 #include "sgm.cuh"
 
 namespace rpdg {
+
+bool rpd_sync_debug() {
+  static const bool on = [] {
+    const char* e = std::getenv("RPD_SYNC_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 void reset_status(rpd_ctx* ctx) {
   RPD_CK(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));

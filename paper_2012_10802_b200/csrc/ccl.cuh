@@ -47,42 +47,100 @@ struct SameMask {  // binary mask components
   __device__ bool same(int p, int q) const { return mask[q] != 0; }
 };
 
-template <typename Pred>
-__global__ void k_uf_init(Pred pr, int h, int w, int* __restrict__ parent) {
-  const long long n = (long long)h * w;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x)
-    parent[p] = pr.fg(int(p)) ? int(p) : -1;
+__global__ void k_uf_flatten(int h, int w, int* parent);
+
+// Block-based union-find: each 32x16 tile is labelled in shared memory
+// (local roots = minimum local index = minimum raster index inside the tile),
+// then only tile-border pixels union across tiles in global memory.
+constexpr int kTileW = 32, kTileH = 16;
+
+__device__ __forceinline__ int uf_find_s(const int* lab, int p) {
+  int q = lab[p];
+  while (q != p) {
+    p = q;
+    q = lab[p];
+  }
+  return p;
 }
 
-// Merge with the already-visited neighbours (left, up-left, up, up-right).
+__device__ __forceinline__ void uf_union_s(int* lab, int a, int b) {
+  while (true) {
+    a = uf_find_s(lab, a);
+    b = uf_find_s(lab, b);
+    if (a == b) return;
+    if (a < b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(&lab[a], b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
 template <typename Pred>
-__global__ void k_uf_merge(Pred pr, int h, int w, int conn8, int* parent) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
-  if (u >= w) return;
+__global__ void __launch_bounds__(kTileW* kTileH)
+    k_uf_local(Pred pr, int h, int w, int conn8, int* __restrict__ parent) {
+  __shared__ int lab[kTileW * kTileH];
+  const int tx = threadIdx.x % kTileW, ty = threadIdx.x / kTileW;
+  const int u0 = blockIdx.x * kTileW, v0 = blockIdx.y * kTileH;
+  const int u = u0 + tx, v = v0 + ty;
+  const bool in = u < w && v < h;
   const int p = v * w + u;
-  if (!pr.fg(p)) return;
-  if (u > 0 && pr.same(p, p - 1)) uf_union(parent, p, p - 1);
-  if (v > 0) {
-    const int up = p - w;
-    if (pr.same(p, up)) uf_union(parent, p, up);
-    if (conn8) {
-      if (u > 0 && pr.same(p, up - 1)) uf_union(parent, p, up - 1);
-      if (u + 1 < w && pr.same(p, up + 1)) uf_union(parent, p, up + 1);
+  const int i = threadIdx.x;
+  const bool fg = in && pr.fg(p);
+  lab[i] = fg ? i : -1;
+  __syncthreads();
+  if (fg) {
+    if (tx > 0 && u - 1 < w && pr.same(p, p - 1)) uf_union_s(lab, i, i - 1);
+    if (ty > 0) {
+      if (pr.same(p, p - w)) uf_union_s(lab, i, i - kTileW);
+      if (conn8) {
+        if (tx > 0 && pr.same(p, p - w - 1)) uf_union_s(lab, i, i - kTileW - 1);
+        if (tx + 1 < kTileW && u + 1 < w && pr.same(p, p - w + 1))
+          uf_union_s(lab, i, i - kTileW + 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (in) {
+    if (fg) {
+      const int r = uf_find_s(lab, i);
+      parent[p] = (v0 + r / kTileW) * w + (u0 + r % kTileW);
+    } else {
+      parent[p] = -1;
     }
   }
 }
 
-__global__ void k_uf_flatten(int h, int w, int* parent);
+template <typename Pred>
+__global__ void k_uf_border(Pred pr, int h, int w, int conn8, int* parent) {
+  const int tx = threadIdx.x % kTileW, ty = threadIdx.x / kTileW;
+  const int u = blockIdx.x * kTileW + tx, v = blockIdx.y * kTileH + ty;
+  if (u >= w || v >= h) return;
+  const bool left = tx == 0, top = ty == 0, right = tx == kTileW - 1;
+  if (!(left || top || right)) return;
+  const int p = v * w + u;
+  if (!pr.fg(p)) return;
+  if (left && u > 0 && pr.same(p, p - 1)) uf_union(parent, p, p - 1);
+  if (v > 0) {
+    if (top && pr.same(p, p - w)) uf_union(parent, p, p - w);
+    if (conn8) {
+      if ((top || left) && u > 0 && pr.same(p, p - w - 1)) uf_union(parent, p, p - w - 1);
+      if ((top || right) && u + 1 < w && pr.same(p, p - w + 1)) uf_union(parent, p, p - w + 1);
+    }
+  }
+}
 
 template <typename Pred>
 void uf_label(Pred pr, int h, int w, int conn8, int* parent, int sm_count, cudaStream_t st) {
   const long long n = (long long)h * w;
   const int blocks = int(std::min<long long>((n + 255) / 256, sm_count * 16));
-  k_uf_init<<<std::max(blocks, 1), 256, 0, st>>>(pr, h, w, parent);
+  const dim3 tiles(cdiv(w, kTileW), cdiv(h, kTileH));
+  k_uf_local<<<tiles, kTileW * kTileH, 0, st>>>(pr, h, w, conn8, parent);
   RPD_LAUNCH_CHECK();
-  k_uf_merge<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(pr, h, w, conn8, parent);
+  k_uf_border<<<tiles, kTileW * kTileH, 0, st>>>(pr, h, w, conn8, parent);
   RPD_LAUNCH_CHECK();
   k_uf_flatten<<<std::max(blocks, 1), 256, 0, st>>>(h, w, parent);
   RPD_LAUNCH_CHECK();

@@ -45,7 +45,19 @@ struct Capacity : std::runtime_error {
       throw ::rpdg::CudaFail(std::string(#x) + ": " + cudaGetErrorString(e_));       \
   } while (0)
 
-#define RPD_LAUNCH_CHECK() RPD_CK(cudaGetLastError())
+// RPD_SYNC_DEBUG=1 in the environment synchronises after every launch and
+// names the failing call site (debugging only; never set in timed runs).
+bool rpd_sync_debug();
+#define RPD_LAUNCH_CHECK()                                                                 \
+  do {                                                                                     \
+    RPD_CK(cudaGetLastError());                                                            \
+    if (::rpdg::rpd_sync_debug()) {                                                        \
+      cudaError_t e2_ = cudaDeviceSynchronize();                                           \
+      if (e2_ != cudaSuccess)                                                              \
+        throw ::rpdg::CudaFail(std::string(__FILE__) + ":" + std::to_string(__LINE__) + \
+                               ": " + cudaGetErrorString(e2_));                            \
+    }                                                                                      \
+  } while (0)
 
 constexpr float kInvalid = -1.0f;  // types.hpp:21
 

@@ -63,11 +63,34 @@ __global__ void k_hist_range(const float* __restrict__ d2, int h, int w,
   double x = 0, y = 0;
   const bool ok = u + 1 < w && v + 1 < h && hist_vector(d2, w, u, v, x, y);
   const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
-  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(reinterpret_cast<unsigned long long*>(&meta[1]),
-                                                (unsigned long long)__popc(bal));
-  if (ok) {
-    atomicMin(&meta[3], min(ordered(x), ordered(y)));
-    atomicMax(&meta[4], max(ordered(x), ordered(y)));
+  long long lo = ok ? min(ordered(x), ordered(y)) : 0x7FFFFFFFFFFFFFFFll;
+  long long hi = ok ? max(ordered(x), ordered(y)) : (long long)0x8000000000000000ull;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, off));
+    hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, off));
+  }
+  __shared__ long long s_lo[32], s_hi[32];
+  __shared__ unsigned long long s_cnt[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+    s_cnt[warp] = __popc(bal);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0;
+    for (int q = 0; q < int(blockDim.x >> 5); ++q) {
+      lo = min(lo, s_lo[q]);
+      hi = max(hi, s_hi[q]);
+      c += s_cnt[q];
+    }
+    if (c) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&meta[1]), c);
+      atomicMin(&meta[3], lo);
+      atomicMax(&meta[4], hi);
+    }
   }
 }
 

@@ -46,6 +46,7 @@ SgmLayout sgm_layout(int h, int w, int levels, int paths) {
     L.wpl = std::max(5, (levels + 4 * G - 1) / (4 * G));
   }
   L.lw = 4 * L.wpl * L.G;
+  L.pitch = size_t(round_up(w * L.lw, 16));  // TMA row strides must be 16-byte multiples
   return L;
 }
 
@@ -217,7 +218,7 @@ void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_v
 // C_R(v,u,d) = popc(cl(u+d) ^ cr(u))  if u+d <  W and in_view(u),   else maxc
 __global__ void k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
                           const uint8_t* __restrict__ iv, int h, int w, int levels, int nw,
-                          uint32_t maxc, uint32_t* __restrict__ vol_l,
+                          size_t pitch_words, uint32_t maxc, uint32_t* __restrict__ vol_l,
                           uint32_t* __restrict__ vol_r) {
   const long long n = (long long)h * w * nw;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -225,6 +226,7 @@ __global__ void k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __res
     const int j = int(i % nw);
     const long long p = i / nw;
     const int u = int(p % w);
+    const size_t o = size_t(p / w) * pitch_words + size_t(u) * nw + j;
     const uint64_t a = cl[p];
     const uint64_t b = cr[p];
     const bool ivu = iv[p] != 0;
@@ -240,20 +242,20 @@ __global__ void k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __res
       wl |= cL << (8 * q);
       wr |= cR << (8 * q);
     }
-    vol_l[i] = wl;
-    vol_r[i] = wr;
+    vol_l[o] = wl;
+    vol_r[o] = wr;
   }
 }
 
-// u8 volume (stride lw) -> float reference layout (parity dumps only).
-__global__ void k_u8vol_to_f32(const uint8_t* __restrict__ vol, long long npix, int lw, int levels,
-                               float* __restrict__ out) {
+// u8 volume (row pitch, pixel stride lw) -> float reference layout (parity dumps only).
+__global__ void k_u8vol_to_f32(const uint8_t* __restrict__ vol, int w, long long npix,
+                               size_t pitch, int lw, int levels, float* __restrict__ out) {
   const long long n = npix * levels;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const long long p = i / levels;
     const int d = int(i % levels);
-    out[i] = float(vol[p * lw + d]);
+    out[i] = float(vol[size_t(p / w) * pitch + size_t(p % w) * lw + d]);
   }
 }
 
@@ -269,6 +271,7 @@ struct AggArgs {
   AggJob job[16];
   int njobs;
   int h, w, lw;
+  size_t pitch;
   uint32_t p1x2, p2x2;
 };
 
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(kAggThreads)
   };
   const uint8_t* __restrict__ cost = J.cost + g * WPL * 4;
   uint8_t* __restrict__ out = J.out + g * WPL * 4;
-  auto offset = [&](const Cursor& c) { return (size_t(c.v) * w + c.u) * lw; };
+  auto offset = [&](const Cursor& c) { return size_t(c.v) * a.pitch + size_t(c.u) * lw; };
 
   uint32_t buf[D][WPL];
   Cursor pc = start();
@@ -453,6 +456,8 @@ struct WtaArgs {
   const uint8_t* path[8];
   int paths;
   long long npix;
+  int w;
+  size_t pitch;
   int lw, levels;
   float* disp;
   float* dump;  // optional S(d) in the reference float layout
@@ -477,6 +482,7 @@ __global__ void k_wta(const __grid_constant__ WtaArgs a) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= a.npix) return;
   const int nw = a.lw / 4;
+  const size_t base = size_t(p / a.w) * a.pitch + size_t(p % a.w) * a.lw;
   uint32_t minv = 0xFFFFFFFFu, last = 0, sbm1 = 0, sbp1 = 0;
   int best = -2, cnt = 0;
   for (int j = 0; j < nw; ++j) {
@@ -485,7 +491,7 @@ __global__ void k_wta(const __grid_constant__ WtaArgs a) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       if (r < a.paths) {
-        const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a.path[r] + p * a.lw) + j);
+        const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a.path[r] + base) + j);
         s01 += __byte_perm(x, 0u, 0x4140);
         s23 += __byte_perm(x, 0u, 0x4342);
       }
@@ -521,7 +527,7 @@ __global__ void k_wta(const __grid_constant__ WtaArgs a) {
 // best sample out of view (:216-222), restore_disparity (perspective.hpp:69-80).
 template <typename CostT>
 __global__ void k_post(const float* __restrict__ dl, const float* __restrict__ dr,
-                       const CostT* __restrict__ cost, int cstride,
+                       const CostT* __restrict__ cost, int cstride, size_t crow,
                        const uint8_t* __restrict__ iv, const double* __restrict__ shifts, int h,
                        int w, int levels, double thr, float* __restrict__ d0,
                        float* __restrict__ d1) {
@@ -529,6 +535,7 @@ __global__ void k_post(const float* __restrict__ dl, const float* __restrict__ d
   const int v = blockIdx.y;
   if (u >= w) return;
   const size_t i = size_t(v) * w + u;
+  const size_t coff = size_t(v) * crow + size_t(u) * cstride;  // element offset of the cost curve
   const size_t row = size_t(v) * w;
   float d = dl[i];
   if (d != kInvalid) {
@@ -542,7 +549,7 @@ __global__ void k_post(const float* __restrict__ dl, const float* __restrict__ d
   }
   if (d != kInvalid) {
     float lo = FLT_MAX, hi = -FLT_MAX;
-    const CostT* c = cost + i * size_t(cstride);
+    const CostT* c = cost + coff;
     for (int k = 0; k < levels; ++k) {
       const int ur = u - k;
       if (ur < 0) break;
@@ -749,51 +756,55 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     if (dump && dump->cost)
       RPD_CK(cudaMemcpyAsync(dump->cost, cost, sizeof(float) * npix * levels,
                              cudaMemcpyDeviceToDevice, st));
-    k_post<float><<<rowgrid, 128, 0, st>>>(dl, dr, cost, levels, iv, shifts, h, w, levels,
-                                           cfg.lr_threshold, d0, d1);
+    k_post<float><<<rowgrid, 128, 0, st>>>(dl, dr, cost, levels, size_t(w) * levels, iv, shifts,
+                                           h, w, levels, cfg.lr_threshold, d0, d1);
     RPD_LAUNCH_CHECK();
   } else {
     const SgmLayout L = sgm_layout(h, w, levels, paths);
     const int nw = L.lw / 4;
-    uint8_t* vol_l = ctx->ws.get<uint8_t>("mp_vol_l", size_t(npix) * L.lw);
-    uint8_t* vol_r = ctx->ws.get<uint8_t>("mp_vol_r", size_t(npix) * L.lw);
-    uint8_t* pathbuf = ctx->ws.get<uint8_t>("mp_paths", size_t(npix) * L.lw * 2 * paths);
+    const size_t vb = L.vol_bytes();
+    uint8_t* vol_l = ctx->ws.get<uint8_t>("mp_vols", 2 * vb);
+    uint8_t* vol_r = vol_l + vb;
+    uint8_t* pathbuf = ctx->ws.get<uint8_t>("mp_paths", vb * 2 * paths);
     {
       const long long n = npix * nw;
       const int blocks = int(std::min<long long>((n + 255) / 256, 148 * 32));
       k_cost_u8<<<std::max(blocks, 1), 256, 0, st>>>(
-          cl, cr, iv, h, w, levels, nw, uint32_t(window * window - 1),
+          cl, cr, iv, h, w, levels, nw, L.pitch / 4, uint32_t(window * window - 1),
           reinterpret_cast<uint32_t*>(vol_l), reinterpret_cast<uint32_t*>(vol_r));
       RPD_LAUNCH_CHECK();
     }
-    AggArgs args{};
-    args.h = h;
-    args.w = w;
-    args.lw = L.lw;
     const uint32_t p1 = uint32_t(l1), p2 = uint32_t(l2);
-    args.p1x2 = p1 | (p1 << 16);
-    args.p2x2 = p2 | (p2 << 16);
-    const int cpb = kAggThreads / L.G;
-    int blocks = 0;
-    for (int vol = 0; vol < 2; ++vol)
-      for (int r = 0; r < paths; ++r) {
-        AggJob& J = args.job[args.njobs];
-        J.cost = vol == 0 ? vol_l : vol_r;
-        J.out = pathbuf + size_t(vol * paths + r) * npix * L.lw;
-        J.du = dirs[2 * r];
-        J.dv = dirs[2 * r + 1];
-        J.nchains = (J.dv == 0) ? h : w;
-        J.block0 = blocks;
-        blocks += cdiv(J.nchains, cpb);
-        ++args.njobs;
-      }
-    // launch horizontal (longest) chains first: jobs are ordered as listed,
-    // blocks are scheduled in index order.
     const int pass = ctx->agg_pass;
     const bool prof = ctx->profile && pass < 2;
     if (prof) record_event(ctx, ctx->agg_ev[pass][0]);
-    agg_kernel(L.wpl, L.G)<<<blocks, kAggThreads, 0, st>>>(args);
-    RPD_LAUNCH_CHECK();
+    if (sgm_tma_supported(L)) {
+      launch_aggregate_tma(ctx, L, vol_l, pathbuf, dirs, paths, p1, p2);
+    } else {
+      AggArgs args{};
+      args.h = h;
+      args.w = w;
+      args.lw = L.lw;
+      args.pitch = L.pitch;
+      args.p1x2 = p1 | (p1 << 16);
+      args.p2x2 = p2 | (p2 << 16);
+      const int cpb = kAggThreads / L.G;
+      int blocks = 0;
+      for (int vol = 0; vol < 2; ++vol)
+        for (int r = 0; r < paths; ++r) {
+          AggJob& J = args.job[args.njobs];
+          J.cost = vol == 0 ? vol_l : vol_r;
+          J.out = pathbuf + size_t(vol * paths + r) * vb;
+          J.du = dirs[2 * r];
+          J.dv = dirs[2 * r + 1];
+          J.nchains = (J.dv == 0) ? h : w;
+          J.block0 = blocks;
+          blocks += cdiv(J.nchains, cpb);
+          ++args.njobs;
+        }
+      agg_kernel(L.wpl, L.G)<<<blocks, kAggThreads, 0, st>>>(args);
+      RPD_LAUNCH_CHECK();
+    }
     if (prof) {
       record_event(ctx, ctx->agg_ev[pass][1]);
       const double cells = double(npix) * levels;
@@ -803,9 +814,11 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     }
     for (int vol = 0; vol < 2; ++vol) {
       WtaArgs wa{};
-      for (int r = 0; r < paths; ++r) wa.path[r] = pathbuf + size_t(vol * paths + r) * npix * L.lw;
+      for (int r = 0; r < paths; ++r) wa.path[r] = pathbuf + size_t(vol * paths + r) * vb;
       wa.paths = paths;
       wa.npix = npix;
+      wa.w = w;
+      wa.pitch = L.pitch;
       wa.lw = L.lw;
       wa.levels = levels;
       wa.disp = vol == 0 ? dl : dr;
@@ -816,11 +829,11 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     if (dump && dump->cost) {
       const long long n = npix * levels;
       k_u8vol_to_f32<<<int(std::min<long long>((n + 255) / 256, 148 * 32)), 256, 0, st>>>(
-          vol_l, npix, L.lw, levels, dump->cost);
+          vol_l, w, npix, L.pitch, L.lw, levels, dump->cost);
       RPD_LAUNCH_CHECK();
     }
-    k_post<uint8_t><<<rowgrid, 128, 0, st>>>(dl, dr, vol_l, L.lw, iv, shifts, h, w, levels,
-                                             cfg.lr_threshold, d0, d1);
+    k_post<uint8_t><<<rowgrid, 128, 0, st>>>(dl, dr, vol_l, L.lw, L.pitch, iv, shifts, h, w,
+                                             levels, cfg.lr_threshold, d0, d1);
     RPD_LAUNCH_CHECK();
   }
   if (dump && dump->disp_left)

@@ -13,8 +13,17 @@ struct SgmLayout {
   int wpl = 1;      // u8 cost words per lane (4 levels per word)
   int lw = 4;       // bytes per pixel in the u8 volumes = 4*wpl*G >= L
   int paths = 8;    // P
+  size_t pitch = 0; // bytes per image row in the u8 volumes (16-byte multiple)
+  size_t vol_bytes() const { return pitch * size_t(h); }
 };
 SgmLayout sgm_layout(int h, int w, int levels, int paths);
+
+// TMA-staged aggregation of all 2P (volume, direction) chains of one pass
+// (sgm_tma.cu).  vol_lr: left- then right-reference u8 cost volumes;
+// paths: 2P per-path u8 output volumes, each vol_bytes() apart.
+bool sgm_tma_supported(const SgmLayout& L);
+void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uint8_t* paths,
+                          const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2);
 
 // Whether the integer u8/u16x2 path reproduces the reference's float
 // arithmetic bit-exactly for these penalties (integral lambdas and

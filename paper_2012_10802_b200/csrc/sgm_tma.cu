@@ -1,0 +1,516 @@
+// sgm_tma.cu — TMA-staged SGM path aggregation (aggregate_costs, sgm.cpp:70-110)
+// for sm_100a.
+//
+// One CTA owns NC = 32 scan chains of one (volume, direction) job; each chain
+// is handled by G lanes, each lane holding WPL u8-cost words (2*WPL packed
+// u16x2 level pairs) of the chain's current pixel in registers.  An elected
+// thread streams the raw cost tiles of the next R steps into a DEPTH-deep
+// shared-memory ring with cp.async.bulk.tensor (completion on mbarriers), and
+// writes the per-path u8 results back with TMA stores from a double-buffered
+// output tile, so the compute threads only touch shared memory.
+//
+// Chains: horizontal = image rows, vertical = columns, diagonal = the W+H-1
+// non-wrapping diagonals u = k + du*s; tiles that stick out of the image are
+// zero-filled by the TMA load and dropped by the TMA store.
+//
+// Recurrence per step (exact integers, sgm.cpp:95-104), per u16x2 pair:
+//   best = min(prev, prev[d-1]+P1, prev[d+1]+P1, min(prev)+P2)   (2x VIADDMNMX + VIMNMX)
+//   cur  = raw + best - min(prev)                                   (IADD3, no carry)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "sgm.cuh"
+
+namespace rpdg {
+
+namespace {
+
+constexpr int kNC = 32;      // chains per CTA
+constexpr int kDepth = 3;    // input ring depth (stages)
+constexpr uint32_t kInf2 = 0x7FFF7FFFu;
+
+enum JobType : int { kHoriz = 0, kVert = 1, kDiag = 2 };
+
+struct TmaJob {
+  int vol;      // 0 left-reference cost, 1 right-reference cost
+  int path;     // output buffer index
+  int du, dv;
+  int type;
+  int kmin;     // diagonal: first chain index (u = k + du*s)
+  int nchains;
+  int block0;
+};
+
+struct TmaArgs {
+  CUtensorMap cost_h, cost_vf, cost_vl, cost_df, cost_dl;
+  CUtensorMap path_h, path_vf, path_vl, path_df, path_dl;
+  TmaJob job[16];
+  int njobs;
+  int h, w;
+  uint32_t p1x2, p2x2;
+  uint8_t* path_base;  // diagonal jobs store directly
+  size_t pitch, vol_bytes;
+  int dbg;  // debugging early-exit level (RPD_TMA_DBG), 0 in production
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z,
+                                             const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(x), "r"(y), "r"(z), "r"(smem_addr(src))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void tma_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int NPL>
+__device__ __forceinline__ uint32_t min_pairs(const uint32_t (&x)[NPL]) {
+  uint32_t t[NPL];
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) t[k] = x[k];
+#pragma unroll
+  for (int width = 1; width < NPL; width *= 2)
+#pragma unroll
+    for (int i = 0; i + width < NPL; i += 2 * width) t[i] = __vminu2(t[i], t[i + width]);
+  return t[0];
+}
+
+// Compile-time tile geometry.
+template <int WPL, int G>
+struct Geo {
+  static constexpr int WPP = WPL * G;                  // words per pixel
+  static constexpr int R = WPP <= 32 ? 8 : (WPP <= 64 ? 4 : (WPP <= 128 ? 2 : 1));
+  static constexpr int ROW = kNC * WPP;                // words of one step (vert / diag)
+  static constexpr int CWF = ROW < 256 ? ROW : 256;    // full chunk width
+  static constexpr int NCH = (ROW + 255) / 256;        // chunks per row
+  static constexpr int CWL = ROW - (NCH - 1) * 256;    // last chunk width
+  static constexpr int STAGE = R * ROW;                // words per output stage
+  // Diagonal rows start at arbitrary columns but TMA box origins must be
+  // 16-byte aligned: each row is loaded from the aligned word below it with
+  // 32 extra words (keeps 128-byte aligned smem rows), read with a shift.
+  static constexpr int DROW = ROW + 32;
+  static constexpr int DNCH = (DROW + 255) / 256;
+  static constexpr int DCWL = DROW - (DNCH - 1) * 256;
+  static constexpr int STAGE_IN = R * DROW;            // words per input stage
+  static constexpr int THREADS = kNC * G;
+};
+
+// Word offset of (step r, chain t, word j of the pixel) inside a stage.
+// `shift` is the diagonal row's alignment shift (0 otherwise).
+template <int WPL, int G>
+__device__ __forceinline__ int stage_off(int type, int r, int t, int j, int shift = 0) {
+  using GE = Geo<WPL, G>;
+  if (type == kHoriz) return t * (GE::R * GE::WPP) + r * GE::WPP + j;
+  if (type == kDiag) {
+    const int wd = shift + t * GE::WPP + j;
+    if (GE::DNCH == 1) return r * GE::DROW + wd;
+    const int ch = wd >> 8, o = wd & 255;
+    const int cw = ch == GE::DNCH - 1 ? GE::DCWL : 256;
+    return ch * (256 * GE::R) + r * cw + o;
+  }
+  const int wd = t * GE::WPP + j;  // word inside the step's row
+  if (GE::NCH == 1) return r * GE::ROW + wd;
+  const int ch = wd >> 8, o = wd & 255;
+  const int cw = ch == GE::NCH - 1 ? GE::CWL : 256;
+  return ch * (256 * GE::R) + r * cw + o;
+}
+
+template <int WPL, int G>
+__global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
+    k_aggregate_tma(const __grid_constant__ TmaArgs a) {
+  using GE = Geo<WPL, G>;
+  constexpr int NPL = 2 * WPL;
+  constexpr int R = GE::R;
+  // TMA tensor copies need 128-byte aligned shared memory; the dynamic block
+  // is over-allocated by 1 KiB and aligned here.
+  extern __shared__ uint8_t dsmem_raw[];
+  uint32_t* smem = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) & ~uintptr_t(1023));
+  uint32_t* in_ring = smem;                                  // kDepth * STAGE_IN
+  uint32_t* out_ring = smem + kDepth * GE::STAGE_IN;         // 2 * STAGE
+  __shared__ __align__(8) uint64_t full[kDepth];
+
+  int jidx = 0;
+#pragma unroll 1
+  while (jidx + 1 < a.njobs && int(blockIdx.x) >= a.job[jidx + 1].block0) ++jidx;
+  const TmaJob& J = a.job[jidx];
+  const int type = J.type, du = J.du, dv = J.dv;
+  const int h = a.h, w = a.w;
+  const int cta = int(blockIdx.x) - J.block0;
+  const int t = int(threadIdx.x) / G;  // chain within CTA
+  const int g = int(threadIdx.x) % G;
+  const unsigned gmask =
+      G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+
+  // chain geometry
+  const int c0 = cta * kNC;                 // first chain (row / column / diagonal offset)
+  const int nsteps = type == kHoriz ? w : h;
+  // Steps are "virtual": horizontal / vertical tiles are aligned to multiples
+  // of R from the image origin so that no TMA store box starts at a negative
+  // coordinate (the hardware faults on those); a backward scan therefore
+  // begins at virtual step T - N.  Diagonals use real steps.
+  const bool backward = (type == kHoriz) ? du < 0 : dv < 0;
+  const int T = (nsteps + R - 1) / R * R;
+  int s_begin = (type != kDiag && backward) ? T - nsteps : 0;
+  int s_end = s_begin + nsteps;
+  int stage_base = 0;
+  int kbase = 0;
+  if (type == kDiag) {
+    kbase = J.kmin + c0;
+    // u = k + du*s in [0, w) for some k in [kbase, kbase+NC)
+    if (du > 0) {
+      s_begin = max(0, -(kbase + kNC - 1));
+      s_end = min(nsteps, w - kbase);
+    } else {
+      s_begin = max(0, kbase - (w - 1));
+      s_end = min(nsteps, kbase + kNC);
+    }
+    stage_base = s_begin;
+  }
+  const int nstage = s_end > stage_base ? (s_end - stage_base + R - 1) / R : 0;
+  const int zc = J.vol, zp = J.path;
+
+  const CUtensorMap* cm_a = type == kHoriz ? &a.cost_h : (type == kVert ? &a.cost_vf : &a.cost_df);
+  const CUtensorMap* cm_b = type == kVert ? &a.cost_vl : &a.cost_dl;
+  const CUtensorMap* pm_a = type == kHoriz ? &a.path_h : (type == kVert ? &a.path_vf : &a.path_df);
+  const CUtensorMap* pm_b = type == kVert ? &a.path_vl : &a.path_dl;
+
+  // Issue (load: true) or store (false) the TMA ops of stage `st` (global step s0).
+  auto tile_ops = [&](int st, bool load, uint32_t* buf, uint64_t* bar) {
+    const int s0 = stage_base + st * R;
+    if (type == kHoriz) {
+      // R columns x NC rows; backward chains walk the tile right to left
+      const int ucol = backward ? T - s0 - R : s0;
+      if (load)
+        tma_load_3d(buf, cm_a, ucol * GE::WPP, c0, zc, bar);
+      else
+        tma_store_3d(pm_a, ucol * GE::WPP, c0, zp, buf);
+    } else if (type == kVert) {
+      const int vrow = backward ? T - s0 - R : s0;
+#pragma unroll
+      for (int ch = 0; ch < GE::NCH; ++ch) {
+        const CUtensorMap* m = ch == GE::NCH - 1 ? (load ? cm_b : pm_b) : (load ? cm_a : pm_a);
+        uint32_t* dst = buf + ch * (256 * R);
+        const int x = c0 * GE::WPP + ch * 256;
+        if (load)
+          tma_load_3d(dst, m, x, vrow, zc, bar);
+        else
+          tma_store_3d(m, x, vrow, zp, dst);
+      }
+    } else if (load) {  // diagonal results are stored directly by the threads
+      for (int r = 0; r < R; ++r) {
+        const int s = s0 + r;
+        if (s >= s_end) break;
+        const int vrow = dv > 0 ? s : h - 1 - s;
+        const int x0 = ((kbase + du * s) * GE::WPP) & ~3;  // floor to a 16-byte boundary
+#pragma unroll
+        for (int ch = 0; ch < GE::DNCH; ++ch) {
+          const bool last = ch == GE::DNCH - 1;
+          uint32_t* p = buf + ch * (256 * R) + r * (last ? GE::DCWL : 256);
+          tma_load_3d(p, last ? cm_b : cm_a, x0 + ch * 256, vrow, zc, bar);
+        }
+      }
+    }
+  };
+  (void)pm_b;
+  auto stage_bytes = [&](int st) -> uint32_t {
+    if (type != kDiag) return uint32_t(GE::STAGE) * 4u;
+    const int s0 = stage_base + st * R;
+    const int rows = min(R, s_end - s0);
+    return uint32_t(rows) * uint32_t(GE::DROW) * 4u;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kDepth; ++i) mbar_init(&full[i], 1);
+    fence_async_smem();
+  }
+  __syncthreads();
+  if (a.dbg == 1) return;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kDepth && st < nstage; ++st) {
+      mbar_expect_tx(&full[st], stage_bytes(st));
+      if (a.dbg != 2) tile_ops(st, true, in_ring + st * GE::STAGE_IN, &full[st]);
+    }
+  }
+  if (a.dbg == 2) return;
+  if (a.dbg == 3) {
+    if (nstage > 0) mbar_wait(&full[0], 0);
+    return;
+  }
+
+  uint32_t prev[NPL];
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) prev[q] = kInf2;
+  uint32_t mnx2 = 0;
+
+  for (int st = 0; st < nstage; ++st) {
+    const int slot = st % kDepth;
+    mbar_wait(&full[slot], uint32_t(st / kDepth) & 1u);
+    const uint32_t* inb = in_ring + slot * GE::STAGE_IN;
+    uint32_t* outb = out_ring + (st & 1) * GE::STAGE;
+    const int s0 = stage_base + st * R;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int s = s0 + r;
+      if (s >= s_end) break;
+      if (s < s_begin) continue;  // padding steps of a backward scan's first tile
+      // position in the smem tile (backward scans walk the tile backwards)
+      const int rr = (type != kDiag && backward) ? R - 1 - r : r;
+      bool has_pred;
+      int du_col = 0, shift = 0;
+      if (type == kDiag) {
+        shift = ((kbase + du * s) * GE::WPP) & 3;
+        du_col = kbase + t + du * s;
+        has_pred = s > 0 && unsigned(du_col - du) < unsigned(w) && unsigned(du_col) < unsigned(w);
+      } else {
+        has_pred = s > s_begin;
+      }
+      uint32_t raw[NPL];
+#pragma unroll
+      for (int q = 0; q < WPL; ++q) {
+        const uint32_t x = inb[stage_off<WPL, G>(type, rr, t, g * WPL + q, shift)];
+        raw[2 * q] = __byte_perm(x, 0u, 0x4140);
+        raw[2 * q + 1] = __byte_perm(x, 0u, 0x4342);
+      }
+      uint32_t cur[NPL];
+      if (!has_pred) {
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) cur[q] = raw[q];
+      } else {
+        uint32_t lo_nb = kInf2, hi_nb = kInf2;
+        if (G > 1) {
+          const uint32_t up = __shfl_up_sync(gmask, prev[NPL - 1], 1, G);
+          const uint32_t dn = __shfl_down_sync(gmask, prev[0], 1, G);
+          if (g > 0) lo_nb = up;
+          if (g < G - 1) hi_nb = dn;
+        }
+        const uint32_t ceil2 = mnx2 + a.p2x2;
+        uint32_t qprev = __byte_perm(lo_nb, prev[0], 0x5432);
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+          const uint32_t nxt = (q + 1 < NPL) ? prev[q + 1] : hi_nb;
+          const uint32_t qn = __byte_perm(prev[q], nxt, 0x5432);
+          uint32_t tt = __viaddmin_u16x2(qprev, a.p1x2, prev[q]);
+          tt = __viaddmin_u16x2(qn, a.p1x2, tt);
+          tt = __vminu2(tt, ceil2);
+          cur[q] = raw[q] + tt - mnx2;
+          qprev = qn;
+        }
+      }
+      if (type == kDiag) {
+        if (unsigned(du_col) < unsigned(w)) {
+          const int vrow = dv > 0 ? s : h - 1 - s;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(
+              a.path_base + size_t(zp) * a.vol_bytes + size_t(vrow) * a.pitch +
+              size_t(du_col) * (GE::WPP * 4)) + g * WPL;
+#pragma unroll
+          for (int q = 0; q < WPL; ++q) dst[q] = __byte_perm(cur[2 * q], cur[2 * q + 1], 0x6420);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < WPL; ++q)
+          outb[stage_off<WPL, G>(type, rr, t, g * WPL + q)] =
+              __byte_perm(cur[2 * q], cur[2 * q + 1], 0x6420);
+      }
+      const uint32_t m2 = min_pairs<NPL>(cur);
+      uint32_t m = min(m2 & 0xFFFFu, m2 >> 16);
+      if (G > 1) {
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(gmask, m, off, G));
+      }
+      mnx2 = m * 0x10001u;
+#pragma unroll
+      for (int q = 0; q < NPL; ++q) prev[q] = cur[q];
+    }
+    fence_async_smem();  // make this thread's output-tile writes visible to the TMA store
+    __syncthreads();     // tile consumed, output tile written
+    if (threadIdx.x == 0) {
+      if (a.dbg != 4) tile_ops(st, false, outb, nullptr);
+      tma_commit();
+      if (st + kDepth < nstage) {
+        mbar_expect_tx(&full[slot], stage_bytes(st + kDepth));
+        tile_ops(st + kDepth, true, in_ring + slot * GE::STAGE_IN, &full[slot]);
+      }
+      tma_wait_read<1>();  // the other output buffer is free again
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tma_wait_all();
+}
+
+using TmaKernel = void (*)(TmaArgs);
+
+struct KernelInfo {
+  TmaKernel fn;
+  int smem;
+  int threads;
+  int R, wpp, row, cwf, cwl, nch, dcwf, dcwl;
+};
+
+template <int WPL, int G>
+KernelInfo info() {
+  using GE = Geo<WPL, G>;
+  return KernelInfo{k_aggregate_tma<WPL, G>,
+                    (kDepth * GE::STAGE_IN + 2 * GE::STAGE) * 4 + 1024,
+                    GE::THREADS, GE::R, GE::WPP, GE::ROW, GE::CWF, GE::CWL, GE::NCH,
+                    GE::DROW < 256 ? GE::DROW : 256, GE::DCWL};
+}
+
+KernelInfo pick(int wpl, int G) {
+#define RPD_TMA_CASE(W_, G_) \
+  if (wpl == W_ && G == G_) return info<W_, G_>();
+  RPD_TMA_CASE(1, 1) RPD_TMA_CASE(2, 1) RPD_TMA_CASE(3, 1) RPD_TMA_CASE(4, 1)
+  RPD_TMA_CASE(5, 1) RPD_TMA_CASE(6, 1) RPD_TMA_CASE(7, 1) RPD_TMA_CASE(8, 1)
+  RPD_TMA_CASE(9, 1)
+  RPD_TMA_CASE(5, 2) RPD_TMA_CASE(6, 2) RPD_TMA_CASE(7, 2) RPD_TMA_CASE(8, 2) RPD_TMA_CASE(9, 2)
+  RPD_TMA_CASE(5, 4) RPD_TMA_CASE(6, 4) RPD_TMA_CASE(7, 4) RPD_TMA_CASE(8, 4) RPD_TMA_CASE(9, 4)
+  RPD_TMA_CASE(5, 8) RPD_TMA_CASE(6, 8) RPD_TMA_CASE(7, 8) RPD_TMA_CASE(8, 8) RPD_TMA_CASE(9, 8)
+#undef RPD_TMA_CASE
+  throw InvalidArg("sgm: unsupported level layout for the TMA aggregation");
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RPD_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess)
+      throw CudaFail("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+CUtensorMap make_map(void* base, int words_per_row, int rows, int depth, size_t pitch,
+                     int box_x, int box_y) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {cuuint64_t(words_per_row), cuuint64_t(rows), cuuint64_t(depth)};
+  const cuuint64_t strides[2] = {cuuint64_t(pitch), cuuint64_t(pitch) * cuuint64_t(rows)};
+  const cuuint32_t box[3] = {cuuint32_t(box_x), cuuint32_t(box_y), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaFail("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+}  // namespace
+
+bool sgm_tma_supported(const SgmLayout& L) {
+  return L.G <= 8 && L.wpl >= 1 && L.wpl <= 9 && (L.G == 1 || L.wpl >= 5);
+}
+
+// Launches the aggregation of all 2P (volume, direction) jobs of one pass.
+void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uint8_t* paths,
+                          const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2) {
+  const KernelInfo ki = pick(L.wpl, L.G);
+  const int wpp = L.lw / 4;
+  const int words_row = L.w * wpp;
+  TmaArgs args{};
+  args.h = L.h;
+  args.w = L.w;
+  args.p1x2 = p1 | (p1 << 16);
+  args.p2x2 = p2 | (p2 << 16);
+  args.path_base = paths;
+  args.pitch = L.pitch;
+  args.vol_bytes = L.vol_bytes();
+  {
+    const char* e = std::getenv("RPD_TMA_DBG");
+    args.dbg = e ? std::atoi(e) : 0;
+  }
+  const int R = ki.R;
+  args.cost_h = make_map(vol_lr, words_row, L.h, 2, L.pitch, R * wpp, kNC);
+  args.cost_vf = make_map(vol_lr, words_row, L.h, 2, L.pitch, ki.cwf, R);
+  args.cost_vl = make_map(vol_lr, words_row, L.h, 2, L.pitch, ki.cwl, R);
+  args.cost_df = make_map(vol_lr, words_row, L.h, 2, L.pitch, ki.dcwf, 1);
+  args.cost_dl = make_map(vol_lr, words_row, L.h, 2, L.pitch, ki.dcwl, 1);
+  args.path_h = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, R * wpp, kNC);
+  args.path_vf = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwf, R);
+  args.path_vl = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwl, R);
+  args.path_df = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwf, 1);
+  args.path_dl = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwl, 1);
+  int blocks = 0;
+  const char* dbg = std::getenv("RPD_TMA_TYPES");  // debugging: bitmask of job types to run
+  const int type_mask = dbg ? std::atoi(dbg) : 7;
+  for (int vol = 0; vol < 2; ++vol)
+    for (int r = 0; r < paths_n; ++r) {
+      const int du = dirs[2 * r], dv = dirs[2 * r + 1];
+      const int ty = dv == 0 ? kHoriz : (du == 0 ? kVert : kDiag);
+      if (!((type_mask >> ty) & 1)) continue;
+      TmaJob& J = args.job[args.njobs++];
+      J.vol = vol;
+      J.path = vol * paths_n + r;
+      J.du = dirs[2 * r];
+      J.dv = dirs[2 * r + 1];
+      if (J.dv == 0) {
+        J.type = kHoriz;
+        J.nchains = L.h;
+      } else if (J.du == 0) {
+        J.type = kVert;
+        J.nchains = L.w;
+      } else {
+        J.type = kDiag;
+        J.nchains = L.w + L.h - 1;
+        J.kmin = J.du > 0 ? -(L.h - 1) : 0;
+      }
+      J.block0 = blocks;
+      blocks += cdiv(J.nchains, kNC);
+    }
+  RPD_CK(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ki.smem));
+  ki.fn<<<blocks, ki.threads, ki.smem, ctx->stream>>>(args);
+  RPD_LAUNCH_CHECK();
+}
+
+}  // namespace rpdg
