@@ -144,67 +144,99 @@ struct Geo {
   static constexpr int THREADS = kNC * G;
 };
 
-// Word offset of (step r, chain t, word j of the pixel) inside a stage.
-// `shift` is the diagonal row's alignment shift (0 otherwise).
-template <int WPL, int G>
-__device__ __forceinline__ int stage_off(int type, int r, int t, int j, int shift = 0) {
+// Shared-memory word offset of word q of this thread's pixel at tile row rr.
+// Everything except (rr, shift) is fixed per thread, so the callers hoist it.
+template <int TYPE, int WPL, int G>
+struct TileAddr {
   using GE = Geo<WPL, G>;
-  if (type == kHoriz) return t * (GE::R * GE::WPP) + r * GE::WPP + j;
-  if (type == kDiag) {
-    const int wd = shift + t * GE::WPP + j;
-    if (GE::DNCH == 1) return r * GE::DROW + wd;
-    const int ch = wd >> 8, o = wd & 255;
-    const int cw = ch == GE::DNCH - 1 ? GE::DCWL : 256;
-    return ch * (256 * GE::R) + r * cw + o;
+  int base[WPL];    // offset at rr = 0 (and shift = 0)
+  int stride[WPL];  // offset increment per tile row
+
+  __device__ __forceinline__ void init(int t, int g) {
+#pragma unroll
+    for (int q = 0; q < WPL; ++q) {
+      if (TYPE == kHoriz) {
+        base[q] = t * (GE::R * GE::WPP) + g * WPL + q;
+        stride[q] = GE::WPP;
+      } else if (TYPE == kVert) {
+        const int wd = t * GE::WPP + g * WPL + q;
+        if (GE::NCH == 1) {
+          base[q] = wd;
+          stride[q] = GE::ROW;
+        } else {
+          const int ch = wd >> 8;
+          base[q] = ch * (256 * GE::R) + (wd & 255);
+          stride[q] = ch == GE::NCH - 1 ? GE::CWL : 256;
+        }
+      } else {
+        base[q] = t * GE::WPP + g * WPL + q;  // + shift, chunked at use
+        stride[q] = GE::DROW;
+      }
+    }
   }
-  const int wd = t * GE::WPP + j;  // word inside the step's row
-  if (GE::NCH == 1) return r * GE::ROW + wd;
-  const int ch = wd >> 8, o = wd & 255;
-  const int cw = ch == GE::NCH - 1 ? GE::CWL : 256;
-  return ch * (256 * GE::R) + r * cw + o;
+  __device__ __forceinline__ int at(int q, int rr, int shift) const {
+    if (TYPE != kDiag || GE::DNCH == 1) return base[q] + shift + rr * stride[q];
+    const int wd = base[q] + shift;
+    const int ch = wd >> 8;
+    const int cw = ch == GE::DNCH - 1 ? GE::DCWL : 256;
+    return ch * (256 * GE::R) + rr * cw + (wd & 255);
+  }
+};
+
+template <int NP>
+__device__ __forceinline__ uint32_t min_pairs3(const uint32_t (&x)[NP]) {
+  // balanced tree of 3-input DPX mins
+  uint32_t t[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) t[k] = x[k];
+  int n = NP;
+#pragma unroll
+  for (int it = 0; it < 6; ++it) {
+    if (n <= 1) break;
+    int m = 0;
+#pragma unroll
+    for (int i = 0; i < NP; i += 3) {
+      if (i >= n) break;
+      if (i + 2 < n)
+        t[m] = __vimin3_u16x2(t[i], t[i + 1], t[i + 2]);
+      else if (i + 1 < n)
+        t[m] = __vminu2(t[i], t[i + 1]);
+      else
+        t[m] = t[i];
+      ++m;
+    }
+    n = m;
+  }
+  return t[0];
 }
 
-template <int WPL, int G>
-__global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
-    k_aggregate_tma(const __grid_constant__ TmaArgs a) {
+// One job type, fully specialised.  NPAIR <= 2*WPL level pairs are computed
+// per lane; a trailing all-padding pair (odd L with G == 1) is skipped.
+template <int TYPE, int WPL, int G, int NPAIR>
+__device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int cta,
+                                         uint32_t* in_ring, uint32_t* out_ring, uint64_t* full) {
   using GE = Geo<WPL, G>;
-  constexpr int NPL = 2 * WPL;
   constexpr int R = GE::R;
-  // TMA tensor copies need 128-byte aligned shared memory; the dynamic block
-  // is over-allocated by 1 KiB and aligned here.
-  extern __shared__ uint8_t dsmem_raw[];
-  uint32_t* smem = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) & ~uintptr_t(1023));
-  uint32_t* in_ring = smem;                                  // kDepth * STAGE_IN
-  uint32_t* out_ring = smem + kDepth * GE::STAGE_IN;         // 2 * STAGE
-  __shared__ __align__(8) uint64_t full[kDepth];
-
-  int jidx = 0;
-#pragma unroll 1
-  while (jidx + 1 < a.njobs && int(blockIdx.x) >= a.job[jidx + 1].block0) ++jidx;
-  const TmaJob& J = a.job[jidx];
-  const int type = J.type, du = J.du, dv = J.dv;
+  const int du = J.du, dv = J.dv;
   const int h = a.h, w = a.w;
-  const int cta = int(blockIdx.x) - J.block0;
   const int t = int(threadIdx.x) / G;  // chain within CTA
   const int g = int(threadIdx.x) % G;
   const unsigned gmask =
       G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
 
-  // chain geometry
-  const int c0 = cta * kNC;                 // first chain (row / column / diagonal offset)
-  const int nsteps = type == kHoriz ? w : h;
+  const int c0 = cta * kNC;  // first chain of this CTA (row / column / diagonal offset)
+  const int nsteps = TYPE == kHoriz ? w : h;
   // Steps are "virtual": horizontal / vertical tiles are aligned to multiples
   // of R from the image origin so that no TMA store box starts at a negative
   // coordinate (the hardware faults on those); a backward scan therefore
   // begins at virtual step T - N.  Diagonals use real steps.
-  const bool backward = (type == kHoriz) ? du < 0 : dv < 0;
+  const bool backward = (TYPE == kHoriz) ? du < 0 : dv < 0;
   const int T = (nsteps + R - 1) / R * R;
-  int s_begin = (type != kDiag && backward) ? T - nsteps : 0;
+  int s_begin = (TYPE != kDiag && backward) ? T - nsteps : 0;
   int s_end = s_begin + nsteps;
   int stage_base = 0;
   int kbase = 0;
-  if (type == kDiag) {
+  if (TYPE == kDiag) {
     kbase = J.kmin + c0;
     // u = k + du*s in [0, w) for some k in [kbase, kbase+NC)
     if (du > 0) {
@@ -219,22 +251,21 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
   const int nstage = s_end > stage_base ? (s_end - stage_base + R - 1) / R : 0;
   const int zc = J.vol, zp = J.path;
 
-  const CUtensorMap* cm_a = type == kHoriz ? &a.cost_h : (type == kVert ? &a.cost_vf : &a.cost_df);
-  const CUtensorMap* cm_b = type == kVert ? &a.cost_vl : &a.cost_dl;
-  const CUtensorMap* pm_a = type == kHoriz ? &a.path_h : (type == kVert ? &a.path_vf : &a.path_df);
-  const CUtensorMap* pm_b = type == kVert ? &a.path_vl : &a.path_dl;
+  const CUtensorMap* cm_a = TYPE == kHoriz ? &a.cost_h : (TYPE == kVert ? &a.cost_vf : &a.cost_df);
+  const CUtensorMap* cm_b = TYPE == kVert ? &a.cost_vl : &a.cost_dl;
+  const CUtensorMap* pm_a = TYPE == kHoriz ? &a.path_h : &a.path_vf;
+  const CUtensorMap* pm_b = &a.path_vl;
 
-  // Issue (load: true) or store (false) the TMA ops of stage `st` (global step s0).
+  // Issue the TMA loads (or, for H/V, the stores) of stage `st`.
   auto tile_ops = [&](int st, bool load, uint32_t* buf, uint64_t* bar) {
     const int s0 = stage_base + st * R;
-    if (type == kHoriz) {
-      // R columns x NC rows; backward chains walk the tile right to left
-      const int ucol = backward ? T - s0 - R : s0;
+    if (TYPE == kHoriz) {
+      const int ucol = backward ? T - s0 - R : s0;  // R columns x NC rows
       if (load)
         tma_load_3d(buf, cm_a, ucol * GE::WPP, c0, zc, bar);
       else
         tma_store_3d(pm_a, ucol * GE::WPP, c0, zp, buf);
-    } else if (type == kVert) {
+    } else if (TYPE == kVert) {
       const int vrow = backward ? T - s0 - R : s0;
 #pragma unroll
       for (int ch = 0; ch < GE::NCH; ++ch) {
@@ -261,36 +292,29 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
       }
     }
   };
-  (void)pm_b;
   auto stage_bytes = [&](int st) -> uint32_t {
-    if (type != kDiag) return uint32_t(GE::STAGE) * 4u;
+    if (TYPE != kDiag) return uint32_t(GE::STAGE) * 4u;
     const int s0 = stage_base + st * R;
     const int rows = min(R, s_end - s0);
     return uint32_t(rows) * uint32_t(GE::DROW) * 4u;
   };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kDepth; ++i) mbar_init(&full[i], 1);
-    fence_async_smem();
-  }
-  __syncthreads();
-  if (a.dbg == 1) return;
-  if (threadIdx.x == 0) {
     for (int st = 0; st < kDepth && st < nstage; ++st) {
       mbar_expect_tx(&full[st], stage_bytes(st));
-      if (a.dbg != 2) tile_ops(st, true, in_ring + st * GE::STAGE_IN, &full[st]);
+      tile_ops(st, true, in_ring + st * GE::STAGE_IN, &full[st]);
     }
   }
-  if (a.dbg == 2) return;
-  if (a.dbg == 3) {
-    if (nstage > 0) mbar_wait(&full[0], 0);
-    return;
-  }
 
-  uint32_t prev[NPL];
+  TileAddr<TYPE, WPL, G> ad;
+  ad.init(t, g);
+  const uint32_t p1x2 = a.p1x2, p2x2 = a.p2x2;
+  uint32_t prev[NPAIR];
 #pragma unroll
-  for (int q = 0; q < NPL; ++q) prev[q] = kInf2;
+  for (int q = 0; q < NPAIR; ++q) prev[q] = kInf2;
   uint32_t mnx2 = 0;
+  // diagonal direct-store row pointer pieces
+  uint8_t* const pbase = a.path_base + size_t(zp) * a.vol_bytes + size_t(g * WPL) * 4;
 
   for (int st = 0; st < nstage; ++st) {
     const int slot = st % kDepth;
@@ -303,65 +327,67 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
       const int s = s0 + r;
       if (s >= s_end) break;
       if (s < s_begin) continue;  // padding steps of a backward scan's first tile
-      // position in the smem tile (backward scans walk the tile backwards)
-      const int rr = (type != kDiag && backward) ? R - 1 - r : r;
+      const int rr = (TYPE != kDiag && backward) ? R - 1 - r : r;
+      int shift = 0, col = 0;
       bool has_pred;
-      int du_col = 0, shift = 0;
-      if (type == kDiag) {
-        shift = ((kbase + du * s) * GE::WPP) & 3;
-        du_col = kbase + t + du * s;
-        has_pred = s > 0 && unsigned(du_col - du) < unsigned(w) && unsigned(du_col) < unsigned(w);
+      if (TYPE == kDiag) {
+        const int cbase = kbase + du * s;
+        shift = (cbase * GE::WPP) & 3;
+        col = cbase + t;
+        has_pred = s > 0 && unsigned(col - du) < unsigned(w) && unsigned(col) < unsigned(w);
       } else {
         has_pred = s > s_begin;
       }
-      uint32_t raw[NPL];
+      uint32_t raw[NPAIR];
 #pragma unroll
       for (int q = 0; q < WPL; ++q) {
-        const uint32_t x = inb[stage_off<WPL, G>(type, rr, t, g * WPL + q, shift)];
+        const uint32_t x = inb[ad.at(q, rr, shift)];
         raw[2 * q] = __byte_perm(x, 0u, 0x4140);
-        raw[2 * q + 1] = __byte_perm(x, 0u, 0x4342);
+        if (2 * q + 1 < NPAIR) raw[2 * q + 1] = __byte_perm(x, 0u, 0x4342);
       }
-      uint32_t cur[NPL];
+      uint32_t cur[NPAIR];
       if (!has_pred) {
 #pragma unroll
-        for (int q = 0; q < NPL; ++q) cur[q] = raw[q];
+        for (int q = 0; q < NPAIR; ++q) cur[q] = raw[q];
       } else {
         uint32_t lo_nb = kInf2, hi_nb = kInf2;
         if (G > 1) {
-          const uint32_t up = __shfl_up_sync(gmask, prev[NPL - 1], 1, G);
+          const uint32_t up = __shfl_up_sync(gmask, prev[NPAIR - 1], 1, G);
           const uint32_t dn = __shfl_down_sync(gmask, prev[0], 1, G);
           if (g > 0) lo_nb = up;
           if (g < G - 1) hi_nb = dn;
         }
-        const uint32_t ceil2 = mnx2 + a.p2x2;
+        const uint32_t ceil2 = mnx2 + p2x2;
         uint32_t qprev = __byte_perm(lo_nb, prev[0], 0x5432);
 #pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-          const uint32_t nxt = (q + 1 < NPL) ? prev[q + 1] : hi_nb;
+        for (int q = 0; q < NPAIR; ++q) {
+          const uint32_t nxt = (q + 1 < NPAIR) ? prev[q + 1] : hi_nb;
           const uint32_t qn = __byte_perm(prev[q], nxt, 0x5432);
-          uint32_t tt = __viaddmin_u16x2(qprev, a.p1x2, prev[q]);
-          tt = __viaddmin_u16x2(qn, a.p1x2, tt);
+          uint32_t tt = __viaddmin_u16x2(qprev, p1x2, prev[q]);
+          tt = __viaddmin_u16x2(qn, p1x2, tt);
           tt = __vminu2(tt, ceil2);
           cur[q] = raw[q] + tt - mnx2;
           qprev = qn;
         }
       }
-      if (type == kDiag) {
-        if (unsigned(du_col) < unsigned(w)) {
-          const int vrow = dv > 0 ? s : h - 1 - s;
-          uint32_t* dst = reinterpret_cast<uint32_t*>(
-              a.path_base + size_t(zp) * a.vol_bytes + size_t(vrow) * a.pitch +
-              size_t(du_col) * (GE::WPP * 4)) + g * WPL;
+      uint32_t packed[WPL];
 #pragma unroll
-          for (int q = 0; q < WPL; ++q) dst[q] = __byte_perm(cur[2 * q], cur[2 * q + 1], 0x6420);
+      for (int q = 0; q < WPL; ++q)
+        packed[q] = __byte_perm(cur[2 * q], (2 * q + 1 < NPAIR) ? cur[2 * q + 1] : 0xFFFFFFFFu,
+                                0x6420);
+      if (TYPE == kDiag) {
+        if (unsigned(col) < unsigned(w)) {
+          const int vrow = dv > 0 ? s : h - 1 - s;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + size_t(vrow) * a.pitch +
+                                                      size_t(col) * (GE::WPP * 4));
+#pragma unroll
+          for (int q = 0; q < WPL; ++q) dst[q] = packed[q];
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < WPL; ++q)
-          outb[stage_off<WPL, G>(type, rr, t, g * WPL + q)] =
-              __byte_perm(cur[2 * q], cur[2 * q + 1], 0x6420);
+        for (int q = 0; q < WPL; ++q) outb[ad.at(q, rr, 0)] = packed[q];
       }
-      const uint32_t m2 = min_pairs<NPL>(cur);
+      const uint32_t m2 = min_pairs3<NPAIR>(cur);
       uint32_t m = min(m2 & 0xFFFFu, m2 >> 16);
       if (G > 1) {
 #pragma unroll
@@ -369,22 +395,54 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
       }
       mnx2 = m * 0x10001u;
 #pragma unroll
-      for (int q = 0; q < NPL; ++q) prev[q] = cur[q];
+      for (int q = 0; q < NPAIR; ++q) prev[q] = cur[q];
     }
-    fence_async_smem();  // make this thread's output-tile writes visible to the TMA store
-    __syncthreads();     // tile consumed, output tile written
+    if (TYPE != kDiag) fence_async_smem();  // output-tile writes -> async proxy
+    __syncthreads();                         // tile consumed, output tile written
     if (threadIdx.x == 0) {
-      if (a.dbg != 4) tile_ops(st, false, outb, nullptr);
-      tma_commit();
+      if (TYPE != kDiag) {
+        tile_ops(st, false, outb, nullptr);
+        tma_commit();
+      }
       if (st + kDepth < nstage) {
         mbar_expect_tx(&full[slot], stage_bytes(st + kDepth));
         tile_ops(st + kDepth, true, in_ring + slot * GE::STAGE_IN, &full[slot]);
       }
-      tma_wait_read<1>();  // the other output buffer is free again
+      if (TYPE != kDiag) tma_wait_read<1>();  // the other output buffer is free again
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) tma_wait_all();
+  if (TYPE != kDiag && threadIdx.x == 0) tma_wait_all();
+}
+
+template <int WPL, int G, int NPAIR>
+__global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
+    k_aggregate_tma(const __grid_constant__ TmaArgs a) {
+  using GE = Geo<WPL, G>;
+  // TMA tensor copies need 128-byte aligned shared memory; the dynamic block
+  // is over-allocated by 1 KiB and aligned here.
+  extern __shared__ uint8_t dsmem_raw[];
+  uint32_t* smem = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) & ~uintptr_t(1023));
+  uint32_t* in_ring = smem;                           // kDepth * STAGE_IN
+  uint32_t* out_ring = smem + kDepth * GE::STAGE_IN;  // 2 * STAGE
+  __shared__ __align__(8) uint64_t full[kDepth];
+  int jidx = 0;
+#pragma unroll 1
+  while (jidx + 1 < a.njobs && int(blockIdx.x) >= a.job[jidx + 1].block0) ++jidx;
+  const TmaJob& J = a.job[jidx];
+  const int cta = int(blockIdx.x) - J.block0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kDepth; ++i) mbar_init(&full[i], 1);
+    fence_async_smem();
+  }
+  __syncthreads();
+  if (J.type == kHoriz)
+    agg_body<kHoriz, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
+  else if (J.type == kVert)
+    agg_body<kVert, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
+  else
+    agg_body<kDiag, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
 }
 
 using TmaKernel = void (*)(TmaArgs);
@@ -396,25 +454,31 @@ struct KernelInfo {
   int R, wpp, row, cwf, cwl, nch, dcwf, dcwl;
 };
 
-template <int WPL, int G>
+template <int WPL, int G, int NPAIR>
 KernelInfo info() {
   using GE = Geo<WPL, G>;
-  return KernelInfo{k_aggregate_tma<WPL, G>,
+  return KernelInfo{k_aggregate_tma<WPL, G, NPAIR>,
                     (kDepth * GE::STAGE_IN + 2 * GE::STAGE) * 4 + 1024,
                     GE::THREADS, GE::R, GE::WPP, GE::ROW, GE::CWF, GE::CWL, GE::NCH,
                     GE::DROW < 256 ? GE::DROW : 256, GE::DCWL};
 }
 
-KernelInfo pick(int wpl, int G) {
-#define RPD_TMA_CASE(W_, G_) \
-  if (wpl == W_ && G == G_) return info<W_, G_>();
-  RPD_TMA_CASE(1, 1) RPD_TMA_CASE(2, 1) RPD_TMA_CASE(3, 1) RPD_TMA_CASE(4, 1)
-  RPD_TMA_CASE(5, 1) RPD_TMA_CASE(6, 1) RPD_TMA_CASE(7, 1) RPD_TMA_CASE(8, 1)
-  RPD_TMA_CASE(9, 1)
-  RPD_TMA_CASE(5, 2) RPD_TMA_CASE(6, 2) RPD_TMA_CASE(7, 2) RPD_TMA_CASE(8, 2) RPD_TMA_CASE(9, 2)
-  RPD_TMA_CASE(5, 4) RPD_TMA_CASE(6, 4) RPD_TMA_CASE(7, 4) RPD_TMA_CASE(8, 4) RPD_TMA_CASE(9, 4)
-  RPD_TMA_CASE(5, 8) RPD_TMA_CASE(6, 8) RPD_TMA_CASE(7, 8) RPD_TMA_CASE(8, 8) RPD_TMA_CASE(9, 8)
-#undef RPD_TMA_CASE
+KernelInfo pick(int wpl, int G, int levels) {
+  const int npair_g1 = (levels + 1) / 2;  // G == 1: skip a trailing all-padding pair
+#define RPD_TMA_G1(W_)                                                       \
+  if (wpl == W_ && G == 1) {                                                 \
+    if (npair_g1 == 2 * W_ - 1) return info<W_, 1, (2 * W_ - 1 > 0 ? 2 * W_ - 1 : 1)>(); \
+    return info<W_, 1, 2 * W_>();                                            \
+  }
+#define RPD_TMA_GN(W_, G_) \
+  if (wpl == W_ && G == G_) return info<W_, G_, 2 * W_>();
+  RPD_TMA_G1(1) RPD_TMA_G1(2) RPD_TMA_G1(3) RPD_TMA_G1(4) RPD_TMA_G1(5) RPD_TMA_G1(6)
+  RPD_TMA_G1(7) RPD_TMA_G1(8) RPD_TMA_G1(9)
+  RPD_TMA_GN(5, 2) RPD_TMA_GN(6, 2) RPD_TMA_GN(7, 2) RPD_TMA_GN(8, 2) RPD_TMA_GN(9, 2)
+  RPD_TMA_GN(5, 4) RPD_TMA_GN(6, 4) RPD_TMA_GN(7, 4) RPD_TMA_GN(8, 4) RPD_TMA_GN(9, 4)
+  RPD_TMA_GN(5, 8) RPD_TMA_GN(6, 8) RPD_TMA_GN(7, 8) RPD_TMA_GN(8, 8) RPD_TMA_GN(9, 8)
+#undef RPD_TMA_G1
+#undef RPD_TMA_GN
   throw InvalidArg("sgm: unsupported level layout for the TMA aggregation");
 }
 
@@ -455,7 +519,7 @@ bool sgm_tma_supported(const SgmLayout& L) {
 // Launches the aggregation of all 2P (volume, direction) jobs of one pass.
 void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uint8_t* paths,
                           const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2) {
-  const KernelInfo ki = pick(L.wpl, L.G);
+  const KernelInfo ki = pick(L.wpl, L.G, L.levels);
   const int wpp = L.lw / 4;
   const int words_row = L.w * wpp;
   TmaArgs args{};
