@@ -144,42 +144,26 @@ struct Geo {
   static constexpr int THREADS = kNC * G;
 };
 
-// Shared-memory word offset of word q of this thread's pixel at tile row rr.
-// Everything except (rr, shift) is fixed per thread, so the callers hoist it.
+// Shared-memory word offsets of this thread's pixel words inside a tile.
+// Unchunked layouts (the common case) reduce to base + q + rr*STRIDE with a
+// compile-time STRIDE, so every access is an LDS/STS with an immediate offset.
 template <int TYPE, int WPL, int G>
 struct TileAddr {
   using GE = Geo<WPL, G>;
-  int base[WPL];    // offset at rr = 0 (and shift = 0)
-  int stride[WPL];  // offset increment per tile row
-
+  static constexpr bool kChunked =
+      (TYPE == kVert && GE::NCH > 1) || (TYPE == kDiag && GE::DNCH > 1);
+  static constexpr int kStride = TYPE == kHoriz ? GE::WPP : (TYPE == kVert ? GE::ROW : GE::DROW);
+  int base;
   __device__ __forceinline__ void init(int t, int g) {
-#pragma unroll
-    for (int q = 0; q < WPL; ++q) {
-      if (TYPE == kHoriz) {
-        base[q] = t * (GE::R * GE::WPP) + g * WPL + q;
-        stride[q] = GE::WPP;
-      } else if (TYPE == kVert) {
-        const int wd = t * GE::WPP + g * WPL + q;
-        if (GE::NCH == 1) {
-          base[q] = wd;
-          stride[q] = GE::ROW;
-        } else {
-          const int ch = wd >> 8;
-          base[q] = ch * (256 * GE::R) + (wd & 255);
-          stride[q] = ch == GE::NCH - 1 ? GE::CWL : 256;
-        }
-      } else {
-        base[q] = t * GE::WPP + g * WPL + q;  // + shift, chunked at use
-        stride[q] = GE::DROW;
-      }
-    }
+    base = (TYPE == kHoriz) ? t * (GE::R * GE::WPP) + g * WPL : t * GE::WPP + g * WPL;
   }
   __device__ __forceinline__ int at(int q, int rr, int shift) const {
-    if (TYPE != kDiag || GE::DNCH == 1) return base[q] + shift + rr * stride[q];
-    const int wd = base[q] + shift;
+    if (!kChunked) return base + shift + q + rr * kStride;
+    const int wd = base + shift + q;
     const int ch = wd >> 8;
-    const int cw = ch == GE::DNCH - 1 ? GE::DCWL : 256;
-    return ch * (256 * GE::R) + rr * cw + (wd & 255);
+    const int last = TYPE == kVert ? GE::NCH - 1 : GE::DNCH - 1;
+    const int cwl = TYPE == kVert ? GE::CWL : GE::DCWL;
+    return ch * (256 * GE::R) + rr * (ch == last ? cwl : 256) + (wd & 255);
   }
 };
 
@@ -208,6 +192,67 @@ __device__ __forceinline__ uint32_t min_pairs3(const uint32_t (&x)[NP]) {
     n = m;
   }
   return t[0];
+}
+
+// Per-chain recurrence state.  A chain (re)starts with prev = INF and
+// min = INF: then best = INF and cur = raw + INF - INF = raw exactly, so the
+// "no predecessor" case needs no branch (sgm.cpp:89-92).
+template <int NPAIR>
+struct ChainState {
+  uint32_t prev[NPAIR];
+  uint32_t mnx2;
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) prev[q] = kInf2;
+    mnx2 = kInf2;
+  }
+};
+
+// One recurrence step on packed u16x2 level pairs; returns the packed u8
+// words of the new costs in `packed` and updates the state.
+template <int WPL, int G, int NPAIR>
+__device__ __forceinline__ void chain_step(ChainState<NPAIR>& cs, const uint32_t (&w8)[WPL],
+                                           uint32_t p1x2, uint32_t p2x2, int g, unsigned gmask,
+                                           uint32_t (&packed)[WPL]) {
+  uint32_t raw[NPAIR];
+#pragma unroll
+  for (int q = 0; q < WPL; ++q) {
+    raw[2 * q] = __byte_perm(w8[q], 0u, 0x4140);
+    if (2 * q + 1 < NPAIR) raw[2 * q + 1] = __byte_perm(w8[q], 0u, 0x4342);
+  }
+  uint32_t lo_nb = kInf2, hi_nb = kInf2;
+  if (G > 1) {
+    const uint32_t up = __shfl_up_sync(gmask, cs.prev[NPAIR - 1], 1, G);
+    const uint32_t dn = __shfl_down_sync(gmask, cs.prev[0], 1, G);
+    if (g > 0) lo_nb = up;
+    if (g < G - 1) hi_nb = dn;
+  }
+  const uint32_t ceil2 = cs.mnx2 + p2x2;
+  uint32_t cur[NPAIR];
+  uint32_t qprev = __byte_perm(lo_nb, cs.prev[0], 0x5432);
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) {
+    const uint32_t nxt = (q + 1 < NPAIR) ? cs.prev[q + 1] : hi_nb;
+    const uint32_t qn = __byte_perm(cs.prev[q], nxt, 0x5432);  // (prev[d+1] of both halves)
+    uint32_t tt = __viaddmin_u16x2(qprev, p1x2, cs.prev[q]);
+    tt = __viaddmin_u16x2(qn, p1x2, tt);
+    tt = __vminu2(tt, ceil2);
+    cur[q] = raw[q] + tt - cs.mnx2;  // per-half exact: tt >= min, no carry
+    qprev = qn;
+  }
+#pragma unroll
+  for (int q = 0; q < WPL; ++q)
+    packed[q] =
+        __byte_perm(cur[2 * q], (2 * q + 1 < NPAIR) ? cur[2 * q + 1] : 0xFFFFFFFFu, 0x6420);
+  const uint32_t m2 = min_pairs3<NPAIR>(cur);
+  uint32_t m = min(m2 & 0xFFFFu, m2 >> 16);
+  if (G > 1) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(gmask, m, off, G));
+  }
+  cs.mnx2 = m * 0x10001u;
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) cs.prev[q] = cur[q];
 }
 
 // One job type, fully specialised.  NPAIR <= 2*WPL level pairs are computed
@@ -309,11 +354,8 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
   TileAddr<TYPE, WPL, G> ad;
   ad.init(t, g);
   const uint32_t p1x2 = a.p1x2, p2x2 = a.p2x2;
-  uint32_t prev[NPAIR];
-#pragma unroll
-  for (int q = 0; q < NPAIR; ++q) prev[q] = kInf2;
-  uint32_t mnx2 = 0;
-  // diagonal direct-store row pointer pieces
+  ChainState<NPAIR> cs;
+  cs.reset();
   uint8_t* const pbase = a.path_base + size_t(zp) * a.vol_bytes + size_t(g * WPL) * 4;
 
   for (int st = 0; st < nstage; ++st) {
@@ -322,61 +364,28 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
     const uint32_t* inb = in_ring + slot * GE::STAGE_IN;
     uint32_t* outb = out_ring + (st & 1) * GE::STAGE;
     const int s0 = stage_base + st * R;
+    // only the first tile of a backward H/V scan holds padding steps
+    const bool check = TYPE != kDiag && s0 < s_begin;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int s = s0 + r;
-      if (s >= s_end) break;
-      if (s < s_begin) continue;  // padding steps of a backward scan's first tile
       const int rr = (TYPE != kDiag && backward) ? R - 1 - r : r;
       int shift = 0, col = 0;
-      bool has_pred;
       if (TYPE == kDiag) {
         const int cbase = kbase + du * s;
         shift = (cbase * GE::WPP) & 3;
         col = cbase + t;
-        has_pred = s > 0 && unsigned(col - du) < unsigned(w) && unsigned(col) < unsigned(w);
-      } else {
-        has_pred = s > s_begin;
+        const bool has_pred = s > 0 && unsigned(col - du) < unsigned(w);
+        if (!has_pred) cs.reset();  // chain (re)enters the image
       }
-      uint32_t raw[NPAIR];
+      uint32_t w8[WPL];
 #pragma unroll
-      for (int q = 0; q < WPL; ++q) {
-        const uint32_t x = inb[ad.at(q, rr, shift)];
-        raw[2 * q] = __byte_perm(x, 0u, 0x4140);
-        if (2 * q + 1 < NPAIR) raw[2 * q + 1] = __byte_perm(x, 0u, 0x4342);
-      }
-      uint32_t cur[NPAIR];
-      if (!has_pred) {
-#pragma unroll
-        for (int q = 0; q < NPAIR; ++q) cur[q] = raw[q];
-      } else {
-        uint32_t lo_nb = kInf2, hi_nb = kInf2;
-        if (G > 1) {
-          const uint32_t up = __shfl_up_sync(gmask, prev[NPAIR - 1], 1, G);
-          const uint32_t dn = __shfl_down_sync(gmask, prev[0], 1, G);
-          if (g > 0) lo_nb = up;
-          if (g < G - 1) hi_nb = dn;
-        }
-        const uint32_t ceil2 = mnx2 + p2x2;
-        uint32_t qprev = __byte_perm(lo_nb, prev[0], 0x5432);
-#pragma unroll
-        for (int q = 0; q < NPAIR; ++q) {
-          const uint32_t nxt = (q + 1 < NPAIR) ? prev[q + 1] : hi_nb;
-          const uint32_t qn = __byte_perm(prev[q], nxt, 0x5432);
-          uint32_t tt = __viaddmin_u16x2(qprev, p1x2, prev[q]);
-          tt = __viaddmin_u16x2(qn, p1x2, tt);
-          tt = __vminu2(tt, ceil2);
-          cur[q] = raw[q] + tt - mnx2;
-          qprev = qn;
-        }
-      }
+      for (int q = 0; q < WPL; ++q) w8[q] = inb[ad.at(q, rr, shift)];
       uint32_t packed[WPL];
-#pragma unroll
-      for (int q = 0; q < WPL; ++q)
-        packed[q] = __byte_perm(cur[2 * q], (2 * q + 1 < NPAIR) ? cur[2 * q + 1] : 0xFFFFFFFFu,
-                                0x6420);
+      if (check && s < s_begin) continue;  // padding step: state stays INF
+      chain_step<WPL, G, NPAIR>(cs, w8, p1x2, p2x2, g, gmask, packed);
       if (TYPE == kDiag) {
-        if (unsigned(col) < unsigned(w)) {
+        if (unsigned(col) < unsigned(w) && s < s_end) {
           const int vrow = dv > 0 ? s : h - 1 - s;
           uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + size_t(vrow) * a.pitch +
                                                       size_t(col) * (GE::WPP * 4));
@@ -387,15 +396,6 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
 #pragma unroll
         for (int q = 0; q < WPL; ++q) outb[ad.at(q, rr, 0)] = packed[q];
       }
-      const uint32_t m2 = min_pairs3<NPAIR>(cur);
-      uint32_t m = min(m2 & 0xFFFFu, m2 >> 16);
-      if (G > 1) {
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(gmask, m, off, G));
-      }
-      mnx2 = m * 0x10001u;
-#pragma unroll
-      for (int q = 0; q < NPAIR; ++q) prev[q] = cur[q];
     }
     if (TYPE != kDiag) fence_async_smem();  // output-tile writes -> async proxy
     __syncthreads();                         // tile consumed, output tile written
@@ -419,13 +419,12 @@ template <int WPL, int G, int NPAIR>
 __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
     k_aggregate_tma(const __grid_constant__ TmaArgs a) {
   using GE = Geo<WPL, G>;
-  // TMA tensor copies need 128-byte aligned shared memory; the dynamic block
-  // is over-allocated by 1 KiB and aligned here.
-  extern __shared__ uint8_t dsmem_raw[];
-  uint32_t* smem = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(dsmem_raw) + 1023) & ~uintptr_t(1023));
-  uint32_t* in_ring = smem;                           // kDepth * STAGE_IN
-  uint32_t* out_ring = smem + kDepth * GE::STAGE_IN;  // 2 * STAGE
+  // TMA tensor copies need 128-byte aligned shared memory: the dynamic block
+  // is over-allocated by 1 KiB and aligned in the shared address space.
+  extern __shared__ __align__(16) uint32_t dsm[];
+  const uint32_t pad_words = ((1024u - (smem_addr(dsm) & 1023u)) & 1023u) >> 2;
+  uint32_t* in_ring = dsm + pad_words;                // kDepth * STAGE_IN
+  uint32_t* out_ring = in_ring + kDepth * GE::STAGE_IN;  // 2 * STAGE
   __shared__ __align__(8) uint64_t full[kDepth];
   int jidx = 0;
 #pragma unroll 1
