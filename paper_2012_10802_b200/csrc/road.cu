@@ -62,17 +62,16 @@ __device__ __forceinline__ DD dd_mul(DD a, DD b) {
   p.lo += a.lo * b.hi;
   return quick_two_sum(p.hi, p.lo);
 }
-__device__ __forceinline__ DD dd_div_d(DD a, double b) {
-  const double q1 = a.hi / b;
-  const DD p = two_prod(q1, b);
-  DD r = two_sum(a.hi, -p.hi);
-  r.lo -= p.lo;
-  r.lo += a.lo;
-  const double q2 = (r.hi + r.lo) / b;
-  return quick_two_sum(q1, q2);
-}
+// (-1)^n / (2n+1)! and (-1)^n / (2n)! as exact double-double constants.
+constexpr int kTaylorTerms = 18;  // enough for |x| <= pi/4 at ~1e-36
+__constant__ double c_sin_hi[kTaylorTerms] = {1.0, -0.16666666666666666, 0.008333333333333333, -0.0001984126984126984, 2.7557319223985893e-06, -2.505210838544172e-08, 1.6059043836821613e-10, -7.647163731819816e-13, 2.8114572543455206e-15, -8.22063524662433e-18, 1.9572941063391263e-20, -3.868170170630684e-23, 6.446950284384474e-26, -9.183689863795546e-29, 1.1309962886447716e-31, -1.216125041553518e-34, 1.151633562077195e-37, -9.67759295863189e-41};
+__constant__ double c_sin_lo[kTaylorTerms] = {0.0, -9.25185853854297e-18, 1.1564823173178714e-19, -1.7209558293420705e-22, -1.858393274046472e-22, 1.448814070935912e-24, 1.2585294588752098e-26, -7.03872877733453e-30, 1.6508842730861433e-31, -2.2141894119604265e-34, -1.3643503830087908e-36, 8.843177655482344e-40, -1.9330404233703465e-42, -1.4303150396787322e-45, 1.0498015412959506e-47, -5.586290567888806e-51, -6.09957445788454e-54, -3.202295548645562e-57};
+__constant__ double c_cos_hi[kTaylorTerms] = {1.0, -0.5, 0.041666666666666664, -0.001388888888888889, 2.48015873015873e-05, -2.755731922398589e-07, 2.08767569878681e-09, -1.1470745597729725e-11, 4.779477332387385e-14, -1.5619206968586225e-16, 4.110317623312165e-19, -8.896791392450574e-22, 1.6117375710961184e-24, -2.4795962632247976e-27, 3.279889237069838e-30, -3.7699876288159054e-33, 3.8003907548547434e-36, -3.387157535521162e-39};
+__constant__ double c_cos_lo[kTaylorTerms] = {0.0, 0.0, 2.3129646346357427e-18, 5.300543954373577e-20, 2.1511947866775882e-23, -2.3767714622250297e-23, -1.20734505911326e-25, -2.0655512752830745e-28, 4.399205485834081e-31, -1.1910679660273754e-32, 1.4412973378659527e-36, 7.911402614872376e-38, -3.6846573564509766e-41, 1.2953730964765229e-43, 1.5117542744029879e-46, -2.5870347832750324e-49, 1.7457158024652518e-52, -5.09056148151085e-56};
 }  // namespace
 
+// Correctly rounded sin/cos (with overwhelming probability): double-double
+// Horner evaluation of the Taylor series after reduction by pi/2.
 __device__ void dd_sincos(double x, double* s_out, double* c_out) {
   const DD pio2 = {1.5707963267948966, 6.123233995736766e-17};
   const double kf = rint(x / pio2.hi);
@@ -82,15 +81,14 @@ __device__ void dd_sincos(double x, double* s_out, double* c_out) {
     r = dd_add(r, DD{-kp.hi, -kp.lo});
   }
   const DD x2 = dd_mul(r, r);
-  DD st = r, ss = r;        // sin series
-  DD ct = {1.0, 0.0}, cs = ct;  // cos series
-  for (int n = 1; n <= 24; ++n) {
-    st = dd_div_d(dd_mul(st, x2), -double((2 * n) * (2 * n + 1)));
-    ct = dd_div_d(dd_mul(ct, x2), -double((2 * n - 1) * (2 * n)));
-    ss = dd_add(ss, st);
-    cs = dd_add(cs, ct);
-    if (fabs(st.hi) < 1e-40 && fabs(ct.hi) < 1e-40) break;
+  DD ps = {c_sin_hi[kTaylorTerms - 1], c_sin_lo[kTaylorTerms - 1]};
+  DD pc = {c_cos_hi[kTaylorTerms - 1], c_cos_lo[kTaylorTerms - 1]};
+#pragma unroll
+  for (int n = kTaylorTerms - 2; n >= 0; --n) {
+    ps = dd_add(dd_mul(ps, x2), DD{c_sin_hi[n], c_sin_lo[n]});
+    pc = dd_add(dd_mul(pc, x2), DD{c_cos_hi[n], c_cos_lo[n]});
   }
+  const DD ss = dd_mul(ps, r), cs = pc;
   const int q = int((long long)kf & 3);
   const double sv = ss.hi, cv = cs.hi;
   switch (q) {
@@ -194,11 +192,13 @@ struct FitKParams {
   double* scr_dv;
 };
 
+constexpr int kMaxNV = 10;  // values per cluster reduction
 struct FitShared {
-  double warp_part[32][4];
-  double cta_part[2][4];
-  double bcast[4];
-  double sc[2];
+  double warp_part[32][kMaxNV];
+  double cta_part[2][kMaxNV];
+  double peer[kMaxNV][kFitCtas];
+  double bcast[kMaxNV];
+  double sc[4][2];  // sin/cos of up to 4 pending probe angles
   int row_cnt[kMaxRowsTrim];
   int row_base[kMaxRowsTrim];
   int warp_cnt[32];
@@ -280,6 +280,7 @@ __device__ void fit_stage(FitState& F) {
 // Cluster-wide sum of NV doubles in the fixed adjacent-pairwise lane order.
 template <int NV>
 __device__ void cluster_sum(FitState& F, double (&x)[NV]) {
+  static_assert(NV <= kMaxNV, "too many values");
   cg::cluster_group cl = cg::this_cluster();
   FitShared& S = *F.S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -304,18 +305,21 @@ __device__ void cluster_sum(FitState& F, double (&x)[NV]) {
       for (int q = 0; q < NV; ++q) S.cta_part[F.slot][q] = y[q];
   }
   cl.sync();
-  if (threadIdx.x == 0) {
+  // every peer partial is fetched by its own thread (parallel DSMEM loads)
+  if (threadIdx.x < NV * kFitCtas) {
+    const int q = threadIdx.x / kFitCtas, r = threadIdx.x % kFitCtas;
+    S.peer[q][r] = *cl.map_shared_rank(&S.cta_part[F.slot][q], r);
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double p[kFitCtas];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      double p[kFitCtas];
+    for (int r = 0; r < kFitCtas; ++r) p[r] = S.peer[threadIdx.x][r];
 #pragma unroll
-      for (int r = 0; r < kFitCtas; ++r) p[r] = *cl.map_shared_rank(&S.cta_part[F.slot][q], r);
+    for (int width = 1; width < kFitCtas; width *= 2)
 #pragma unroll
-      for (int width = 1; width < kFitCtas; width *= 2)
-#pragma unroll
-        for (int j = 0; j < kFitCtas; j += 2 * width) p[j] += p[j + width];
-      S.bcast[q] = p[0];
-    }
+      for (int j = 0; j < kFitCtas; j += 2 * width) p[j] += p[j + width];
+    S.bcast[threadIdx.x] = p[0];
   }
   __syncthreads();
 #pragma unroll
@@ -323,95 +327,237 @@ __device__ void cluster_sum(FitState& F, double (&x)[NV]) {
   F.slot ^= 1;
 }
 
-__device__ double fit_sum_d(FitState& F) {
-  double x[1] = {0.0};
-  for (int m = 0; m < F.rows; ++m) {
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (i >= F.k) break;
-    double d, u, v;
-    fit_get(F, m, i, d, u, v);
-    x[0] += d;
-  }
-  cluster_sum<1>(F, x);
-  return x[0];
-}
-
-// fit_line, road_geometry.cpp:12-39.  Returns false when the normal matrix is
-// singular (the reference throws runtime_error).
-__device__ bool fit_probe(FitState& F, double phi, double sd, LineFitD& out) {
+// sin/cos of up to 4 angles, one per warp in parallel, broadcast to the CTA.
+__device__ void fit_sincos(FitState& F, int n, const double* phi, double (*cs)[2]) {
   FitShared& S = *F.S;
-  if (threadIdx.x == 0) {
-    double s, c;
-    dd_sincos(phi, &s, &c);
-    S.sc[0] = s;
-    S.sc[1] = c;
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && warp < n) dd_sincos(phi[warp], &S.sc[warp][0], &S.sc[warp][1]);
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    cs[i][0] = S.sc[i][1];  // cos
+    cs[i][1] = S.sc[i][0];  // sin
   }
   __syncthreads();
-  const double s = S.sc[0], c = S.sc[1];
-  double acc[3] = {0.0, 0.0, 0.0};
+}
+
+// One sweep over the observations + one cluster reduction computing
+//   [sd]                          if SD
+//   (st, stt, sdt) for NS angles  t = c*v - s*u   (road_geometry.cpp:17-24)
+//   sum r^2 for NR fitted lines   r = d - a0 - a1*t (road_geometry.cpp:37)
+// Each sum is its own lane accumulator, so every value is bit-identical to
+// a separate pass in the oracle's lane order.
+template <bool SD, int NS, int NR>
+__device__ void fit_pass(FitState& F, const double (*ang)[2], const double (*line)[4],
+                         double* out) {
+  constexpr int NV = (SD ? 1 : 0) + 3 * NS + NR;
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  double c[NS > 0 ? NS : 1], s[NS > 0 ? NS : 1];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    c[j] = ang[j][0];
+    s[j] = ang[j][1];
+  }
+  double la0[NR > 0 ? NR : 1], la1[NR > 0 ? NR : 1], lc[NR > 0 ? NR : 1], ls[NR > 0 ? NR : 1];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    la0[j] = line[j][0];
+    la1[j] = line[j][1];
+    lc[j] = line[j][2];
+    ls[j] = line[j][3];
+  }
   for (int m = 0; m < F.rows; ++m) {
     const long long i = (long long)m * kFitLanes + F.lane;
     if (i >= F.k) break;
     double d, u, v;
     fit_get(F, m, i, d, u, v);
-    const double t = c * v - s * u;
-    acc[0] += t;
-    acc[1] += t * t;
-    acc[2] += d * t;
+    int q = 0;
+    if (SD) acc[q++] += d;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const double t = c[j] * v - s[j] * u;
+      acc[q] += t;
+      acc[q + 1] += t * t;
+      acc[q + 2] += d * t;
+      q += 3;
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const double t = lc[j] * v - ls[j] * u;
+      const double r = d - la0[j] - la1[j] * t;
+      acc[q++] += r * r;
+    }
   }
-  cluster_sum<3>(F, acc);
-  const double kk = double(F.k);
-  const double st = acc[0], stt = acc[1], sdt = acc[2];
+  cluster_sum<NV>(F, acc);
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = acc[q];
+}
+
+// Closed-form normal equations of fit_line (road_geometry.cpp:26-34).
+__device__ __forceinline__ bool solve_line(double kk, double sd, const double* st3, double& a0,
+                                           double& a1) {
+  const double st = st3[0], stt = st3[1], sdt = st3[2];
   const double det = kk * stt - st * st;
   const double prod = kk * stt;
   const double scale = (prod < 1.0) ? 1.0 : prod;
   if (fabs(det) < 1e-12 * scale) return false;
-  const double a0 = (stt * sd - st * sdt) / det;
-  const double a1 = (kk * sdt - st * sd) / det;
-  double e[1] = {0.0};
-  for (int m = 0; m < F.rows; ++m) {
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (i >= F.k) break;
-    double d, u, v;
-    fit_get(F, m, i, d, u, v);
-    const double t = c * v - s * u;
-    const double r = d - a0 - a1 * t;
-    e[0] += r * r;
-  }
-  cluster_sum<1>(F, e);
-  out = LineFitD{a0, a1, phi, e[0], c, s};
+  a0 = (stt * sd - st * sdt) / det;
+  a1 = (kk * sdt - st * sd) / det;
   return true;
 }
 
-// estimate_roll, road_geometry.cpp:41-68 (golden section, f1 < f2 branch).
+// fit_line at one angle (road_geometry.cpp:12-39): two sweeps.
+__device__ bool fit_probe(FitState& F, double phi, LineFitD& out) {
+  double cs[1][2];
+  fit_sincos(F, 1, &phi, cs);
+  double r1[4];
+  fit_pass<true, 1, 0>(F, cs, nullptr, r1);
+  double a0, a1;
+  if (!solve_line(double(F.k), r1[0], r1 + 1, a0, a1)) return false;
+  const double ln[1][4] = {{a0, a1, cs[0][0], cs[0][1]}};
+  double e[1];
+  fit_pass<false, 0, 1>(F, nullptr, ln, e);
+  out = LineFitD{a0, a1, phi, e[0], cs[0][0], cs[0][1]};
+  return true;
+}
+
+// estimate_roll, road_geometry.cpp:41-68: golden section with the f1 < f2
+// branch, evaluated speculatively.  Every sweep computes the energy of the
+// newest point AND the normal-equation sums of the point the next iteration
+// will evaluate on either branch, so each iteration costs one sweep and one
+// cluster reduction.  The sequence of evaluated angles, every value and every
+// branch are exactly those of the sequential reference.
 __device__ bool fit_golden(FitState& F, double lo, double hi, double tol, LineFitD& out) {
-  const double sd = fit_sum_d(F);
   constexpr double g = 0.6180339887498949;
+  const double kk = double(F.k);
   double a = lo, b = hi;
   double x1 = b - g * (b - a), x2 = a + g * (b - a);
-  LineFitD f;
-  if (!fit_probe(F, x1, sd, f)) return false;
-  double f1 = f.e0min;
-  if (!fit_probe(F, x2, sd, f)) return false;
-  double f2 = f.e0min;
-  while (b - a > tol) {
-    if (f1 < f2) {
+  // sweep 0: sd and the sums of x1, x2
+  double ang[2][2];
+  {
+    const double ph[2] = {x1, x2};
+    fit_sincos(F, 2, ph, ang);
+  }
+  double r0[7];
+  fit_pass<true, 2, 0>(F, ang, nullptr, r0);
+  const double sd = r0[0];
+  double l1[4], l2[4];
+  if (!solve_line(kk, sd, r0 + 1, l1[0], l1[1])) return false;
+  if (!solve_line(kk, sd, r0 + 4, l2[0], l2[1])) return false;
+  l1[2] = ang[0][0];
+  l1[3] = ang[0][1];
+  l2[2] = ang[1][0];
+  l2[3] = ang[1][1];
+
+  // Candidate angle evaluated next on each branch given the current state
+  // (after the comparison of f1, f2): the golden point if the loop body runs,
+  // otherwise the final midpoint.
+  auto next_angle = [&](bool branch_a, double& a_, double& b_) -> double {
+    double na = a, nb = b;
+    if (branch_a) {
+      nb = x2;
+      a_ = na;
+      b_ = nb;
+      return nb - g * (nb - na);
+    }
+    na = x1;
+    a_ = na;
+    b_ = nb;
+    return na + g * (nb - na);
+  };
+
+  // sweep 1: energies of x1 and x2 + sums of both possible next angles
+  bool loop = b - a > tol;
+  double ca[2];
+  int ncand;
+  if (loop) {
+    double ta, tb;
+    ca[0] = next_angle(true, ta, tb);
+    ca[1] = next_angle(false, ta, tb);
+    ncand = 2;
+  } else {
+    ca[0] = ca[1] = 0.5 * (a + b);
+    ncand = 1;
+  }
+  double cang[2][2];
+  fit_sincos(F, ncand, ca, cang);
+  if (ncand == 1) {
+    cang[1][0] = cang[0][0];
+    cang[1][1] = cang[0][1];
+  }
+  double f1, f2;
+  double res[8];
+  {
+    const double lines[2][4] = {{l1[0], l1[1], l1[2], l1[3]}, {l2[0], l2[1], l2[2], l2[3]}};
+    fit_pass<false, 2, 2>(F, cang, lines, res);
+    // res = [S(cand0) x3, S(cand1) x3, E(x1), E(x2)]
+    f1 = res[6];
+    f2 = res[7];
+  }
+  double cs_sum[2][3] = {{res[0], res[1], res[2]}, {res[3], res[4], res[5]}};
+  while (loop) {
+    // iteration body: branch on f1 < f2, adopt the matching candidate
+    const bool br = f1 < f2;
+    const int pick = br ? 0 : 1;
+    double na, nb;
+    const double xn = next_angle(br, na, nb);
+    double ln[4];
+    if (!solve_line(kk, sd, cs_sum[pick], ln[0], ln[1])) return false;
+    ln[2] = cang[pick][0];
+    ln[3] = cang[pick][1];
+    if (br) {
       b = x2;
       x2 = x1;
       f2 = f1;
-      x1 = b - g * (b - a);
-      if (!fit_probe(F, x1, sd, f)) return false;
-      f1 = f.e0min;
+      x1 = xn;
     } else {
       a = x1;
       x1 = x2;
       f1 = f2;
-      x2 = a + g * (b - a);
-      if (!fit_probe(F, x2, sd, f)) return false;
-      f2 = f.e0min;
+      x2 = xn;
     }
+    (void)na;
+    (void)nb;
+    loop = b - a > tol;
+    if (loop) {
+      double ta, tb;
+      ca[0] = next_angle(true, ta, tb);
+      ca[1] = next_angle(false, ta, tb);
+      ncand = 2;
+    } else {
+      ca[0] = ca[1] = 0.5 * (a + b);
+      ncand = 1;
+    }
+    fit_sincos(F, ncand, ca, cang);
+    if (ncand == 1) {
+      cang[1][0] = cang[0][0];
+      cang[1][1] = cang[0][1];
+    }
+    const double lines[1][4] = {{ln[0], ln[1], ln[2], ln[3]}};
+    double r[7];
+    fit_pass<false, 2, 1>(F, cang, lines, r);
+    // energy of the point just evaluated in the body
+    if (br)
+      f1 = r[6];
+    else
+      f2 = r[6];
+    cs_sum[0][0] = r[0];
+    cs_sum[0][1] = r[1];
+    cs_sum[0][2] = r[2];
+    cs_sum[1][0] = r[3];
+    cs_sum[1][1] = r[4];
+    cs_sum[1][2] = r[5];
   }
-  return fit_probe(F, 0.5 * (a + b), sd, out);
+  // final fit_line at the midpoint: its sums are cs_sum[0]
+  const double mid = 0.5 * (a + b);
+  double fa0, fa1;
+  if (!solve_line(kk, sd, cs_sum[0], fa0, fa1)) return false;
+  const double lines[1][4] = {{fa0, fa1, cang[0][0], cang[0][1]}};
+  double e[1];
+  fit_pass<false, 0, 1>(F, nullptr, lines, e);
+  out = LineFitD{fa0, fa1, mid, e[0], cang[0][0], cang[0][1]};
+  return true;
 }
 
 // Stable cluster-wide compaction of the survivors of fit_road's trimming
@@ -524,8 +670,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ 
     LineFitD f{};
     long long used = F.k;
     if (R.mode == kFitLine) {
-      const double sd = fit_sum_d(F);
-      ok = fit_probe(F, R.phi, sd, f);
+      ok = fit_probe(F, R.phi, f);
     } else if (R.mode == kEstimateRoll) {
       ok = fit_golden(F, R.lo, R.hi, R.tol, f);
     } else {

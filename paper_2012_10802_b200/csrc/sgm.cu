@@ -522,6 +522,71 @@ __global__ void k_wta(const __grid_constant__ WtaArgs a) {
   a.disp[p] = r;
 }
 
+// Tiled WTA: a CTA takes kWtaPx consecutive pixels of one image row.  Phase 1
+// sums the P per-path u8 words of the tile with fully coalesced loads (thread
+// i owns tile words i, i+kWtaPx, ...) into exact u16x2 pairs; phase 2 hands
+// each pixel's pairs to its own thread through shared memory.
+constexpr int kWtaPx = 128;
+constexpr int kWtaMaxWords = 36;  // lw <= 144 bytes (L <= 144)
+
+__global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ WtaArgs a) {
+  extern __shared__ uint32_t sums[];  // [pixel][2*nw + 1] u16x2 pairs (odd stride: no conflicts)
+  const int nw = a.lw / 4;
+  const int row = blockIdx.y;
+  const int u0 = blockIdx.x * kWtaPx;
+  const int npx = min(kWtaPx, a.w - u0);
+  const int tile_words = npx * nw;
+  const int stride = 2 * nw + 1;
+  const size_t base = size_t(row) * a.pitch + size_t(u0) * a.lw;
+  for (int i = threadIdx.x; i < tile_words; i += kWtaPx) {
+    uint32_t s01 = 0, s23 = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < a.paths) {
+        const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a.path[r] + base) + i);
+        s01 += __byte_perm(x, 0u, 0x4140);
+        s23 += __byte_perm(x, 0u, 0x4342);
+      }
+    }
+    const int px = i / nw, j = i - px * nw;
+    sums[px * stride + 2 * j] = s01;
+    sums[px * stride + 2 * j + 1] = s23;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= npx) return;
+  const long long p = (long long)row * a.w + u0 + t;
+  uint32_t minv = 0xFFFFFFFFu, last = 0, sbm1 = 0, sbp1 = 0;
+  int best = -2, cnt = 0;
+  const uint32_t* my = sums + t * stride;
+  for (int j = 0; j < nw; ++j) {
+    if (4 * j >= a.levels) break;
+    const uint32_t s01 = my[2 * j], s23 = my[2 * j + 1];
+    const uint32_t sv[4] = {s01 & 0xFFFFu, s01 >> 16, s23 & 0xFFFFu, s23 >> 16};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int d = 4 * j + q;
+      if (d < a.levels) {
+        wta_visit(sv[q], d, minv, best, cnt, last, sbm1, sbp1);
+        if (a.dump) a.dump[p * a.levels + d] = float(sv[q]);
+      }
+    }
+  }
+  const int near = (best + 1 < a.levels && sbp1 == minv) ? 1 : 0;
+  float r;
+  if (cnt - 1 - near > 0) {
+    r = kInvalid;
+  } else {
+    r = float(best);
+    if (best > 0 && best < a.levels - 1) {
+      const float cm = float(sbm1), cb = float(minv), cp = float(sbp1);
+      const float denom = cm + cp - 2.0f * cb;
+      if (denom > 0.0f) r += (cm - cp) / (2.0f * denom);
+    }
+  }
+  a.disp[p] = r;
+}
+
 // ------------------------------------------- LR check + post filters ----
 // consistency_filter (sgm.cpp:155-170), flat raw cost curve (:200-212),
 // best sample out of view (:216-222), restore_disparity (perspective.hpp:69-80).
@@ -823,7 +888,12 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
       wa.levels = levels;
       wa.disp = vol == 0 ? dl : dr;
       wa.dump = dump ? (vol == 0 ? dump->agg_left : dump->agg_right) : nullptr;
-      k_wta<<<cdiv(npix, 128), 128, 0, st>>>(wa);
+      if (L.lw / 4 <= kWtaMaxWords) {
+        const int smem = kWtaPx * (2 * (L.lw / 4) + 1) * 4;
+        k_wta_tiled<<<dim3(cdiv(w, kWtaPx), h), kWtaPx, smem, st>>>(wa);
+      } else {
+        k_wta<<<cdiv(npix, 128), 128, 0, st>>>(wa);
+      }
       RPD_LAUNCH_CHECK();
     }
     if (dump && dump->cost) {
