@@ -173,12 +173,13 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
 }
 
 // ----------------------------------------------------------- fit kernel ----
-constexpr int kFitCtas = 8;
-constexpr int kFitThreads = 1024;
-constexpr int kFitLanes = kFitCtas * kFitThreads;  // == oracle kFitLanes
+constexpr int kFitCtas = 16;      // non-portable cluster: 16 SMs share one fit
+constexpr int kFitThreads = 512;
+constexpr int kFitWarps = kFitThreads / 32;
+constexpr int kFitLanes = kFitCtas * kFitThreads;  // == oracle kFitLanes (8192)
 constexpr int kFitDynSmem = 192 * 1024;
-constexpr int kRowsCompact = kFitDynSmem / (kFitThreads * 8);   // 24
-constexpr int kRowsDouble = kFitDynSmem / (kFitThreads * 24);   // 8
+// observations are staged as SoA doubles (d, u, v): 24 B per element
+constexpr int kRowsStaged = kFitDynSmem / (kFitThreads * 24);  // 16 rows -> 131072 elements
 constexpr int kMaxRowsTrim = 64;
 
 struct FitKParams {
@@ -194,14 +195,14 @@ struct FitKParams {
 
 constexpr int kMaxNV = 10;  // values per cluster reduction
 struct FitShared {
-  double warp_part[32][kMaxNV];
+  double warp_part[kFitWarps][kMaxNV];
   double cta_part[2][kMaxNV];
   double peer[kMaxNV][kFitCtas];
   double bcast[kMaxNV];
   double sc[4][2];  // sin/cos of up to 4 pending probe angles
   int row_cnt[kMaxRowsTrim];
   int row_base[kMaxRowsTrim];
-  int warp_cnt[32];
+  int warp_cnt[kFitWarps];
 };
 
 struct LineFitD {
@@ -228,51 +229,48 @@ struct FitState {
 
 __device__ __forceinline__ void fit_get(const FitState& F, int m, long long i, double& d, double& u,
                                         double& v) {
-  if (F.compact) {
-    uint32_t uv;
-    float df;
-    if (F.staged) {
-      const uint2 e = reinterpret_cast<const uint2*>(F.dyn)[m * kFitThreads + threadIdx.x];
-      uv = e.x;
-      df = __uint_as_float(e.y);
-    } else {
-      uv = F.g_uv[i];
-      df = F.g_d[i];
-    }
+  if (F.staged) {
+    const double* e = reinterpret_cast<const double*>(F.dyn);
+    const int o = m * kFitThreads + threadIdx.x;
+    d = e[o];
+    u = e[kRowsStaged * kFitThreads + o];
+    v = e[2 * kRowsStaged * kFitThreads + o];
+  } else if (F.compact) {
+    const uint32_t uv = F.g_uv[i];
     u = double(uv & 0xFFFFu);
     v = double(uv >> 16);
-    d = double(df);
+    d = double(F.g_d[i]);
   } else {
-    if (F.staged) {
-      const double* e = reinterpret_cast<const double*>(F.dyn) + 3 * (m * kFitThreads + threadIdx.x);
-      d = e[0];
-      u = e[1];
-      v = e[2];
+    d = F.g_dd[i];
+    u = F.g_du[i];
+    v = F.g_dv[i];
+  }
+}
+
+// Stage the current source into shared memory as exact doubles (when it fits).
+__device__ void fit_stage(FitState& F) {
+  F.rows = int((F.k + kFitLanes - 1) / kFitLanes);
+  F.staged = F.rows <= kRowsStaged;
+  if (!F.staged) return;
+  double* e = reinterpret_cast<double*>(F.dyn);
+  for (int m = 0; m < F.rows; ++m) {
+    const long long i = (long long)m * kFitLanes + F.lane;
+    if (i >= F.k) break;
+    double d, u, v;
+    if (F.compact) {
+      const uint32_t uv = F.g_uv[i];
+      u = double(uv & 0xFFFFu);
+      v = double(uv >> 16);
+      d = double(F.g_d[i]);
     } else {
       d = F.g_dd[i];
       u = F.g_du[i];
       v = F.g_dv[i];
     }
-  }
-}
-
-// Stage the current source into shared memory (when it fits).
-__device__ void fit_stage(FitState& F) {
-  F.rows = int((F.k + kFitLanes - 1) / kFitLanes);
-  F.staged = F.rows <= (F.compact ? kRowsCompact : kRowsDouble);
-  if (!F.staged) return;
-  for (int m = 0; m < F.rows; ++m) {
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (i >= F.k) break;
-    if (F.compact) {
-      reinterpret_cast<uint2*>(F.dyn)[m * kFitThreads + threadIdx.x] =
-          make_uint2(F.g_uv[i], __float_as_uint(F.g_d[i]));
-    } else {
-      double* e = reinterpret_cast<double*>(F.dyn) + 3 * (m * kFitThreads + threadIdx.x);
-      e[0] = F.g_dd[i];
-      e[1] = F.g_du[i];
-      e[2] = F.g_dv[i];
-    }
+    const int o = m * kFitThreads + threadIdx.x;
+    e[o] = d;
+    e[kRowsStaged * kFitThreads + o] = u;
+    e[2 * kRowsStaged * kFitThreads + o] = v;
   }
   __syncthreads();
 }
@@ -295,9 +293,9 @@ __device__ void cluster_sum(FitState& F, double (&x)[NV]) {
   if (warp == 0) {
     double y[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) y[q] = S.warp_part[lane][q];
+    for (int q = 0; q < NV; ++q) y[q] = lane < kFitWarps ? S.warp_part[lane][q] : 0.0;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1)
+    for (int off = 1; off < kFitWarps; off <<= 1)
 #pragma unroll
       for (int q = 0; q < NV; ++q) y[q] += __shfl_down_sync(0xFFFFFFFFu, y[q], off);
     if (lane == 0)
@@ -586,7 +584,7 @@ __device__ long long fit_trim(FitState& F, const LineFitD& first, double rms) {
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
-      for (int q = 0; q < 32; ++q) t += S.warp_cnt[q];
+      for (int q = 0; q < kFitWarps; ++q) t += S.warp_cnt[q];
       S.row_cnt[m] = t;
     }
     __syncthreads();
@@ -707,7 +705,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ 
 
 void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
   RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitDynSmem));
-  RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+  RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   if (!req.compact && req.k_host > (long long)kMaxRowsTrim * kFitLanes)
     throw InvalidArg("fit: too many observations for the device fit (max 524288)");
   FitKParams P{};
