@@ -10,7 +10,7 @@
 
 namespace rpdg {
 
-__device__ __forceinline__ int uf_find(const int* __restrict__ parent, int p) {
+__device__ __forceinline__ int uf_find(const int* parent, int p) {
   int q = parent[p];
   while (q != p) {
     p = q;
@@ -54,11 +54,15 @@ __global__ void k_uf_flatten(int h, int w, int* parent);
 // then only tile-border pixels union across tiles in global memory.
 constexpr int kTileW = 32, kTileH = 16;
 
-__device__ __forceinline__ int uf_find_s(const int* lab, int p) {
+// find with path halving: every write re-points a node to one of its own
+// ancestors, so concurrent halving by other threads is benign.
+__device__ __forceinline__ int uf_find_s(int* lab, int p) {
   int q = lab[p];
   while (q != p) {
+    const int r = lab[q];
+    if (r != q) lab[p] = r;
     p = q;
-    q = lab[p];
+    q = r;
   }
   return p;
 }

@@ -129,6 +129,7 @@ __global__ void k_hist_bin(const float* __restrict__ d2, int h, int w, double bw
   double x = 0, y = 0;
   bool ok = n > 0 && u + 1 < w && v + 1 < h && hist_vector(d2, w, u, v, x, y);
   bool outside = false;
+  long long slot = -1;
   if (ok) {
     const double o = *origin;
     long long i = (long long)floor((x - o) / bw), j = (long long)floor((y - o) / bw);
@@ -138,8 +139,13 @@ __global__ void k_hist_bin(const float* __restrict__ d2, int h, int w, double bw
     if (dj < -half || dj > half)
       outside = true;
     else
-      atomicAdd(reinterpret_cast<unsigned long long*>(&band[i * (2 * half + 1) + (dj + half)]), 1ull);
+      slot = i * (2 * half + 1) + (dj + half);
   }
+  // neighbouring pixels mostly share a bin: one atomic per distinct bin per warp
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, slot);
+  if (slot >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&band[slot]),
+              (unsigned long long)__popc(peers));
   const unsigned bal = __ballot_sync(0xFFFFFFFFu, outside);
   if ((threadIdx.x & 31) == 0 && bal)
     atomicAdd(reinterpret_cast<unsigned long long*>(&meta[2]), (unsigned long long)__popc(bal));

@@ -426,9 +426,14 @@ __global__ void __launch_bounds__(kBfsThreads)
 // First appearance of each label in scan order (:218-224).
 __global__ void k_label_minidx(const int32_t* __restrict__ labels, long long n,
                                int* __restrict__ minidx) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x)
-    atomicMin(&minidx[labels[p]], int(p));
+  for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < n;
+       p0 += (long long)gridDim.x * blockDim.x) {
+    const long long p = p0 + threadIdx.x;
+    const int l = p < n ? labels[p] : -1;
+    // lanes of a warp sharing a label: only the lowest index competes
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, l);
+    if (l >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minidx[l], int(p));
+  }
 }
 
 __global__ void k_first_flags(const int32_t* __restrict__ labels, const int* __restrict__ minidx,
