@@ -1,0 +1,427 @@
+// rpd_b200.hpp — header-only C++17 drop-in for the reference `namespace rpd`
+// hot path (/root/reference/proj/include/rpd/*.hpp), implemented over the
+// C-ABI of include/rpd_b200.h (link with -lrpd_b200).
+//
+// Same function names, argument meaning, result types and exception types
+// (std::invalid_argument, std::runtime_error, DegenerateFitError).  The only
+// representational change: rasters are a small row-major std::vector raster
+// instead of Eigen arrays (Eigen is not a dependency of this library); index
+// (v, u) = v*W + u exactly like Raster<T> (types.hpp:9-10).
+//
+// Each calling thread gets its own device context (rpd_ctx) on the current
+// device, created lazily: functions are reentrant like the reference's.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rpd_b200.h"
+
+namespace rpd_b200 {
+
+// ------------------------------------------------------------------- types --
+template <typename T>
+struct Raster {  // types.hpp:9-10 (row-major, (v, u))
+  std::vector<T> data;
+  int h = 0, w = 0;
+  Raster() = default;
+  Raster(int rows, int cols, T fill = T{}) : data(size_t(rows) * cols, fill), h(rows), w(cols) {}
+  static Raster Constant(int rows, int cols, T v) { return Raster(rows, cols, v); }
+  static Raster Zero(int rows, int cols) { return Raster(rows, cols, T{}); }
+  int rows() const { return h; }
+  int cols() const { return w; }
+  T& operator()(int v, int u) { return data[size_t(v) * w + u]; }
+  const T& operator()(int v, int u) const { return data[size_t(v) * w + u]; }
+  T* ptr() { return data.data(); }
+  const T* ptr() const { return data.data(); }
+};
+using GrayImage = Raster<float>;     // types.hpp:13
+using DisparityMap = Raster<float>;  // types.hpp:16
+using LabelMap = Raster<int>;        // types.hpp:19
+inline constexpr float kInvalidDisparity = -1.0f;  // types.hpp:21
+inline bool is_valid(float d) { return d != kInvalidDisparity; }
+
+struct RoadModel {  // types.hpp:33-37
+  double a0 = 0.0, a1 = 0.0, phi = 0.0;
+};
+inline double road_disparity_at(const RoadModel& m, double u, double v) {  // types.hpp:39-41
+  return m.a0 + m.a1 * (v * std::cos(m.phi) - u * std::sin(m.phi));
+}
+
+struct DegenerateFitError : std::runtime_error {  // pipeline.hpp:17-19
+  using std::runtime_error::runtime_error;
+};
+
+// PipelineConfig (config.hpp:10-36) with the `sgm_paths` extension.
+struct PipelineConfig : rpd_config {
+  PipelineConfig() { rpd_config_default(this); }
+  void validate() const;
+};
+
+// ----------------------------------------------------------------- context --
+namespace detail {
+struct CtxDeleter {
+  void operator()(rpd_ctx* c) const { rpd_ctx_destroy(c); }
+};
+inline int& device_slot() {
+  thread_local int dev = 0;
+  return dev;
+}
+inline rpd_ctx* ctx() {
+  thread_local std::unique_ptr<rpd_ctx, CtxDeleter> c;
+  thread_local int bound = -1;
+  if (!c || bound != device_slot()) {
+    rpd_ctx* raw = nullptr;
+    const rpd_status st = rpd_ctx_create(device_slot(), 0, 0, 0, &raw);
+    if (st != RPD_OK) throw std::runtime_error("rpd_b200: cannot create a CUDA context");
+    c.reset(raw);
+    bound = device_slot();
+  }
+  return c.get();
+}
+inline void check(rpd_status st) {
+  if (st == RPD_OK) return;
+  const std::string msg = rpd_last_error(ctx());
+  switch (st) {
+    case RPD_EINVAL: throw std::invalid_argument(msg);
+    case RPD_EDEGENERATE:
+      if (msg.rfind("road fit failed", 0) == 0 || msg.rfind("road refit failed", 0) == 0)
+        throw DegenerateFitError(msg);
+      throw std::runtime_error(msg);
+    default: throw std::runtime_error("rpd_b200: " + msg);
+  }
+}
+}  // namespace detail
+
+// Selects the CUDA device used by the calling thread.
+inline void set_device(int device) { detail::device_slot() = device; }
+
+inline void PipelineConfig::validate() const { detail::check(rpd_config_validate(detail::ctx(), this)); }
+
+inline void apply_key_value(PipelineConfig& c, const std::string& key, const std::string& value) {
+  detail::check(rpd_config_set(detail::ctx(), &c, key.c_str(), value.c_str()));
+}
+
+// ------------------------------------------------------------ perspective --
+struct RowShiftTable {  // perspective.hpp:15-18
+  std::vector<double> shifts;
+  double delta_pt = 0.0;
+};
+inline RowShiftTable compute_row_shifts(const RoadModel& m, int width, int height,
+                                        double delta_pt) {
+  RowShiftTable t;
+  t.delta_pt = delta_pt;
+  t.shifts.resize(size_t(height));
+  const rpd_road_model rm{m.a0, m.a1, m.phi};
+  detail::check(rpd_compute_row_shifts(detail::ctx(), &rm, width, height, delta_pt,
+                                       t.shifts.data()));
+  return t;
+}
+struct WarpResult {  // perspective.hpp:37-40
+  GrayImage image;
+  Raster<unsigned char> in_view;
+};
+inline WarpResult warp_right_image(const GrayImage& right, const RowShiftTable& t) {
+  if (int(t.shifts.size()) != right.rows())
+    throw std::invalid_argument("warp_right_image: table length != image height");
+  WarpResult r{GrayImage(right.rows(), right.cols()),
+               Raster<unsigned char>(right.rows(), right.cols())};
+  detail::check(rpd_warp_right_image(detail::ctx(), right.ptr(), right.rows(), right.cols(),
+                                     t.shifts.data(), r.image.ptr(), r.in_view.ptr()));
+  return r;
+}
+inline DisparityMap restore_disparity(const DisparityMap& d0, const RowShiftTable& t) {
+  if (int(t.shifts.size()) != d0.rows())
+    throw std::invalid_argument("restore_disparity: table length != map height");
+  DisparityMap d1(d0.rows(), d0.cols());
+  detail::check(rpd_restore_disparity(detail::ctx(), d0.ptr(), d0.rows(), d0.cols(),
+                                      t.shifts.data(), d1.ptr()));
+  return d1;
+}
+
+// -------------------------------------------------------------------- SGM --
+struct CostVolume {  // sgm.hpp:15-33
+  int width = 0, height = 0, d_max = 0;
+  std::vector<float> costs;
+  CostVolume() = default;
+  CostVolume(int w, int h, int dm)
+      : width(w), height(h), d_max(dm), costs(size_t(w) * h * (dm + 1), 0.0f) {}
+  int levels() const { return d_max + 1; }
+  float& at(int v, int u, int d) { return costs[(size_t(v) * width + u) * levels() + d]; }
+  float at(int v, int u, int d) const { return costs[(size_t(v) * width + u) * levels() + d]; }
+};
+struct SgmParams {  // sgm.hpp:35-44
+  float lambda1 = 8.0f, lambda2 = 32.0f;
+  std::vector<std::array<int, 2>> directions = kEightDirections();
+  int census_window = 5;
+  static std::vector<std::array<int, 2>> kEightDirections() {
+    return {{{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {1, 1}, {-1, 1}, {1, -1}, {-1, -1}}};
+  }
+};
+inline CostVolume census_cost_volume(const GrayImage& left, const GrayImage& right, int d_max,
+                                     int window, const Raster<unsigned char>* in_view = nullptr) {
+  if (left.rows() != right.rows() || left.cols() != right.cols())
+    throw std::invalid_argument("census_cost_volume: dimension mismatch");
+  if (d_max >= left.cols()) throw std::invalid_argument("census_cost_volume: d_max >= width");
+  CostVolume vol(left.cols(), left.rows(), d_max);
+  detail::check(rpd_census_cost_volume(detail::ctx(), left.ptr(), right.ptr(), left.rows(),
+                                       left.cols(), d_max, window,
+                                       in_view ? in_view->ptr() : nullptr, vol.costs.data()));
+  return vol;
+}
+inline CostVolume aggregate_costs(const CostVolume& vol, const SgmParams& p) {
+  CostVolume out(vol.width, vol.height, vol.d_max);
+  std::vector<int32_t> dirs;
+  for (const auto& d : p.directions) {
+    dirs.push_back(d[0]);
+    dirs.push_back(d[1]);
+  }
+  detail::check(rpd_aggregate_costs(detail::ctx(), vol.costs.data(), vol.height, vol.width,
+                                    vol.d_max, dirs.data(), int(p.directions.size()), p.lambda1,
+                                    p.lambda2, out.costs.data()));
+  return out;
+}
+inline CostVolume swap_reference(const CostVolume& vol) {
+  CostVolume out(vol.width, vol.height, vol.d_max);
+  detail::check(rpd_swap_reference(detail::ctx(), vol.costs.data(), vol.height, vol.width,
+                                   vol.d_max, out.costs.data()));
+  return out;
+}
+inline DisparityMap select_disparity(const CostVolume& agg) {
+  DisparityMap d(agg.height, agg.width);
+  detail::check(rpd_select_disparity(detail::ctx(), agg.costs.data(), agg.height, agg.width,
+                                     agg.d_max, d.ptr()));
+  return d;
+}
+inline void consistency_filter(DisparityMap& left, const DisparityMap& right, double thr) {
+  detail::check(rpd_consistency_filter(detail::ctx(), left.ptr(), right.ptr(), left.rows(),
+                                       left.cols(), thr));
+}
+struct MatchResult {  // sgm.hpp:69-73
+  DisparityMap d0, d1;
+  RowShiftTable shifts;
+};
+inline MatchResult match_pair(const GrayImage& left, const GrayImage& right, const RoadModel& m,
+                              const PipelineConfig& cfg, int d_max) {
+  if (left.rows() != right.rows() || left.cols() != right.cols())
+    throw std::invalid_argument("match_pair: dimension mismatch");
+  MatchResult r{DisparityMap(left.rows(), left.cols()), DisparityMap(left.rows(), left.cols()),
+                RowShiftTable{std::vector<double>(size_t(left.rows())), cfg.delta_pt}};
+  const rpd_road_model rm{m.a0, m.a1, m.phi};
+  detail::check(rpd_match_pair(detail::ctx(), left.ptr(), right.ptr(), left.rows(), left.cols(),
+                               &rm, &cfg, d_max, r.d0.ptr(), r.d1.ptr(), r.shifts.shifts.data()));
+  return r;
+}
+
+// ---------------------------------------------------------- road geometry --
+struct RoadObservations {  // road_geometry.hpp:12-18
+  std::vector<double> d, u, v;
+  long count() const { return long(d.size()); }
+};
+struct LineFit {  // road_geometry.hpp:20-23
+  RoadModel model;
+  double e0min = 0.0;
+};
+struct RoadFit {  // road_geometry.hpp:34-38
+  RoadModel model;
+  double e0min = 0.0;
+  long used = 0;
+};
+struct RectRoi {  // road_geometry.hpp:45-47
+  int u0, v0, width, height;
+};
+struct TransformResult {  // road_geometry.hpp:55-58
+  DisparityMap d2;
+  long clamped = 0;
+};
+inline LineFit fit_line(const RoadObservations& o, double phi) {
+  rpd_line_fit f{};
+  detail::check(rpd_fit_line(detail::ctx(), o.d.data(), o.u.data(), o.v.data(), o.count(), phi, &f));
+  return LineFit{{f.model.a0, f.model.a1, f.model.phi}, f.e0min};
+}
+inline RoadModel estimate_roll(const RoadObservations& o, double lo, double hi, double tol) {
+  rpd_road_model m{};
+  detail::check(rpd_estimate_roll(detail::ctx(), o.d.data(), o.u.data(), o.v.data(), o.count(),
+                                  lo, hi, tol, &m));
+  return RoadModel{m.a0, m.a1, m.phi};
+}
+inline RoadFit fit_road(const RoadObservations& o, double bracket, double tol) {
+  rpd_road_fit f{};
+  detail::check(rpd_fit_road(detail::ctx(), o.d.data(), o.u.data(), o.v.data(), o.count(),
+                             bracket, tol, &f));
+  return RoadFit{{f.model.a0, f.model.a1, f.model.phi}, f.e0min, long(f.used)};
+}
+inline RoadObservations sample_observations(const DisparityMap& d1, const RectRoi* roi = nullptr,
+                                            long cap = 100000) {
+  const size_t n = std::min<size_t>(size_t(d1.rows()) * d1.cols(), size_t(cap));
+  RoadObservations o;
+  o.d.resize(n);
+  o.u.resize(n);
+  o.v.resize(n);
+  int64_t k = 0;
+  rpd_rect_roi r{};
+  if (roi) r = rpd_rect_roi{roi->u0, roi->v0, roi->width, roi->height};
+  detail::check(rpd_sample_observations(detail::ctx(), d1.ptr(), d1.rows(), d1.cols(),
+                                        roi ? &r : nullptr, cap, o.d.data(), o.u.data(),
+                                        o.v.data(), &k));
+  o.d.resize(size_t(k));
+  o.u.resize(size_t(k));
+  o.v.resize(size_t(k));
+  return o;
+}
+inline TransformResult transform_disparity(const DisparityMap& d1, const RoadModel& m,
+                                           double delta_dt) {
+  TransformResult t{DisparityMap(d1.rows(), d1.cols()), 0};
+  const rpd_road_model rm{m.a0, m.a1, m.phi};
+  int64_t c = 0;
+  detail::check(rpd_transform_disparity(detail::ctx(), d1.ptr(), d1.rows(), d1.cols(), &rm,
+                                        delta_dt, t.d2.ptr(), &c));
+  t.clamped = long(c);
+  return t;
+}
+
+// ----------------------------------------------------------- segmentation --
+struct SuperpixelMap {  // segmentation.hpp:10-20
+  struct Center {
+    double cu = 0.0, cv = 0.0, value = 0.0;
+  };
+  LabelMap labels;
+  std::vector<Center> centers;
+  int count = 0;
+  double spacing = 0.0;
+};
+struct Histogram2D {  // segmentation.hpp:34-41
+  double bin_width = 0.25;
+  double origin = 0.0;
+  Raster<long long> counts;
+  long long total = 0;
+  double center(long bin) const { return origin + (bin + 0.5) * bin_width; }
+};
+struct ThresholdResult {  // segmentation.hpp:48-55
+  double t_r = 0.0, t_s = 0.0, mu1 = 0.0, mu2 = 0.0, excluded_fraction = 0.0;
+  bool degenerate = false;
+};
+inline SuperpixelMap slic(const DisparityMap& d2, int p, double compactness, int iterations) {
+  SuperpixelMap sp;
+  sp.labels = LabelMap(d2.rows(), d2.cols());
+  const int cap = std::max(1, std::min(d2.rows() * d2.cols(), 4 * std::max(p, 1) + 64));
+  std::vector<rpd_center> c(static_cast<size_t>(cap));
+  int32_t count = 0;
+  detail::check(rpd_slic(detail::ctx(), d2.ptr(), d2.rows(), d2.cols(), p, compactness,
+                         iterations, sp.labels.ptr(), c.data(), cap, &count, &sp.spacing));
+  sp.count = count;
+  for (int k = 0; k < std::min(count, cap); ++k)
+    sp.centers.push_back({c[size_t(k)].cu, c[size_t(k)].cv, c[size_t(k)].value});
+  return sp;
+}
+inline DisparityMap pool_superpixels(const DisparityMap& d2, const SuperpixelMap& sp) {
+  if (d2.rows() != sp.labels.rows() || d2.cols() != sp.labels.cols())
+    throw std::invalid_argument("pool_superpixels: dimension mismatch");
+  DisparityMap d3(d2.rows(), d2.cols());
+  detail::check(rpd_pool_superpixels(detail::ctx(), d2.ptr(), sp.labels.ptr(), sp.count,
+                                     d2.rows(), d2.cols(), d3.ptr()));
+  return d3;
+}
+inline Histogram2D build_histogram(const DisparityMap& d2, double bin_width) {
+  Histogram2D hist;
+  hist.bin_width = bin_width;
+  int64_t n = 0, total = 0;
+  const rpd_status st = rpd_build_histogram(detail::ctx(), d2.ptr(), d2.rows(), d2.cols(),
+                                            bin_width, nullptr, 0, &n, &hist.origin, &total);
+  if (st != RPD_ECAPACITY) detail::check(st);
+  hist.counts = Raster<long long>(int(n), int(n));
+  if (n > 0)
+    detail::check(rpd_build_histogram(detail::ctx(), d2.ptr(), d2.rows(), d2.cols(), bin_width,
+                                      reinterpret_cast<int64_t*>(hist.counts.ptr()), n, &n,
+                                      &hist.origin, &total));
+  hist.total = total;
+  return hist;
+}
+inline ThresholdResult find_road_threshold(const Histogram2D& h, double delta_pd,
+                                           double tau = 3.0) {
+  rpd_threshold t{};
+  detail::check(rpd_find_road_threshold(detail::ctx(),
+                                        reinterpret_cast<const int64_t*>(h.counts.ptr()),
+                                        h.counts.rows(), h.bin_width, h.origin, h.total, delta_pd,
+                                        tau, &t));
+  return ThresholdResult{t.t_r, t.t_s, t.mu1, t.mu2, t.excluded_fraction, t.degenerate != 0};
+}
+inline LabelMap connected_components(const LabelMap& mask, int connectivity = 8) {
+  LabelMap out(mask.rows(), mask.cols());
+  detail::check(rpd_connected_components(detail::ctx(), mask.ptr(), mask.rows(), mask.cols(),
+                                         connectivity, out.ptr()));
+  return out;
+}
+inline LabelMap detect_potholes(const DisparityMap& d3, const SuperpixelMap& sp,
+                                const ThresholdResult& thr, int border_margin,
+                                int min_superpixels, int connectivity = 8) {
+  LabelMap out(d3.rows(), d3.cols());
+  const rpd_threshold t{thr.t_r, thr.t_s, thr.mu1, thr.mu2, thr.excluded_fraction,
+                        thr.degenerate ? 1 : 0};
+  detail::check(rpd_detect_potholes(detail::ctx(), d3.ptr(), sp.labels.ptr(), sp.spacing,
+                                    d3.rows(), d3.cols(), &t, border_margin, min_superpixels,
+                                    connectivity, out.ptr()));
+  return out;
+}
+
+// --------------------------------------------------------------- pipeline --
+struct StageTime {  // pipeline.hpp:21-24
+  std::string name;
+  double ms;
+};
+struct DetectResult {  // pipeline.hpp:26-38
+  DisparityMap d0, d1, d2, d3;
+  SuperpixelMap superpixels;
+  LabelMap labels;
+  RoadFit fit;
+  ThresholdResult threshold;
+  long clamped = 0;
+  std::vector<StageTime> stage_times;  // device time per StageClock lap
+  double total_ms = 0.0;
+};
+inline DetectResult detect_potholes_pipeline(const GrayImage& left, const GrayImage& right,
+                                             const PipelineConfig& cfg) {
+  if (left.rows() != right.rows() || left.cols() != right.cols())
+    throw std::invalid_argument("match_pair: dimension mismatch");
+  const int h = left.rows(), w = left.cols();
+  DetectResult r;
+  r.d0 = r.d1 = r.d2 = r.d3 = DisparityMap(h, w);
+  r.labels = LabelMap(h, w);
+  r.superpixels.labels = LabelMap(h, w);
+  std::vector<rpd_center> centers(size_t(std::max(1, h * w)));
+  rpd_detect_out out{};
+  out.d0 = r.d0.ptr();
+  out.d1 = r.d1.ptr();
+  out.d2 = r.d2.ptr();
+  out.d3 = r.d3.ptr();
+  out.labels = r.labels.ptr();
+  out.sp_labels = r.superpixels.labels.ptr();
+  out.centers = centers.data();
+  out.centers_cap = int(centers.size());
+  detail::check(rpd_detect(detail::ctx(), left.ptr(), right.ptr(), h, w, &cfg, &out));
+  r.superpixels.count = out.sp_count;
+  r.superpixels.spacing = out.sp_spacing;
+  for (int k = 0; k < out.sp_count; ++k)
+    r.superpixels.centers.push_back({centers[size_t(k)].cu, centers[size_t(k)].cv,
+                                     centers[size_t(k)].value});
+  r.fit = RoadFit{{out.fit.model.a0, out.fit.model.a1, out.fit.model.phi}, out.fit.e0min,
+                  long(out.fit.used)};
+  r.threshold = ThresholdResult{out.threshold.t_r, out.threshold.t_s, out.threshold.mu1,
+                                out.threshold.mu2, out.threshold.excluded_fraction,
+                                out.threshold.degenerate != 0};
+  r.clamped = long(out.clamped);
+  static const char* names[RPD_NUM_STAGES] = {"sgm_bootstrap", "road_fit", "sgm_pt",
+                                              "road_refit", "disparity_transform", "slic",
+                                              "detect"};
+  for (int i = 0; i < RPD_NUM_STAGES; ++i) r.stage_times.push_back({names[i], out.stage_ms[i]});
+  r.total_ms = out.total_ms;
+  return r;
+}
+
+}  // namespace rpd_b200

@@ -25,6 +25,13 @@ ORACLE_LIB = ROOT / "oracle" / "_build" / "librpd_oracle.so"
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running parity case")
+    # host-only helper libraries (scene generator, oracle) are built on demand
+    synth_src = ROOT / "paper_2012_10802_b200" / "synth" / "rpd_synth.cpp"
+    synth_so = ROOT / "paper_2012_10802_b200" / "_lib" / "librpd_synth.so"
+    if not synth_so.exists():
+        synth_so.parent.mkdir(exist_ok=True)
+        subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", str(synth_so),
+                        str(synth_src)], check=True)
 
 
 def _ensure_oracle():

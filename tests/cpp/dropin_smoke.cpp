@@ -1,0 +1,86 @@
+// C++ drop-in smoke test: a handful of the reference's own unit-test known
+// answers (test_sgm.cpp, test_perspective.cpp, test_segmentation.cpp) written
+// against rpd_b200.hpp exactly as they are written against rpd::.  Compiled
+// on CPU by tests/test_abi.py; run on the GPU by tests/test_cpp_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "rpd_b200.hpp"
+
+using namespace rpd_b200;
+
+static int failures = 0;
+#define CHECK(x)                                                       \
+  do {                                                                 \
+    if (!(x)) {                                                        \
+      std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #x);         \
+      ++failures;                                                      \
+    }                                                                  \
+  } while (0)
+
+int main() {
+  {  // test_sgm.cpp:86-93
+    GrayImage img = GrayImage::Constant(8, 8, 100.0f);
+    CostVolume vol = census_cost_volume(img, img, 3, 5);
+    for (int v = 0; v < 8; ++v)
+      for (int u = 3; u < 8; ++u)
+        for (int d = 0; d <= 3; ++d) CHECK(vol.at(v, u, d) == 0.0f);
+    CHECK(vol.at(0, 0, 1) == 24.0f);
+  }
+  {  // test_sgm.cpp:158-181 parabola
+    CostVolume vol(1, 1, 6);
+    const float c[7] = {40, 30, 4, 2, 4, 31, 41};
+    for (int d = 0; d <= 6; ++d) vol.at(0, 0, d) = c[d];
+    CHECK(std::fabs(select_disparity(vol)(0, 0) - 3.0f) < 1e-6f);
+  }
+  {  // test_perspective.cpp:36-61
+    GrayImage img(1, 4);
+    img(0, 0) = 10; img(0, 1) = 20; img(0, 2) = 30; img(0, 3) = 40;
+    WarpResult w1 = warp_right_image(img, {{1.0}, 0.0});
+    CHECK(w1.image(0, 0) == 0.0f && w1.in_view(0, 0) == 0 && w1.image(0, 1) == 10.0f);
+  }
+  {  // test_segmentation.cpp:294-299 diagonal touch
+    LabelMap m = LabelMap::Zero(3, 3);
+    m(0, 0) = 1;
+    m(1, 1) = 1;
+    LabelMap a = connected_components(m, 8), b = connected_components(m, 4);
+    int ma = 0, mb = 0;
+    for (int x : a.data) ma = std::max(ma, x);
+    for (int x : b.data) mb = std::max(mb, x);
+    CHECK(ma == 1 && mb == 2);
+  }
+  {  // test_sgm.cpp:224-230 error behaviour
+    GrayImage a = GrayImage::Zero(4, 8), b = GrayImage::Zero(4, 9);
+    bool threw = false;
+    try {
+      census_cost_volume(a, b, 2, 5);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // full pipeline on a textured pair: left(u) = right(u - 6)
+    const int h = 96, w = 160;
+    GrayImage left(h, w), right(h, w);
+    unsigned s = 12345;
+    for (int v = 0; v < h; ++v)
+      for (int u = 0; u < w; ++u) {
+        s = s * 1103515245u + 12345u;
+        right(v, u) = float((s >> 16) & 255);
+      }
+    for (int v = 0; v < h; ++v)
+      for (int u = 0; u < w; ++u) left(v, u) = right(v, std::max(0, u - 6));
+    PipelineConfig cfg;
+    cfg.d_max = 31;
+    cfg.superpixels = 100;
+    try {
+      DetectResult r = detect_potholes_pipeline(left, right, cfg);
+      CHECK(r.superpixels.count > 50 && r.stage_times.size() == 7);
+    } catch (const DegenerateFitError& e) {
+      std::printf("degenerate fit (acceptable for a planar-free pair): %s\n", e.what());
+    }
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
