@@ -197,6 +197,10 @@ typedef struct rpd_stats {
 rpd_status rpd_ctx_set_profiling(rpd_ctx* ctx, int enable);
 rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out);
 
+/* Test hook: the device's roll-angle sin/cos (double-double, correctly
+ * rounded with overwhelming probability) for n angles. */
+rpd_status rpd_debug_sincos(rpd_ctx* ctx, const double* x, int n, double* s, double* c);
+
 /* Parity extension: runs the production match_pair SGM path and materialises
  * its intermediates in the reference float layout (v*W+u)*(d_max+1)+d:
  * census_cost_volume, aggregate_costs of it and of swap_reference(it), and the

@@ -244,6 +244,7 @@ _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
     "rpd_detect_fetch": (C.c_int, [_vp, C.POINTER(DetectOut)]),
     "rpd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rpd_ctx_stats": (C.c_int, [_vp, C.POINTER(Stats)]),
+    "rpd_debug_sincos": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
 }
 _SIGS["rpd_match_pair_dump"] = (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
                                           C.POINTER(Config), C.c_int, _vp, _vp, _vp, _vp, _vp])
@@ -393,6 +394,13 @@ class Context:
         out = out if out is not None else DetectOut()
         self._check(self.dll.rpd_detect_fetch(self.handle, C.byref(out)))
         return out
+
+    def debug_sincos(self, x):
+        x = _f64(x)
+        s = np.empty_like(x)
+        c = np.empty_like(x)
+        self._check(self.dll.rpd_debug_sincos(self.handle, _ptr(x), x.shape[0], _ptr(s), _ptr(c)))
+        return s, c
 
     def set_profiling(self, enable: bool):
         self._check(self.dll.rpd_ctx_set_profiling(self.handle, 1 if enable else 0))

@@ -11,6 +11,10 @@
 
 using namespace rpdg;
 
+namespace rpdg {
+void sincos_probe_dev(const double* x, int n, double* s, double* c, cudaStream_t st);
+}
+
 namespace {
 
 FitOut run_fit(rpd_ctx* ctx, FitRequest req) {
@@ -231,6 +235,18 @@ rpd_status rpd_detect_potholes(rpd_ctx* ctx, const float* d3, const int32_t* sp_
     int32_t* o = ctx->ws.get<int32_t>("abi_lab1", n);
     detect_potholes_dev(ctx, a, l, spacing, h, w, t, margin, min_sp, conn, o, nullptr);
     download(ctx, out, o, sizeof(int32_t) * n);
+  });
+}
+
+rpd_status rpd_debug_sincos(rpd_ctx* ctx, const double* x, int n, double* s, double* c) {
+  return guard(ctx, [&] {
+    if (n <= 0) return;
+    const double* dx = upload(ctx, "abi_dbg_x", x, size_t(n));
+    double* ds = ctx->ws.get<double>("abi_dbg_s", size_t(n));
+    double* dc = ctx->ws.get<double>("abi_dbg_c", size_t(n));
+    sincos_probe_dev(dx, n, ds, dc, ctx->stream);
+    download(ctx, s, ds, sizeof(double) * size_t(n));
+    download(ctx, c, dc, sizeof(double) * size_t(n));
   });
 }
 
