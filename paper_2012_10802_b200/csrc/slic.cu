@@ -101,11 +101,28 @@ constexpr int kMaxBuckets = kBucketThreads * kBucketItems;
 
 __global__ void __launch_bounds__(kBucketThreads)
     k_buckets(Centers c, int K, int w, int h, int B, int nbx, int nby, int* __restrict__ cell_start,
-              int* __restrict__ cell_items) {
+              int* __restrict__ cell_items, CenterSums s, int finalize) {
   using Scan = cub::BlockScan<int, kBucketThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int cnt[kMaxBuckets];
   const int nb = nbx * nby;
+  if (finalize) {  // update_centers tail (segmentation.cpp:88-92) of the previous assignment
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      const int l = k + 1;
+      const int n = s.n[l];
+      if (n > 0) {
+        const double dn = double(n);
+        c.cu[k] = double(s.su[l]) / dn;
+        c.cv[k] = double(s.sv[l]) / dn;
+        c.val[k] = fixed_to_double(s.sx[l]) / dn;
+      }
+      s.n[l] = 0;
+      s.su[l] = 0;
+      s.sv[l] = 0;
+      s.sx[l] = Acc128{0ull, 0ll};
+    }
+    __syncthreads();
+  }
   for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -154,15 +171,12 @@ struct AssignArgs {
   int32_t* labels;
   int* orphan_list;
   int* orphan_count;
+  int* inexact;
 };
 
-// assign_pixels, segmentation.cpp:30-57 (windowed part).
-__global__ void k_assign(const __grid_constant__ AssignArgs a) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
-  if (u >= a.w) return;
-  const size_t p = size_t(v) * a.w + u;
-  const double x = double(a.vals[p]);
+// assign_pixels, segmentation.cpp:30-57 (windowed part) for one pixel by
+// walking the bucket grid; used when a tile's candidate list overflows.
+__device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, double x) {
   const int bx0 = u - a.win < 0 ? 0 : (u - a.win) / a.B;
   const int bx1 = min(a.nbx - 1, (u + a.win) / a.B);
   const int by0 = v - a.win < 0 ? 0 : (v - a.win) / a.B;
@@ -185,18 +199,111 @@ __global__ void k_assign(const __grid_constant__ AssignArgs a) {
         }
       }
     }
-  if (bk < 0) {
-    a.labels[p] = 0;
-    const int slot = atomicAdd(a.orphan_count, 1);
-    a.orphan_list[slot] = int(p);
-  } else {
-    a.labels[p] = bk + 1;
+  return bk;
+}
+
+// Tiled assign_pixels with the next update_centers' sums fused in.  A CTA owns
+// a 32x8 pixel tile; the centres of every bucket that can reach the tile are
+// staged once in shared memory, each pixel keeps the lexicographic minimum
+// (dist, k) of the centres whose window holds it (== ascending-k strict `<`),
+// and — when SUMS — the pixel's (1, u, v, value) is added to its label's sums
+// with warp run aggregation (a warp is one tile row).  Pixels without a window
+// are left for the fallback kernel, which adds their sums itself.
+constexpr int kTileU = 32, kTileV = 8, kMaxTileCenters = 384;
+
+template <bool SUMS>
+__global__ void __launch_bounds__(kTileU* kTileV)
+    k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
+  __shared__ int s_cnt;
+  __shared__ int s_k[kMaxTileCenters], s_icu[kMaxTileCenters], s_icv[kMaxTileCenters];
+  __shared__ double s_cu[kMaxTileCenters], s_cv[kMaxTileCenters], s_val[kMaxTileCenters];
+  const int tx = threadIdx.x % kTileU, ty = threadIdx.x / kTileU;
+  const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
+  const int u = u0 + tx, v = v0 + ty;
+  const bool in = u < a.w && v < a.h;
+  const int bx0 = u0 - a.win < 0 ? 0 : (u0 - a.win) / a.B;
+  const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + a.win) / a.B);
+  const int by0 = v0 - a.win < 0 ? 0 : (v0 - a.win) / a.B;
+  const int by1 = min(a.nby - 1, (v0 + kTileV - 1 + a.win) / a.B);
+  const int nbxr = bx1 - bx0 + 1, nbr = nbxr * (by1 - by0 + 1);
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbr; b += blockDim.x) {
+    const int bucket = (by0 + b / nbxr) * a.nbx + bx0 + b % nbxr;
+    const int e = a.cell_start[bucket + 1];
+    for (int idx = a.cell_start[bucket]; idx < e; ++idx) {
+      const int k = a.cell_items[idx];
+      const int slot = atomicAdd(&s_cnt, 1);
+      if (slot < kMaxTileCenters) {
+        s_k[slot] = k;
+        s_icu[slot] = a.c.icu[k];
+        s_icv[slot] = a.c.icv[k];
+        s_cu[slot] = a.c.cu[k];
+        s_cv[slot] = a.c.cv[k];
+        s_val[slot] = a.c.val[k];
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = s_cnt;
+  int label = -1;  // -1: outside the image
+  size_t p = 0;
+  double x = 0.0;
+  if (in) {
+    p = size_t(v) * a.w + u;
+    x = double(a.vals[p]);
+    double best = __longlong_as_double(0x7FF0000000000000ll);
+    int bk = -1;
+    if (nc <= kMaxTileCenters) {
+      for (int i = 0; i < nc; ++i) {
+        if (abs(u - s_icu[i]) > a.win || abs(v - s_icv[i]) > a.win) continue;
+        const int k = s_k[i];
+        const double dval = x - s_val[i];
+        const double du = double(u) - s_cu[i], dv = double(v) - s_cv[i];
+        const double dist = dval * dval + (du * du + dv * dv) * a.sw;
+        if (dist < best || (dist == best && k < bk)) {
+          best = dist;
+          bk = k;
+        }
+      }
+    } else {  // pathological centre pile-up: per-pixel bucket walk
+      bk = assign_walk(a, u, v, x);
+    }
+    if (bk < 0) {
+      a.labels[p] = 0;
+      const int slot = atomicAdd(a.orphan_count, 1);
+      a.orphan_list[slot] = int(p);
+      label = 0;
+    } else {
+      a.labels[p] = bk + 1;
+      label = bk + 1;
+    }
+  }
+  if (SUMS) {
+    const int key = label > 0 ? label : -1;
+    const RunInfo ri = run_info(key);
+    int bad = 0;
+    Acc128 ax = key > 0 ? to_fixed(float(x), &bad) : Acc128{0ull, 0ll};
+    if (bad) atomicOr(a.inexact, 1);
+    const int cnt = run_sum(key > 0 ? 1 : 0, ri);
+    ax = run_sum(ax, ri);
+    const long long su = run_sum(key > 0 ? (long long)u : 0ll, ri);
+    const long long sv = run_sum(key > 0 ? (long long)v : 0ll, ri);
+    if (ri.head) {
+      atomicAdd(&s.n[key], cnt);
+      atomic_add_acc(&s.sx[key], ax);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
+    }
   }
 }
 
 // Nearest-centre fallback, segmentation.cpp:59-71 (one warp per pixel).
+template <bool SUMS>
 __global__ void k_assign_fallback(int w, Centers c, int K, int32_t* __restrict__ labels,
-                                  const int* __restrict__ list, const int* __restrict__ count) {
+                                  const int* __restrict__ list, const int* __restrict__ count,
+                                  const float* __restrict__ vals, CenterSums s,
+                                  int* __restrict__ inexact) {
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int n = *count;
@@ -222,7 +329,18 @@ __global__ void k_assign_fallback(int w, Centers c, int K, int32_t* __restrict__
         bk = ok;
       }
     }
-    if (lane == 0 && bk >= 0) labels[p] = bk + 1;
+    if (lane == 0 && bk >= 0) {
+      labels[p] = bk + 1;
+      if (SUMS) {
+        int bad = 0;
+        const int l = bk + 1;
+        atomicAdd(&s.n[l], 1);
+        atomic_add_acc(&s.sx[l], to_fixed(vals[p], &bad));
+        if (bad) atomicOr(inexact, 1);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[l]), (unsigned long long)u);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[l]), (unsigned long long)v);
+      }
+    }
   }
 }
 
@@ -539,15 +657,26 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_CK(cudaMemsetAsync(orphan_count, 0, 2 * sizeof(int), st));
 
   AssignArgs aa{vals, h, w, c, cell_start, cell_items, B, nbx, nby, win, sw, labels,
-                orphan_list, orphan_count};
-  auto assign = [&]() {
-    k_buckets<<<1, kBucketThreads, 0, st>>>(c, K, w, h, B, nbx, nby, cell_start, cell_items);
+                orphan_list, orphan_count, inexact};
+  const dim3 tgrid(cdiv(w, kTileU), cdiv(h, kTileV));
+  // One round = bucket build (finalising the previous round's sums first) +
+  // assignment that accumulates the sums the next round needs.
+  auto assign = [&](bool finalize, bool sums) {
+    k_buckets<<<1, kBucketThreads, 0, st>>>(c, K, w, h, B, nbx, nby, cell_start, cell_items, s,
+                                            finalize ? 1 : 0);
     RPD_LAUNCH_CHECK();
     RPD_CK(cudaMemsetAsync(orphan_count, 0, sizeof(int), st));
-    k_assign<<<rowgrid, 128, 0, st>>>(aa);
+    if (sums)
+      k_assign_tile<true><<<tgrid, kTileU * kTileV, 0, st>>>(aa, s);
+    else
+      k_assign_tile<false><<<tgrid, kTileU * kTileV, 0, st>>>(aa, s);
     RPD_LAUNCH_CHECK();
-    k_assign_fallback<<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
-                                                         orphan_count);
+    if (sums)
+      k_assign_fallback<true><<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
+                                                                  orphan_count, vals, s, inexact);
+    else
+      k_assign_fallback<false><<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
+                                                                   orphan_count, vals, s, inexact);
     RPD_LAUNCH_CHECK();
   };
   auto update = [&]() {
@@ -556,11 +685,8 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
     k_center_finalize<<<cdiv(K, 256), 256, 0, st>>>(s, c, K);
     RPD_LAUNCH_CHECK();
   };
-  assign();
-  for (int it = 0; it < iterations; ++it) {
-    update();
-    assign();
-  }
+  assign(false, iterations > 0);
+  for (int it = 0; it < iterations; ++it) assign(true, it + 1 < iterations);
 
   // enforce_connectivity
   int* parent = ctx->ws.get<int>("slic_parent", n);
