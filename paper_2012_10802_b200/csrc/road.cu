@@ -4,28 +4,28 @@
 // Reference: /root/reference/proj/src/road_geometry.cpp:12-151.
 //
 // The whole golden-section roll search (18 iterations + trimming + second
-// search at the default bracket/tol) runs inside ONE launch of an 8-CTA thread
-// block cluster (8 x 1024 threads).  The observations (<= 100 000, 8 B each in
-// the compact format) are staged once into the CTAs' shared memory; every
-// fit_line probe is two cluster-wide reductions whose partials are exchanged
-// through distributed shared memory (DSMEM).  No host round trip per probe.
+// search at the default bracket/tol) runs inside ONE cooperative launch of
+// 128 co-resident CTAs (one per SM; 64 summation lanes + one helper warp
+// each).  The observations (<= 524 288) are staged once into shared memory as
+// exact doubles; every sweep ends in one grid-wide reduction whose CTA
+// partials are exchanged through flag-tagged 64-bit words in L2 (no barrier,
+// no host round trip); the helper warp computes the correctly rounded sin/cos
+// the next sweep may need while the current one runs.
 //
 // Reduction order (shared with the CPU oracle, oracle/rpd_oracle.cpp
-// lane_tree_sum): element i belongs to lane i mod 8192 (lane = CTA*1024 +
+// lane_tree_sum): element i belongs to lane i mod 8192 (lane = CTA*64 +
 // thread) and is added sequentially; lanes are then combined by an adjacent-
-// pairwise binary tree (warp shuffles, then CTA, then the 8 cluster partials).
+// pairwise binary tree (warp shuffles, CTA, then the 128 CTA partials).
 // Eigen's own SIMD order (road_geometry.cpp:20-24, 37) is not reproducible
 // without Eigen; the reference tests pin these sums to 1e-9 relative.
 
 #include <algorithm>
 
-#include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
 
 #include "road.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace rpdg {
 
@@ -71,10 +71,10 @@ __constant__ double c_cos_lo[kTaylorTerms] = {0.0, 0.0, 2.3129646346357427e-18, 
 // sin/cos of a_k = k/64 as double-double (generated offline with 60-digit
 // decimal arithmetic).
 constexpr int kSinTabHalf = 48;  // a_k = k/64, k in [-48, 48]
-__constant__ double c_tab_sin_hi[97] = {-0.6816387600233341, -0.6701233804731629, -0.6584443999105676, -0.6466046695911524, -0.6346070800152693, -0.6224545602223437, -0.6101500770757914, -0.5976966345387015, -0.5850972729404622, -0.5723550682345072, -0.5594731312473669, -0.5464546069192036, -0.5333026735360201, -0.520020541953727, -0.5066114548142574, -0.49307868575392305, -0.479425538604203, -0.46565534658516017, -0.4517714714916838, -0.4377773028727551, -0.42367625720393803, -0.40947177705329507, -0.39516733024093426, -0.38076640899239017, -0.36627252908604757, -0.3516892289948141, -0.33702006902225307, -0.3222686304333866, -0.30743851458038085, -0.29253334202332754, -0.2775567516463363, -0.2625123997691533, -0.24740395925452294, -0.23223511861151147, -0.21700958109501015, -0.2017310638016388, -0.18640329676226988, -0.17103002203139503, -0.15561499277355603, -0.1401619723470637, -0.12467473338522769, -0.10915705687532236, -0.09361273123551289, -0.07804555138996731, -0.0624593178423802, -0.04685783574813424, -0.03124491398532608, -0.015624364224883372, 0.0, 0.015624364224883372, 0.03124491398532608, 0.04685783574813424, 0.0624593178423802, 0.07804555138996731, 0.09361273123551289, 0.10915705687532236, 0.12467473338522769, 0.1401619723470637, 0.15561499277355603, 0.17103002203139503, 0.18640329676226988, 0.2017310638016388, 0.21700958109501015, 0.23223511861151147, 0.24740395925452294, 0.2625123997691533, 0.2775567516463363, 0.29253334202332754, 0.30743851458038085, 0.3222686304333866, 0.33702006902225307, 0.3516892289948141, 0.36627252908604757, 0.38076640899239017, 0.39516733024093426, 0.40947177705329507, 0.42367625720393803, 0.4377773028727551, 0.4517714714916838, 0.46565534658516017, 0.479425538604203, 0.49307868575392305, 0.5066114548142574, 0.520020541953727, 0.5333026735360201, 0.5464546069192036, 0.5594731312473669, 0.5723550682345072, 0.5850972729404622, 0.5976966345387015, 0.6101500770757914, 0.6224545602223437, 0.6346070800152693, 0.6466046695911524, 0.6584443999105676, 0.6701233804731629, 0.6816387600233341};
-__constant__ double c_tab_sin_lo[97] = {-4.410467313197903e-17, -6.183536725574959e-18, 3.7736386700306717e-17, -4.567647714393289e-19, 3.4568582392624965e-17, 6.049035765709707e-18, 1.479826990758988e-17, -5.450323593054385e-17, 5.4883972461161805e-17, -2.6575872357215316e-17, -1.575565514488728e-17, -8.399754840929507e-18, -5.129318115032044e-17, 3.983266745698455e-17, 3.269413423618168e-17, -5.605083973871755e-18, 5.103969860556013e-18, -1.459870391051426e-17, 8.234073942098903e-18, -7.64345629962023e-18, 2.331800700068871e-17, 5.679403000091266e-18, 1.9613487871414228e-17, -2.1372528646211374e-17, 9.938814562106524e-18, 2.5616208736069942e-17, -1.0312279860787216e-17, -2.093773358126606e-17, -1.1004366442765296e-19, -7.516944930327352e-18, -1.7674070262791822e-17, 2.2534597527902125e-17, 7.53102495590706e-18, 8.318080852687206e-18, -1.1170071073364376e-17, -5.587232815460113e-18, -2.3493796901281573e-18, 9.954774726452923e-18, -8.886053372342288e-18, 9.946847113883478e-18, 2.925947496057858e-18, -6.6284699502736666e-18, -1.4628632005878733e-18, 5.449443782005793e-18, 2.040259504585711e-18, 2.3419368365610254e-18, 1.562781562225433e-18, 1.2650937552759816e-19, 0.0, -1.2650937552759816e-19, -1.562781562225433e-18, -2.3419368365610254e-18, -2.040259504585711e-18, -5.449443782005793e-18, 1.4628632005878733e-18, 6.6284699502736666e-18, -2.925947496057858e-18, -9.946847113883478e-18, 8.886053372342288e-18, -9.954774726452923e-18, 2.3493796901281573e-18, 5.587232815460113e-18, 1.1170071073364376e-17, -8.318080852687206e-18, -7.53102495590706e-18, -2.2534597527902125e-17, 1.7674070262791822e-17, 7.516944930327352e-18, 1.1004366442765296e-19, 2.093773358126606e-17, 1.0312279860787216e-17, -2.5616208736069942e-17, -9.938814562106524e-18, 2.1372528646211374e-17, -1.9613487871414228e-17, -5.679403000091266e-18, -2.331800700068871e-17, 7.64345629962023e-18, -8.234073942098903e-18, 1.459870391051426e-17, -5.103969860556013e-18, 5.605083973871755e-18, -3.269413423618168e-17, -3.983266745698455e-17, 5.129318115032044e-17, 8.399754840929507e-18, 1.575565514488728e-17, 2.6575872357215316e-17, -5.4883972461161805e-17, 5.450323593054385e-17, -1.479826990758988e-17, -6.049035765709707e-18, -3.4568582392624965e-17, 4.567647714393289e-19, -3.7736386700306717e-17, 6.183536725574959e-18, 4.410467313197903e-17};
-__constant__ double c_tab_cos_hi[97] = {0.7316888688738209, 0.7422497254585013, 0.7526293724180665, 0.7628252757105762, 0.7728349461524715, 0.7826559400262728, 0.7922858596771786, 0.8017223540984184, 0.8109631195052179, 0.820005899897234, 0.8288484876093257, 0.8374887238505236, 0.8459244992310679, 0.8541537542773854, 0.8621744799348805, 0.8699847180584174, 0.8775825618903728, 0.8849661565261433, 0.8921336993669944, 0.8990834405601384, 0.9058136834259364, 0.9123227848721178, 0.9186091557949183, 0.924671261467036, 0.9305076219123143, 0.9361168122670553, 0.9414974631278811, 0.9466482608860534, 0.9515679480481722, 0.9562553235431753, 0.9607092430155619, 0.964928619104771, 0.9689124217106447, 0.9726596782449127, 0.9761694738686353, 0.9794409517155483, 0.9824733131012553, 0.9852658177182139, 0.9878177838164719, 0.9901285883701071, 0.992197667229329, 0.9940245152582091, 0.9956086864580017, 0.9969497940760287, 0.9980475107000991, 0.9989015683384429, 0.9995117584851364, 0.9998779321710066, 1.0, 0.9998779321710066, 0.9995117584851364, 0.9989015683384429, 0.9980475107000991, 0.9969497940760287, 0.9956086864580017, 0.9940245152582091, 0.992197667229329, 0.9901285883701071, 0.9878177838164719, 0.9852658177182139, 0.9824733131012553, 0.9794409517155483, 0.9761694738686353, 0.9726596782449127, 0.9689124217106447, 0.964928619104771, 0.9607092430155619, 0.9562553235431753, 0.9515679480481722, 0.9466482608860534, 0.9414974631278811, 0.9361168122670553, 0.9305076219123143, 0.924671261467036, 0.9186091557949183, 0.9123227848721178, 0.9058136834259364, 0.8990834405601384, 0.8921336993669944, 0.8849661565261433, 0.8775825618903728, 0.8699847180584174, 0.8621744799348805, 0.8541537542773854, 0.8459244992310679, 0.8374887238505236, 0.8288484876093257, 0.820005899897234, 0.8109631195052179, 0.8017223540984184, 0.7922858596771786, 0.7826559400262728, 0.7728349461524715, 0.7628252757105762, 0.7526293724180665, 0.7422497254585013, 0.7316888688738209};
-__constant__ double c_tab_cos_lo[97] = {-1.0475824306512768e-17, -1.2339303604869521e-17, -1.2970993013150526e-17, 1.6672995021546628e-17, 4.231014921891023e-17, -1.474071641211487e-17, -2.9049779312834576e-17, 4.0134533311087014e-17, -3.091333486122179e-17, -3.912431748209128e-17, 1.1163935406617444e-17, 4.3337026043948396e-17, 1.549506647350329e-17, 5.420565102675286e-18, 4.4132427578105805e-18, 1.657385110740923e-17, -4.2623149864279997e-17, -7.690557775987357e-18, 2.3160655211380166e-17, 9.076951775075616e-18, 4.2864666490805214e-17, 2.6349040211413332e-17, -4.0564150104514996e-17, 5.5444125388034563e-17, 4.488760003328074e-18, -5.2350302039683216e-17, -4.8523830236797095e-18, -3.911683334934152e-17, -3.8614834675674123e-17, -3.148450868841629e-17, -2.807827063516729e-17, -3.0345542681018625e-18, 5.071436662403936e-17, 2.3920264546490165e-17, -7.850690609285027e-18, 1.3108769521526758e-17, -3.919920375420088e-17, -4.925721262944555e-17, 4.91917302237681e-17, -4.589906353553811e-18, 4.754870575189364e-17, 1.3287985046260087e-17, 3.312922430932991e-17, -1.2467075728553626e-17, 3.3232291674141346e-17, -2.1425557800399754e-17, -3.418806487972947e-17, 3.216122229972341e-17, 0.0, 3.216122229972341e-17, -3.418806487972947e-17, -2.1425557800399754e-17, 3.3232291674141346e-17, -1.2467075728553626e-17, 3.312922430932991e-17, 1.3287985046260087e-17, 4.754870575189364e-17, -4.589906353553811e-18, 4.91917302237681e-17, -4.925721262944555e-17, -3.919920375420088e-17, 1.3108769521526758e-17, -7.850690609285027e-18, 2.3920264546490165e-17, 5.071436662403936e-17, -3.0345542681018625e-18, -2.807827063516729e-17, -3.148450868841629e-17, -3.8614834675674123e-17, -3.911683334934152e-17, -4.8523830236797095e-18, -5.2350302039683216e-17, 4.488760003328074e-18, 5.5444125388034563e-17, -4.0564150104514996e-17, 2.6349040211413332e-17, 4.2864666490805214e-17, 9.076951775075616e-18, 2.3160655211380166e-17, -7.690557775987357e-18, -4.2623149864279997e-17, 1.657385110740923e-17, 4.4132427578105805e-18, 5.420565102675286e-18, 1.549506647350329e-17, 4.3337026043948396e-17, 1.1163935406617444e-17, -3.912431748209128e-17, -3.091333486122179e-17, 4.0134533311087014e-17, -2.9049779312834576e-17, -1.474071641211487e-17, 4.231014921891023e-17, 1.6672995021546628e-17, -1.2970993013150526e-17, -1.2339303604869521e-17, -1.0475824306512768e-17};
+__device__ const double c_tab_sin_hi[97] = {-0.6816387600233341, -0.6701233804731629, -0.6584443999105676, -0.6466046695911524, -0.6346070800152693, -0.6224545602223437, -0.6101500770757914, -0.5976966345387015, -0.5850972729404622, -0.5723550682345072, -0.5594731312473669, -0.5464546069192036, -0.5333026735360201, -0.520020541953727, -0.5066114548142574, -0.49307868575392305, -0.479425538604203, -0.46565534658516017, -0.4517714714916838, -0.4377773028727551, -0.42367625720393803, -0.40947177705329507, -0.39516733024093426, -0.38076640899239017, -0.36627252908604757, -0.3516892289948141, -0.33702006902225307, -0.3222686304333866, -0.30743851458038085, -0.29253334202332754, -0.2775567516463363, -0.2625123997691533, -0.24740395925452294, -0.23223511861151147, -0.21700958109501015, -0.2017310638016388, -0.18640329676226988, -0.17103002203139503, -0.15561499277355603, -0.1401619723470637, -0.12467473338522769, -0.10915705687532236, -0.09361273123551289, -0.07804555138996731, -0.0624593178423802, -0.04685783574813424, -0.03124491398532608, -0.015624364224883372, 0.0, 0.015624364224883372, 0.03124491398532608, 0.04685783574813424, 0.0624593178423802, 0.07804555138996731, 0.09361273123551289, 0.10915705687532236, 0.12467473338522769, 0.1401619723470637, 0.15561499277355603, 0.17103002203139503, 0.18640329676226988, 0.2017310638016388, 0.21700958109501015, 0.23223511861151147, 0.24740395925452294, 0.2625123997691533, 0.2775567516463363, 0.29253334202332754, 0.30743851458038085, 0.3222686304333866, 0.33702006902225307, 0.3516892289948141, 0.36627252908604757, 0.38076640899239017, 0.39516733024093426, 0.40947177705329507, 0.42367625720393803, 0.4377773028727551, 0.4517714714916838, 0.46565534658516017, 0.479425538604203, 0.49307868575392305, 0.5066114548142574, 0.520020541953727, 0.5333026735360201, 0.5464546069192036, 0.5594731312473669, 0.5723550682345072, 0.5850972729404622, 0.5976966345387015, 0.6101500770757914, 0.6224545602223437, 0.6346070800152693, 0.6466046695911524, 0.6584443999105676, 0.6701233804731629, 0.6816387600233341};
+__device__ const double c_tab_sin_lo[97] = {-4.410467313197903e-17, -6.183536725574959e-18, 3.7736386700306717e-17, -4.567647714393289e-19, 3.4568582392624965e-17, 6.049035765709707e-18, 1.479826990758988e-17, -5.450323593054385e-17, 5.4883972461161805e-17, -2.6575872357215316e-17, -1.575565514488728e-17, -8.399754840929507e-18, -5.129318115032044e-17, 3.983266745698455e-17, 3.269413423618168e-17, -5.605083973871755e-18, 5.103969860556013e-18, -1.459870391051426e-17, 8.234073942098903e-18, -7.64345629962023e-18, 2.331800700068871e-17, 5.679403000091266e-18, 1.9613487871414228e-17, -2.1372528646211374e-17, 9.938814562106524e-18, 2.5616208736069942e-17, -1.0312279860787216e-17, -2.093773358126606e-17, -1.1004366442765296e-19, -7.516944930327352e-18, -1.7674070262791822e-17, 2.2534597527902125e-17, 7.53102495590706e-18, 8.318080852687206e-18, -1.1170071073364376e-17, -5.587232815460113e-18, -2.3493796901281573e-18, 9.954774726452923e-18, -8.886053372342288e-18, 9.946847113883478e-18, 2.925947496057858e-18, -6.6284699502736666e-18, -1.4628632005878733e-18, 5.449443782005793e-18, 2.040259504585711e-18, 2.3419368365610254e-18, 1.562781562225433e-18, 1.2650937552759816e-19, 0.0, -1.2650937552759816e-19, -1.562781562225433e-18, -2.3419368365610254e-18, -2.040259504585711e-18, -5.449443782005793e-18, 1.4628632005878733e-18, 6.6284699502736666e-18, -2.925947496057858e-18, -9.946847113883478e-18, 8.886053372342288e-18, -9.954774726452923e-18, 2.3493796901281573e-18, 5.587232815460113e-18, 1.1170071073364376e-17, -8.318080852687206e-18, -7.53102495590706e-18, -2.2534597527902125e-17, 1.7674070262791822e-17, 7.516944930327352e-18, 1.1004366442765296e-19, 2.093773358126606e-17, 1.0312279860787216e-17, -2.5616208736069942e-17, -9.938814562106524e-18, 2.1372528646211374e-17, -1.9613487871414228e-17, -5.679403000091266e-18, -2.331800700068871e-17, 7.64345629962023e-18, -8.234073942098903e-18, 1.459870391051426e-17, -5.103969860556013e-18, 5.605083973871755e-18, -3.269413423618168e-17, -3.983266745698455e-17, 5.129318115032044e-17, 8.399754840929507e-18, 1.575565514488728e-17, 2.6575872357215316e-17, -5.4883972461161805e-17, 5.450323593054385e-17, -1.479826990758988e-17, -6.049035765709707e-18, -3.4568582392624965e-17, 4.567647714393289e-19, -3.7736386700306717e-17, 6.183536725574959e-18, 4.410467313197903e-17};
+__device__ const double c_tab_cos_hi[97] = {0.7316888688738209, 0.7422497254585013, 0.7526293724180665, 0.7628252757105762, 0.7728349461524715, 0.7826559400262728, 0.7922858596771786, 0.8017223540984184, 0.8109631195052179, 0.820005899897234, 0.8288484876093257, 0.8374887238505236, 0.8459244992310679, 0.8541537542773854, 0.8621744799348805, 0.8699847180584174, 0.8775825618903728, 0.8849661565261433, 0.8921336993669944, 0.8990834405601384, 0.9058136834259364, 0.9123227848721178, 0.9186091557949183, 0.924671261467036, 0.9305076219123143, 0.9361168122670553, 0.9414974631278811, 0.9466482608860534, 0.9515679480481722, 0.9562553235431753, 0.9607092430155619, 0.964928619104771, 0.9689124217106447, 0.9726596782449127, 0.9761694738686353, 0.9794409517155483, 0.9824733131012553, 0.9852658177182139, 0.9878177838164719, 0.9901285883701071, 0.992197667229329, 0.9940245152582091, 0.9956086864580017, 0.9969497940760287, 0.9980475107000991, 0.9989015683384429, 0.9995117584851364, 0.9998779321710066, 1.0, 0.9998779321710066, 0.9995117584851364, 0.9989015683384429, 0.9980475107000991, 0.9969497940760287, 0.9956086864580017, 0.9940245152582091, 0.992197667229329, 0.9901285883701071, 0.9878177838164719, 0.9852658177182139, 0.9824733131012553, 0.9794409517155483, 0.9761694738686353, 0.9726596782449127, 0.9689124217106447, 0.964928619104771, 0.9607092430155619, 0.9562553235431753, 0.9515679480481722, 0.9466482608860534, 0.9414974631278811, 0.9361168122670553, 0.9305076219123143, 0.924671261467036, 0.9186091557949183, 0.9123227848721178, 0.9058136834259364, 0.8990834405601384, 0.8921336993669944, 0.8849661565261433, 0.8775825618903728, 0.8699847180584174, 0.8621744799348805, 0.8541537542773854, 0.8459244992310679, 0.8374887238505236, 0.8288484876093257, 0.820005899897234, 0.8109631195052179, 0.8017223540984184, 0.7922858596771786, 0.7826559400262728, 0.7728349461524715, 0.7628252757105762, 0.7526293724180665, 0.7422497254585013, 0.7316888688738209};
+__device__ const double c_tab_cos_lo[97] = {-1.0475824306512768e-17, -1.2339303604869521e-17, -1.2970993013150526e-17, 1.6672995021546628e-17, 4.231014921891023e-17, -1.474071641211487e-17, -2.9049779312834576e-17, 4.0134533311087014e-17, -3.091333486122179e-17, -3.912431748209128e-17, 1.1163935406617444e-17, 4.3337026043948396e-17, 1.549506647350329e-17, 5.420565102675286e-18, 4.4132427578105805e-18, 1.657385110740923e-17, -4.2623149864279997e-17, -7.690557775987357e-18, 2.3160655211380166e-17, 9.076951775075616e-18, 4.2864666490805214e-17, 2.6349040211413332e-17, -4.0564150104514996e-17, 5.5444125388034563e-17, 4.488760003328074e-18, -5.2350302039683216e-17, -4.8523830236797095e-18, -3.911683334934152e-17, -3.8614834675674123e-17, -3.148450868841629e-17, -2.807827063516729e-17, -3.0345542681018625e-18, 5.071436662403936e-17, 2.3920264546490165e-17, -7.850690609285027e-18, 1.3108769521526758e-17, -3.919920375420088e-17, -4.925721262944555e-17, 4.91917302237681e-17, -4.589906353553811e-18, 4.754870575189364e-17, 1.3287985046260087e-17, 3.312922430932991e-17, -1.2467075728553626e-17, 3.3232291674141346e-17, -2.1425557800399754e-17, -3.418806487972947e-17, 3.216122229972341e-17, 0.0, 3.216122229972341e-17, -3.418806487972947e-17, -2.1425557800399754e-17, 3.3232291674141346e-17, -1.2467075728553626e-17, 3.312922430932991e-17, 1.3287985046260087e-17, 4.754870575189364e-17, -4.589906353553811e-18, 4.91917302237681e-17, -4.925721262944555e-17, -3.919920375420088e-17, 1.3108769521526758e-17, -7.850690609285027e-18, 2.3920264546490165e-17, 5.071436662403936e-17, -3.0345542681018625e-18, -2.807827063516729e-17, -3.148450868841629e-17, -3.8614834675674123e-17, -3.911683334934152e-17, -4.8523830236797095e-18, -5.2350302039683216e-17, 4.488760003328074e-18, 5.5444125388034563e-17, -4.0564150104514996e-17, 2.6349040211413332e-17, 4.2864666490805214e-17, 9.076951775075616e-18, 2.3160655211380166e-17, -7.690557775987357e-18, -4.2623149864279997e-17, 1.657385110740923e-17, 4.4132427578105805e-18, 5.420565102675286e-18, 1.549506647350329e-17, 4.3337026043948396e-17, 1.1163935406617444e-17, -3.912431748209128e-17, -3.091333486122179e-17, 4.0134533311087014e-17, -2.9049779312834576e-17, -1.474071641211487e-17, 4.231014921891023e-17, 1.6672995021546628e-17, -1.2970993013150526e-17, -1.2339303604869521e-17, -1.0475824306512768e-17};
 }  // namespace
 
 // Correctly rounded sin/cos (with overwhelming probability).  Fast path for
@@ -205,14 +205,29 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
 }
 
 // ----------------------------------------------------------- fit kernel ----
-constexpr int kFitCtas = 16;      // non-portable cluster: 16 SMs share one fit
-constexpr int kFitThreads = 512;
-constexpr int kFitWarps = kFitThreads / 32;
-constexpr int kFitLanes = kFitCtas * kFitThreads;  // == oracle kFitLanes (8192)
-constexpr int kFitDynSmem = 192 * 1024;
-// observations are staged as SoA doubles (d, u, v): 24 B per element
-constexpr int kRowsStaged = kFitDynSmem / (kFitThreads * 24);  // 16 rows -> 131072 elements
-constexpr int kMaxRowsTrim = 64;
+// One cooperative grid of kFitCtas CTAs (co-resident, one per SM) runs the
+// whole fit.  CTA c owns lanes [c*kFitSweep, (c+1)*kFitSweep) of the 8192
+// summation lanes; its observations (rows m: element m*8192 + lane) are staged
+// once in shared memory as exact doubles.  Every reduction is: per-lane
+// sequential sums -> warp shuffle tree -> CTA partial -> global partials +
+// one grid barrier -> every CTA combines the kFitCtas partials with the same
+// pairwise tree, so all CTAs hold bit-identical sums and run the (scalar)
+// golden-section logic redundantly.  A helper warp per CTA computes the
+// double-double sin/cos of the angles the NEXT sweep may need (both outcomes
+// of the pending comparison) while the current sweep runs.
+constexpr int kFitCtas = 128;
+constexpr int kFitSweep = 64;                      // sweep threads per CTA
+constexpr int kFitSweepWarps = kFitSweep / 32;
+constexpr int kFitThreads = kFitSweep + 32;        // + helper warp
+constexpr int kFitLanes = kFitCtas * kFitSweep;    // == oracle kFitLanes (8192)
+constexpr int kMaxRows = 64;                       // 524288 observations
+constexpr int kFitStageBytes = kMaxRows * kFitSweep * 3 * int(sizeof(double));  // 96 KB
+constexpr int kFitDynSmem = kFitStageBytes + kMaxRows * (kFitCtas + 1) * int(sizeof(int));
+constexpr int kMaxNV = 8;                          // values per reduction
+constexpr int kPartReplicas = 8;  // copies of the CTA partials (spreads the polling over L2)
+constexpr int kPartWords = 2 * kPartReplicas * kFitCtas * kMaxNV * 2;
+static_assert(kFitSweep % 32 == 0 && (kFitSweepWarps & (kFitSweepWarps - 1)) == 0, "warps");
+static_assert((kFitCtas & (kFitCtas - 1)) == 0 && kFitCtas / 2 <= kFitSweep, "ctas");
 
 struct FitKParams {
   FitRequest r;
@@ -223,18 +238,21 @@ struct FitKParams {
   double* scr_dd;
   double* scr_du;
   double* scr_dv;
+  unsigned long long* part;  // [2][kFitCtas][kMaxNV][2] flag-tagged CTA partials (zeroed)
+  int* rowcnt;     // [kMaxRows][kFitCtas] trimming survivors per row and CTA
+  unsigned* bar;   // grid barrier counter, zeroed before the launch
+  int trace;       // debug (RPD_FIT_TRACE=1): per-phase clock64 trace of CTA 0
 };
 
-constexpr int kMaxNV = 10;  // values per cluster reduction
 struct FitShared {
-  double warp_part[kFitWarps][kMaxNV];
-  double cta_part[2][kMaxNV];
-  double peer[kMaxNV][kFitCtas];
-  double bcast[kMaxNV];
-  double sc[4][2];  // sin/cos of up to 4 pending probe angles
-  int row_cnt[kMaxRowsTrim];
-  int row_base[kMaxRowsTrim];
-  int warp_cnt[kFitWarps];
+  double warp_part[kFitSweepWarps][kMaxNV];
+  double red[kFitSweepWarps][kMaxNV];
+  double sc[2][4][2];  // helper output (double-buffered): sin/cos of up to 4 angles
+  int wcnt[kFitSweepWarps][kMaxRows];
+  int row_base[kMaxRows];
+  long long tr[512];
+  long long htr[256];
+  int ntr, nh;
 };
 
 struct LineFitD {
@@ -244,133 +262,229 @@ struct LineFitD {
 struct FitState {
   const FitKParams* P;
   FitShared* S;
-  unsigned char* dyn;
-  bool compact;
-  bool staged;
+  double* e;  // staged SoA doubles: d | u | v, each [kMaxRows][kFitSweep]
   long long k;
   int rows;
   int lane;
-  int slot;
-  // current (global) source when not staged
-  const uint32_t* g_uv;
-  const float* g_d;
-  const double* g_dd;
-  const double* g_du;
-  const double* g_dv;
+  unsigned calls;  // grid_sum calls so far (the exchange flag)
+  int scbuf;     // helper output buffer
+  unsigned target;
 };
 
-__device__ __forceinline__ void fit_get(const FitState& F, int m, long long i, double& d, double& u,
-                                        double& v) {
-  if (F.staged) {
-    const double* e = reinterpret_cast<const double*>(F.dyn);
-    const int o = m * kFitThreads + threadIdx.x;
-    d = e[o];
-    u = e[kRowsStaged * kFitThreads + o];
-    v = e[2 * kRowsStaged * kFitThreads + o];
-  } else if (F.compact) {
-    const uint32_t uv = F.g_uv[i];
-    u = double(uv & 0xFFFFu);
-    v = double(uv >> 16);
-    d = double(F.g_d[i]);
-  } else {
-    d = F.g_dd[i];
-    u = F.g_du[i];
-    v = F.g_dv[i];
-  }
+__device__ __forceinline__ void fit_tr(FitState& F, int tag) {
+  if (F.P->trace && blockIdx.x == 0 && threadIdx.x == 0 && F.S->ntr < 512)
+    F.S->tr[F.S->ntr++] = ((long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFll);
 }
 
-// Stage the current source into shared memory as exact doubles (when it fits).
-__device__ void fit_stage(FitState& F) {
-  F.rows = int((F.k + kFitLanes - 1) / kFitLanes);
-  F.staged = F.rows <= kRowsStaged;
-  if (!F.staged) return;
-  double* e = reinterpret_cast<double*>(F.dyn);
-  for (int m = 0; m < F.rows; ++m) {
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (i >= F.k) break;
-    double d, u, v;
-    if (F.compact) {
-      const uint32_t uv = F.g_uv[i];
-      u = double(uv & 0xFFFFu);
-      v = double(uv >> 16);
-      d = double(F.g_d[i]);
-    } else {
-      d = F.g_dd[i];
-      u = F.g_du[i];
-      v = F.g_dv[i];
-    }
-    const int o = m * kFitThreads + threadIdx.x;
-    e[o] = d;
-    e[kRowsStaged * kFitThreads + o] = u;
-    e[2 * kRowsStaged * kFitThreads + o] = v;
+__device__ __forceinline__ bool is_sweep() { return threadIdx.x < kFitSweep; }
+
+__device__ __forceinline__ void sweep_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kFitSweep) : "memory");
+}
+
+constexpr unsigned kSpinLimit = 1u << 24;  // ~seconds: a lost peer traps, never hangs
+
+// Grid-wide barrier of the cooperative launch (thread 0 of every CTA arrives
+// with release semantics and spins with acquire loads); all threads of the
+// CTA must call it.  Used by trimming only; the per-sweep reductions use the
+// flag-tagged exchange of grid_sum.
+__device__ void grid_bar(FitState& F) {
+  F.target += kFitCtas;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* bar = F.P->bar;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v, spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (++spins > kSpinLimit) __trap();
+    } while (v < F.target);
   }
   __syncthreads();
 }
 
-// Cluster-wide sum of NV doubles in the fixed adjacent-pairwise lane order.
+// Stage the first k elements of the source into shared memory (sweep threads).
+template <bool COMPACT>
+__device__ void fit_stage_from(FitState& F, const uint32_t* g_uv, const float* g_d,
+                               const double* g_dd, const double* g_du, const double* g_dv) {
+  F.rows = int((F.k + kFitLanes - 1) / kFitLanes);
+  if (is_sweep()) {
+    constexpr int U = 8;  // loads in flight per thread
+    for (int m0 = 0; m0 < F.rows; m0 += U) {
+      double d[U], u[U], v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const long long i = (long long)(m0 + j) * kFitLanes + F.lane;
+        if (i < F.k) {
+          if (COMPACT) {
+            const uint32_t uv = __ldcg(g_uv + i);
+            u[j] = double(uv & 0xFFFFu);
+            v[j] = double(uv >> 16);
+            d[j] = double(__ldcg(g_d + i));
+          } else {
+            d[j] = __ldcg(g_dd + i);
+            u[j] = __ldcg(g_du + i);
+            v[j] = __ldcg(g_dv + i);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const long long i = (long long)(m0 + j) * kFitLanes + F.lane;
+        if (i < F.k) {
+          const int o = (m0 + j) * kFitSweep + threadIdx.x;
+          F.e[o] = d[j];
+          F.e[kMaxRows * kFitSweep + o] = u[j];
+          F.e[2 * kMaxRows * kFitSweep + o] = v[j];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void fit_get(const FitState& F, int m, double& d, double& u, double& v) {
+  const int o = m * kFitSweep + threadIdx.x;
+  d = F.e[o];
+  u = F.e[kMaxRows * kFitSweep + o];
+  v = F.e[2 * kMaxRows * kFitSweep + o];
+}
+
+// Grid-wide sum of NV doubles in the fixed adjacent-pairwise lane order.
+// Called by all threads; only sweep threads contribute.  CTA partials are
+// exchanged without a barrier: each double travels as two 64-bit words
+// (flag << 32 | 32 data bits), each single-copy atomic, so a reader that sees
+// the call's flag in both words holds the value (the LL protocol of NCCL).
+// Slots alternate by call parity: a CTA rewrites a slot only after every CTA
+// has published the following call, i.e. finished reading this one.
 template <int NV>
-__device__ void cluster_sum(FitState& F, double (&x)[NV]) {
+__device__ void grid_sum(FitState& F, double (&x)[NV]) {
   static_assert(NV <= kMaxNV, "too many values");
-  cg::cluster_group cl = cg::this_cluster();
   FitShared& S = *F.S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned flag = ++F.calls;
+  unsigned long long* part =
+      F.P->part + size_t(flag & 1u) * (kPartReplicas * kFitCtas * kMaxNV * 2);
+  const unsigned long long ftag = (unsigned long long)flag << 32;
+  fit_tr(F, 3);
+  if (is_sweep()) {
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1)
+    for (int off = 1; off < 32; off <<= 1)
 #pragma unroll
-    for (int q = 0; q < NV; ++q) x[q] += __shfl_down_sync(0xFFFFFFFFu, x[q], off);
-  if (lane == 0)
+      for (int q = 0; q < NV; ++q) x[q] += __shfl_down_sync(0xFFFFFFFFu, x[q], off);
+    if (lane == 0)
 #pragma unroll
-    for (int q = 0; q < NV; ++q) S.warp_part[warp][q] = x[q];
-  __syncthreads();
-  if (warp == 0) {
+      for (int q = 0; q < NV; ++q) S.warp_part[warp][q] = x[q];
+    sweep_bar();
+    if (threadIdx.x < NV) {
+      const int q = threadIdx.x;
+      double p[kFitSweepWarps];
+#pragma unroll
+      for (int r = 0; r < kFitSweepWarps; ++r) p[r] = S.warp_part[r][q];
+#pragma unroll
+      for (int width = 1; width < kFitSweepWarps; width *= 2)
+#pragma unroll
+        for (int j = 0; j < kFitSweepWarps; j += 2 * width) p[j] += p[j + width];
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(p[0]);
+      const unsigned long long w0 = ftag | (bits & 0xFFFFFFFFull), w1 = ftag | (bits >> 32);
+#pragma unroll
+      for (int rep = 0; rep < kPartReplicas; ++rep) {
+        unsigned long long* dst =
+            part + ((size_t(rep) * kFitCtas + blockIdx.x) * kMaxNV + q) * 2;
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
+                     : "memory");
+      }
+    }
+  }
+  fit_tr(F, 4);
+  // combine the kFitCtas partials: thread j holds pair (2j, 2j+1)
+  constexpr int kPairs = kFitCtas / 2;
+  if (threadIdx.x < kPairs) {
     double y[NV];
+    const unsigned long long* src =
+        part + (size_t(blockIdx.x % kPartReplicas) * kFitCtas + 2 * threadIdx.x) * kMaxNV * 2;
+    unsigned spins = 0;
+    while (true) {
+      unsigned long long w[2][NV][2];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) y[q] = lane < kFitWarps ? S.warp_part[lane][q] : 0.0;
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
-    for (int off = 1; off < kFitWarps; off <<= 1)
+        for (int q = 0; q < NV; ++q)
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(w[c][q][0]), "=l"(w[c][q][1])
+                       : "l"(src + (c * kMaxNV + q) * 2)
+                       : "memory");
+      bool ready = true;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          ready &= (w[c][q][0] >> 32) == flag && (w[c][q][1] >> 32) == flag;
+      if (ready) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const double a = __longlong_as_double(
+              (long long)((w[0][q][0] & 0xFFFFFFFFull) | (w[0][q][1] << 32)));
+          const double b = __longlong_as_double(
+              (long long)((w[1][q][0] & 0xFFFFFFFFull) | (w[1][q][1] << 32)));
+          y[q] = a + b;
+        }
+        break;
+      }
+      if (++spins > kSpinLimit) __trap();
+    }
+    fit_tr(F, 41);
+    constexpr int kW = kPairs < 32 ? kPairs : 32;
+#pragma unroll
+    for (int off = 1; off < kW; off <<= 1)
 #pragma unroll
       for (int q = 0; q < NV; ++q) y[q] += __shfl_down_sync(0xFFFFFFFFu, y[q], off);
     if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < NV; ++q) S.cta_part[F.slot][q] = y[q];
-  }
-  cl.sync();
-  // every peer partial is fetched by its own thread (parallel DSMEM loads)
-  if (threadIdx.x < NV * kFitCtas) {
-    const int q = threadIdx.x / kFitCtas, r = threadIdx.x % kFitCtas;
-    S.peer[q][r] = *cl.map_shared_rank(&S.cta_part[F.slot][q], r);
+      for (int q = 0; q < NV; ++q) S.red[warp][q] = y[q];
   }
   __syncthreads();
-  if (threadIdx.x < NV) {
-    double p[kFitCtas];
+  constexpr int kRW = (kPairs + 31) / 32;
 #pragma unroll
-    for (int r = 0; r < kFitCtas; ++r) p[r] = S.peer[threadIdx.x][r];
+  for (int q = 0; q < NV; ++q) {
+    double p[kRW];
 #pragma unroll
-    for (int width = 1; width < kFitCtas; width *= 2)
+    for (int r = 0; r < kRW; ++r) p[r] = S.red[r][q];
 #pragma unroll
-      for (int j = 0; j < kFitCtas; j += 2 * width) p[j] += p[j + width];
-    S.bcast[threadIdx.x] = p[0];
+    for (int width = 1; width < kRW; width *= 2)
+#pragma unroll
+      for (int j = 0; j < kRW; j += 2 * width) p[j] += p[j + width];
+    x[q] = p[0];
   }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NV; ++q) x[q] = S.bcast[q];
-  F.slot ^= 1;
+  fit_tr(F, 5);
 }
 
-// sin/cos of up to 4 angles, one per warp in parallel, broadcast to the CTA.
-__device__ void fit_sincos(FitState& F, int n, const double* phi, double (*cs)[2]) {
-  FitShared& S = *F.S;
-  const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0 && warp < n) dd_sincos(phi[warp], &S.sc[warp][0], &S.sc[warp][1]);
+// Helper warp: sin/cos of n <= 4 angles into S.sc[F.scbuf] (visible after
+// the next __syncthreads of the CTA).
+__device__ __forceinline__ void helper_sincos(FitState& F, int n, const double* phi) {
+  if ((threadIdx.x >> 5) == kFitSweepWarps) {
+    const int l = threadIdx.x & 31;
+    const bool tr = F.P->trace && blockIdx.x == 0 && l == 0 && F.S->nh < 254;
+    if (tr) F.S->htr[F.S->nh++] = clock64();
+    if (l < n) dd_sincos(phi[l], &F.S->sc[F.scbuf][l][0], &F.S->sc[F.scbuf][l][1]);
+    if (tr) F.S->htr[F.S->nh++] = clock64();
+  }
+}
+
+// Non-speculative sin/cos (used before the first sweeps): cs[i] = {cos, sin}.
+__device__ void fit_sincos_now(FitState& F, int n, const double* phi, double (*cs)[2]) {
+  fit_tr(F, 1);
+  helper_sincos(F, n, phi);
   __syncthreads();
   for (int i = 0; i < n; ++i) {
-    cs[i][0] = S.sc[i][1];  // cos
-    cs[i][1] = S.sc[i][0];  // sin
+    cs[i][0] = F.S->sc[F.scbuf][i][1];
+    cs[i][1] = F.S->sc[F.scbuf][i][0];
   }
   __syncthreads();
+  fit_tr(F, 2);
 }
 
-// One sweep over the observations + one cluster reduction computing
+// One sweep over the observations + one grid reduction computing
 //   [sd]                          if SD
 //   (st, stt, sdt) for NS angles  t = c*v - s*u   (road_geometry.cpp:17-24)
 //   sum r^2 for NR fitted lines   r = d - a0 - a1*t (road_geometry.cpp:37)
@@ -383,43 +497,47 @@ __device__ void fit_pass(FitState& F, const double (*ang)[2], const double (*lin
   double acc[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-  double c[NS > 0 ? NS : 1], s[NS > 0 ? NS : 1];
-#pragma unroll
-  for (int j = 0; j < NS; ++j) {
-    c[j] = ang[j][0];
-    s[j] = ang[j][1];
-  }
-  double la0[NR > 0 ? NR : 1], la1[NR > 0 ? NR : 1], lc[NR > 0 ? NR : 1], ls[NR > 0 ? NR : 1];
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    la0[j] = line[j][0];
-    la1[j] = line[j][1];
-    lc[j] = line[j][2];
-    ls[j] = line[j][3];
-  }
-  for (int m = 0; m < F.rows; ++m) {
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (i >= F.k) break;
-    double d, u, v;
-    fit_get(F, m, i, d, u, v);
-    int q = 0;
-    if (SD) acc[q++] += d;
+  if (is_sweep()) {
+    double c[NS > 0 ? NS : 1], s[NS > 0 ? NS : 1];
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
-      const double t = c[j] * v - s[j] * u;
-      acc[q] += t;
-      acc[q + 1] += t * t;
-      acc[q + 2] += d * t;
-      q += 3;
+      c[j] = ang[j][0];
+      s[j] = ang[j][1];
     }
+    double la0[NR > 0 ? NR : 1], la1[NR > 0 ? NR : 1], lc[NR > 0 ? NR : 1], ls[NR > 0 ? NR : 1];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const double t = lc[j] * v - ls[j] * u;
-      const double r = d - la0[j] - la1[j] * t;
-      acc[q++] += r * r;
+      la0[j] = line[j][0];
+      la1[j] = line[j][1];
+      lc[j] = line[j][2];
+      ls[j] = line[j][3];
+    }
+    fit_tr(F, 7);
+    const long long full = F.k / kFitLanes;  // rows every lane owns
+    const int nm = int(full) + (F.lane < F.k - full * kFitLanes ? 1 : 0);
+#pragma unroll 4
+    for (int m = 0; m < nm; ++m) {
+      double d, u, v;
+      fit_get(F, m, d, u, v);
+      int q = 0;
+      if (SD) acc[q++] += d;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        const double t = c[j] * v - s[j] * u;
+        acc[q] += t;
+        acc[q + 1] += t * t;
+        acc[q + 2] += d * t;
+        q += 3;
+      }
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const double t = lc[j] * v - ls[j] * u;
+        const double r = d - la0[j] - la1[j] * t;
+        acc[q++] += r * r;
+      }
     }
   }
-  cluster_sum<NV>(F, acc);
+  grid_sum<NV>(F, acc);
 #pragma unroll
   for (int q = 0; q < NV; ++q) out[q] = acc[q];
 }
@@ -440,7 +558,7 @@ __device__ __forceinline__ bool solve_line(double kk, double sd, const double* s
 // fit_line at one angle (road_geometry.cpp:12-39): two sweeps.
 __device__ bool fit_probe(FitState& F, double phi, LineFitD& out) {
   double cs[1][2];
-  fit_sincos(F, 1, &phi, cs);
+  fit_sincos_now(F, 1, &phi, cs);
   double r1[4];
   fit_pass<true, 1, 0>(F, cs, nullptr, r1);
   double a0, a1;
@@ -452,23 +570,72 @@ __device__ bool fit_probe(FitState& F, double phi, LineFitD& out) {
   return true;
 }
 
-// estimate_roll, road_geometry.cpp:41-68: golden section with the f1 < f2
-// branch, evaluated speculatively.  Every sweep computes the energy of the
-// newest point AND the normal-equation sums of the point the next iteration
-// will evaluate on either branch, so each iteration costs one sweep and one
-// cluster reduction.  The sequence of evaluated angles, every value and every
-// branch are exactly those of the sequential reference.
+// Golden-section bracket state of estimate_roll (road_geometry.cpp:41-68).
+struct GState {
+  double a, b, x1, x2;
+};
+constexpr double kGolden = 0.6180339887498949;
+
+// The f1 < f2 (br) / else update; returns the newly evaluated point.
+__device__ __forceinline__ double g_advance(GState& s, bool br) {
+  if (br) {
+    s.b = s.x2;
+    s.x2 = s.x1;
+    s.x1 = s.b - kGolden * (s.b - s.a);
+    return s.x1;
+  }
+  s.a = s.x1;
+  s.x1 = s.x2;
+  s.x2 = s.a + kGolden * (s.b - s.a);
+  return s.x2;
+}
+
+// Angles whose sums the sweep after state s computes: the point the next
+// iteration evaluates on either branch, or the final midpoint.
+__device__ __forceinline__ int g_cands(const GState& s, double tol, double* ca) {
+  if (s.b - s.a > tol) {
+    GState t = s;
+    ca[0] = g_advance(t, true);
+    t = s;
+    ca[1] = g_advance(t, false);
+    return 2;
+  }
+  ca[0] = ca[1] = 0.5 * (s.a + s.b);
+  return 1;
+}
+
+// Speculative helper request: candidates after either outcome of the pending
+// comparison, packed [br=true: 0,1 | br=false: 2,3].
+__device__ __forceinline__ void g_speculate(FitState& F, const GState& s, double tol) {
+  double ang[4];
+  GState t = s;
+  g_advance(t, true);
+  g_cands(t, tol, ang);
+  t = s;
+  g_advance(t, false);
+  g_cands(t, tol, ang + 2);
+  helper_sincos(F, 4, ang);
+}
+
+// estimate_roll with the f1 < f2 branch evaluated speculatively: every sweep
+// computes the energy of the newest point AND the normal-equation sums of the
+// point the next iteration will evaluate on either branch, so an iteration
+// costs one sweep and one grid reduction; the sin/cos the following sweep may
+// need are computed by the helper warp meanwhile.  The evaluated angles,
+// every value and every branch are exactly those of the sequential reference.
 __device__ bool fit_golden(FitState& F, double lo, double hi, double tol, LineFitD& out) {
-  constexpr double g = 0.6180339887498949;
   const double kk = double(F.k);
-  double a = lo, b = hi;
-  double x1 = b - g * (b - a), x2 = a + g * (b - a);
-  // sweep 0: sd and the sums of x1, x2
+  GState s{lo, hi, hi - kGolden * (hi - lo), lo + kGolden * (hi - lo)};
   double ang[2][2];
   {
-    const double ph[2] = {x1, x2};
-    fit_sincos(F, 2, ph, ang);
+    const double ph[2] = {s.x1, s.x2};
+    fit_sincos_now(F, 2, ph, ang);
   }
+  // sweep 0: sd and the sums of x1, x2; the helper prepares cands(s)
+  double ca[2];
+  const int n0 = g_cands(s, tol, ca);
+  F.scbuf ^= 1;
+  helper_sincos(F, n0, ca);
   double r0[7];
   fit_pass<true, 2, 0>(F, ang, nullptr, r0);
   const double sd = r0[0];
@@ -479,95 +646,57 @@ __device__ bool fit_golden(FitState& F, double lo, double hi, double tol, LineFi
   l1[3] = ang[0][1];
   l2[2] = ang[1][0];
   l2[3] = ang[1][1];
-
-  // Candidate angle evaluated next on each branch given the current state
-  // (after the comparison of f1, f2): the golden point if the loop body runs,
-  // otherwise the final midpoint.
-  auto next_angle = [&](bool branch_a, double& a_, double& b_) -> double {
-    double na = a, nb = b;
-    if (branch_a) {
-      nb = x2;
-      a_ = na;
-      b_ = nb;
-      return nb - g * (nb - na);
-    }
-    na = x1;
-    a_ = na;
-    b_ = nb;
-    return na + g * (nb - na);
-  };
-
-  // sweep 1: energies of x1 and x2 + sums of both possible next angles
-  bool loop = b - a > tol;
-  double ca[2];
-  int ncand;
-  if (loop) {
-    double ta, tb;
-    ca[0] = next_angle(true, ta, tb);
-    ca[1] = next_angle(false, ta, tb);
-    ncand = 2;
-  } else {
-    ca[0] = ca[1] = 0.5 * (a + b);
-    ncand = 1;
-  }
   double cang[2][2];
-  fit_sincos(F, ncand, ca, cang);
-  if (ncand == 1) {
-    cang[1][0] = cang[0][0];
-    cang[1][1] = cang[0][1];
+  {
+    const int b = F.scbuf;
+    for (int i = 0; i < 2; ++i) {
+      const int src = n0 == 2 ? i : 0;
+      cang[i][0] = F.S->sc[b][src][1];
+      cang[i][1] = F.S->sc[b][src][0];
+    }
   }
+  // sweep 1: energies of x1 and x2 + sums of cands(s); the helper speculates
+  bool loop = s.b - s.a > tol;
+  F.scbuf ^= 1;
+  if (loop) g_speculate(F, s, tol);
   double f1, f2;
   double res[8];
   {
     const double lines[2][4] = {{l1[0], l1[1], l1[2], l1[3]}, {l2[0], l2[1], l2[2], l2[3]}};
     fit_pass<false, 2, 2>(F, cang, lines, res);
-    // res = [S(cand0) x3, S(cand1) x3, E(x1), E(x2)]
     f1 = res[6];
     f2 = res[7];
   }
   double cs_sum[2][3] = {{res[0], res[1], res[2]}, {res[3], res[4], res[5]}};
   while (loop) {
-    // iteration body: branch on f1 < f2, adopt the matching candidate
     const bool br = f1 < f2;
     const int pick = br ? 0 : 1;
-    double na, nb;
-    const double xn = next_angle(br, na, nb);
     double ln[4];
     if (!solve_line(kk, sd, cs_sum[pick], ln[0], ln[1])) return false;
     ln[2] = cang[pick][0];
     ln[3] = cang[pick][1];
-    if (br) {
-      b = x2;
-      x2 = x1;
+    g_advance(s, br);
+    if (br)
       f2 = f1;
-      x1 = xn;
-    } else {
-      a = x1;
-      x1 = x2;
+    else
       f1 = f2;
-      x2 = xn;
+    loop = s.b - s.a > tol;
+    // sin/cos of cands(s) were speculated during the previous sweep
+    {
+      const int b = F.scbuf;
+      const int base = br ? 0 : 2;
+      const int n = loop ? 2 : 1;
+      for (int i = 0; i < 2; ++i) {
+        const int src = base + (n == 2 ? i : 0);
+        cang[i][0] = F.S->sc[b][src][1];
+        cang[i][1] = F.S->sc[b][src][0];
+      }
     }
-    (void)na;
-    (void)nb;
-    loop = b - a > tol;
-    if (loop) {
-      double ta, tb;
-      ca[0] = next_angle(true, ta, tb);
-      ca[1] = next_angle(false, ta, tb);
-      ncand = 2;
-    } else {
-      ca[0] = ca[1] = 0.5 * (a + b);
-      ncand = 1;
-    }
-    fit_sincos(F, ncand, ca, cang);
-    if (ncand == 1) {
-      cang[1][0] = cang[0][0];
-      cang[1][1] = cang[0][1];
-    }
+    F.scbuf ^= 1;
+    if (loop) g_speculate(F, s, tol);
     const double lines[1][4] = {{ln[0], ln[1], ln[2], ln[3]}};
     double r[7];
     fit_pass<false, 2, 1>(F, cang, lines, r);
-    // energy of the point just evaluated in the body
     if (br)
       f1 = r[6];
     else
@@ -580,7 +709,7 @@ __device__ bool fit_golden(FitState& F, double lo, double hi, double tol, LineFi
     cs_sum[1][2] = r[5];
   }
   // final fit_line at the midpoint: its sums are cs_sum[0]
-  const double mid = 0.5 * (a + b);
+  const double mid = 0.5 * (s.a + s.b);
   double fa0, fa1;
   if (!solve_line(kk, sd, cs_sum[0], fa0, fa1)) return false;
   const double lines[1][4] = {{fa0, fa1, cang[0][0], cang[0][1]}};
@@ -590,160 +719,211 @@ __device__ bool fit_golden(FitState& F, double lo, double hi, double tol, LineFi
   return true;
 }
 
-// Stable cluster-wide compaction of the survivors of fit_road's trimming
-// (road_geometry.cpp:83-97) into the scratch buffers.  Returns the new count.
+// Stable grid-wide compaction of the survivors of fit_road's trimming
+// (road_geometry.cpp:83-97) into the scratch buffers, then re-staging.
+// Returns the new count.
+template <bool COMPACT>
 __device__ long long fit_trim(FitState& F, const LineFitD& first, double rms) {
-  cg::cluster_group cl = cg::this_cluster();
   FitShared& S = *F.S;
   const FitKParams& P = *F.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double lim = 3.0 * rms;
-  const int rank = int(cl.block_rank());
-  // keep bits of this thread's rows
   unsigned long long keep = 0;
-  for (int m = 0; m < F.rows; ++m) {
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (i >= F.k) break;
-    double d, u, v;
-    fit_get(F, m, i, d, u, v);
-    const double r = d - (first.a0 + first.a1 * (v * first.c - u * first.s));
-    if (fabs(r) <= lim) keep |= 1ull << m;
-  }
-  // per-row counts of this CTA (rows <= kMaxRowsTrim enforced by the host)
-  for (int m = 0; m < F.rows; ++m) {
-    const unsigned bal = __ballot_sync(0xFFFFFFFFu, (keep >> m) & 1ull);
-    if (lane == 0) S.warp_cnt[warp] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int q = 0; q < kFitWarps; ++q) t += S.warp_cnt[q];
-      S.row_cnt[m] = t;
-    }
-    __syncthreads();
-  }
-  cl.sync();  // row counts of every CTA are visible
-  if (threadIdx.x == 0) {
-    long long base = 0;
+  if (is_sweep()) {
     for (int m = 0; m < F.rows; ++m) {
-      long long mine = 0;
-      for (int r = 0; r < kFitCtas; ++r) {
-        const int cnt = *cl.map_shared_rank(&S.row_cnt[m], r);
-        if (r == rank) mine = base;
-        base += cnt;
-      }
-      S.row_base[m] = int(mine);
-    }
-    S.bcast[0] = double(base);
-  }
-  cl.sync();  // peers finished reading row_cnt
-  const long long kept = (long long)S.bcast[0];
-  if (kept < 3 || kept == F.k) return kept;
-  // scatter survivors in element order
-  for (int m = 0; m < F.rows; ++m) {
-    const bool kb = (keep >> m) & 1ull;
-    const unsigned bal = __ballot_sync(0xFFFFFFFFu, kb);
-    if (lane == 0) S.warp_cnt[warp] = __popc(bal);
-    __syncthreads();
-    int woff = 0;
-    for (int q = 0; q < warp; ++q) woff += S.warp_cnt[q];
-    const long long i = (long long)m * kFitLanes + F.lane;
-    if (kb && i < F.k) {
-      const long long dst = S.row_base[m] + woff + __popc(bal & ((1u << lane) - 1u));
+      const long long i = (long long)m * kFitLanes + F.lane;
+      if (i >= F.k) break;
       double d, u, v;
-      fit_get(F, m, i, d, u, v);
-      if (F.compact) {
-        P.scr_uv[dst] = uint32_t(u) | (uint32_t(v) << 16);
-        P.scr_d[dst] = float(d);
-      } else {
-        P.scr_dd[dst] = d;
-        P.scr_du[dst] = u;
-        P.scr_dv[dst] = v;
-      }
+      fit_get(F, m, d, u, v);
+      const double r = d - (first.a0 + first.a1 * (v * first.c - u * first.s));
+      if (fabs(r) <= lim) keep |= 1ull << m;
     }
-    __syncthreads();
+    for (int m = 0; m < F.rows; ++m) {
+      const unsigned bal = __ballot_sync(0xFFFFFFFFu, (keep >> m) & 1ull);
+      if (lane == 0) S.wcnt[warp][m] = __popc(bal);
+    }
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < F.rows; m += blockDim.x) {
+    int t = 0;
+    for (int w = 0; w < kFitSweepWarps; ++w) t += S.wcnt[w][m];
+    __stcg(P.rowcnt + m * kFitCtas + blockIdx.x, t);
   }
   __threadfence();
-  cl.sync();
+  grid_bar(F);
+  // row totals and this CTA's offset within each row (counts staged in smem,
+  // row stride kFitCtas + 1 so the per-row scans below are conflict-free)
+  int* s_cnt = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(F.e) + kFitStageBytes);
+  __shared__ long long s_tot[kMaxRows];
+  {
+    const int n = F.rows * kFitCtas;
+    constexpr int U = 8;
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * kFitThreads) {
+      int x[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = i0 + j * kFitThreads;
+        x[j] = i < n ? __ldcg(P.rowcnt + i) : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = i0 + j * kFitThreads;
+        if (i < n) s_cnt[(i / kFitCtas) * (kFitCtas + 1) + i % kFitCtas] = x[j];
+      }
+    }
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < F.rows; m += blockDim.x) {
+    long long tot = 0, before = 0;
+    for (int c = 0; c < kFitCtas; ++c) {
+      const int x = s_cnt[m * (kFitCtas + 1) + c];
+      if (c < int(blockIdx.x)) before += x;
+      tot += x;
+    }
+    s_tot[m] = tot;
+    S.row_base[m] = int(before);
+  }
+  __shared__ long long s_kept;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int m = 0; m < F.rows; ++m) {
+      S.row_base[m] += int(acc);
+      acc += s_tot[m];
+    }
+    s_kept = acc;
+  }
+  __syncthreads();
+  const long long kept = s_kept;
+  if (kept < 3 || kept == F.k) return kept;
+  if (is_sweep()) {
+    for (int m = 0; m < F.rows; ++m) {
+      const bool kb = (keep >> m) & 1ull;
+      if (!__any_sync(0xFFFFFFFFu, kb)) continue;
+      const unsigned bal = __ballot_sync(0xFFFFFFFFu, kb);
+      int woff = 0;
+      for (int w = 0; w < warp; ++w) woff += S.wcnt[w][m];
+      if (kb) {
+        const long long dst = S.row_base[m] + woff + __popc(bal & ((1u << lane) - 1u));
+        double d, u, v;
+        fit_get(F, m, d, u, v);
+        if (COMPACT) {
+          __stcg(P.scr_uv + dst, uint32_t(u) | (uint32_t(v) << 16));
+          __stcg(P.scr_d + dst, float(d));
+        } else {
+          __stcg(P.scr_dd + dst, d);
+          __stcg(P.scr_du + dst, u);
+          __stcg(P.scr_dv + dst, v);
+        }
+      }
+    }
+  }
+  __threadfence();
+  grid_bar(F);
   F.k = kept;
-  F.g_uv = P.scr_uv;
-  F.g_d = P.scr_d;
-  F.g_dd = P.scr_dd;
-  F.g_du = P.scr_du;
-  F.g_dv = P.scr_dv;
-  fit_stage(F);
+  fit_stage_from<COMPACT>(F, P.scr_uv, P.scr_d, P.scr_dd, P.scr_du, P.scr_dv);
   return kept;
+}
+
+template <bool COMPACT>
+__device__ void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok) {
+  const FitRequest& R = P.r;
+  fit_stage_from<COMPACT>(F, R.obs.uv, R.obs.d, R.dd, R.du, R.dv);
+  LineFitD f{};
+  long long used = F.k;
+  if (R.mode == kFitLine) {
+    ok = fit_probe(F, R.phi, f);
+  } else if (R.mode == kEstimateRoll) {
+    ok = fit_golden(F, R.lo, R.hi, R.tol, f);
+  } else {
+    ok = fit_golden(F, -R.hi, R.hi, R.tol, f);  // fit_road: first = fit_line(obs, m.phi)
+    if (ok) {
+      const double rms = sqrt(f.e0min / double(F.k));
+      if (!(rms <= 0.0)) {
+        const long long k0 = F.k;
+        const long long kept = fit_trim<COMPACT>(F, f, rms);
+        if (kept >= 3 && kept != k0) {
+          ok = fit_golden(F, -R.hi, R.hi, R.tol, f);
+          used = kept;
+        }
+      }
+    }
+  }
+  if (ok) {
+    res.a0 = f.a0 * R.a0_scale;
+    res.a1 = f.a1;
+    res.phi = f.phi;
+    res.e0min = f.e0min;
+    res.used = used;
+    res.model = DevModel{res.a0, f.a1, f.phi, f.c, f.s};
+  }
 }
 
 __global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ FitKParams P) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FitShared S;
-  cg::cluster_group cl = cg::this_cluster();
   const FitRequest& R = P.r;
   FitState F;
   F.P = &P;
   F.S = &S;
-  F.dyn = dyn;
-  F.compact = R.compact;
-  F.lane = int(cl.block_rank()) * kFitThreads + threadIdx.x;
-  F.slot = 0;
-  F.g_uv = R.obs.uv;
-  F.g_d = R.obs.d;
-  F.g_dd = R.dd;
-  F.g_du = R.du;
-  F.g_dv = R.dv;
+  F.e = reinterpret_cast<double*>(dyn);
+  F.lane = int(blockIdx.x) * kFitSweep + int(threadIdx.x);
+  F.calls = 0;
+  F.scbuf = 0;
+  F.target = 0;
+  if (threadIdx.x == 0) S.ntr = S.nh = 0;
+  __syncthreads();
+  fit_tr(F, 0);
   const bool failed_before = P.status->code != 0;
   F.k = R.compact ? (long long)(failed_before ? 0 : *R.obs.count) : R.k_host;
   FitOut res{};
   bool ok = !failed_before && F.k >= 3;
-  if (ok) {
-    fit_stage(F);
-    LineFitD f{};
-    long long used = F.k;
-    if (R.mode == kFitLine) {
-      ok = fit_probe(F, R.phi, f);
-    } else if (R.mode == kEstimateRoll) {
-      ok = fit_golden(F, R.lo, R.hi, R.tol, f);
-    } else {
-      ok = fit_golden(F, -R.hi, R.hi, R.tol, f);  // fit_road: first = fit_line(obs, m.phi)
-      if (ok) {
-        const double rms = sqrt(f.e0min / double(F.k));
-        if (!(rms <= 0.0)) {
-          const long long k0 = F.k;
-          const long long kept = fit_trim(F, f, rms);
-          if (kept >= 3 && kept != k0) {
-            ok = fit_golden(F, -R.hi, R.hi, R.tol, f);
-            used = kept;
-          }
-        }
-      }
-    }
-    if (ok) {
-      res.a0 = f.a0 * R.a0_scale;
-      res.a1 = f.a1;
-      res.phi = f.phi;
-      res.e0min = f.e0min;
-      res.used = used;
-      res.model = DevModel{res.a0, f.a1, f.phi, f.c, f.s};
-    }
+  if (ok && F.k > (long long)kMaxRows * kFitLanes) {  // host checks the double input
+    ok = false;
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_status(P.status, RPD_EINVAL, R.where, F.k);
   }
-  if (!ok && !failed_before && cl.block_rank() == 0 && threadIdx.x == 0)
-    set_status(P.status, RPD_EDEGENERATE, R.where);
-  if (cl.block_rank() == 0 && threadIdx.x == 0) {
+  if (ok) {
+    if (R.compact)
+      fit_run<true>(F, P, res, ok);
+    else
+      fit_run<false>(F, P, res, ok);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (!ok && !failed_before) set_status(P.status, RPD_EDEGENERATE, R.where);
     if (!ok) res = FitOut{0.0, 0.0, 0.0, 0.0, 0, DevModel{0.0, 0.0, 0.0, 1.0, 0.0}};
     *R.out = res;
   }
-  cl.sync();  // keep shared memory alive until every peer is done with DSMEM
+  fit_tr(F, 9);
+  if (P.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = S.tr[0] & 0xFFFFFFFFFFFFll;
+    for (int i = 0; i < S.ntr; ++i) {
+      const long long t = S.tr[i] & 0xFFFFFFFFFFFFll;
+      printf("FITTR %d %d %lld\n", i, int(S.tr[i] >> 48), t - t0);
+    }
+    for (int i = 0; i < S.nh; ++i)
+      printf("FITH %d %lld\n", i, (S.htr[i] & 0xFFFFFFFFFFFFll) - t0);
+  }
 }
 
 void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
-  RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitDynSmem));
-  RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  if (!req.compact && req.k_host > (long long)kMaxRowsTrim * kFitLanes)
+  static bool attr_done = false;
+  if (!attr_done) {
+    RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, kFitDynSmem));
+    int per_sm = 0;
+    RPD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit, kFitThreads,
+                                                         kFitDynSmem));
+    if (per_sm * ctx->sm_count < kFitCtas)
+      throw CudaFail("fit: device cannot co-schedule the fit grid");
+    attr_done = true;
+  }
+  if (!req.compact && req.k_host > (long long)kMaxRows * kFitLanes)
     throw InvalidArg("fit: too many observations for the device fit (max 524288)");
   FitKParams P{};
   P.r = req;
   P.status = ctx->status;
-  const long long scratch = req.compact ? (long long)kMaxRowsTrim * kFitLanes
+  static const bool trace = getenv("RPD_FIT_TRACE") != nullptr;
+  P.trace = trace ? 1 : 0;
+  const long long scratch = req.compact ? (long long)kMaxRows * kFitLanes
                                         : std::max<long long>(req.k_host, 1);
   if (req.mode == kFitRoad) {
     if (req.compact) {
@@ -755,16 +935,19 @@ void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
       P.scr_dv = ctx->ws.get<double>("fit_scr_dv", scratch);
     }
   }
+  P.part = ctx->ws.get<unsigned long long>("fit_part", kPartWords);
+  RPD_CK(cudaMemsetAsync(P.part, 0, sizeof(unsigned long long) * kPartWords, ctx->stream));
+  P.rowcnt = ctx->ws.get<int>("fit_rowcnt", kMaxRows * kFitCtas);
+  P.bar = ctx->ws.get<unsigned>("fit_bar", 1);
+  RPD_CK(cudaMemsetAsync(P.bar, 0, sizeof(unsigned), ctx->stream));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kFitCtas);
   cfg.blockDim = dim3(kFitThreads);
   cfg.dynamicSmemBytes = kFitDynSmem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kFitCtas;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   RPD_CK(cudaLaunchKernelEx(&cfg, k_fit, P));

@@ -16,7 +16,7 @@ frame = data[s:e]
 agg = collections.OrderedDict()
 tot = 0.0
 unit = frame[0]["Metric Unit"]
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
 for d in frame:
     n = d["Kernel Name"].split("(")[0].replace("rpdg::", "").replace("<unnamed>::", "")[:58]
     t = float(d["Metric Value"]) * scale
