@@ -6,18 +6,25 @@ D=128 (d_max=127, bootstrap L=65 at half resolution, PT pass L=17), 8 SGM
 paths, P1=10, P2=120, SLIC p=2000.  Seeded synthetic scene (the paper's
 datasets are not available; paper_2012_10802_b200/synth.py).
 
-A step = one full detect_potholes_pipeline (pipeline.cpp:47-109) on one pair:
-bootstrap SGM, road fit, PT SGM, road refit, DT, SLIC + pooling, threshold,
-labelling.  N GPUs = N independent ranks (frames are independent; weak
-scaling, no collective on the data path).
+A step = F full detect_potholes_pipeline runs (pipeline.cpp:47-109; default
+F = 2 x streams) on the pair: bootstrap SGM, road fit, PT SGM, road refit,
+DT, SLIC + pooling, threshold, labelling.  The frames are independent, so a
+GPU keeps S pipeline contexts (one CUDA stream + workspace + captured graph
+each) in flight, as a stream server would.  N GPUs = N independent ranks
+(weak scaling, no collective on the data path).
 
   value  frames/s with the pair resident in HBM; device time per step from
-         CUDA events on the library's stream; L2 flushed (256 MiB write)
-         between steps outside the timed events; max over ranks.
+         CUDA events (start on a master stream that every context stream
+         waits on, end after all of them); L2 flushed (256 MiB write) between
+         steps outside the timed events; max over ranks.
+  value_serial  the same with one frame at a time on one stream (also the
+         pass the per-stage times and the roofline come from).
   e2e    frames/s through the C-ABI call rpd_detect_u8 with pinned HOST
-         buffers: H2D of the pair, the pipeline, D2H of labels + d1 + d2.
+         buffers (S host threads, one context each): H2D of the pair, the
+         pipeline, D2H of labels + d1 + d2 every call.
   roofline  the SGM path-aggregation kernel (dominant): SURVEY.md §8(d)
-         algorithmic bytes 2*(5P-2)*cells per launch / its CUDA-event time.
+         algorithmic bytes 2*(5P-2)*cells per launch / its CUDA-event time
+         in the serial pass.
   cpu_baseline  the CPU oracle (scalar restatement of the reference) on all
          host cores, one frame per thread.
 
@@ -52,6 +59,10 @@ def parse():
     ap.add_argument("--config", type=int, default=2, help="BASELINE config index (1-5)")
     ap.add_argument("--cpu-threads", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=4,
+                    help="concurrent pipeline contexts (one CUDA stream each) per GPU")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="frames per step per GPU (0 = 2 x streams)")
     return ap.parse_args()
 
 
@@ -230,34 +241,81 @@ def gpu_arm(args, rank, world, local):
         agg_bytes.append(sum(st.sgm_agg_alg_bytes[i] for i in range(st.sgm_passes)))
         sgm_ms.append(out.stage_ms[0] + out.stage_ms[2])
         npot.append(out.n_potholes)
-    barrier()
-    clk = clocks.stop()
-    total_ms = allmax(sum(step_ms))
-    value = world * args.steps / (total_ms / 1e3)
+    serial_ms = allmax(sum(step_ms))
+    value_serial = world * args.steps / (serial_ms / 1e3)
     sgm_total_ms = allmax(sum(sgm_ms))
     sgm_gdes = world * args.steps * gde / (sgm_total_ms / 1e3) / 1e9
 
-    # ---- e2e through the C-ABI with pinned host buffers
+    # ---- throughput: F frames per step over S concurrent contexts (streams)
+    S = max(1, args.streams)
+    F = args.frames or 2 * S
+    ctx.set_profiling(False)
+    ctxs = [ctx] + [lib.context(local) for _ in range(S - 1)]
+    streams = [torch.cuda.ExternalStream(c.stream) for c in ctxs]
+    master = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for i in range(F):
+            ctxs[i % S].detect_async_u8(left_d.data_ptr(), right_d.data_ptr(), h, w, cfg)
+        for c_ in ctxs:
+            c_.fetch()
+    barrier()
+    conc_ms = []
+    for _ in range(args.steps):
+        flush.zero_()  # on the master stream, before e0
+        e0.record(master)
+        for st_ in streams:
+            st_.wait_event(e0)
+        for i in range(F):
+            ctxs[i % S].detect_async_u8(left_d.data_ptr(), right_d.data_ptr(), h, w, cfg)
+        for st_ in streams:
+            ev = torch.cuda.Event()
+            ev.record(st_)
+            master.wait_event(ev)
+        e1.record(master)
+        e1.synchronize()
+        conc_ms.append(e0.elapsed_time(e1))
+        for c_ in ctxs:
+            npot.append(c_.fetch().n_potholes)  # checks every context's device status
+    barrier()
+    clk = clocks.stop()
+    total_ms = allmax(sum(conc_ms))
+    value = world * args.steps * F / (total_ms / 1e3)
+
+    # ---- e2e through the C-ABI with pinned host buffers: S host threads, one
+    # context each, every call = H2D pair + pipeline + D2H labels/d1/d2
     n = h * w
     lh = torch.from_numpy(scene.left).pin_memory()
     rh = torch.from_numpy(scene.right).pin_memory()
-    labels_h = torch.empty(n, dtype=torch.int32).pin_memory()
-    d1_h = torch.empty(n, dtype=torch.float32).pin_memory()
-    d2_h = torch.empty(n, dtype=torch.float32).pin_memory()
-    o = DetectOut()
-    o.labels = C.cast(labels_h.data_ptr(), C.POINTER(C.c_int32))
-    o.d1 = C.cast(d1_h.data_ptr(), C.POINTER(C.c_float))
-    o.d2 = C.cast(d2_h.data_ptr(), C.POINTER(C.c_float))
-    ctx.set_profiling(False)
-    for _ in range(max(1, args.warmup)):
-        ctx.detect_raw(lh.data_ptr(), rh.data_ptr(), h, w, cfg, o)
+
+    def make_out():
+        bufs = (torch.empty(n, dtype=torch.int32).pin_memory(),
+                torch.empty(n, dtype=torch.float32).pin_memory(),
+                torch.empty(n, dtype=torch.float32).pin_memory())
+        o = DetectOut()
+        o.labels = C.cast(bufs[0].data_ptr(), C.POINTER(C.c_int32))
+        o.d1 = C.cast(bufs[1].data_ptr(), C.POINTER(C.c_float))
+        o.d2 = C.cast(bufs[2].data_ptr(), C.POINTER(C.c_float))
+        return o, bufs
+    outs = [make_out() for _ in ctxs]
+
+    def e2e_run(frames_per_ctx):
+        def work(j):
+            for _ in range(frames_per_ctx[j]):
+                ctxs[j].detect_raw(lh.data_ptr(), rh.data_ptr(), h, w, cfg, outs[j][0])
+        ths = [threading.Thread(target=work, args=(j,)) for j in range(S)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    total_frames = args.steps * F
+    per_ctx = [total_frames // S + (1 if j < total_frames % S else 0) for j in range(S)]
+    e2e_run([max(1, args.warmup)] * S)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        ctx.detect_raw(lh.data_ptr(), rh.data_ptr(), h, w, cfg, o)
+    e2e_run(per_ctx)
     e2e_s = allmax(time.perf_counter() - t0)
     barrier()
-    e2e = world * args.steps / e2e_s
+    e2e = world * total_frames / e2e_s
 
     # ---- roofline of the aggregation kernel
     pk = peaks()
@@ -277,12 +335,15 @@ def gpu_arm(args, rank, world, local):
         "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "value_serial": round(value_serial, 3),
         "scaling": "weak", "vs_baseline": None, "dtype": "u8/u16 (SGM), f32/f64 (fit, SLIC)",
         "data": "synthetic (seeded BASELINE cfg%d scene, synth.py; paper datasets unavailable)" % c,
         "config": {"workload": "cfg%d: %dx%d uint8 pair, D=%d, P=%d, P1=%g, P2=%g, SLIC p=%d" % (
             c, h, w, cfg.d_max + 1, cfg.sgm_paths, cfg.lambda1, cfg.lambda2, cfg.superpixels),
-            "frames_per_step_per_gpu": 1, "l2": "flushed (256 MiB write) between timed steps",
-            "parallelism": "frame replicas per GPU, no collective"},
+            "frames_per_step_per_gpu": F, "streams_per_gpu": S,
+            "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": "independent frames: %d concurrent pipeline contexts per GPU, "
+                           "ranks = GPUs, no collective" % S},
         "sgm_gdes": round(sgm_gdes, 3),
         "gde_per_frame": gde,
         "stage_ms": {k: round(v, 4) for k, v in zip(
@@ -291,7 +352,7 @@ def gpu_arm(args, rank, world, local):
         "n_potholes": npot[-1] if npot else None,
         "e2e": {"value": round(e2e, 3), "unit": "frames/s", "h2d_bytes_per_step": 2 * n,
                 "d2h_bytes_per_step": 12 * n},
-        "gpu_launches": kernels * args.steps,
+        "gpu_launches": kernels * args.steps * F,
         "roofline": {"bound": "hbm", "kernel": "k_aggregate (SGM path aggregation, 2P paths)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
