@@ -21,6 +21,8 @@
 
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "sgm.cuh"
 
 namespace rpdg {
@@ -40,7 +42,11 @@ SgmLayout sgm_layout(int h, int w, int levels, int paths) {
     L.G = 1;
     L.wpl = (levels + 3) / 4;
   } else {
-    int G = 2;
+    static const int gmin = [] {  // 4 lanes per chain: 2x the warps of G = 2 (tuning: RPD_SGM_GMIN)
+      const char* e = std::getenv("RPD_SGM_GMIN");
+      return e ? std::max(2, std::atoi(e)) : 4;
+    }();
+    int G = gmin;
     while (4 * 9 * G < levels) G *= 2;
     L.G = G;
     L.wpl = std::max(5, (levels + 4 * G - 1) / (4 * G));

@@ -29,6 +29,14 @@ namespace {
 
 constexpr int kNC = 32;      // chains per CTA
 constexpr int kDepth = 3;    // input ring depth (stages)
+#ifndef RPD_AGG_RBASE
+#define RPD_AGG_RBASE 4      // steps per stage for <= 32 words per pixel
+#endif
+#ifndef RPD_AGG_UNROLL
+#define RPD_AGG_UNROLL 4     // unrolled steps of the inner loop (code size vs ILP)
+#endif
+constexpr int kRBase = RPD_AGG_RBASE;
+constexpr int kStepUnroll = RPD_AGG_UNROLL;
 constexpr uint32_t kInf2 = 0x7FFF7FFFu;
 
 enum JobType : int { kHoriz = 0, kVert = 1, kDiag = 2 };
@@ -128,7 +136,7 @@ __device__ __forceinline__ uint32_t min_pairs(const uint32_t (&x)[NPL]) {
 template <int WPL, int G>
 struct Geo {
   static constexpr int WPP = WPL * G;                  // words per pixel
-  static constexpr int R = WPP <= 32 ? 8 : (WPP <= 64 ? 4 : (WPP <= 128 ? 2 : 1));
+  static constexpr int R = WPP <= 32 ? kRBase : (WPP <= 64 ? (kRBase + 1) / 2 : 1);
   static constexpr int ROW = kNC * WPP;                // words of one step (vert / diag)
   static constexpr int CWF = ROW < 256 ? ROW : 256;    // full chunk width
   static constexpr int NCH = (ROW + 255) / 256;        // chunks per row
@@ -366,7 +374,7 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
     const int s0 = stage_base + st * R;
     // only the first tile of a backward H/V scan holds padding steps
     const bool check = TYPE != kDiag && s0 < s_begin;
-#pragma unroll
+#pragma unroll(kStepUnroll)
     for (int r = 0; r < R; ++r) {
       const int s = s0 + r;
       const int rr = (TYPE != kDiag && backward) ? R - 1 - r : r;
