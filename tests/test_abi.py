@@ -74,7 +74,8 @@ def test_cuda_library_has_tma_and_dpx_sass(cuda_lib_path):
                           text=True).stdout
     assert "UTMALDG" in sass and "UTMASTG" in sass  # TMA tensor loads / stores
     assert "VIADDMNMX" in sass                      # DPX fused add+min (SGM recurrence)
-    assert "UCGABAR" in sass                        # thread-block cluster barrier (road fit)
+    # road fit: flag-tagged 128-bit partial exchange between the cooperative CTAs
+    assert "STG.E.128.STRONG.GPU" in sass and "LDG.E.128.STRONG.GPU" in sass
 
 
 def test_no_cpu_fallback_without_gpu(cuda_lib_path):
