@@ -222,7 +222,53 @@ void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_v
 // One thread per (pixel, 4-level word).  Levels >= L are padded with 0xFF.
 // C_L(v,u,d) = popc(cl(u) ^ cr(u-d))  if u-d >= 0 and in_view(u-d), else maxc
 // C_R(v,u,d) = popc(cl(u+d) ^ cr(u))  if u+d <  W and in_view(u),   else maxc
-__global__ void k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
+// One CTA per image row: the row's census words and validity flags are
+// staged in shared memory, then the row's volume words (4 levels each) are
+// produced in storage order, so every store is coalesced.
+__global__ void __launch_bounds__(256)
+    k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
+              const uint8_t* __restrict__ iv, int h, int w, int levels, int nw,
+              size_t pitch_words, uint32_t maxc, uint32_t* __restrict__ vol_l,
+              uint32_t* __restrict__ vol_r) {
+  extern __shared__ uint64_t csm[];  // cl[w] | cr[w] | iv[w] bytes
+  uint64_t* s_cl = csm;
+  uint64_t* s_cr = csm + w;
+  uint8_t* s_iv = reinterpret_cast<uint8_t*>(csm + 2 * w);
+  const int v = blockIdx.y;
+  const long long row = (long long)v * w;
+  for (int u = threadIdx.x; u < w; u += blockDim.x) {
+    s_cl[u] = cl[row + u];
+    s_cr[u] = cr[row + u];
+    s_iv[u] = iv[row + u];
+  }
+  __syncthreads();
+  uint32_t* ol = vol_l + size_t(v) * pitch_words;
+  uint32_t* orr = vol_r + size_t(v) * pitch_words;
+  const int total = w * nw;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int u = i / nw, j = i - u * nw;
+    const uint64_t a = s_cl[u];
+    const uint64_t b = s_cr[u];
+    const bool ivu = s_iv[u] != 0;
+    uint32_t wl = 0, wr = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int d = 4 * j + q;
+      uint32_t cL = 0xFF, cR = 0xFF;
+      if (d < levels) {
+        cL = (u - d < 0 || !s_iv[u - d]) ? maxc : uint32_t(__popcll(a ^ s_cr[u - d]));
+        cR = (u + d >= w || !ivu) ? maxc : uint32_t(__popcll(s_cl[u + d] ^ b));
+      }
+      wl |= cL << (8 * q);
+      wr |= cR << (8 * q);
+    }
+    ol[i] = wl;
+    orr[i] = wr;
+  }
+}
+
+// Rows too wide to stage in shared memory.
+__global__ void k_cost_u8_flat(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
                           const uint8_t* __restrict__ iv, int h, int w, int levels, int nw,
                           size_t pitch_words, uint32_t maxc, uint32_t* __restrict__ vol_l,
                           uint32_t* __restrict__ vol_r) {
@@ -544,7 +590,35 @@ __global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ Wt
   const int tile_words = npx * nw;
   const int stride = 2 * nw + 1;
   const size_t base = size_t(row) * a.pitch + size_t(u0) * a.lw;
-  for (int i = threadIdx.x; i < tile_words; i += kWtaPx) {
+  // 16-byte loads: 8 paths x 16 B in flight per thread (tile bases are
+  // 16-byte aligned: pitch and u0 * lw are multiples of 16)
+  const int nvec = tile_words >> 2;
+  for (int i4 = threadIdx.x; i4 < nvec; i4 += kWtaPx) {
+    uint4 x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < a.paths) x[r] = __ldg(reinterpret_cast<const uint4*>(a.path[r] + base) + i4);
+    int px = (4 * i4) / nw, j = 4 * i4 - px * nw;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t s01 = 0, s23 = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (r < a.paths) {
+          const uint32_t xe = e == 0 ? x[r].x : (e == 1 ? x[r].y : (e == 2 ? x[r].z : x[r].w));
+          s01 += __byte_perm(xe, 0u, 0x4140);
+          s23 += __byte_perm(xe, 0u, 0x4342);
+        }
+      }
+      sums[px * stride + 2 * j] = s01;
+      sums[px * stride + 2 * j + 1] = s23;
+      if (++j == nw) {
+        j = 0;
+        ++px;
+      }
+    }
+  }
+  for (int i = 4 * nvec + threadIdx.x; i < tile_words; i += kWtaPx) {
     uint32_t s01 = 0, s23 = 0;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -838,11 +912,21 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     uint8_t* vol_r = vol_l + vb;
     uint8_t* pathbuf = ctx->ws.get<uint8_t>("mp_paths", vb * 2 * paths);
     {
-      const long long n = npix * nw;
-      const int blocks = int(std::min<long long>((n + 255) / 256, 148 * 32));
-      k_cost_u8<<<std::max(blocks, 1), 256, 0, st>>>(
-          cl, cr, iv, h, w, levels, nw, L.pitch / 4, uint32_t(window * window - 1),
-          reinterpret_cast<uint32_t*>(vol_l), reinterpret_cast<uint32_t*>(vol_r));
+      const int smem = w * 17;
+      if (smem <= 200 * 1024) {
+        if (smem > 48 * 1024)
+          RPD_CK(cudaFuncSetAttribute(k_cost_u8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem));
+        k_cost_u8<<<dim3(1, h), 256, smem, st>>>(
+            cl, cr, iv, h, w, levels, nw, L.pitch / 4, uint32_t(window * window - 1),
+            reinterpret_cast<uint32_t*>(vol_l), reinterpret_cast<uint32_t*>(vol_r));
+      } else {
+        const long long n = npix * nw;
+        const int blocks = int(std::min<long long>((n + 255) / 256, 148 * 32));
+        k_cost_u8_flat<<<std::max(blocks, 1), 256, 0, st>>>(
+            cl, cr, iv, h, w, levels, nw, L.pitch / 4, uint32_t(window * window - 1),
+            reinterpret_cast<uint32_t*>(vol_l), reinterpret_cast<uint32_t*>(vol_r));
+      }
       RPD_LAUNCH_CHECK();
     }
     const uint32_t p1 = uint32_t(l1), p2 = uint32_t(l2);

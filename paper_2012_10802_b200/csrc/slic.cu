@@ -215,16 +215,18 @@ template <bool SUMS>
 __global__ void __launch_bounds__(kTileU* kTileV)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
   __shared__ int s_cnt;
-  __shared__ int s_k[kMaxTileCenters], s_icu[kMaxTileCenters], s_icv[kMaxTileCenters];
-  __shared__ double s_cu[kMaxTileCenters], s_cv[kMaxTileCenters], s_val[kMaxTileCenters];
+  __shared__ int4 s_ci[kMaxTileCenters];     // icu, icv, k
+  __shared__ double2 s_cd[kMaxTileCenters];  // cu, cv
+  __shared__ double s_val[kMaxTileCenters];
   const int tx = threadIdx.x % kTileU, ty = threadIdx.x / kTileU;
   const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
-  const int u = u0 + tx, v = v0 + ty;
+  const int u = u0 + tx, v = v0 + ty;  // v is uniform across a warp (one tile row)
+  const int win = a.win;
   const bool in = u < a.w && v < a.h;
-  const int bx0 = u0 - a.win < 0 ? 0 : (u0 - a.win) / a.B;
-  const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + a.win) / a.B);
-  const int by0 = v0 - a.win < 0 ? 0 : (v0 - a.win) / a.B;
-  const int by1 = min(a.nby - 1, (v0 + kTileV - 1 + a.win) / a.B);
+  const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
+  const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B);
+  const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
+  const int by1 = min(a.nby - 1, (v0 + kTileV - 1 + win) / a.B);
   const int nbxr = bx1 - bx0 + 1, nbr = nbxr * (by1 - by0 + 1);
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
@@ -233,13 +235,15 @@ __global__ void __launch_bounds__(kTileU* kTileV)
     const int e = a.cell_start[bucket + 1];
     for (int idx = a.cell_start[bucket]; idx < e; ++idx) {
       const int k = a.cell_items[idx];
+      const int icu = a.c.icu[k], icv = a.c.icv[k];
+      // keep only centres whose window reaches the tile
+      const int du = icu < u0 ? u0 - icu : (icu > u0 + kTileU - 1 ? icu - (u0 + kTileU - 1) : 0);
+      const int dv = icv < v0 ? v0 - icv : (icv > v0 + kTileV - 1 ? icv - (v0 + kTileV - 1) : 0);
+      if (du > win || dv > win) continue;
       const int slot = atomicAdd(&s_cnt, 1);
       if (slot < kMaxTileCenters) {
-        s_k[slot] = k;
-        s_icu[slot] = a.c.icu[k];
-        s_icv[slot] = a.c.icv[k];
-        s_cu[slot] = a.c.cu[k];
-        s_cv[slot] = a.c.cv[k];
+        s_ci[slot] = make_int4(icu, icv, k, 0);
+        s_cd[slot] = make_double2(a.c.cu[k], a.c.cv[k]);
         s_val[slot] = a.c.val[k];
       }
     }
@@ -252,22 +256,26 @@ __global__ void __launch_bounds__(kTileU* kTileV)
   if (in) {
     p = size_t(v) * a.w + u;
     x = double(a.vals[p]);
-    double best = __longlong_as_double(0x7FF0000000000000ll);
-    int bk = -1;
-    if (nc <= kMaxTileCenters) {
-      for (int i = 0; i < nc; ++i) {
-        if (abs(u - s_icu[i]) > a.win || abs(v - s_icv[i]) > a.win) continue;
-        const int k = s_k[i];
-        const double dval = x - s_val[i];
-        const double du = double(u) - s_cu[i], dv = double(v) - s_cv[i];
-        const double dist = dval * dval + (du * du + dv * dv) * a.sw;
-        if (dist < best || (dist == best && k < bk)) {
-          best = dist;
-          bk = k;
-        }
-      }
-    } else {  // pathological centre pile-up: per-pixel bucket walk
-      bk = assign_walk(a, u, v, x);
+  }
+  double best = __longlong_as_double(0x7FF0000000000000ll);
+  int bk = -1;
+  if (nc <= kMaxTileCenters) {
+    const double du0 = double(u), dv0 = double(v), sw = a.sw;
+    for (int i = 0; i < nc; ++i) {
+      const int4 ci = s_ci[i];
+      if (abs(v - ci.y) > win) continue;  // warp-uniform
+      const double2 cd = s_cd[i];
+      const double dval = x - s_val[i];
+      const double du = du0 - cd.x, dv = dv0 - cd.y;
+      const double dist = dval * dval + (du * du + dv * dv) * sw;
+      const bool take = abs(u - ci.x) <= win && (dist < best || (dist == best && ci.z < bk));
+      best = take ? dist : best;
+      bk = take ? ci.z : bk;
+    }
+  }
+  if (in) {
+    if (nc > kMaxTileCenters) {
+      bk = assign_walk(a, u, v, x);  // pathological centre pile-up: per-pixel bucket walk
     }
     if (bk < 0) {
       a.labels[p] = 0;
