@@ -222,42 +222,50 @@ void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_v
 // One thread per (pixel, 4-level word).  Levels >= L are padded with 0xFF.
 // C_L(v,u,d) = popc(cl(u) ^ cr(u-d))  if u-d >= 0 and in_view(u-d), else maxc
 // C_R(v,u,d) = popc(cl(u+d) ^ cr(u))  if u+d <  W and in_view(u),   else maxc
-// One CTA per image row: the row's census words and validity flags are
-// staged in shared memory, then the row's volume words (4 levels each) are
-// produced in storage order, so every store is coalesced.
+// One CTA per image row: the row's census words are staged in shared memory
+// with `levels` padding entries on both sides, and an override byte per entry
+// (0xFF for an invalid or out-of-row pixel, else 0), so every cost is
+// branch-free: min(popc(a ^ b) | ov, maxc) == maxc exactly when the reference
+// substitutes maxc (sgm.cpp:40-60; a valid popcount never exceeds maxc).
+// Volume words are produced in storage order (coalesced stores).
 __global__ void __launch_bounds__(256)
     k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
               const uint8_t* __restrict__ iv, int h, int w, int levels, int nw,
               size_t pitch_words, uint32_t maxc, uint32_t* __restrict__ vol_l,
               uint32_t* __restrict__ vol_r) {
-  extern __shared__ uint64_t csm[];  // cl[w] | cr[w] | iv[w] bytes
-  uint64_t* s_cl = csm;
-  uint64_t* s_cr = csm + w;
-  uint8_t* s_iv = reinterpret_cast<uint8_t*>(csm + 2 * w);
+  extern __shared__ uint64_t csm[];  // cl[W] | cr[W] | ov[W] bytes, W = w + 2*levels
+  const int W = w + 2 * levels;
+  uint64_t* s_cl = csm + levels;  // s_cl[u], u in [-levels, w + levels)
+  uint64_t* s_cr = csm + W + levels;
+  uint8_t* s_ov = reinterpret_cast<uint8_t*>(csm + 2 * W) + levels;
   const int v = blockIdx.y;
   const long long row = (long long)v * w;
-  for (int u = threadIdx.x; u < w; u += blockDim.x) {
-    s_cl[u] = cl[row + u];
-    s_cr[u] = cr[row + u];
-    s_iv[u] = iv[row + u];
+  for (int u = int(threadIdx.x) - levels; u < w + levels; u += blockDim.x) {
+    const bool in = u >= 0 && u < w;
+    s_cl[u] = in ? cl[row + u] : 0ull;
+    s_cr[u] = in ? cr[row + u] : 0ull;
+    s_ov[u] = (in && iv[row + u]) ? 0 : 0xFF;
   }
   __syncthreads();
   uint32_t* ol = vol_l + size_t(v) * pitch_words;
   uint32_t* orr = vol_r + size_t(v) * pitch_words;
   const int total = w * nw;
+  const float inv_nw = 1.0f / float(nw);
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int u = i / nw, j = i - u * nw;
+    // i / nw exactly: (i + 0.5) / nw is >= 1/(2 nw) away from an integer
+    const int u = int(__fmul_rn(float(i) + 0.5f, inv_nw));
+    const int j = i - u * nw;
     const uint64_t a = s_cl[u];
     const uint64_t b = s_cr[u];
-    const bool ivu = s_iv[u] != 0;
+    const uint32_t ovu = s_ov[u];
     uint32_t wl = 0, wr = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int d = 4 * j + q;
       uint32_t cL = 0xFF, cR = 0xFF;
       if (d < levels) {
-        cL = (u - d < 0 || !s_iv[u - d]) ? maxc : uint32_t(__popcll(a ^ s_cr[u - d]));
-        cR = (u + d >= w || !ivu) ? maxc : uint32_t(__popcll(s_cl[u + d] ^ b));
+        cL = min(uint32_t(__popcll(a ^ s_cr[u - d])) | s_ov[u - d], maxc);
+        cR = min(uint32_t(__popcll(s_cl[u + d] ^ b)) | ovu | (u + d >= w ? 0xFFu : 0u), maxc);
       }
       wl |= cL << (8 * q);
       wr |= cR << (8 * q);
@@ -912,7 +920,7 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     uint8_t* vol_r = vol_l + vb;
     uint8_t* pathbuf = ctx->ws.get<uint8_t>("mp_paths", vb * 2 * paths);
     {
-      const int smem = w * 17;
+      const int smem = (w + 2 * levels) * 17;
       if (smem <= 200 * 1024) {
         if (smem > 48 * 1024)
           RPD_CK(cudaFuncSetAttribute(k_cost_u8, cudaFuncAttributeMaxDynamicSharedMemorySize,

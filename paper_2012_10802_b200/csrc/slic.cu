@@ -223,6 +223,8 @@ __global__ void __launch_bounds__(kTileU* kTileV)
   const int u = u0 + tx, v = v0 + ty;  // v is uniform across a warp (one tile row)
   const int win = a.win;
   const bool in = u < a.w && v < a.h;
+  const size_t p = in ? size_t(v) * a.w + u : 0;
+  const float xf = in ? a.vals[p] : 0.0f;  // issued before the candidate fill
   const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
   const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B);
   const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
@@ -251,12 +253,7 @@ __global__ void __launch_bounds__(kTileU* kTileV)
   __syncthreads();
   const int nc = s_cnt;
   int label = -1;  // -1: outside the image
-  size_t p = 0;
-  double x = 0.0;
-  if (in) {
-    p = size_t(v) * a.w + u;
-    x = double(a.vals[p]);
-  }
+  const double x = double(xf);
   double best = __longlong_as_double(0x7FF0000000000000ll);
   int bk = -1;
   if (nc <= kMaxTileCenters) {
@@ -291,12 +288,14 @@ __global__ void __launch_bounds__(kTileU* kTileV)
     const int key = label > 0 ? label : -1;
     const RunInfo ri = run_info(key);
     int bad = 0;
-    Acc128 ax = key > 0 ? to_fixed(float(x), &bad) : Acc128{0ull, 0ll};
+    Acc128 ax = key > 0 ? to_fixed(xf, &bad) : Acc128{0ull, 0ll};
     if (bad) atomicOr(a.inexact, 1);
-    const int cnt = run_sum(key > 0 ? 1 : 0, ri);
     ax = run_sum(ax, ri);
-    const long long su = run_sum(key > 0 ? (long long)u : 0ll, ri);
-    const long long sv = run_sum(key > 0 ? (long long)v : 0ll, ri);
+    // a run is a contiguous pixel segment of one row: count and coordinate
+    // sums follow from its bounds
+    const int cnt = ri.end - (threadIdx.x & 31) + 1;
+    const long long su = (long long)cnt * u + (long long)cnt * (cnt - 1) / 2;
+    const long long sv = (long long)cnt * v;
     if (ri.head) {
       atomicAdd(&s.n[key], cnt);
       atomic_add_acc(&s.sx[key], ax);
