@@ -203,6 +203,27 @@ __device__ __forceinline__ T run_sum(T x, const RunInfo& ri) {
   return x;
 }
 
+// Exact 128-bit sums accumulated with fire-and-forget reductions: v = a2*2^64
+// + a1*2^32 + a0 where every added term of a0 / a1 is < 2^32 (no carries to
+// track), a2 takes the signed top word.
+struct __align__(16) AccSum {
+  unsigned long long a0, a1;
+  long long a2;
+  long long pad;
+};
+
+__device__ __forceinline__ void red_add_acc(AccSum* s, Acc128 x) {
+  atomicAdd(&s->a0, x.lo & 0xFFFFFFFFull);
+  atomicAdd(&s->a1, x.lo >> 32);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&s->a2), (unsigned long long)x.hi);
+}
+
+__device__ __forceinline__ Acc128 acc_value(const AccSum& s) {
+  const unsigned long long lo = s.a0 + (s.a1 << 32);
+  const long long carry = lo < s.a0 ? 1 : 0;
+  return Acc128{lo, s.a2 + (long long)(s.a1 >> 32) + carry};
+}
+
 __device__ __forceinline__ void atomic_add_acc(Acc128* a, Acc128 x) {
   const unsigned long long old = atomicAdd(&a->lo, x.lo);
   const unsigned long long carry = (old + x.lo) < old ? 1ull : 0ull;

@@ -21,6 +21,7 @@
 
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "sgm.cuh"
@@ -38,18 +39,25 @@ SgmLayout sgm_layout(int h, int w, int levels, int paths) {
   L.w = w;
   L.levels = levels;
   L.paths = paths;
+  // tuning overrides "G,WPL" (RPD_SGM_LAYOUT_SMALL for <= 36 levels, _BIG otherwise)
+  auto env_layout = [&](const char* name, int& G, int& wpl) {
+    const char* e = std::getenv(name);
+    int g = 0, wp = 0;
+    if (e && std::sscanf(e, "%d,%d", &g, &wp) == 2 && g >= 1 && wp >= 1 && 4 * g * wp >= levels) {
+      G = g;
+      wpl = wp;
+    }
+  };
   if (levels <= 36) {
     L.G = 1;
     L.wpl = (levels + 3) / 4;
+    env_layout("RPD_SGM_LAYOUT_SMALL", L.G, L.wpl);
   } else {
-    static const int gmin = [] {  // 4 lanes per chain: 2x the warps of G = 2 (tuning: RPD_SGM_GMIN)
-      const char* e = std::getenv("RPD_SGM_GMIN");
-      return e ? std::max(2, std::atoi(e)) : 4;
-    }();
-    int G = gmin;
+    int G = 4;  // 4 lanes per chain: 2x the warps of G = 2
     while (4 * 9 * G < levels) G *= 2;
     L.G = G;
     L.wpl = std::max(5, (levels + 4 * G - 1) / (4 * G));
+    env_layout("RPD_SGM_LAYOUT_BIG", L.G, L.wpl);
   }
   L.lw = 4 * L.wpl * L.G;
   L.pitch = size_t(round_up(w * L.lw, 16));  // TMA row strides must be 16-byte multiples

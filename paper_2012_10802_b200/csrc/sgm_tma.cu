@@ -481,6 +481,9 @@ KernelInfo pick(int wpl, int G, int levels) {
   if (wpl == W_ && G == G_) return info<W_, G_, 2 * W_>();
   RPD_TMA_G1(1) RPD_TMA_G1(2) RPD_TMA_G1(3) RPD_TMA_G1(4) RPD_TMA_G1(5) RPD_TMA_G1(6)
   RPD_TMA_G1(7) RPD_TMA_G1(8) RPD_TMA_G1(9)
+  RPD_TMA_GN(2, 2) RPD_TMA_GN(3, 2) RPD_TMA_GN(4, 2)
+  RPD_TMA_GN(2, 4) RPD_TMA_GN(3, 4) RPD_TMA_GN(4, 4)
+  RPD_TMA_GN(2, 8) RPD_TMA_GN(3, 8) RPD_TMA_GN(4, 8)
   RPD_TMA_GN(5, 2) RPD_TMA_GN(6, 2) RPD_TMA_GN(7, 2) RPD_TMA_GN(8, 2) RPD_TMA_GN(9, 2)
   RPD_TMA_GN(5, 4) RPD_TMA_GN(6, 4) RPD_TMA_GN(7, 4) RPD_TMA_GN(8, 4) RPD_TMA_GN(9, 4)
   RPD_TMA_GN(5, 8) RPD_TMA_GN(6, 8) RPD_TMA_GN(7, 8) RPD_TMA_GN(8, 8) RPD_TMA_GN(9, 8)
@@ -520,7 +523,8 @@ CUtensorMap make_map(void* base, int words_per_row, int rows, int depth, size_t 
 }  // namespace
 
 bool sgm_tma_supported(const SgmLayout& L) {
-  return L.G <= 8 && L.wpl >= 1 && L.wpl <= 9 && (L.G == 1 || L.wpl >= 5);
+  return (L.G == 1 || L.G == 2 || L.G == 4 || L.G == 8) && L.wpl >= 1 && L.wpl <= 9 &&
+         (L.G == 1 || L.wpl >= 2);
 }
 
 // Launches the aggregation of all 2P (volume, direction) jobs of one pass.

@@ -50,7 +50,7 @@ struct CenterSums {
   int* n;
   long long* su;
   long long* sv;
-  Acc128* sx;
+  AccSum* sx;
 };
 
 // values_or_zero, segmentation.cpp:13-19
@@ -94,6 +94,13 @@ __global__ void k_seeds(const float* __restrict__ vals, int h, int w, int nu, in
   c.val[k] = double(vals[size_t(bv) * w + bu]);
 }
 
+// A centre as the assignment tiles read it, stored in bucket order.
+struct __align__(16) CRec {
+  int4 ik;       // icu, icv, k, 0
+  double2 cuv;   // cu, cv
+  double2 val;   // val, 0
+};
+
 // Single-CTA counting sort of the centres into the bucket grid.
 constexpr int kBucketThreads = 1024;
 constexpr int kBucketItems = 8;  // supports up to 8192 buckets (32 KB smem)
@@ -101,7 +108,7 @@ constexpr int kMaxBuckets = kBucketThreads * kBucketItems;
 
 __global__ void __launch_bounds__(kBucketThreads)
     k_buckets(Centers c, int K, int w, int h, int B, int nbx, int nby, int* __restrict__ cell_start,
-              int* __restrict__ cell_items, CenterSums s, int finalize) {
+              int* __restrict__ cell_items, CRec* __restrict__ recs, CenterSums s, int finalize) {
   using Scan = cub::BlockScan<int, kBucketThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int cnt[kMaxBuckets];
@@ -114,12 +121,12 @@ __global__ void __launch_bounds__(kBucketThreads)
         const double dn = double(n);
         c.cu[k] = double(s.su[l]) / dn;
         c.cv[k] = double(s.sv[l]) / dn;
-        c.val[k] = fixed_to_double(s.sx[l]) / dn;
+        c.val[k] = fixed_to_double(acc_value(s.sx[l])) / dn;
       }
       s.n[l] = 0;
       s.su[l] = 0;
       s.sv[l] = 0;
-      s.sx[l] = Acc128{0ull, 0ll};
+      s.sx[l] = AccSum{0ull, 0ull, 0ll, 0ll};
     }
     __syncthreads();
   }
@@ -157,6 +164,8 @@ __global__ void __launch_bounds__(kBucketThreads)
     const int bx = min(max(iu, 0) / B, nbx - 1), by = min(max(iv, 0) / B, nby - 1);
     const int pos = atomicAdd(&cnt[by * nbx + bx], 1);
     cell_items[pos] = k;
+    recs[pos] = CRec{make_int4(iu, iv, k, 0), make_double2(c.cu[k], c.cv[k]),
+                     make_double2(c.val[k], 0.0)};
   }
 }
 
@@ -166,6 +175,7 @@ struct AssignArgs {
   Centers c;
   const int* cell_start;
   const int* cell_items;
+  const CRec* recs;
   int B, nbx, nby, win;
   double sw;
   int32_t* labels;
@@ -209,98 +219,141 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 // and — when SUMS — the pixel's (1, u, v, value) is added to its label's sums
 // with warp run aggregation (a warp is one tile row).  Pixels without a window
 // are left for the fallback kernel, which adds their sums itself.
-constexpr int kTileU = 32, kTileV = 8, kMaxTileCenters = 384;
+constexpr int kTileU = 32, kTileV = 16, kMaxTileCenters = 384;
+constexpr int kAssignThreads = 256;
+constexpr int kRowsPerWarp = kTileV / (kAssignThreads / 32);  // a warp owns rows w, w+8
 
 template <bool SUMS>
-__global__ void __launch_bounds__(kTileU* kTileV)
+__global__ void __launch_bounds__(kAssignThreads)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_nrows, s_rs[8], s_rb[9];
+  __shared__ int s_rowcnt[kTileV];
   __shared__ int4 s_ci[kMaxTileCenters];     // icu, icv, k
   __shared__ double2 s_cd[kMaxTileCenters];  // cu, cv
   __shared__ double s_val[kMaxTileCenters];
-  const int tx = threadIdx.x % kTileU, ty = threadIdx.x / kTileU;
+  __shared__ short s_row[kTileV][kMaxTileCenters];  // per tile row: candidates reaching it
+  const int tx = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
-  const int u = u0 + tx, v = v0 + ty;  // v is uniform across a warp (one tile row)
+  const int u = u0 + tx;
   const int win = a.win;
-  const bool in = u < a.w && v < a.h;
-  const size_t p = in ? size_t(v) * a.w + u : 0;
-  const float xf = in ? a.vals[p] : 0.0f;  // issued before the candidate fill
-  const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
-  const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B);
-  const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
-  const int by1 = min(a.nby - 1, (v0 + kTileV - 1 + win) / a.B);
-  const int nbxr = bx1 - bx0 + 1, nbr = nbxr * (by1 - by0 + 1);
-  if (threadIdx.x == 0) s_cnt = 0;
+  // pixel values first (their loads overlap the candidate fill)
+  float xf[kRowsPerWarp];
+#pragma unroll
+  for (int q = 0; q < kRowsPerWarp; ++q) {
+    const int v = v0 + wid + 8 * q;
+    xf[q] = (u < a.w && v < a.h) ? a.vals[size_t(v) * a.w + u] : 0.0f;
+  }
+  if (threadIdx.x < kTileV) s_rowcnt[threadIdx.x] = 0;
+  // bucket range of the tile +- win; each bucket row's centres are one
+  // contiguous range of the bucket-ordered records
+  if (threadIdx.x < 32) {
+    const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
+    const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
+    const int nrows = min(a.nby - 1, (v0 + kTileV - 1 + win) / a.B) - by0 + 1;
+    if (tx < min(nrows, 8)) {
+      const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B);
+      const int r0 = (by0 + tx) * a.nbx;
+      const int st = a.cell_start[r0 + bx0];
+      s_rs[tx] = st;
+      s_rb[tx + 1] = a.cell_start[r0 + bx1 + 1] - st;
+    }
+    if (tx == 0) {
+      s_cnt = 0;
+      s_nrows = nrows;
+    }
+  }
   __syncthreads();
-  for (int b = threadIdx.x; b < nbr; b += blockDim.x) {
-    const int bucket = (by0 + b / nbxr) * a.nbx + bx0 + b % nbxr;
-    const int e = a.cell_start[bucket + 1];
-    for (int idx = a.cell_start[bucket]; idx < e; ++idx) {
-      const int k = a.cell_items[idx];
-      const int icu = a.c.icu[k], icv = a.c.icv[k];
+  if (threadIdx.x == 0) {
+    s_rb[0] = 0;
+    for (int r = 0; r < min(s_nrows, 8); ++r) s_rb[r + 1] += s_rb[r];
+  }
+  __syncthreads();
+  const int nrows = s_nrows;
+  const int ntot = nrows <= 8 ? s_rb[nrows] : (kMaxTileCenters + 1);
+  if (ntot > kMaxTileCenters) {
+    if (threadIdx.x == 0) s_cnt = kMaxTileCenters + 1;  // per-pixel bucket walk below
+  } else {
+    for (int t = threadIdx.x; t < ntot; t += blockDim.x) {
+      int r = 0;
+      while (t >= s_rb[r + 1]) ++r;
+      const CRec* rec = a.recs + s_rs[r] + (t - s_rb[r]);
+      const int4 ik = rec->ik;
       // keep only centres whose window reaches the tile
-      const int du = icu < u0 ? u0 - icu : (icu > u0 + kTileU - 1 ? icu - (u0 + kTileU - 1) : 0);
-      const int dv = icv < v0 ? v0 - icv : (icv > v0 + kTileV - 1 ? icv - (v0 + kTileV - 1) : 0);
+      const int du = ik.x < u0 ? u0 - ik.x : (ik.x > u0 + kTileU - 1 ? ik.x - (u0 + kTileU - 1) : 0);
+      const int dv = ik.y < v0 ? v0 - ik.y : (ik.y > v0 + kTileV - 1 ? ik.y - (v0 + kTileV - 1) : 0);
       if (du > win || dv > win) continue;
       const int slot = atomicAdd(&s_cnt, 1);
-      if (slot < kMaxTileCenters) {
-        s_ci[slot] = make_int4(icu, icv, k, 0);
-        s_cd[slot] = make_double2(a.c.cu[k], a.c.cv[k]);
-        s_val[slot] = a.c.val[k];
-      }
+      s_ci[slot] = ik;
+      s_cd[slot] = rec->cuv;
+      s_val[slot] = rec->val.x;
     }
   }
   __syncthreads();
   const int nc = s_cnt;
-  int label = -1;  // -1: outside the image
-  const double x = double(xf);
-  double best = __longlong_as_double(0x7FF0000000000000ll);
-  int bk = -1;
-  if (nc <= kMaxTileCenters) {
-    const double du0 = double(u), dv0 = double(v), sw = a.sw;
-    for (int i = 0; i < nc; ++i) {
-      const int4 ci = s_ci[i];
-      if (abs(v - ci.y) > win) continue;  // warp-uniform
-      const double2 cd = s_cd[i];
-      const double dval = x - s_val[i];
-      const double du = du0 - cd.x, dv = dv0 - cd.y;
-      const double dist = dval * dval + (du * du + dv * dv) * sw;
-      const bool take = abs(u - ci.x) <= win && (dist < best || (dist == best && ci.z < bk));
-      best = take ? dist : best;
-      bk = take ? ci.z : bk;
+  if (nc <= kMaxTileCenters) {  // distribute the candidates over the rows they reach
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      const int icv = s_ci[i].y;
+      const int r0 = max(icv - win, v0) - v0, r1 = min(icv + win, v0 + kTileV - 1) - v0;
+      for (int r = r0; r <= r1; ++r) s_row[r][atomicAdd(&s_rowcnt[r], 1)] = short(i);
     }
   }
-  if (in) {
-    if (nc > kMaxTileCenters) {
-      bk = assign_walk(a, u, v, x);  // pathological centre pile-up: per-pixel bucket walk
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kRowsPerWarp; ++q) {
+    const int ty = wid + 8 * q;
+    const int v = v0 + ty;  // uniform across the warp
+    const bool in = u < a.w && v < a.h;
+    const size_t p = size_t(v) * a.w + u;
+    const double x = double(xf[q]);
+    double best = __longlong_as_double(0x7FF0000000000000ll);
+    int bk = -1;
+    if (nc <= kMaxTileCenters) {
+      const double du0 = double(u), dv0 = double(v), sw = a.sw;
+      const int nr = s_rowcnt[ty];
+      for (int j = 0; j < nr; ++j) {
+        const int i = s_row[ty][j];
+        const int4 ci = s_ci[i];
+        const double2 cd = s_cd[i];
+        const double dval = x - s_val[i];
+        const double du = du0 - cd.x, dv = dv0 - cd.y;
+        const double dist = dval * dval + (du * du + dv * dv) * sw;
+        const bool take = abs(u - ci.x) <= win && (dist < best || (dist == best && ci.z < bk));
+        best = take ? dist : best;
+        bk = take ? ci.z : bk;
+      }
     }
-    if (bk < 0) {
-      a.labels[p] = 0;
-      const int slot = atomicAdd(a.orphan_count, 1);
-      a.orphan_list[slot] = int(p);
-      label = 0;
-    } else {
-      a.labels[p] = bk + 1;
-      label = bk + 1;
+    int label = -1;  // -1: outside the image
+    if (in) {
+      if (nc > kMaxTileCenters)
+        bk = assign_walk(a, u, v, x);  // pathological centre pile-up: per-pixel bucket walk
+      if (bk < 0) {
+        a.labels[p] = 0;
+        const int slot = atomicAdd(a.orphan_count, 1);
+        a.orphan_list[slot] = int(p);
+        label = 0;
+      } else {
+        a.labels[p] = bk + 1;
+        label = bk + 1;
+      }
     }
-  }
-  if (SUMS) {
-    const int key = label > 0 ? label : -1;
-    const RunInfo ri = run_info(key);
-    int bad = 0;
-    Acc128 ax = key > 0 ? to_fixed(xf, &bad) : Acc128{0ull, 0ll};
-    if (bad) atomicOr(a.inexact, 1);
-    ax = run_sum(ax, ri);
-    // a run is a contiguous pixel segment of one row: count and coordinate
-    // sums follow from its bounds
-    const int cnt = ri.end - (threadIdx.x & 31) + 1;
-    const long long su = (long long)cnt * u + (long long)cnt * (cnt - 1) / 2;
-    const long long sv = (long long)cnt * v;
-    if (ri.head) {
-      atomicAdd(&s.n[key], cnt);
-      atomic_add_acc(&s.sx[key], ax);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
+    if (SUMS) {
+      const int key = label > 0 ? label : -1;
+      const RunInfo ri = run_info(key);
+      int bad = 0;
+      Acc128 ax = key > 0 ? to_fixed(xf[q], &bad) : Acc128{0ull, 0ll};
+      if (bad) atomicOr(a.inexact, 1);
+      ax = run_sum(ax, ri);
+      // a run is a contiguous pixel segment of one row: count and coordinate
+      // sums follow from its bounds
+      const int cnt = ri.end - tx + 1;
+      const long long su = (long long)cnt * u + (long long)cnt * (cnt - 1) / 2;
+      const long long sv = (long long)cnt * v;
+      if (ri.head) {
+        atomicAdd(&s.n[key], cnt);
+        red_add_acc(&s.sx[key], ax);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
+      }
     }
   }
 }
@@ -342,7 +395,7 @@ __global__ void k_assign_fallback(int w, Centers c, int K, int32_t* __restrict__
         int bad = 0;
         const int l = bk + 1;
         atomicAdd(&s.n[l], 1);
-        atomic_add_acc(&s.sx[l], to_fixed(vals[p], &bad));
+        red_add_acc(&s.sx[l], to_fixed(vals[p], &bad));
         if (bad) atomicOr(inexact, 1);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[l]), (unsigned long long)u);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[l]), (unsigned long long)v);
@@ -380,7 +433,7 @@ __global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __re
     }
     if (ri.head) {
       atomicAdd(&s.n[key], cnt);
-      atomic_add_acc(&s.sx[key], ax);
+      red_add_acc(&s.sx[key], ax);
       if (coords) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
@@ -400,12 +453,12 @@ __global__ void k_center_finalize(CenterSums s, Centers c, int K) {
     const double dn = double(n);
     c.cu[k] = double(s.su[l]) / dn;
     c.cv[k] = double(s.sv[l]) / dn;
-    c.val[k] = fixed_to_double(s.sx[l]) / dn;
+    c.val[k] = fixed_to_double(acc_value(s.sx[l])) / dn;
   }
   s.n[l] = 0;
   s.su[l] = 0;
   s.sv[l] = 0;
-  s.sx[l] = Acc128{0ull, 0ll};
+  s.sx[l] = AccSum{0ull, 0ull, 0ll, 0ll};
 }
 
 __global__ void k_zero_sums(CenterSums s, int nlabels) {
@@ -414,7 +467,7 @@ __global__ void k_zero_sums(CenterSums s, int nlabels) {
   s.n[l] = 0;
   s.su[l] = 0;
   s.sv[l] = 0;
-  s.sx[l] = Acc128{0ull, 0ll};
+  s.sx[l] = AccSum{0ull, 0ull, 0ll, 0ll};
 }
 
 // ------------------------------------------------ enforce_connectivity ----
@@ -606,7 +659,7 @@ __global__ void k_pool_write(const int32_t* __restrict__ labels, CenterSums s, l
     float r = kInvalid;
     if (l >= 0 && l <= max_label) {
       const int c = s.n[l];
-      if (c > 0) r = float(fixed_to_double(s.sx[l]) / double(c));
+      if (c > 0) r = float(fixed_to_double(acc_value(s.sx[l])) / double(c));
     }
     d3[p] = r;
   }
@@ -648,9 +701,10 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
             ctx->ws.get<double>("slic_val", K), ctx->ws.get<int>("slic_icu", K),
             ctx->ws.get<int>("slic_icv", K)};
   CenterSums s{ctx->ws.get<int>("slic_n", K + 1), ctx->ws.get<long long>("slic_su", K + 1),
-               ctx->ws.get<long long>("slic_sv", K + 1), ctx->ws.get<Acc128>("slic_sx", K + 1)};
+               ctx->ws.get<long long>("slic_sv", K + 1), ctx->ws.get<AccSum>("slic_sx", K + 1)};
   int* cell_start = ctx->ws.get<int>("slic_cell_start", nbx * nby + 1);
   int* cell_items = ctx->ws.get<int>("slic_cell_items", K);
+  CRec* recs = ctx->ws.get<CRec>("slic_recs", K);
   int* orphan_list = ctx->ws.get<int>("slic_orphans", n);
   int* orphan_count = ctx->ws.get<int>("slic_orphan_count", 2);
   int* inexact = orphan_count + 1;
@@ -663,20 +717,20 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_LAUNCH_CHECK();
   RPD_CK(cudaMemsetAsync(orphan_count, 0, 2 * sizeof(int), st));
 
-  AssignArgs aa{vals, h, w, c, cell_start, cell_items, B, nbx, nby, win, sw, labels,
+  AssignArgs aa{vals, h, w, c, cell_start, cell_items, recs, B, nbx, nby, win, sw, labels,
                 orphan_list, orphan_count, inexact};
   const dim3 tgrid(cdiv(w, kTileU), cdiv(h, kTileV));
   // One round = bucket build (finalising the previous round's sums first) +
   // assignment that accumulates the sums the next round needs.
   auto assign = [&](bool finalize, bool sums) {
-    k_buckets<<<1, kBucketThreads, 0, st>>>(c, K, w, h, B, nbx, nby, cell_start, cell_items, s,
+    k_buckets<<<1, kBucketThreads, 0, st>>>(c, K, w, h, B, nbx, nby, cell_start, cell_items, recs, s,
                                             finalize ? 1 : 0);
     RPD_LAUNCH_CHECK();
     RPD_CK(cudaMemsetAsync(orphan_count, 0, sizeof(int), st));
     if (sums)
-      k_assign_tile<true><<<tgrid, kTileU * kTileV, 0, st>>>(aa, s);
+      k_assign_tile<true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
     else
-      k_assign_tile<false><<<tgrid, kTileU * kTileV, 0, st>>>(aa, s);
+      k_assign_tile<false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
     RPD_LAUNCH_CHECK();
     if (sums)
       k_assign_fallback<true><<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
@@ -762,10 +816,10 @@ void pool_superpixels_dev(rpd_ctx* ctx, const float* d2, const int32_t* labels, 
   const int gblocks = int(std::max<long long>(1, std::min<long long>((n + 255) / 256,
                                                                       ctx->sm_count * 16)));
   CenterSums s{ctx->ws.get<int>("pool_n", max_count + 1), nullptr, nullptr,
-               ctx->ws.get<Acc128>("pool_sx", max_count + 1)};
+               ctx->ws.get<AccSum>("pool_sx", max_count + 1)};
   int* inexact = ctx->ws.get<int>("pool_inexact", 1);
   RPD_CK(cudaMemsetAsync(s.n, 0, sizeof(int) * (max_count + 1), st));
-  RPD_CK(cudaMemsetAsync(s.sx, 0, sizeof(Acc128) * (max_count + 1), st));
+  RPD_CK(cudaMemsetAsync(s.sx, 0, sizeof(AccSum) * (max_count + 1), st));
   k_label_sums<<<gblocks, 256, 0, st>>>(d2, labels, h, w, max_count, true, false, s, inexact);
   RPD_LAUNCH_CHECK();
   k_pool_write<<<gblocks, 256, 0, st>>>(labels, s, n, max_count, d3);
