@@ -23,6 +23,8 @@ namespace rpdg {
 
 namespace {
 
+constexpr long long kPipelineObsCap = 100000;  // sample_observations cap (pipeline.cpp:66, :81)
+
 struct FrameBuffers {
   float* left;
   float* right;
@@ -122,8 +124,8 @@ FrameBuffers alloc_frame(rpd_ctx* ctx, int h, int w, int K) {
   f.thr = ws.get<rpd_threshold>("pl_thr", 1);
   f.clamped = ws.get<unsigned long long>("pl_clamped", 1);
   f.flat = ws.get<DevModel>("pl_flat", 1);
-  f.obs.uv = ws.get<uint32_t>("pl_obs_uv", 100000);
-  f.obs.d = ws.get<float>("pl_obs_d", 100000);
+  f.obs.uv = ws.get<uint32_t>("pl_obs_uv", kPipelineObsCap);
+  f.obs.d = ws.get<float>("pl_obs_d", kPipelineObsCap);
   f.obs.count = ws.get<int>("pl_obs_count", 1);
   (void)K;
   return f;
@@ -158,11 +160,12 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   }
   record_stage(ctx, 1);
   // pipeline.cpp:66-73 coarse road fit (a0 *= 2 when halved)
-  sample_observations_dev(ctx, f.b_d1, bh, bw, nullptr, 100000, f.obs, kWhereSampleBoot);
+  sample_observations_dev(ctx, f.b_d1, bh, bw, nullptr, kPipelineObsCap, f.obs, kWhereSampleBoot);
   FitRequest fr;
   fr.mode = kFitRoad;
   fr.compact = true;
   fr.obs = f.obs;
+  fr.kmax = kPipelineObsCap;
   fr.hi = c.roll_bracket;
   fr.tol = c.roll_tol;
   fr.a0_scale = halve ? 2.0 : 1.0;
@@ -175,7 +178,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
                  f.shifts);
   record_stage(ctx, 3);
   // pipeline.cpp:81-86 refit
-  sample_observations_dev(ctx, f.d1, h, w, nullptr, 100000, f.obs, kWhereSamplePt);
+  sample_observations_dev(ctx, f.d1, h, w, nullptr, kPipelineObsCap, f.obs, kWhereSamplePt);
   fr.a0_scale = 1.0;
   fr.where = kWhereFitPt;
   fr.out = f.fit;

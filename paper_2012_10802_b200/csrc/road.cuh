@@ -40,6 +40,7 @@ struct FitRequest {
   const double* du = nullptr;
   const double* dv = nullptr;
   long long k_host = 0;
+  long long kmax = 0;            // compact input: capacity (observation cap); 0 = max
   double phi = 0.0;              // kFitLine
   double lo = 0.0, hi = 0.0;     // kEstimateRoll bracket, kFitRoad uses [-hi, hi]
   double tol = 1e-4;
