@@ -290,6 +290,12 @@ __device__ __forceinline__ void sweep_bar() {
 }
 
 constexpr unsigned kSpinLimit = 1u << 24;  // ~seconds: a lost peer traps, never hangs
+#ifndef RPD_FIT_BACKOFF
+#define RPD_FIT_BACKOFF 0  // ns between unsuccessful partial polls
+#endif
+#ifndef RPD_FIT_SMALL_SMEM
+#define RPD_FIT_SMALL_SMEM 0
+#endif
 
 // Grid-wide barrier of the cooperative launch (thread 0 of every CTA arrives
 // with release semantics and spins with acquire loads); all threads of the
@@ -439,6 +445,7 @@ __device__ void grid_sum(FitState& F, double (&x)[NV]) {
         break;
       }
       if (++spins > kSpinLimit) __trap();
+      if (RPD_FIT_BACKOFF > 0) __nanosleep(RPD_FIT_BACKOFF);
     }
     fit_tr(F, 41);
     constexpr int kW = kPairs < 32 ? kPairs : 32;
@@ -931,8 +938,12 @@ void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
   // down to the observation cap lets other streams' CTAs share the fit's SMs,
   // which stretches every grid-wide exchange (measured: -7% frames/s with 8
   // concurrent pipelines).
-  (void)req.kmax;
-  const int rows_cap = kMaxRows;
+  int rows_cap = kMaxRows;
+  if (RPD_FIT_SMALL_SMEM) {
+    const long long kcap = req.compact ? (req.kmax > 0 ? req.kmax : (long long)kMaxRows * kFitLanes)
+                                       : req.k_host;
+    rows_cap = int(std::min<long long>(kMaxRows, std::max<long long>(1, (kcap + kFitLanes - 1) / kFitLanes)));
+  }
   FitKParams P{};
   P.r = req;
   P.status = ctx->status;

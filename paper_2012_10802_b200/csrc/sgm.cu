@@ -236,6 +236,7 @@ void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_v
 // branch-free: min(popc(a ^ b) | ov, maxc) == maxc exactly when the reference
 // substitutes maxc (sgm.cpp:40-60; a valid popcount never exceeds maxc).
 // Volume words are produced in storage order (coalesced stores).
+template <typename CW>  // staged census word: uint32_t when the window has <= 32 bits
 __global__ void __launch_bounds__(256)
     k_cost_u8(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
               const uint8_t* __restrict__ iv, int h, int w, int levels, int nw,
@@ -243,15 +244,15 @@ __global__ void __launch_bounds__(256)
               uint32_t* __restrict__ vol_r) {
   extern __shared__ uint64_t csm[];  // cl[W] | cr[W] | ov[W] bytes, W = w + 2*levels
   const int W = w + 2 * levels;
-  uint64_t* s_cl = csm + levels;  // s_cl[u], u in [-levels, w + levels)
-  uint64_t* s_cr = csm + W + levels;
-  uint8_t* s_ov = reinterpret_cast<uint8_t*>(csm + 2 * W) + levels;
+  CW* s_cl = reinterpret_cast<CW*>(csm) + levels;  // s_cl[u], u in [-levels, w + levels)
+  CW* s_cr = reinterpret_cast<CW*>(csm) + W + levels;
+  uint8_t* s_ov = reinterpret_cast<uint8_t*>(reinterpret_cast<CW*>(csm) + 2 * W) + levels;
   const int v = blockIdx.y;
   const long long row = (long long)v * w;
   for (int u = int(threadIdx.x) - levels; u < w + levels; u += blockDim.x) {
     const bool in = u >= 0 && u < w;
-    s_cl[u] = in ? cl[row + u] : 0ull;
-    s_cr[u] = in ? cr[row + u] : 0ull;
+    s_cl[u] = in ? CW(cl[row + u]) : CW(0);
+    s_cr[u] = in ? CW(cr[row + u]) : CW(0);
     s_ov[u] = (in && iv[row + u]) ? 0 : 0xFF;
   }
   __syncthreads();
@@ -259,24 +260,46 @@ __global__ void __launch_bounds__(256)
   uint32_t* orr = vol_r + size_t(v) * pitch_words;
   const int total = w * nw;
   const float inv_nw = 1.0f / float(nw);
+  auto popc = [](CW x) -> uint32_t {
+    if constexpr (sizeof(CW) == 8)
+      return uint32_t(__popcll(x));
+    else
+      return uint32_t(__popc(x));
+  };
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
     // i / nw exactly: (i + 0.5) / nw is >= 1/(2 nw) away from an integer
     const int u = int(__fmul_rn(float(i) + 0.5f, inv_nw));
     const int j = i - u * nw;
-    const uint64_t a = s_cl[u];
-    const uint64_t b = s_cr[u];
+    const CW a = s_cl[u];
+    const CW b = s_cr[u];
     const uint32_t ovu = s_ov[u];
-    uint32_t wl = 0, wr = 0;
+    const int d0 = 4 * j;
+    const CW* crd = s_cr + (u - d0);
+    const uint8_t* ovd = s_ov + (u - d0);
+    const CW* cld = s_cl + (u + d0);
+    uint32_t wl, wr;
+    if (d0 + 3 < levels) {  // full word
+      uint32_t cL[4], cR[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int d = 4 * j + q;
-      uint32_t cL = 0xFF, cR = 0xFF;
-      if (d < levels) {
-        cL = min(uint32_t(__popcll(a ^ s_cr[u - d])) | s_ov[u - d], maxc);
-        cR = min(uint32_t(__popcll(s_cl[u + d] ^ b)) | ovu | (u + d >= w ? 0xFFu : 0u), maxc);
+      for (int q = 0; q < 4; ++q) {
+        cL[q] = min(popc(a ^ crd[-q]) | ovd[-q], maxc);
+        cR[q] = min(popc(cld[q] ^ b) | ovu | (u + d0 + q >= w ? 0xFFu : 0u), maxc);
       }
-      wl |= cL << (8 * q);
-      wr |= cR << (8 * q);
+      wl = __byte_perm(__byte_perm(cL[0], cL[1], 0x0040), __byte_perm(cL[2], cL[3], 0x0040), 0x5410);
+      wr = __byte_perm(__byte_perm(cR[0], cR[1], 0x0040), __byte_perm(cR[2], cR[3], 0x0040), 0x5410);
+    } else {
+      wl = 0;
+      wr = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t x = 0xFF, y = 0xFF;
+        if (d0 + q < levels) {
+          x = min(popc(a ^ crd[-q]) | ovd[-q], maxc);
+          y = min(popc(cld[q] ^ b) | ovu | (u + d0 + q >= w ? 0xFFu : 0u), maxc);
+        }
+        wl |= x << (8 * q);
+        wr |= y << (8 * q);
+      }
     }
     ol[i] = wl;
     orr[i] = wr;
@@ -928,12 +951,13 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     uint8_t* vol_r = vol_l + vb;
     uint8_t* pathbuf = ctx->ws.get<uint8_t>("mp_paths", vb * 2 * paths);
     {
-      const int smem = (w + 2 * levels) * 17;
+      const bool narrow = window * window - 1 <= 32;
+      const int smem = (w + 2 * levels) * (narrow ? 9 : 17);
       if (smem <= 200 * 1024) {
+        auto* kfn = narrow ? k_cost_u8<uint32_t> : k_cost_u8<uint64_t>;
         if (smem > 48 * 1024)
-          RPD_CK(cudaFuncSetAttribute(k_cost_u8, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem));
-        k_cost_u8<<<dim3(1, h), 256, smem, st>>>(
+          RPD_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kfn<<<dim3(1, h), 256, smem, st>>>(
             cl, cr, iv, h, w, levels, nw, L.pitch / 4, uint32_t(window * window - 1),
             reinterpret_cast<uint32_t*>(vol_l), reinterpret_cast<uint32_t*>(vol_r));
       } else {
