@@ -168,19 +168,30 @@ void launch_restore(const float* d0, const double* shifts, int h, int w, float* 
 // census_transform, sgm.cpp:13-34: MSB-first bits over the row-major window,
 // centre skipped, coordinates clamped.
 template <int R>
-__global__ void k_census(const float* __restrict__ img, int h, int w, uint64_t* __restrict__ out) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128)
+    k_census(const float* __restrict__ img, int h, int w, uint64_t* __restrict__ out) {
+  // the (2R+1) x (128+2R) window of this 128-pixel row segment, staged with
+  // clamped coordinates (== the reference's clamped reads)
+  constexpr int TW = 128 + 2 * R;
+  __shared__ float tile[2 * R + 1][TW];
+  const int u0 = blockIdx.x * 128;
   const int v = blockIdx.y;
+  for (int i = threadIdx.x; i < (2 * R + 1) * TW; i += 128) {
+    const int r = i / TW, c = i - r * TW;
+    const int vv = min(max(v + r - R, 0), h - 1), uu = min(max(u0 + c - R, 0), w - 1);
+    tile[r][c] = img[size_t(vv) * w + uu];
+  }
+  __syncthreads();
+  const int u = u0 + threadIdx.x;
   if (u >= w) return;
-  const float c = img[size_t(v) * w + u];
+  const float c = tile[R][threadIdx.x + R];
   uint64_t bits = 0;
 #pragma unroll
   for (int dv = -R; dv <= R; ++dv) {
-    const float* row = img + size_t(min(max(v + dv, 0), h - 1)) * w;
 #pragma unroll
     for (int du = -R; du <= R; ++du) {
       if (dv == 0 && du == 0) continue;
-      bits = (bits << 1) | (row[min(max(u + du, 0), w - 1)] < c ? 1ull : 0ull);
+      bits = (bits << 1) | (tile[dv + R][threadIdx.x + R + du] < c ? 1ull : 0ull);
     }
   }
   out[size_t(v) * w + u] = bits;

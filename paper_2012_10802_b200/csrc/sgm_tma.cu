@@ -35,6 +35,13 @@ constexpr int kDepth = 3;    // input ring depth (stages)
 #ifndef RPD_AGG_UNROLL
 #define RPD_AGG_UNROLL 4     // unrolled steps of the inner loop (code size vs ILP)
 #endif
+#ifndef RPD_AGG_REC
+#define RPD_AGG_REC 2  // recurrence form: 0 = 2x add-min + min, 1 = min3 + add-min, 2 = min3 + add + min3
+#endif
+#ifndef RPD_AGG_OUTDEPTH
+#define RPD_AGG_OUTDEPTH 2  // output tiles in flight (TMA stores not yet read)
+#endif
+constexpr int kOutDepth = RPD_AGG_OUTDEPTH;
 constexpr int kRBase = RPD_AGG_RBASE;
 constexpr int kStepUnroll = RPD_AGG_UNROLL;
 constexpr uint32_t kInf2 = 0x7FFF7FFFu;
@@ -235,9 +242,10 @@ __device__ __forceinline__ void chain_step(ChainState<NPAIR>& cs, const uint32_t
     if (g > 0) lo_nb = up;
     if (g < G - 1) hi_nb = dn;
   }
-  const uint32_t ceil2 = cs.mnx2 + p2x2;
   uint32_t cur[NPAIR];
   uint32_t qprev = __byte_perm(lo_nb, cs.prev[0], 0x5432);
+#if RPD_AGG_REC == 0
+  const uint32_t ceil2 = cs.mnx2 + p2x2;
 #pragma unroll
   for (int q = 0; q < NPAIR; ++q) {
     const uint32_t nxt = (q + 1 < NPAIR) ? cs.prev[q + 1] : hi_nb;
@@ -248,6 +256,26 @@ __device__ __forceinline__ void chain_step(ChainState<NPAIR>& cs, const uint32_t
     cur[q] = raw[q] + tt - cs.mnx2;  // per-half exact: tt >= min, no carry
     qprev = qn;
   }
+#else
+  // min(prev[d-1]+P1, prev[d+1]+P1, min+P2) = min(prev[d-1], prev[d+1], min+P2-P1) + P1
+  // (P2 >= P1): one 3-input DPX min (half rate) instead of two fused add-mins
+  // (quarter rate on sm_100, tools/dpx_probe.cu).
+  const uint32_t ceilm = cs.mnx2 + (p2x2 - p1x2);
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) {
+    const uint32_t nxt = (q + 1 < NPAIR) ? cs.prev[q + 1] : hi_nb;
+    const uint32_t qn = __byte_perm(cs.prev[q], nxt, 0x5432);  // (prev[d+1] of both halves)
+    const uint32_t a = __vimin3_u16x2(qprev, qn, ceilm);
+#if RPD_AGG_REC == 1
+    const uint32_t tt = __viaddmin_u16x2(a, p1x2, cs.prev[q]);
+#else
+    const uint32_t ap = a + p1x2;
+    const uint32_t tt = __vimin3_u16x2(ap, cs.prev[q], cs.prev[q]);
+#endif
+    cur[q] = raw[q] + tt - cs.mnx2;  // per-half exact: tt >= min, no carry
+    qprev = qn;
+  }
+#endif
 #pragma unroll
   for (int q = 0; q < WPL; ++q)
     packed[q] =
@@ -370,7 +398,7 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
     const int slot = st % kDepth;
     mbar_wait(&full[slot], uint32_t(st / kDepth) & 1u);
     const uint32_t* inb = in_ring + slot * GE::STAGE_IN;
-    uint32_t* outb = out_ring + (st & 1) * GE::STAGE;
+    uint32_t* outb = out_ring + (st % kOutDepth) * GE::STAGE;
     const int s0 = stage_base + st * R;
     // only the first tile of a backward H/V scan holds padding steps
     const bool check = TYPE != kDiag && s0 < s_begin;
@@ -416,7 +444,7 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
         mbar_expect_tx(&full[slot], stage_bytes(st + kDepth));
         tile_ops(st + kDepth, true, in_ring + slot * GE::STAGE_IN, &full[slot]);
       }
-      if (TYPE != kDiag) tma_wait_read<1>();  // the other output buffer is free again
+      if (TYPE != kDiag) tma_wait_read<kOutDepth - 1>();  // the next output buffer is free again
     }
     __syncthreads();
   }
@@ -432,7 +460,7 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
   extern __shared__ __align__(16) uint32_t dsm[];
   const uint32_t pad_words = ((1024u - (smem_addr(dsm) & 1023u)) & 1023u) >> 2;
   uint32_t* in_ring = dsm + pad_words;                // kDepth * STAGE_IN
-  uint32_t* out_ring = in_ring + kDepth * GE::STAGE_IN;  // 2 * STAGE
+  uint32_t* out_ring = in_ring + kDepth * GE::STAGE_IN;  // kOutDepth * STAGE
   __shared__ __align__(8) uint64_t full[kDepth];
   int jidx = 0;
 #pragma unroll 1
@@ -444,12 +472,21 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
     fence_async_smem();
   }
   __syncthreads();
+  unsigned long long t0 = 0;
+  if (a.dbg == 100 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   if (J.type == kHoriz)
     agg_body<kHoriz, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
   else if (J.type == kVert)
     agg_body<kVert, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
   else
     agg_body<kDiag, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
+  if (a.dbg == 100 && threadIdx.x == 0) {  // RPD_TMA_DBG=100: per-CTA timeline
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("AGGTR %d %d %d %d %u %llu %llu\n", WPL, int(blockIdx.x), jidx, J.type, smid, t0, t1);
+  }
 }
 
 using TmaKernel = void (*)(TmaArgs);
@@ -465,7 +502,7 @@ template <int WPL, int G, int NPAIR>
 KernelInfo info() {
   using GE = Geo<WPL, G>;
   return KernelInfo{k_aggregate_tma<WPL, G, NPAIR>,
-                    (kDepth * GE::STAGE_IN + 2 * GE::STAGE) * 4 + 1024,
+                    (kDepth * GE::STAGE_IN + kOutDepth * GE::STAGE) * 4 + 1024,
                     GE::THREADS, GE::R, GE::WPP, GE::ROW, GE::CWF, GE::CWL, GE::NCH,
                     GE::DROW < 256 ? GE::DROW : 256, GE::DCWL};
 }
