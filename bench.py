@@ -209,6 +209,11 @@ def gpu_arm(args, rank, world, local):
     h, w = SHAPES[c]
     scene = make_scene(c, 0)  # replicas of the config's pair on every rank
     cfg = pipeline_config(lib, c)
+    override = os.environ.get("RPD_BENCH_CFG")  # experiments only: "key=value,..." (marked in config)
+    if override:
+        for kv in override.split(","):
+            k, v = kv.split("=")
+            setattr(cfg, k, type(getattr(cfg, k))(v))
     gde = gde_per_frame(h, w, cfg)
 
     # ---- device-resident value
@@ -343,7 +348,8 @@ def gpu_arm(args, rank, world, local):
             "frames_per_step_per_gpu": F, "streams_per_gpu": S,
             "l2": "flushed (256 MiB write) between timed steps",
             "parallelism": "independent frames: %d concurrent pipeline contexts per GPU, "
-                           "ranks = GPUs, no collective" % S},
+                           "ranks = GPUs, no collective" % S,
+            **({"override": override} if override else {})},
         "sgm_gdes": round(sgm_gdes, 3),
         "gde_per_frame": gde,
         "stage_ms": {k: round(v, 4) for k, v in zip(

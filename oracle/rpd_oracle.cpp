@@ -15,7 +15,9 @@
 //  * fit_line reductions (road_geometry.cpp:20-24, 37) are Eigen reductions
 //    whose SIMD order cannot be reproduced without Eigen.  The oracle fixes one
 //    order — kFitLanes strided lanes, then an adjacent-pairwise tree — which is
-//    also the device kernel's order (DESIGN.md §road fit).
+//    also the device kernel's order (DESIGN.md §road fit).  The normal
+//    equations and the search energies come from double-double observation
+//    moments (exact products); the reported e0min keeps the residual form.
 //  * `sgm_paths` (4 or 8) selects the first entries of kEightDirections
 //    (sgm.hpp:41-43); the reference always uses 8 (sgm.cpp:183-186).
 //
@@ -377,15 +379,132 @@ struct Obs {
 
 // Fixed reduction order shared with the device kernel: element i goes to lane
 // i mod kFitLanes (sequential within a lane, starting from +0.0), then lanes
-// are combined by an adjacent-pairwise tree.
+// are combined by an adjacent-pairwise tree.  `mask` (optional) drops
+// elements in place: survivors keep their lanes.
 constexpr int kFitLanes = 8192;
 template <typename F>
-double lane_tree_sum(size_t k, F term) {
+double lane_tree_sum(size_t k, F term, const std::vector<char>* mask = nullptr) {
   std::vector<double> lane(kFitLanes, 0.0);
-  for (size_t i = 0; i < k; ++i) lane[i % kFitLanes] += term(i);
+  for (size_t i = 0; i < k; ++i)
+    if (!mask || (*mask)[i]) lane[i % kFitLanes] += term(i);
   for (int width = 1; width < kFitLanes; width *= 2)
     for (int j = 0; j < kFitLanes; j += 2 * width) lane[size_t(j)] += lane[size_t(j + width)];
   return lane[0];
+}
+
+// Double-double arithmetic (Dekker, Knuth): the error-free transformations
+// and the usual normalised sum / product / quotient.  Operation order is part
+// of the contract with the device (road.cu), so is the non-commutative
+// dd_add argument order (lower lane first).
+struct DD {
+  double hi = 0.0, lo = 0.0;
+};
+inline DD two_sum(double a, double b) {
+  const double s = a + b;
+  const double bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+inline DD quick_two_sum(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+inline DD two_prod(double a, double b) {
+  const double p = a * b;
+  return {p, std::fma(a, b, -p)};
+}
+inline DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  const DD t = two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo += t.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+inline DD dd_add_d(DD a, double b) {
+  DD s = two_sum(a.hi, b);
+  s.lo += a.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+inline DD dd_sub(DD a, DD b) { return dd_add(a, DD{-b.hi, -b.lo}); }
+inline DD dd_mul(DD a, DD b) {
+  DD p = two_prod(a.hi, b.hi);
+  p.lo += a.hi * b.lo;
+  p.lo += a.lo * b.hi;
+  return quick_two_sum(p.hi, p.lo);
+}
+inline DD dd_mul_d(DD a, double b) {
+  DD p = two_prod(a.hi, b);
+  p.lo += a.lo * b;
+  return quick_two_sum(p.hi, p.lo);
+}
+inline DD dd_div(DD a, DD b) {
+  const double q1 = a.hi / b.hi;
+  DD r = dd_sub(a, dd_mul_d(b, q1));
+  const double q2 = r.hi / b.hi;
+  r = dd_sub(r, dd_mul_d(b, q2));
+  const double q3 = r.hi / b.hi;
+  return dd_add_d(quick_two_sum(q1, q2), q3);
+}
+inline bool dd_lt(DD a, DD b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
+
+// Observation moments su, sv, sd, suu, svv, suv, sdu, sdv, sdd, n in
+// double-double (exact products), summed in the lane order.
+struct Moments {
+  std::array<DD, 10> m;
+};
+Moments moments(const Obs& o, const std::vector<char>* mask = nullptr) {
+  std::vector<std::array<DD, 10>> lane(kFitLanes);
+  for (size_t i = 0; i < o.count(); ++i) {
+    if (mask && !(*mask)[i]) continue;
+    auto& a = lane[i % kFitLanes];
+    const double u = o.u[i], v = o.v[i], d = o.d[i];
+    a[0] = dd_add_d(a[0], u);
+    a[1] = dd_add_d(a[1], v);
+    a[2] = dd_add_d(a[2], d);
+    a[3] = dd_add(a[3], two_prod(u, u));
+    a[4] = dd_add(a[4], two_prod(v, v));
+    a[5] = dd_add(a[5], two_prod(u, v));
+    a[6] = dd_add(a[6], two_prod(d, u));
+    a[7] = dd_add(a[7], two_prod(d, v));
+    a[8] = dd_add(a[8], two_prod(d, d));
+    a[9] = dd_add_d(a[9], 1.0);
+  }
+  for (int width = 1; width < kFitLanes; width *= 2)
+    for (int j = 0; j < kFitLanes; j += 2 * width)
+      for (int q = 0; q < 10; ++q)
+        lane[size_t(j)][q] = dd_add(lane[size_t(j)][q], lane[size_t(j + width)][q]);
+  return Moments{lane[0]};
+}
+
+// fit_line's normal equations (road_geometry.cpp:16-34) and its energy, from
+// the moments at (c, s) = (cos phi, sin phi), in double-double.  The expanded
+// energy d'd - 2 a'T'd + a'T'Ta is what the reference's residual form avoids
+// in double (:35-37); at ~106 bits the cancellation is harmless.
+struct LineDD {
+  DD a0, a1, e;
+};
+LineDD line_eval(const Moments& M, double c, double s) {
+  const DD N = M.m[9];
+  const DD cc = two_prod(c, c), ss = two_prod(s, s), cs = two_prod(c, s);
+  const DD T1 = dd_sub(dd_mul_d(M.m[1], c), dd_mul_d(M.m[0], s));
+  const DD T2 =
+      dd_add(dd_sub(dd_mul(cc, M.m[4]), dd_mul_d(dd_mul(cs, M.m[5]), 2.0)), dd_mul(ss, M.m[3]));
+  const DD TD = dd_sub(dd_mul_d(M.m[7], c), dd_mul_d(M.m[6], s));
+  const DD D1 = M.m[2], D2 = M.m[8];
+  const DD nT2 = dd_mul(N, T2);
+  const DD det = dd_sub(nT2, dd_mul(T1, T1));
+  const double scale = nT2.hi < 1.0 ? 1.0 : nT2.hi;
+  if (std::abs(det.hi) < 1e-12 * scale)
+    throw Degenerate("fit_line: degenerate observations (singular normal matrix)");
+  const DD a0 = dd_div(dd_sub(dd_mul(T2, D1), dd_mul(T1, TD)), det);
+  const DD a1 = dd_div(dd_sub(dd_mul(N, TD), dd_mul(T1, D1)), det);
+  DD e = D2;
+  e = dd_sub(e, dd_mul_d(dd_mul(a0, D1), 2.0));
+  e = dd_sub(e, dd_mul_d(dd_mul(a1, TD), 2.0));
+  e = dd_add(e, dd_mul(N, dd_mul(a0, a0)));
+  e = dd_add(e, dd_mul_d(dd_mul(dd_mul(a0, a1), T1), 2.0));
+  e = dd_add(e, dd_mul(dd_mul(a1, a1), T2));
+  return {a0, a1, e};
 }
 
 struct LineFit {
@@ -393,55 +512,64 @@ struct LineFit {
   double e0min = 0;
 };
 
-// road_geometry.cpp:12-39
-LineFit fit_line(const Obs& o, double phi) {
-  const size_t k = o.count();
-  if (k < 3) throw std::invalid_argument("fit_line: need at least 3 observations");
+// road_geometry.cpp:12-39: a0, a1 from the moments (rounded to double), e0min
+// in the reference's residual form, summed in the lane order over `mask`.
+LineFit fit_line_m(const Obs& o, const Moments& M, double phi,
+                   const std::vector<char>* mask = nullptr) {
   const double c = std::cos(phi), s = std::sin(phi);
-  auto t = [&](size_t i) { return c * o.v[i] - s * o.u[i]; };
-  const double kk = double(k);
-  const double st = lane_tree_sum(k, [&](size_t i) { return t(i); });
-  const double stt = lane_tree_sum(k, [&](size_t i) { const double x = t(i); return x * x; });
-  const double sd = lane_tree_sum(k, [&](size_t i) { return o.d[i]; });
-  const double sdt = lane_tree_sum(k, [&](size_t i) { return o.d[i] * t(i); });
-  const double det = kk * stt - st * st;
-  const double scale = std::max(kk * stt, 1.0);
-  if (std::abs(det) < 1e-12 * scale)
-    throw Degenerate("fit_line: degenerate observations (singular normal matrix)");
+  const LineDD L = line_eval(M, c, s);
   LineFit f;
   f.model.phi = phi;
-  f.model.a0 = (stt * sd - st * sdt) / det;
-  f.model.a1 = (kk * sdt - st * sd) / det;
-  f.e0min = lane_tree_sum(k, [&](size_t i) {
-    const double r = o.d[i] - f.model.a0 - f.model.a1 * t(i);
-    return r * r;
-  });
+  f.model.a0 = L.a0.hi;
+  f.model.a1 = L.a1.hi;
+  f.e0min = lane_tree_sum(
+      o.count(),
+      [&](size_t i) {
+        const double t = c * o.v[i] - s * o.u[i];
+        const double r = o.d[i] - f.model.a0 - f.model.a1 * t;
+        return r * r;
+      },
+      mask);
   return f;
 }
 
-// road_geometry.cpp:41-68 — golden-section search on e0min(phi).
-Model estimate_roll(const Obs& o, double lo, double hi, double tol) {
-  if (tol <= 0) throw std::invalid_argument("estimate_roll: tol must be > 0");
+LineFit fit_line(const Obs& o, double phi) {
+  if (o.count() < 3) throw std::invalid_argument("fit_line: need at least 3 observations");
+  return fit_line_m(o, moments(o), phi);
+}
+
+// road_geometry.cpp:41-68 — golden-section search on the energy; every
+// probe is evaluated from the moments (same angles and branches as the
+// reference's loop).  Returns the final midpoint.
+double golden(const Moments& M, double lo, double hi, double tol) {
   constexpr double g = 0.6180339887498949;
+  auto energy = [&](double phi) { return line_eval(M, std::cos(phi), std::sin(phi)).e; };
   double a = lo, b = hi;
   double x1 = b - g * (b - a), x2 = a + g * (b - a);
-  double f1 = fit_line(o, x1).e0min, f2 = fit_line(o, x2).e0min;
+  DD f1 = energy(x1), f2 = energy(x2);
   while (b - a > tol) {
-    if (f1 < f2) {
+    if (dd_lt(f1, f2)) {
       b = x2;
       x2 = x1;
       f2 = f1;
       x1 = b - g * (b - a);
-      f1 = fit_line(o, x1).e0min;
+      f1 = energy(x1);
     } else {
       a = x1;
       x1 = x2;
       f1 = f2;
       x2 = a + g * (b - a);
-      f2 = fit_line(o, x2).e0min;
+      f2 = energy(x2);
     }
   }
-  return fit_line(o, 0.5 * (a + b)).model;
+  return 0.5 * (a + b);
+}
+
+Model estimate_roll(const Obs& o, double lo, double hi, double tol) {
+  if (tol <= 0) throw std::invalid_argument("estimate_roll: tol must be > 0");
+  if (o.count() < 3) throw std::invalid_argument("fit_line: need at least 3 observations");
+  const Moments M = moments(o);
+  return fit_line_m(o, M, golden(M, lo, hi, tol)).model;
 }
 
 struct RoadFit {
@@ -450,27 +578,30 @@ struct RoadFit {
   int64_t used = 0;
 };
 
-// road_geometry.cpp:70-101
+// road_geometry.cpp:70-101 (trimming by an in-place mask: survivors keep
+// their summation lanes)
 RoadFit fit_road(const Obs& o, double bracket, double tol) {
-  const Model m = estimate_roll(o, -bracket, bracket, tol);
-  const LineFit first = fit_line(o, m.phi);
+  if (tol <= 0) throw std::invalid_argument("estimate_roll: tol must be > 0");
   const size_t k = o.count();
+  if (k < 3) throw std::invalid_argument("fit_line: need at least 3 observations");
+  const Moments M = moments(o);
+  const LineFit first = fit_line_m(o, M, golden(M, -bracket, bracket, tol));
   const double rms = std::sqrt(first.e0min / double(k));
   RoadFit out{first.model, first.e0min, int64_t(k)};
   if (rms <= 0) return out;
-  Obs kept;
+  std::vector<char> keep(k, 0);
+  size_t kept = 0;
   for (size_t i = 0; i < k; ++i) {
     const double r = o.d[i] - road_at(first.model, o.u[i], o.v[i]);
     if (std::abs(r) <= 3.0 * rms) {
-      kept.d.push_back(o.d[i]);
-      kept.u.push_back(o.u[i]);
-      kept.v.push_back(o.v[i]);
+      keep[i] = 1;
+      ++kept;
     }
   }
-  if (kept.count() < 3 || kept.count() == k) return out;
-  const Model m2 = estimate_roll(kept, -bracket, bracket, tol);
-  const LineFit second = fit_line(kept, m2.phi);
-  return RoadFit{second.model, second.e0min, int64_t(kept.count())};
+  if (kept < 3 || kept == k) return out;
+  const Moments M2 = moments(o, &keep);
+  const LineFit second = fit_line_m(o, M2, golden(M2, -bracket, bracket, tol), &keep);
+  return RoadFit{second.model, second.e0min, int64_t(kept)};
 }
 
 // road_geometry.cpp:103-134

@@ -3,21 +3,20 @@
 //
 // Reference: /root/reference/proj/src/road_geometry.cpp:12-151.
 //
-// The whole golden-section roll search (18 iterations + trimming + second
-// search at the default bracket/tol) runs inside ONE cooperative launch of
-// 128 co-resident CTAs (one per SM; 64 summation lanes + one helper warp
-// each).  The observations (<= 524 288) are staged once into shared memory as
-// exact doubles; every sweep ends in one grid-wide reduction whose CTA
-// partials are exchanged through flag-tagged 64-bit words in L2 (no barrier,
-// no host round trip); the helper warp computes the correctly rounded sin/cos
-// the next sweep may need while the current one runs.
+// The whole fit_road (golden-section roll search, trimming, second search)
+// runs inside ONE cooperative launch of 128 co-resident CTAs (one per SM,
+// 64 summation lanes each). The observations (<= 524 288) are staged once in
+// shared memory as exact doubles; the searches run on double-double moments
+// (one pass), only the reported residual energies need further passes. Every
+// pass ends in one grid-wide reduction whose CTA partials are exchanged
+// through flag-tagged 64-bit words in L2 (no barrier, no host round trip).
 //
 // Reduction order (shared with the CPU oracle, oracle/rpd_oracle.cpp
-// lane_tree_sum): element i belongs to lane i mod 8192 (lane = CTA*64 +
-// thread) and is added sequentially; lanes are then combined by an adjacent-
-// pairwise binary tree (warp shuffles, CTA, then the 128 CTA partials).
-// Eigen's own SIMD order (road_geometry.cpp:20-24, 37) is not reproducible
-// without Eigen; the reference tests pin these sums to 1e-9 relative.
+// lane_tree_sum / moments): element i belongs to lane i mod 8192 (lane =
+// CTA*64 + thread) and is added sequentially; lanes are then combined by an
+// adjacent-pairwise binary tree (warp shuffles, CTA, then the 128 CTA
+// partials). Eigen's own SIMD order (road_geometry.cpp:20-24, 37) is not
+// reproducible without Eigen; the reference tests pin these sums to 1e-9.
 
 #include <algorithm>
 
@@ -205,77 +204,66 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
 }
 
 // ----------------------------------------------------------- fit kernel ----
-// One cooperative grid of kFitCtas CTAs (co-resident, one per SM) runs the
-// whole fit.  CTA c owns lanes [c*kFitSweep, (c+1)*kFitSweep) of the 8192
-// summation lanes; its observations (rows m: element m*8192 + lane) are staged
-// once in shared memory as exact doubles.  Every reduction is: per-lane
-// sequential sums -> warp shuffle tree -> CTA partial -> global partials +
-// one grid barrier -> every CTA combines the kFitCtas partials with the same
-// pairwise tree, so all CTAs hold bit-identical sums and run the (scalar)
-// golden-section logic redundantly.  A helper warp per CTA computes the
-// double-double sin/cos of the angles the NEXT sweep may need (both outcomes
-// of the pending comparison) while the current sweep runs.
+// One cooperative grid of kFitCtas CTAs (co-resident, one per SM) runs a whole
+// fit.  CTA c owns lanes [c*kFitSweep, (c+1)*kFitSweep) of the 8192 summation
+// lanes; its observations (rows m: element m*8192 + lane) are staged once in
+// shared memory as exact doubles.
+//
+// The golden-section search evaluates fit_line's energy from the observation
+// moments (n, Σu, Σv, Σd, Σuu, Σvv, Σuv, Σdu, Σdv, Σdd) in double-double
+// arithmetic: the products are exact (two_prod) and the moments are summed in
+// double-double in the fixed lane order, so one pass over the data replaces
+// one pass per probe and the expanded energy keeps ~30 significant digits
+// (the cancellation the reference avoids with its residual form,
+// road_geometry.cpp:35-37, is harmless at that precision).  The reported
+// e0min of every final fit_line is still the residual form in double, summed
+// in the lane order.  Trimming (road_geometry.cpp:83-97) masks elements in
+// place; the survivors keep their lanes.  A fit_road is therefore four
+// grid-wide reductions (moments, residual, survivor moments, residual); each
+// CTA combines the 128 CTA partials with the same pairwise tree, so all CTAs
+// hold bit-identical sums and run the scalar search redundantly.
+// oracle/rpd_oracle.cpp restates exactly this arithmetic.
 constexpr int kFitCtas = 128;
-constexpr int kFitSweep = 64;                      // sweep threads per CTA
+constexpr int kFitSweep = 64;                      // summation lanes per CTA
 constexpr int kFitSweepWarps = kFitSweep / 32;
-constexpr int kFitThreads = kFitSweep + 32;        // + helper warp
+constexpr int kFitThreads = kFitSweep;
 constexpr int kFitLanes = kFitCtas * kFitSweep;    // == oracle kFitLanes (8192)
 constexpr int kMaxRows = 64;                       // 524288 observations
-// dynamic shared memory for `rows` staged rows: SoA doubles + trimming counts
-__host__ __device__ constexpr int fit_stage_bytes(int rows) {
-  return rows * kFitSweep * 3 * int(sizeof(double));
-}
-__host__ __device__ constexpr int fit_dyn_smem(int rows) {
-  return fit_stage_bytes(rows) + rows * (kFitCtas + 1) * int(sizeof(int));
-}
-constexpr int kMaxNV = 8;                          // values per reduction
+constexpr int kMaxNV = 20;                         // doubles per reduction (10 DD moments)
 constexpr int kPartReplicas = 8;  // copies of the CTA partials (spreads the polling over L2)
 constexpr int kPartWords = 2 * kPartReplicas * kFitCtas * kMaxNV * 2;
-static_assert(kFitSweep % 32 == 0 && (kFitSweepWarps & (kFitSweepWarps - 1)) == 0, "warps");
+static_assert((kFitSweepWarps & (kFitSweepWarps - 1)) == 0, "warps");
 static_assert((kFitCtas & (kFitCtas - 1)) == 0 && kFitCtas / 2 <= kFitSweep, "ctas");
+
+// dynamic shared memory for `rows` staged rows (SoA doubles d | u | v)
+__host__ __device__ constexpr int fit_dyn_smem(int rows) {
+  return rows * kFitSweep * 3 * int(sizeof(double));
+}
 
 struct FitKParams {
   FitRequest r;
   DevStatus* status;
-  // trimming scratch (same format as the input)
-  uint32_t* scr_uv;
-  float* scr_d;
-  double* scr_dd;
-  double* scr_du;
-  double* scr_dv;
-  unsigned long long* part;  // [2][kFitCtas][kMaxNV][2] flag-tagged CTA partials (zeroed)
-  int* rowcnt;     // [kMaxRows][kFitCtas] trimming survivors per row and CTA
-  unsigned* bar;   // grid barrier counter, zeroed before the launch
-  int trace;       // debug (RPD_FIT_TRACE=1): per-phase clock64 trace of CTA 0
-  int rows_cap;    // staged rows the dynamic shared memory holds
+  unsigned long long* part;  // [2][kPartReplicas][kFitCtas][kMaxNV][2] flag-tagged partials
+  int trace;                 // debug (RPD_FIT_TRACE=1): per-phase clock64 trace of CTA 0
+  int rows_cap;              // staged rows the dynamic shared memory holds
 };
 
 struct FitShared {
   double warp_part[kFitSweepWarps][kMaxNV];
   double red[kFitSweepWarps][kMaxNV];
-  double sc[2][4][2];  // helper output (double-buffered): sin/cos of up to 4 angles
-  int wcnt[kFitSweepWarps][kMaxRows];
-  int row_base[kMaxRows];
   long long tr[512];
-  long long htr[256];
-  int ntr, nh;
-};
-
-struct LineFitD {
-  double a0, a1, phi, e0min, c, s;
+  int ntr;
 };
 
 struct FitState {
   const FitKParams* P;
   FitShared* S;
-  double* e;  // staged SoA doubles: d | u | v, each [rows_cap][kFitSweep]
-  int rstride;  // rows_cap * kFitSweep
+  double* e;     // staged SoA doubles: d | u | v, each [rows_cap][kFitSweep]
+  int rstride;   // rows_cap * kFitSweep
   long long k;
-  int rows;
+  int rows;      // rows this lane owns
   int lane;
-  unsigned calls;  // grid_sum calls so far (the exchange flag)
-  int scbuf;     // helper output buffer
-  unsigned target;
+  unsigned calls;  // grid reductions so far (the exchange flag)
 };
 
 __device__ __forceinline__ void fit_tr(FitState& F, int tag) {
@@ -283,73 +271,71 @@ __device__ __forceinline__ void fit_tr(FitState& F, int tag) {
     F.S->tr[F.S->ntr++] = ((long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFll);
 }
 
-__device__ __forceinline__ bool is_sweep() { return threadIdx.x < kFitSweep; }
-
-__device__ __forceinline__ void sweep_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kFitSweep) : "memory");
-}
-
 constexpr unsigned kSpinLimit = 1u << 24;  // ~seconds: a lost peer traps, never hangs
-#ifndef RPD_FIT_BACKOFF
-#define RPD_FIT_BACKOFF 0  // ns between unsuccessful partial polls
-#endif
-#ifndef RPD_FIT_SMALL_SMEM
-#define RPD_FIT_SMALL_SMEM 0
-#endif
 
-// Grid-wide barrier of the cooperative launch (thread 0 of every CTA arrives
-// with release semantics and spins with acquire loads); all threads of the
-// CTA must call it.  Used by trimming only; the per-sweep reductions use the
-// flag-tagged exchange of grid_sum.
-__device__ void grid_bar(FitState& F) {
-  F.target += kFitCtas;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned* bar = F.P->bar;
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v, spins = 0;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-      if (++spins > kSpinLimit) __trap();
-    } while (v < F.target);
-  }
-  __syncthreads();
+// ----- double-double arithmetic (Dekker / Knuth; restated in the oracle) ----
+__device__ __forceinline__ DD dd_add_d(DD a, double b) {
+  DD s = two_sum(a.hi, b);
+  s.lo += a.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ DD dd_neg(DD a) { return DD{-a.hi, -a.lo}; }
+__device__ __forceinline__ DD dd_sub(DD a, DD b) { return dd_add(a, dd_neg(b)); }
+__device__ __forceinline__ DD dd_mul_d(DD a, double b) {
+  DD p = two_prod(a.hi, b);
+  p.lo += a.lo * b;
+  return quick_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ DD dd_div(DD a, DD b) {
+  const double q1 = a.hi / b.hi;
+  DD r = dd_sub(a, dd_mul_d(b, q1));
+  const double q2 = r.hi / b.hi;
+  r = dd_sub(r, dd_mul_d(b, q2));
+  const double q3 = r.hi / b.hi;
+  return dd_add_d(quick_two_sum(q1, q2), q3);
+}
+__device__ __forceinline__ bool dd_lt(DD a, DD b) {
+  return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
 }
 
-// Stage the first k elements of the source into shared memory (sweep threads).
+// Moments in double-double: su, sv, sd, suu, svv, suv, sdu, sdv, sdd, n.
+constexpr int kNMom = 10;
+struct Moments {
+  DD m[kNMom];
+};
+
+// Stage the first k elements of the request's input into shared memory.
 template <bool COMPACT>
-__device__ void fit_stage_from(FitState& F, const uint32_t* g_uv, const float* g_d,
-                               const double* g_dd, const double* g_du, const double* g_dv) {
-  F.rows = int((F.k + kFitLanes - 1) / kFitLanes);
-  if (is_sweep()) {
-    constexpr int U = 8;  // loads in flight per thread
-    for (int m0 = 0; m0 < F.rows; m0 += U) {
-      double d[U], u[U], v[U];
+__device__ void fit_stage(FitState& F, const FitRequest& R) {
+  const int rows_total = int((F.k + kFitLanes - 1) / kFitLanes);
+  const long long full = F.k / kFitLanes;
+  F.rows = int(full) + (F.lane < F.k - full * kFitLanes ? 1 : 0);
+  constexpr int U = 8;  // loads in flight per thread
+  for (int m0 = 0; m0 < rows_total; m0 += U) {
+    double d[U], u[U], v[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const long long i = (long long)(m0 + j) * kFitLanes + F.lane;
-        if (i < F.k) {
-          if (COMPACT) {
-            const uint32_t uv = __ldcg(g_uv + i);
-            u[j] = double(uv & 0xFFFFu);
-            v[j] = double(uv >> 16);
-            d[j] = double(__ldcg(g_d + i));
-          } else {
-            d[j] = __ldcg(g_dd + i);
-            u[j] = __ldcg(g_du + i);
-            v[j] = __ldcg(g_dv + i);
-          }
+    for (int j = 0; j < U; ++j) {
+      const long long i = (long long)(m0 + j) * kFitLanes + F.lane;
+      if (m0 + j < F.rows) {
+        if (COMPACT) {
+          const uint32_t uv = __ldcg(R.obs.uv + i);
+          u[j] = double(uv & 0xFFFFu);
+          v[j] = double(uv >> 16);
+          d[j] = double(__ldcg(R.obs.d + i));
+        } else {
+          d[j] = __ldcg(R.dd + i);
+          u[j] = __ldcg(R.du + i);
+          v[j] = __ldcg(R.dv + i);
         }
       }
+    }
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const long long i = (long long)(m0 + j) * kFitLanes + F.lane;
-        if (i < F.k) {
-          const int o = (m0 + j) * kFitSweep + threadIdx.x;
-          F.e[o] = d[j];
-          F.e[F.rstride + o] = u[j];
-          F.e[2 * F.rstride + o] = v[j];
-        }
+    for (int j = 0; j < U; ++j) {
+      if (m0 + j < F.rows) {
+        const int o = (m0 + j) * kFitSweep + threadIdx.x;
+        F.e[o] = d[j];
+        F.e[F.rstride + o] = u[j];
+        F.e[2 * F.rstride + o] = v[j];
       }
     }
   }
@@ -363,47 +349,68 @@ __device__ __forceinline__ void fit_get(const FitState& F, int m, double& d, dou
   v = F.e[2 * F.rstride + o];
 }
 
-// Grid-wide sum of NV doubles in the fixed adjacent-pairwise lane order.
-// Called by all threads; only sweep threads contribute.  CTA partials are
-// exchanged without a barrier: each double travels as two 64-bit words
-// (flag << 32 | 32 data bits), each single-copy atomic, so a reader that sees
-// the call's flag in both words holds the value (the LL protocol of NCCL).
-// Slots alternate by call parity: a CTA rewrites a slot only after every CTA
-// has published the following call, i.e. finished reading this one.
-template <int NV>
+// Grid-wide sum of NV values (doubles, or NV/2 double-doubles when DD) in the
+// fixed adjacent-pairwise lane order.  CTA partials are exchanged without a
+// barrier: each double travels as two 64-bit words (flag << 32 | 32 data
+// bits), each single-copy atomic, so a reader that sees the call's flag in
+// both words holds the value (the LL protocol of NCCL).  Slots alternate by
+// call parity: a CTA rewrites a slot only after every CTA has published the
+// following call, i.e. finished reading this one.
+template <int NV, bool DDV>
 __device__ void grid_sum(FitState& F, double (&x)[NV]) {
-  static_assert(NV <= kMaxNV, "too many values");
+  static_assert(NV <= kMaxNV && (!DDV || NV % 2 == 0), "values");
   FitShared& S = *F.S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned flag = ++F.calls;
   unsigned long long* part =
       F.P->part + size_t(flag & 1u) * (kPartReplicas * kFitCtas * kMaxNV * 2);
   const unsigned long long ftag = (unsigned long long)flag << 32;
+  auto plus = [](double (&a)[NV], const double (&b)[NV]) {
+    if (DDV) {
+#pragma unroll
+      for (int q = 0; q < NV; q += 2) {
+        const DD r = dd_add(DD{a[q], a[q + 1]}, DD{b[q], b[q + 1]});
+        a[q] = r.hi;
+        a[q + 1] = r.lo;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) a[q] += b[q];
+    }
+  };
   fit_tr(F, 3);
-  if (is_sweep()) {
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1)
+  for (int off = 1; off < 32; off <<= 1) {
+    double o[NV];
 #pragma unroll
-      for (int q = 0; q < NV; ++q) x[q] += __shfl_down_sync(0xFFFFFFFFu, x[q], off);
-    if (lane == 0)
+    for (int q = 0; q < NV; ++q) o[q] = __shfl_down_sync(0xFFFFFFFFu, x[q], off);
+    plus(x, o);
+  }
+  if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < NV; ++q) S.warp_part[warp][q] = x[q];
-    sweep_bar();
+    for (int q = 0; q < NV; ++q) S.warp_part[warp][q] = x[q];
+  __syncthreads();
+  if (threadIdx.x < 32) {  // one warp publishes the CTA partial
+    double p[kFitSweepWarps][NV];
+#pragma unroll
+    for (int r = 0; r < kFitSweepWarps; ++r)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) p[r][q] = S.warp_part[r][q];
+#pragma unroll
+    for (int width = 1; width < kFitSweepWarps; width *= 2)
+#pragma unroll
+      for (int j = 0; j < kFitSweepWarps; j += 2 * width) plus(p[j], p[j + width]);
     if (threadIdx.x < NV) {
       const int q = threadIdx.x;
-      double p[kFitSweepWarps];
+      double val = p[0][0];
 #pragma unroll
-      for (int r = 0; r < kFitSweepWarps; ++r) p[r] = S.warp_part[r][q];
-#pragma unroll
-      for (int width = 1; width < kFitSweepWarps; width *= 2)
-#pragma unroll
-        for (int j = 0; j < kFitSweepWarps; j += 2 * width) p[j] += p[j + width];
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(p[0]);
+      for (int qq = 1; qq < NV; ++qq)
+        if (qq == q) val = p[0][qq];
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(val);
       const unsigned long long w0 = ftag | (bits & 0xFFFFFFFFull), w1 = ftag | (bits >> 32);
 #pragma unroll
       for (int rep = 0; rep < kPartReplicas; ++rep) {
-        unsigned long long* dst =
-            part + ((size_t(rep) * kFitCtas + blockIdx.x) * kMaxNV + q) * 2;
+        unsigned long long* dst = part + ((size_t(rep) * kFitCtas + blockIdx.x) * kMaxNV + q) * 2;
         asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
                      : "memory");
       }
@@ -434,153 +441,133 @@ __device__ void grid_sum(FitState& F, double (&x)[NV]) {
         for (int q = 0; q < NV; ++q)
           ready &= (w[c][q][0] >> 32) == flag && (w[c][q][1] >> 32) == flag;
       if (ready) {
+        double b[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-          const double a = __longlong_as_double(
+          y[q] = __longlong_as_double(
               (long long)((w[0][q][0] & 0xFFFFFFFFull) | (w[0][q][1] << 32)));
-          const double b = __longlong_as_double(
+          b[q] = __longlong_as_double(
               (long long)((w[1][q][0] & 0xFFFFFFFFull) | (w[1][q][1] << 32)));
-          y[q] = a + b;
         }
+        plus(y, b);
         break;
       }
       if (++spins > kSpinLimit) __trap();
-      if (RPD_FIT_BACKOFF > 0) __nanosleep(RPD_FIT_BACKOFF);
     }
     fit_tr(F, 41);
     constexpr int kW = kPairs < 32 ? kPairs : 32;
 #pragma unroll
-    for (int off = 1; off < kW; off <<= 1)
+    for (int off = 1; off < kW; off <<= 1) {
+      double o[NV];
 #pragma unroll
-      for (int q = 0; q < NV; ++q) y[q] += __shfl_down_sync(0xFFFFFFFFu, y[q], off);
+      for (int q = 0; q < NV; ++q) o[q] = __shfl_down_sync(0xFFFFFFFFu, y[q], off);
+      plus(y, o);
+    }
     if (lane == 0)
 #pragma unroll
       for (int q = 0; q < NV; ++q) S.red[warp][q] = y[q];
   }
   __syncthreads();
   constexpr int kRW = (kPairs + 31) / 32;
+  double p[kRW][NV];
 #pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    double p[kRW];
+  for (int r = 0; r < kRW; ++r)
 #pragma unroll
-    for (int r = 0; r < kRW; ++r) p[r] = S.red[r][q];
+    for (int q = 0; q < NV; ++q) p[r][q] = S.red[r][q];
 #pragma unroll
-    for (int width = 1; width < kRW; width *= 2)
+  for (int width = 1; width < kRW; width *= 2)
 #pragma unroll
-      for (int j = 0; j < kRW; j += 2 * width) p[j] += p[j + width];
-    x[q] = p[0];
-  }
+    for (int j = 0; j < kRW; j += 2 * width) plus(p[j], p[j + width]);
+#pragma unroll
+  for (int q = 0; q < NV; ++q) x[q] = p[0][q];
+  __syncthreads();  // S.red / S.warp_part reusable
   fit_tr(F, 5);
 }
 
-// Helper warp: sin/cos of n <= 4 angles into S.sc[F.scbuf] (visible after
-// the next __syncthreads of the CTA).
-__device__ __forceinline__ void helper_sincos(FitState& F, int n, const double* phi) {
-  if ((threadIdx.x >> 5) == kFitSweepWarps) {
-    const int l = threadIdx.x & 31;
-    const bool tr = F.P->trace && blockIdx.x == 0 && l == 0 && F.S->nh < 254;
-    if (tr) F.S->htr[F.S->nh++] = clock64();
-    if (l < n) dd_sincos(phi[l], &F.S->sc[F.scbuf][l][0], &F.S->sc[F.scbuf][l][1]);
-    if (tr) F.S->htr[F.S->nh++] = clock64();
+// Moments of the elements whose row bit is set in `mask` (this lane's rows).
+__device__ Moments fit_moments(FitState& F, unsigned long long mask) {
+  DD acc[kNMom];
+#pragma unroll
+  for (int q = 0; q < kNMom; ++q) acc[q] = DD{0.0, 0.0};
+  for (int m = 0; m < F.rows; ++m) {
+    if (!((mask >> m) & 1ull)) continue;
+    double d, u, v;
+    fit_get(F, m, d, u, v);
+    acc[0] = dd_add_d(acc[0], u);
+    acc[1] = dd_add_d(acc[1], v);
+    acc[2] = dd_add_d(acc[2], d);
+    acc[3] = dd_add(acc[3], two_prod(u, u));
+    acc[4] = dd_add(acc[4], two_prod(v, v));
+    acc[5] = dd_add(acc[5], two_prod(u, v));
+    acc[6] = dd_add(acc[6], two_prod(d, u));
+    acc[7] = dd_add(acc[7], two_prod(d, v));
+    acc[8] = dd_add(acc[8], two_prod(d, d));
+    acc[9] = dd_add_d(acc[9], 1.0);
   }
+  double x[2 * kNMom];
+#pragma unroll
+  for (int q = 0; q < kNMom; ++q) {
+    x[2 * q] = acc[q].hi;
+    x[2 * q + 1] = acc[q].lo;
+  }
+  grid_sum<2 * kNMom, true>(F, x);
+  Moments M;
+#pragma unroll
+  for (int q = 0; q < kNMom; ++q) M.m[q] = DD{x[2 * q], x[2 * q + 1]};
+  return M;
 }
 
-// Non-speculative sin/cos (used before the first sweeps): cs[i] = {cos, sin}.
-__device__ void fit_sincos_now(FitState& F, int n, const double* phi, double (*cs)[2]) {
-  fit_tr(F, 1);
-  helper_sincos(F, n, phi);
-  __syncthreads();
-  for (int i = 0; i < n; ++i) {
-    cs[i][0] = F.S->sc[F.scbuf][i][1];
-    cs[i][1] = F.S->sc[F.scbuf][i][0];
-  }
-  __syncthreads();
-  fit_tr(F, 2);
-}
-
-// One sweep over the observations + one grid reduction computing
-//   [sd]                          if SD
-//   (st, stt, sdt) for NS angles  t = c*v - s*u   (road_geometry.cpp:17-24)
-//   sum r^2 for NR fitted lines   r = d - a0 - a1*t (road_geometry.cpp:37)
-// Each sum is its own lane accumulator, so every value is bit-identical to
-// a separate pass in the oracle's lane order.
-template <bool SD, int NS, int NR>
-__device__ void fit_pass(FitState& F, const double (*ang)[2], const double (*line)[4],
-                         double* out) {
-  constexpr int NV = (SD ? 1 : 0) + 3 * NS + NR;
-  double acc[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-  if (is_sweep()) {
-    double c[NS > 0 ? NS : 1], s[NS > 0 ? NS : 1];
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      c[j] = ang[j][0];
-      s[j] = ang[j][1];
-    }
-    double la0[NR > 0 ? NR : 1], la1[NR > 0 ? NR : 1], lc[NR > 0 ? NR : 1], ls[NR > 0 ? NR : 1];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      la0[j] = line[j][0];
-      la1[j] = line[j][1];
-      lc[j] = line[j][2];
-      ls[j] = line[j][3];
-    }
-    fit_tr(F, 7);
-    const long long full = F.k / kFitLanes;  // rows every lane owns
-    const int nm = int(full) + (F.lane < F.k - full * kFitLanes ? 1 : 0);
-#pragma unroll 4
-    for (int m = 0; m < nm; ++m) {
-      double d, u, v;
-      fit_get(F, m, d, u, v);
-      int q = 0;
-      if (SD) acc[q++] += d;
-#pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        const double t = c[j] * v - s[j] * u;
-        acc[q] += t;
-        acc[q + 1] += t * t;
-        acc[q + 2] += d * t;
-        q += 3;
-      }
-#pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const double t = lc[j] * v - ls[j] * u;
-        const double r = d - la0[j] - la1[j] * t;
-        acc[q++] += r * r;
-      }
-    }
-  }
-  grid_sum<NV>(F, acc);
-#pragma unroll
-  for (int q = 0; q < NV; ++q) out[q] = acc[q];
-}
-
-// Closed-form normal equations of fit_line (road_geometry.cpp:26-34).
-__device__ __forceinline__ bool solve_line(double kk, double sd, const double* st3, double& a0,
-                                           double& a1) {
-  const double st = st3[0], stt = st3[1], sdt = st3[2];
-  const double det = kk * stt - st * st;
-  const double prod = kk * stt;
-  const double scale = (prod < 1.0) ? 1.0 : prod;
-  if (fabs(det) < 1e-12 * scale) return false;
-  a0 = (stt * sd - st * sdt) / det;
-  a1 = (kk * sdt - st * sd) / det;
+// fit_line's normal equations and energy at (c, s) = (cos phi, sin phi) from
+// the moments (road_geometry.cpp:16-37), all in double-double.
+struct LineDD {
+  DD a0, a1, e;
+};
+__device__ bool line_eval(const Moments& M, double c, double s, LineDD& out) {
+  const DD N = M.m[9];
+  const DD cc = two_prod(c, c), ss = two_prod(s, s), cs = two_prod(c, s);
+  const DD T1 = dd_sub(dd_mul_d(M.m[1], c), dd_mul_d(M.m[0], s));
+  const DD T2 = dd_add(dd_sub(dd_mul(cc, M.m[4]), dd_mul_d(dd_mul(cs, M.m[5]), 2.0)),
+                       dd_mul(ss, M.m[3]));
+  const DD TD = dd_sub(dd_mul_d(M.m[7], c), dd_mul_d(M.m[6], s));
+  const DD D1 = M.m[2], D2 = M.m[8];
+  const DD nT2 = dd_mul(N, T2);
+  const DD det = dd_sub(nT2, dd_mul(T1, T1));
+  const double scale = nT2.hi < 1.0 ? 1.0 : nT2.hi;
+  if (fabs(det.hi) < 1e-12 * scale) return false;  // road_geometry.cpp:26-29
+  const DD a0 = dd_div(dd_sub(dd_mul(T2, D1), dd_mul(T1, TD)), det);
+  const DD a1 = dd_div(dd_sub(dd_mul(N, TD), dd_mul(T1, D1)), det);
+  DD e = D2;
+  e = dd_sub(e, dd_mul_d(dd_mul(a0, D1), 2.0));
+  e = dd_sub(e, dd_mul_d(dd_mul(a1, TD), 2.0));
+  e = dd_add(e, dd_mul(N, dd_mul(a0, a0)));
+  e = dd_add(e, dd_mul_d(dd_mul(dd_mul(a0, a1), T1), 2.0));
+  e = dd_add(e, dd_mul(dd_mul(a1, a1), T2));
+  out = LineDD{a0, a1, e};
   return true;
 }
 
-// fit_line at one angle (road_geometry.cpp:12-39): two sweeps.
-__device__ bool fit_probe(FitState& F, double phi, LineFitD& out) {
-  double cs[1][2];
-  fit_sincos_now(F, 1, &phi, cs);
-  double r1[4];
-  fit_pass<true, 1, 0>(F, cs, nullptr, r1);
-  double a0, a1;
-  if (!solve_line(double(F.k), r1[0], r1 + 1, a0, a1)) return false;
-  const double ln[1][4] = {{a0, a1, cs[0][0], cs[0][1]}};
-  double e[1];
-  fit_pass<false, 0, 1>(F, nullptr, ln, e);
-  out = LineFitD{a0, a1, phi, e[0], cs[0][0], cs[0][1]};
+struct LineFitD {
+  double a0, a1, phi, e0min, c, s;
+};
+
+// Final fit_line at phi: a0/a1 from the moments (rounded), e0min in the
+// reference's residual form over the masked elements (one grid reduction).
+__device__ bool fit_line_final(FitState& F, const Moments& M, double phi, double c, double s,
+                               unsigned long long mask, LineFitD& out) {
+  LineDD L;
+  if (!line_eval(M, c, s, L)) return false;
+  const double a0 = L.a0.hi, a1 = L.a1.hi;
+  double acc[1] = {0.0};
+  for (int m = 0; m < F.rows; ++m) {
+    if (!((mask >> m) & 1ull)) continue;
+    double d, u, v;
+    fit_get(F, m, d, u, v);
+    const double t = c * v - s * u;
+    const double r = d - a0 - a1 * t;
+    acc[0] += r * r;
+  }
+  grid_sum<1, false>(F, acc);
+  out = LineFitD{a0, a1, phi, acc[0], c, s};
   return true;
 }
 
@@ -604,260 +591,102 @@ __device__ __forceinline__ double g_advance(GState& s, bool br) {
   return s.x2;
 }
 
-// Angles whose sums the sweep after state s computes: the point the next
-// iteration evaluates on either branch, or the final midpoint.
-__device__ __forceinline__ int g_cands(const GState& s, double tol, double* ca) {
-  if (s.b - s.a > tol) {
-    GState t = s;
-    ca[0] = g_advance(t, true);
-    t = s;
-    ca[1] = g_advance(t, false);
-    return 2;
-  }
-  ca[0] = ca[1] = 0.5 * (s.a + s.b);
-  return 1;
-}
+// sin/cos of one angle per lane, then broadcast lane `src`'s pair.
+__device__ __forceinline__ void warp_sincos(double x, double& s, double& c) { dd_sincos(x, &s, &c); }
 
-// Speculative helper request: candidates after either outcome of the pending
-// comparison, packed [br=true: 0,1 | br=false: 2,3].
-__device__ __forceinline__ void g_speculate(FitState& F, const GState& s, double tol) {
-  double ang[4];
-  GState t = s;
-  g_advance(t, true);
-  g_cands(t, tol, ang);
-  t = s;
-  g_advance(t, false);
-  g_cands(t, tol, ang + 2);
-  helper_sincos(F, 4, ang);
-}
-
-// estimate_roll with the f1 < f2 branch evaluated speculatively: every sweep
-// computes the energy of the newest point AND the normal-equation sums of the
-// point the next iteration will evaluate on either branch, so an iteration
-// costs one sweep and one grid reduction; the sin/cos the following sweep may
-// need are computed by the helper warp meanwhile.  The evaluated angles,
-// every value and every branch are exactly those of the sequential reference.
-__device__ bool fit_golden(FitState& F, double lo, double hi, double tol, LineFitD& out) {
-  const double kk = double(F.k);
-  GState s{lo, hi, hi - kGolden * (hi - lo), lo + kGolden * (hi - lo)};
-  double ang[2][2];
-  {
-    const double ph[2] = {s.x1, s.x2};
-    fit_sincos_now(F, 2, ph, ang);
-  }
-  // sweep 0: sd and the sums of x1, x2; the helper prepares cands(s)
-  double ca[2];
-  const int n0 = g_cands(s, tol, ca);
-  F.scbuf ^= 1;
-  helper_sincos(F, n0, ca);
-  double r0[7];
-  fit_pass<true, 2, 0>(F, ang, nullptr, r0);
-  const double sd = r0[0];
-  double l1[4], l2[4];
-  if (!solve_line(kk, sd, r0 + 1, l1[0], l1[1])) return false;
-  if (!solve_line(kk, sd, r0 + 4, l2[0], l2[1])) return false;
-  l1[2] = ang[0][0];
-  l1[3] = ang[0][1];
-  l2[2] = ang[1][0];
-  l2[3] = ang[1][1];
-  double cang[2][2];
-  {
-    const int b = F.scbuf;
-    for (int i = 0; i < 2; ++i) {
-      const int src = n0 == 2 ? i : 0;
-      cang[i][0] = F.S->sc[b][src][1];
-      cang[i][1] = F.S->sc[b][src][0];
+// estimate_roll on moments.  The sin/cos of the next kLevels iterations'
+// possible angles (1 + 2 + 4 + 8 + 16 = 31 nodes of the decision tree) are
+// computed by the warp's lanes in one batch, so the search runs ~5 iterations
+// per double-double sin/cos latency.  All lanes (and CTAs) follow the same
+// decisions.  Returns the final midpoint and its sin/cos.
+__device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, double tol,
+                           double& phi, double& cphi, double& sphi) {
+  constexpr int kLevels = 5;
+  const int lane = threadIdx.x & 31;
+  GState st{lo, hi, hi - kGolden * (hi - lo), lo + kGolden * (hi - lo)};
+  double bs, bc;
+  warp_sincos(lane == 0 ? st.x1 : st.x2, bs, bc);
+  LineDD L;
+  double c = __shfl_sync(0xFFFFFFFFu, bc, 0), s = __shfl_sync(0xFFFFFFFFu, bs, 0);
+  if (!line_eval(M, c, s, L)) return false;
+  DD f1 = L.e;
+  c = __shfl_sync(0xFFFFFFFFu, bc, 1);
+  s = __shfl_sync(0xFFFFFFFFu, bs, 1);
+  if (!line_eval(M, c, s, L)) return false;
+  DD f2 = L.e;
+  int left = 0, node = 0;
+  while (st.b - st.a > tol) {
+    const bool br = dd_lt(f1, f2);
+    if (left == 0) {  // new batch: node 0 is the next point, then the decision tree
+      GState t = st;
+      double x = g_advance(t, br);
+      const int lv = 31 - __clz(lane + 1);  // level of this lane's node
+      const int bits = lane + 1 - (1 << lv);
+      for (int j = lv - 1; j >= 0; --j) x = g_advance(t, ((bits >> j) & 1) != 0);
+      warp_sincos(x, bs, bc);
+      node = 0;
+      left = kLevels;
     }
-  }
-  // sweep 1: energies of x1 and x2 + sums of cands(s); the helper speculates
-  bool loop = s.b - s.a > tol;
-  F.scbuf ^= 1;
-  if (loop) g_speculate(F, s, tol);
-  double f1, f2;
-  double res[8];
-  {
-    const double lines[2][4] = {{l1[0], l1[1], l1[2], l1[3]}, {l2[0], l2[1], l2[2], l2[3]}};
-    fit_pass<false, 2, 2>(F, cang, lines, res);
-    f1 = res[6];
-    f2 = res[7];
-  }
-  double cs_sum[2][3] = {{res[0], res[1], res[2]}, {res[3], res[4], res[5]}};
-  while (loop) {
-    const bool br = f1 < f2;
-    const int pick = br ? 0 : 1;
-    double ln[4];
-    if (!solve_line(kk, sd, cs_sum[pick], ln[0], ln[1])) return false;
-    ln[2] = cang[pick][0];
-    ln[3] = cang[pick][1];
-    g_advance(s, br);
+    c = __shfl_sync(0xFFFFFFFFu, bc, node);
+    s = __shfl_sync(0xFFFFFFFFu, bs, node);
+    g_advance(st, br);
     if (br)
       f2 = f1;
     else
       f1 = f2;
-    loop = s.b - s.a > tol;
-    // sin/cos of cands(s) were speculated during the previous sweep
-    {
-      const int b = F.scbuf;
-      const int base = br ? 0 : 2;
-      const int n = loop ? 2 : 1;
-      for (int i = 0; i < 2; ++i) {
-        const int src = base + (n == 2 ? i : 0);
-        cang[i][0] = F.S->sc[b][src][1];
-        cang[i][1] = F.S->sc[b][src][0];
-      }
-    }
-    F.scbuf ^= 1;
-    if (loop) g_speculate(F, s, tol);
-    const double lines[1][4] = {{ln[0], ln[1], ln[2], ln[3]}};
-    double r[7];
-    fit_pass<false, 2, 1>(F, cang, lines, r);
+    if (!line_eval(M, c, s, L)) return false;
     if (br)
-      f1 = r[6];
+      f1 = L.e;
     else
-      f2 = r[6];
-    cs_sum[0][0] = r[0];
-    cs_sum[0][1] = r[1];
-    cs_sum[0][2] = r[2];
-    cs_sum[1][0] = r[3];
-    cs_sum[1][1] = r[4];
-    cs_sum[1][2] = r[5];
+      f2 = L.e;
+    --left;
+    node = 2 * node + (dd_lt(f1, f2) ? 2 : 1);
   }
-  // final fit_line at the midpoint: its sums are cs_sum[0]
-  const double mid = 0.5 * (s.a + s.b);
-  double fa0, fa1;
-  if (!solve_line(kk, sd, cs_sum[0], fa0, fa1)) return false;
-  const double lines[1][4] = {{fa0, fa1, cang[0][0], cang[0][1]}};
-  double e[1];
-  fit_pass<false, 0, 1>(F, nullptr, lines, e);
-  out = LineFitD{fa0, fa1, mid, e[0], cang[0][0], cang[0][1]};
+  phi = 0.5 * (st.a + st.b);
+  warp_sincos(phi, bs, bc);
+  cphi = __shfl_sync(0xFFFFFFFFu, bc, 0);
+  sphi = __shfl_sync(0xFFFFFFFFu, bs, 0);
   return true;
-}
-
-// Stable grid-wide compaction of the survivors of fit_road's trimming
-// (road_geometry.cpp:83-97) into the scratch buffers, then re-staging.
-// Returns the new count.
-template <bool COMPACT>
-__device__ long long fit_trim(FitState& F, const LineFitD& first, double rms) {
-  FitShared& S = *F.S;
-  const FitKParams& P = *F.P;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double lim = 3.0 * rms;
-  unsigned long long keep = 0;
-  if (is_sweep()) {
-    for (int m = 0; m < F.rows; ++m) {
-      const long long i = (long long)m * kFitLanes + F.lane;
-      if (i >= F.k) break;
-      double d, u, v;
-      fit_get(F, m, d, u, v);
-      const double r = d - (first.a0 + first.a1 * (v * first.c - u * first.s));
-      if (fabs(r) <= lim) keep |= 1ull << m;
-    }
-    for (int m = 0; m < F.rows; ++m) {
-      const unsigned bal = __ballot_sync(0xFFFFFFFFu, (keep >> m) & 1ull);
-      if (lane == 0) S.wcnt[warp][m] = __popc(bal);
-    }
-  }
-  __syncthreads();
-  for (int m = threadIdx.x; m < F.rows; m += blockDim.x) {
-    int t = 0;
-    for (int w = 0; w < kFitSweepWarps; ++w) t += S.wcnt[w][m];
-    __stcg(P.rowcnt + m * kFitCtas + blockIdx.x, t);
-  }
-  __threadfence();
-  grid_bar(F);
-  // row totals and this CTA's offset within each row (counts staged in smem,
-  // row stride kFitCtas + 1 so the per-row scans below are conflict-free)
-  int* s_cnt = reinterpret_cast<int*>(F.e + 3 * F.rstride);
-  __shared__ long long s_tot[kMaxRows];
-  {
-    const int n = F.rows * kFitCtas;
-    constexpr int U = 8;
-    for (int i0 = threadIdx.x; i0 < n; i0 += U * kFitThreads) {
-      int x[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int i = i0 + j * kFitThreads;
-        x[j] = i < n ? __ldcg(P.rowcnt + i) : 0;
-      }
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int i = i0 + j * kFitThreads;
-        if (i < n) s_cnt[(i / kFitCtas) * (kFitCtas + 1) + i % kFitCtas] = x[j];
-      }
-    }
-  }
-  __syncthreads();
-  for (int m = threadIdx.x; m < F.rows; m += blockDim.x) {
-    long long tot = 0, before = 0;
-    for (int c = 0; c < kFitCtas; ++c) {
-      const int x = s_cnt[m * (kFitCtas + 1) + c];
-      if (c < int(blockIdx.x)) before += x;
-      tot += x;
-    }
-    s_tot[m] = tot;
-    S.row_base[m] = int(before);
-  }
-  __shared__ long long s_kept;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long acc = 0;
-    for (int m = 0; m < F.rows; ++m) {
-      S.row_base[m] += int(acc);
-      acc += s_tot[m];
-    }
-    s_kept = acc;
-  }
-  __syncthreads();
-  const long long kept = s_kept;
-  if (kept < 3 || kept == F.k) return kept;
-  if (is_sweep()) {
-    for (int m = 0; m < F.rows; ++m) {
-      const bool kb = (keep >> m) & 1ull;
-      if (!__any_sync(0xFFFFFFFFu, kb)) continue;
-      const unsigned bal = __ballot_sync(0xFFFFFFFFu, kb);
-      int woff = 0;
-      for (int w = 0; w < warp; ++w) woff += S.wcnt[w][m];
-      if (kb) {
-        const long long dst = S.row_base[m] + woff + __popc(bal & ((1u << lane) - 1u));
-        double d, u, v;
-        fit_get(F, m, d, u, v);
-        if (COMPACT) {
-          __stcg(P.scr_uv + dst, uint32_t(u) | (uint32_t(v) << 16));
-          __stcg(P.scr_d + dst, float(d));
-        } else {
-          __stcg(P.scr_dd + dst, d);
-          __stcg(P.scr_du + dst, u);
-          __stcg(P.scr_dv + dst, v);
-        }
-      }
-    }
-  }
-  __threadfence();
-  grid_bar(F);
-  F.k = kept;
-  fit_stage_from<COMPACT>(F, P.scr_uv, P.scr_d, P.scr_dd, P.scr_du, P.scr_dv);
-  return kept;
 }
 
 template <bool COMPACT>
 __device__ void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok) {
   const FitRequest& R = P.r;
-  fit_stage_from<COMPACT>(F, R.obs.uv, R.obs.d, R.dd, R.du, R.dv);
+  fit_stage<COMPACT>(F, R);
+  fit_tr(F, 1);
+  const unsigned long long all = F.rows >= 64 ? ~0ull : ((1ull << F.rows) - 1ull);
+  const Moments M = fit_moments(F, all);
   LineFitD f{};
   long long used = F.k;
+  double phi = 0.0, c = 1.0, s = 0.0;
   if (R.mode == kFitLine) {
-    ok = fit_probe(F, R.phi, f);
-  } else if (R.mode == kEstimateRoll) {
-    ok = fit_golden(F, R.lo, R.hi, R.tol, f);
+    phi = R.phi;
+    double bs, bc;
+    warp_sincos(phi, bs, bc);
+    c = __shfl_sync(0xFFFFFFFFu, bc, 0);
+    s = __shfl_sync(0xFFFFFFFFu, bs, 0);
+    ok = fit_line_final(F, M, phi, c, s, all, f);
   } else {
-    ok = fit_golden(F, -R.hi, R.hi, R.tol, f);  // fit_road: first = fit_line(obs, m.phi)
-    if (ok) {
+    const double lo = R.mode == kEstimateRoll ? R.lo : -R.hi;
+    ok = fit_golden(F, M, lo, R.hi, R.tol, phi, c, s) && fit_line_final(F, M, phi, c, s, all, f);
+    fit_tr(F, 2);
+    if (ok && R.mode == kFitRoad) {
       const double rms = sqrt(f.e0min / double(F.k));
       if (!(rms <= 0.0)) {
-        const long long k0 = F.k;
-        const long long kept = fit_trim<COMPACT>(F, f, rms);
-        if (kept >= 3 && kept != k0) {
-          ok = fit_golden(F, -R.hi, R.hi, R.tol, f);
+        // road_geometry.cpp:83-97: keep |d - road(u, v)| <= 3 rms, in place
+        const double lim = 3.0 * rms;
+        unsigned long long keep = 0;
+        for (int m = 0; m < F.rows; ++m) {
+          double d, u, v;
+          fit_get(F, m, d, u, v);
+          const double r = d - (f.a0 + f.a1 * (v * f.c - u * f.s));
+          if (fabs(r) <= lim) keep |= 1ull << m;
+        }
+        const Moments M2 = fit_moments(F, keep);
+        const long long kept = (long long)M2.m[9].hi;
+        if (kept >= 3 && kept != F.k) {
+          ok = fit_golden(F, M2, -R.hi, R.hi, R.tol, phi, c, s) &&
+               fit_line_final(F, M2, phi, c, s, keep, f);
           used = kept;
         }
       }
@@ -884,9 +713,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ 
   F.rstride = P.rows_cap * kFitSweep;
   F.lane = int(blockIdx.x) * kFitSweep + int(threadIdx.x);
   F.calls = 0;
-  F.scbuf = 0;
-  F.target = 0;
-  if (threadIdx.x == 0) S.ntr = S.nh = 0;
+  if (threadIdx.x == 0) S.ntr = 0;
   __syncthreads();
   fit_tr(F, 0);
   const bool failed_before = P.status->code != 0;
@@ -915,8 +742,6 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ 
       const long long t = S.tr[i] & 0xFFFFFFFFFFFFll;
       printf("FITTR %d %d %lld\n", i, int(S.tr[i] >> 48), t - t0);
     }
-    for (int i = 0; i < S.nh; ++i)
-      printf("FITH %d %lld\n", i, (S.htr[i] & 0xFFFFFFFFFFFFll) - t0);
   }
 }
 
@@ -938,35 +763,15 @@ void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
   // down to the observation cap lets other streams' CTAs share the fit's SMs,
   // which stretches every grid-wide exchange (measured: -7% frames/s with 8
   // concurrent pipelines).
-  int rows_cap = kMaxRows;
-  if (RPD_FIT_SMALL_SMEM) {
-    const long long kcap = req.compact ? (req.kmax > 0 ? req.kmax : (long long)kMaxRows * kFitLanes)
-                                       : req.k_host;
-    rows_cap = int(std::min<long long>(kMaxRows, std::max<long long>(1, (kcap + kFitLanes - 1) / kFitLanes)));
-  }
+  const int rows_cap = kMaxRows;
   FitKParams P{};
   P.r = req;
   P.status = ctx->status;
   P.rows_cap = rows_cap;
   static const bool trace = getenv("RPD_FIT_TRACE") != nullptr;
   P.trace = trace ? 1 : 0;
-  const long long scratch = req.compact ? (long long)kMaxRows * kFitLanes
-                                        : std::max<long long>(req.k_host, 1);
-  if (req.mode == kFitRoad) {
-    if (req.compact) {
-      P.scr_uv = ctx->ws.get<uint32_t>("fit_scr_uv", scratch);
-      P.scr_d = ctx->ws.get<float>("fit_scr_d", scratch);
-    } else {
-      P.scr_dd = ctx->ws.get<double>("fit_scr_dd", scratch);
-      P.scr_du = ctx->ws.get<double>("fit_scr_du", scratch);
-      P.scr_dv = ctx->ws.get<double>("fit_scr_dv", scratch);
-    }
-  }
   P.part = ctx->ws.get<unsigned long long>("fit_part", kPartWords);
   RPD_CK(cudaMemsetAsync(P.part, 0, sizeof(unsigned long long) * kPartWords, ctx->stream));
-  P.rowcnt = ctx->ws.get<int>("fit_rowcnt", kMaxRows * kFitCtas);
-  P.bar = ctx->ws.get<unsigned>("fit_bar", 1);
-  RPD_CK(cudaMemsetAsync(P.bar, 0, sizeof(unsigned), ctx->stream));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kFitCtas);
   cfg.blockDim = dim3(kFitThreads);
