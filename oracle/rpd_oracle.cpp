@@ -428,13 +428,13 @@ inline DD dd_add_d(DD a, double b) {
 inline DD dd_sub(DD a, DD b) { return dd_add(a, DD{-b.hi, -b.lo}); }
 inline DD dd_mul(DD a, DD b) {
   DD p = two_prod(a.hi, b.hi);
-  p.lo += a.hi * b.lo;
-  p.lo += a.lo * b.hi;
+  p.lo = std::fma(a.hi, b.lo, p.lo);
+  p.lo = std::fma(a.lo, b.hi, p.lo);
   return quick_two_sum(p.hi, p.lo);
 }
 inline DD dd_mul_d(DD a, double b) {
   DD p = two_prod(a.hi, b);
-  p.lo += a.lo * b;
+  p.lo = std::fma(a.lo, b, p.lo);
   return quick_two_sum(p.hi, p.lo);
 }
 inline DD dd_div(DD a, DD b) {
@@ -476,35 +476,37 @@ Moments moments(const Obs& o, const std::vector<char>* mask = nullptr) {
   return Moments{lane[0]};
 }
 
-// fit_line's normal equations (road_geometry.cpp:16-34) and its energy, from
-// the moments at (c, s) = (cos phi, sin phi), in double-double.  The expanded
-// energy d'd - 2 a'T'd + a'T'Ta is what the reference's residual form avoids
-// in double (:35-37); at ~106 bits the cancellation is harmless.
-struct LineDD {
-  DD a0, a1, e;
+// fit_line at (c, s) = (cos phi, sin phi) from the moments
+// (road_geometry.cpp:16-37), in double-double: st = c Sv - s Su,
+// stt = c^2 Svv - 2cs Suv + s^2 Suu, sdt = c Sdv - s Sdu, det = n stt - st^2
+// (singular test as :26-29), then either the minimal energy
+// E = Sdd - (stt Sd^2 - 2 st Sd sdt + n sdt^2) / det  (the search; the
+// expanded form the reference's residual form avoids in double, :35-37, is
+// harmless at ~106 bits) or the coefficients a0, a1 (:31-32).
+struct LineSums {
+  DD N, T1, T2, TD, det;
 };
-LineDD line_eval(const Moments& M, double c, double s) {
-  const DD N = M.m[9];
+LineSums line_sums(const Moments& M, double c, double s) {
+  LineSums o;
+  o.N = M.m[9];
   const DD cc = two_prod(c, c), ss = two_prod(s, s), cs = two_prod(c, s);
-  const DD T1 = dd_sub(dd_mul_d(M.m[1], c), dd_mul_d(M.m[0], s));
-  const DD T2 =
-      dd_add(dd_sub(dd_mul(cc, M.m[4]), dd_mul_d(dd_mul(cs, M.m[5]), 2.0)), dd_mul(ss, M.m[3]));
-  const DD TD = dd_sub(dd_mul_d(M.m[7], c), dd_mul_d(M.m[6], s));
-  const DD D1 = M.m[2], D2 = M.m[8];
-  const DD nT2 = dd_mul(N, T2);
-  const DD det = dd_sub(nT2, dd_mul(T1, T1));
+  o.T1 = dd_sub(dd_mul_d(M.m[1], c), dd_mul_d(M.m[0], s));
+  o.T2 = dd_add(dd_sub(dd_mul(cc, M.m[4]), dd_mul_d(dd_mul(cs, M.m[5]), 2.0)), dd_mul(ss, M.m[3]));
+  o.TD = dd_sub(dd_mul_d(M.m[7], c), dd_mul_d(M.m[6], s));
+  const DD nT2 = dd_mul(o.N, o.T2);
+  o.det = dd_sub(nT2, dd_mul(o.T1, o.T1));
   const double scale = nT2.hi < 1.0 ? 1.0 : nT2.hi;
-  if (std::abs(det.hi) < 1e-12 * scale)
+  if (std::abs(o.det.hi) < 1e-12 * scale)
     throw Degenerate("fit_line: degenerate observations (singular normal matrix)");
-  const DD a0 = dd_div(dd_sub(dd_mul(T2, D1), dd_mul(T1, TD)), det);
-  const DD a1 = dd_div(dd_sub(dd_mul(N, TD), dd_mul(T1, D1)), det);
-  DD e = D2;
-  e = dd_sub(e, dd_mul_d(dd_mul(a0, D1), 2.0));
-  e = dd_sub(e, dd_mul_d(dd_mul(a1, TD), 2.0));
-  e = dd_add(e, dd_mul(N, dd_mul(a0, a0)));
-  e = dd_add(e, dd_mul_d(dd_mul(dd_mul(a0, a1), T1), 2.0));
-  e = dd_add(e, dd_mul(dd_mul(a1, a1), T2));
-  return {a0, a1, e};
+  return o;
+}
+DD line_energy(const Moments& M, double c, double s) {
+  const LineSums L = line_sums(M, c, s);
+  const DD D1 = M.m[2];
+  DD q = dd_mul(L.T2, dd_mul(D1, D1));
+  q = dd_sub(q, dd_mul_d(dd_mul(dd_mul(L.T1, D1), L.TD), 2.0));
+  q = dd_add(q, dd_mul(L.N, dd_mul(L.TD, L.TD)));
+  return dd_sub(M.m[8], dd_div(q, L.det));
 }
 
 struct LineFit {
@@ -517,11 +519,12 @@ struct LineFit {
 LineFit fit_line_m(const Obs& o, const Moments& M, double phi,
                    const std::vector<char>* mask = nullptr) {
   const double c = std::cos(phi), s = std::sin(phi);
-  const LineDD L = line_eval(M, c, s);
+  const LineSums L = line_sums(M, c, s);
+  const DD D1 = M.m[2];
   LineFit f;
   f.model.phi = phi;
-  f.model.a0 = L.a0.hi;
-  f.model.a1 = L.a1.hi;
+  f.model.a0 = dd_div(dd_sub(dd_mul(L.T2, D1), dd_mul(L.T1, L.TD)), L.det).hi;
+  f.model.a1 = dd_div(dd_sub(dd_mul(L.N, L.TD), dd_mul(L.T1, D1)), L.det).hi;
   f.e0min = lane_tree_sum(
       o.count(),
       [&](size_t i) {
@@ -543,7 +546,7 @@ LineFit fit_line(const Obs& o, double phi) {
 // reference's loop).  Returns the final midpoint.
 double golden(const Moments& M, double lo, double hi, double tol) {
   constexpr double g = 0.6180339887498949;
-  auto energy = [&](double phi) { return line_eval(M, std::cos(phi), std::sin(phi)).e; };
+  auto energy = [&](double phi) { return line_energy(M, std::cos(phi), std::sin(phi)); };
   double a = lo, b = hi;
   double x1 = b - g * (b - a), x2 = a + g * (b - a);
   DD f1 = energy(x1), f2 = energy(x2);

@@ -251,6 +251,8 @@ struct FitKParams {
 struct FitShared {
   double warp_part[kFitSweepWarps][kMaxNV];
   double red[kFitSweepWarps][kMaxNV];
+  DD g_e[kFitThreads];  // golden-search decision tree: node energies
+  int g_bad[kFitThreads];  // node probe degenerate
   long long tr[512];
   int ntr;
 };
@@ -283,7 +285,14 @@ __device__ __forceinline__ DD dd_neg(DD a) { return DD{-a.hi, -a.lo}; }
 __device__ __forceinline__ DD dd_sub(DD a, DD b) { return dd_add(a, dd_neg(b)); }
 __device__ __forceinline__ DD dd_mul_d(DD a, double b) {
   DD p = two_prod(a.hi, b);
-  p.lo += a.lo * b;
+  p.lo = __fma_rn(a.lo, b, p.lo);
+  return quick_two_sum(p.hi, p.lo);
+}
+// product with fused low-order terms (the fit's arithmetic; dd_sincos keeps dd_mul)
+__device__ __forceinline__ DD dd_mulf(DD a, DD b) {
+  DD p = two_prod(a.hi, b.hi);
+  p.lo = __fma_rn(a.hi, b.lo, p.lo);
+  p.lo = __fma_rn(a.lo, b.hi, p.lo);
   return quick_two_sum(p.hi, p.lo);
 }
 __device__ __forceinline__ DD dd_div(DD a, DD b) {
@@ -517,32 +526,43 @@ __device__ Moments fit_moments(FitState& F, unsigned long long mask) {
   return M;
 }
 
-// fit_line's normal equations and energy at (c, s) = (cos phi, sin phi) from
-// the moments (road_geometry.cpp:16-37), all in double-double.
-struct LineDD {
-  DD a0, a1, e;
+// fit_line at (c, s) = (cos phi, sin phi) from the moments
+// (road_geometry.cpp:16-37), in double-double: the angle-dependent sums
+// st = c Sv - s Su, stt = c^2 Svv - 2cs Suv + s^2 Suu, sdt = c Sdv - s Sdu,
+// det = n stt - st^2 (singular test as :26-29), and either the minimal
+// energy  E = Sdd - (stt Sd^2 - 2 st Sd sdt + n sdt^2) / det  (the search) or
+// the coefficients a0 = (stt Sd - st sdt)/det, a1 = (n sdt - st Sd)/det.
+struct LineSums {
+  DD N, T1, T2, TD, det;
 };
-__device__ bool line_eval(const Moments& M, double c, double s, LineDD& out) {
-  const DD N = M.m[9];
+__device__ __forceinline__ bool line_sums(const Moments& M, double c, double s, LineSums& o) {
+  o.N = M.m[9];
   const DD cc = two_prod(c, c), ss = two_prod(s, s), cs = two_prod(c, s);
-  const DD T1 = dd_sub(dd_mul_d(M.m[1], c), dd_mul_d(M.m[0], s));
-  const DD T2 = dd_add(dd_sub(dd_mul(cc, M.m[4]), dd_mul_d(dd_mul(cs, M.m[5]), 2.0)),
-                       dd_mul(ss, M.m[3]));
-  const DD TD = dd_sub(dd_mul_d(M.m[7], c), dd_mul_d(M.m[6], s));
-  const DD D1 = M.m[2], D2 = M.m[8];
-  const DD nT2 = dd_mul(N, T2);
-  const DD det = dd_sub(nT2, dd_mul(T1, T1));
+  o.T1 = dd_sub(dd_mul_d(M.m[1], c), dd_mul_d(M.m[0], s));
+  o.T2 = dd_add(dd_sub(dd_mulf(cc, M.m[4]), dd_mul_d(dd_mulf(cs, M.m[5]), 2.0)),
+                dd_mulf(ss, M.m[3]));
+  o.TD = dd_sub(dd_mul_d(M.m[7], c), dd_mul_d(M.m[6], s));
+  const DD nT2 = dd_mulf(o.N, o.T2);
+  o.det = dd_sub(nT2, dd_mulf(o.T1, o.T1));
   const double scale = nT2.hi < 1.0 ? 1.0 : nT2.hi;
-  if (fabs(det.hi) < 1e-12 * scale) return false;  // road_geometry.cpp:26-29
-  const DD a0 = dd_div(dd_sub(dd_mul(T2, D1), dd_mul(T1, TD)), det);
-  const DD a1 = dd_div(dd_sub(dd_mul(N, TD), dd_mul(T1, D1)), det);
-  DD e = D2;
-  e = dd_sub(e, dd_mul_d(dd_mul(a0, D1), 2.0));
-  e = dd_sub(e, dd_mul_d(dd_mul(a1, TD), 2.0));
-  e = dd_add(e, dd_mul(N, dd_mul(a0, a0)));
-  e = dd_add(e, dd_mul_d(dd_mul(dd_mul(a0, a1), T1), 2.0));
-  e = dd_add(e, dd_mul(dd_mul(a1, a1), T2));
-  out = LineDD{a0, a1, e};
+  return !(fabs(o.det.hi) < 1e-12 * scale);
+}
+__device__ bool line_energy(const Moments& M, double c, double s, DD& e) {
+  LineSums L;
+  if (!line_sums(M, c, s, L)) return false;
+  const DD D1 = M.m[2];
+  DD q = dd_mulf(L.T2, dd_mulf(D1, D1));
+  q = dd_sub(q, dd_mul_d(dd_mulf(dd_mulf(L.T1, D1), L.TD), 2.0));
+  q = dd_add(q, dd_mulf(L.N, dd_mulf(L.TD, L.TD)));
+  e = dd_sub(M.m[8], dd_div(q, L.det));
+  return true;
+}
+__device__ bool line_coef(const Moments& M, double c, double s, DD& a0, DD& a1) {
+  LineSums L;
+  if (!line_sums(M, c, s, L)) return false;
+  const DD D1 = M.m[2];
+  a0 = dd_div(dd_sub(dd_mulf(L.T2, D1), dd_mulf(L.T1, L.TD)), L.det);
+  a1 = dd_div(dd_sub(dd_mulf(L.N, L.TD), dd_mulf(L.T1, D1)), L.det);
   return true;
 }
 
@@ -554,9 +574,9 @@ struct LineFitD {
 // reference's residual form over the masked elements (one grid reduction).
 __device__ bool fit_line_final(FitState& F, const Moments& M, double phi, double c, double s,
                                unsigned long long mask, LineFitD& out) {
-  LineDD L;
-  if (!line_eval(M, c, s, L)) return false;
-  const double a0 = L.a0.hi, a1 = L.a1.hi;
+  DD A0, A1;
+  if (!line_coef(M, c, s, A0, A1)) return false;
+  const double a0 = A0.hi, a1 = A1.hi;
   double acc[1] = {0.0};
   for (int m = 0; m < F.rows; ++m) {
     if (!((mask >> m) & 1ull)) continue;
@@ -591,61 +611,84 @@ __device__ __forceinline__ double g_advance(GState& s, bool br) {
   return s.x2;
 }
 
-// sin/cos of one angle per lane, then broadcast lane `src`'s pair.
-__device__ __forceinline__ void warp_sincos(double x, double& s, double& c) { dd_sincos(x, &s, &c); }
-
-// estimate_roll on moments.  The sin/cos of the next kLevels iterations'
-// possible angles (1 + 2 + 4 + 8 + 16 = 31 nodes of the decision tree) are
-// computed by the warp's lanes in one batch, so the search runs ~5 iterations
-// per double-double sin/cos latency.  All lanes (and CTAs) follow the same
-// decisions.  Returns the final midpoint and its sin/cos.
+// estimate_roll on moments.  The search walks a binary decision tree: from
+// the current state, the next point is fixed (the pending comparison is
+// known) and every later point depends on the comparisons in between.  Each
+// batch evaluates a 63-node subtree (6 iterations) in parallel — thread t of
+// the CTA takes node t (level floor(log2 t), path bits t - 2^level, MSB
+// first) and computes its point's sin/cos and energy — into a shared table;
+// the walk then only compares.  The first batch holds the two initial probes
+// (nodes 0, 1) and the 62 nodes of the five iterations after them.  All
+// threads (and CTAs) follow the same decisions.  Returns the final midpoint
+// and its sin/cos.
 __device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, double tol,
                            double& phi, double& cphi, double& sphi) {
-  constexpr int kLevels = 5;
-  const int lane = threadIdx.x & 31;
+  static_assert(kFitThreads == 64, "the tree batches use 64 threads");
+  FitShared& S = *F.S;
+  const int t = threadIdx.x;
   GState st{lo, hi, hi - kGolden * (hi - lo), lo + kGolden * (hi - lo)};
-  double bs, bc;
-  warp_sincos(lane == 0 ? st.x1 : st.x2, bs, bc);
-  LineDD L;
-  double c = __shfl_sync(0xFFFFFFFFu, bc, 0), s = __shfl_sync(0xFFFFFFFFu, bs, 0);
-  if (!line_eval(M, c, s, L)) return false;
-  DD f1 = L.e;
-  c = __shfl_sync(0xFFFFFFFFu, bc, 1);
-  s = __shfl_sync(0xFFFFFFFFu, bs, 1);
-  if (!line_eval(M, c, s, L)) return false;
-  DD f2 = L.e;
-  int left = 0, node = 0;
-  while (st.b - st.a > tol) {
-    const bool br = dd_lt(f1, f2);
-    if (left == 0) {  // new batch: node 0 is the next point, then the decision tree
-      GState t = st;
-      double x = g_advance(t, br);
-      const int lv = 31 - __clz(lane + 1);  // level of this lane's node
-      const int bits = lane + 1 - (1 << lv);
-      for (int j = lv - 1; j >= 0; --j) x = g_advance(t, ((bits >> j) & 1) != 0);
-      warp_sincos(x, bs, bc);
-      node = 0;
-      left = kLevels;
+  auto eval_node = [&](double x) {
+    double bs, bc;
+    dd_sincos(x, &bs, &bc);
+    DD e{0.0, 0.0};
+    const bool ok = line_energy(M, bc, bs, e);
+    S.g_e[t] = e;
+    S.g_bad[t] = ok ? 0 : 1;
+  };
+  // batch 0: initial probes and the tree below them
+  {
+    double x;
+    if (t < 2) {
+      x = t == 0 ? st.x1 : st.x2;
+    } else {
+      GState g = st;
+      const int lv = 31 - __clz(t);
+      const int bits = t - (1 << lv);
+      x = 0.0;
+      for (int j = lv - 1; j >= 0; --j) x = g_advance(g, ((bits >> j) & 1) != 0);
     }
-    c = __shfl_sync(0xFFFFFFFFu, bc, node);
-    s = __shfl_sync(0xFFFFFFFFu, bs, node);
+    fit_tr(F, 6);
+    eval_node(x);
+    __syncthreads();
+    fit_tr(F, 8);
+  }
+  if (S.g_bad[0] | S.g_bad[1]) return false;
+  DD f1 = S.g_e[0], f2 = S.g_e[1];
+  int node = 1, left = 5;  // the tree below the probes: children of virtual node 1
+  bool br = dd_lt(f1, f2);
+  node = 2 * node + (br ? 1 : 0);
+  while (st.b - st.a > tol) {
+    if (left == 0) {  // new batch from the current state (br known)
+      __syncthreads();  // everyone is done with the previous table
+      GState g = st;
+      double x = g_advance(g, br);
+      const int lv = t == 0 ? 0 : 31 - __clz(t);
+      const int bits = t - (1 << lv);
+      for (int j = lv - 1; j >= 0; --j) x = g_advance(g, ((bits >> j) & 1) != 0);
+      fit_tr(F, 6);
+      eval_node(x);
+      __syncthreads();
+      fit_tr(F, 8);
+      node = 1;
+      left = 6;
+    }
+    if (S.g_bad[node]) return false;  // fit_line throws on this probe
     g_advance(st, br);
     if (br)
       f2 = f1;
     else
       f1 = f2;
-    if (!line_eval(M, c, s, L)) return false;
     if (br)
-      f1 = L.e;
+      f1 = S.g_e[node];
     else
-      f2 = L.e;
+      f2 = S.g_e[node];
     --left;
-    node = 2 * node + (dd_lt(f1, f2) ? 2 : 1);
+    br = dd_lt(f1, f2);
+    node = 2 * node + (br ? 1 : 0);
   }
   phi = 0.5 * (st.a + st.b);
-  warp_sincos(phi, bs, bc);
-  cphi = __shfl_sync(0xFFFFFFFFu, bc, 0);
-  sphi = __shfl_sync(0xFFFFFFFFu, bs, 0);
+  dd_sincos(phi, &sphi, &cphi);
+  __syncthreads();  // the table is free for the next search
   return true;
 }
 
@@ -661,10 +704,7 @@ __device__ void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok)
   double phi = 0.0, c = 1.0, s = 0.0;
   if (R.mode == kFitLine) {
     phi = R.phi;
-    double bs, bc;
-    warp_sincos(phi, bs, bc);
-    c = __shfl_sync(0xFFFFFFFFu, bc, 0);
-    s = __shfl_sync(0xFFFFFFFFu, bs, 0);
+    dd_sincos(phi, &s, &c);
     ok = fit_line_final(F, M, phi, c, s, all, f);
   } else {
     const double lo = R.mode == kEstimateRoll ? R.lo : -R.hi;
