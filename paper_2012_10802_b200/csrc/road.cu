@@ -799,11 +799,15 @@ void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
   }
   if (!req.compact && req.k_host > (long long)kMaxRows * kFitLanes)
     throw InvalidArg("fit: too many observations for the device fit (max 524288)");
-  // Shared memory for the largest input regardless of the request: sizing it
-  // down to the observation cap lets other streams' CTAs share the fit's SMs,
-  // which stretches every grid-wide exchange (measured: -7% frames/s with 8
-  // concurrent pipelines).
-  const int rows_cap = kMaxRows;
+  // Shared memory sized to the request's observation cap (13 rows for the
+  // pipeline's 100 000).  With the moment-based search the fit makes only
+  // four grid-wide exchanges, so sharing its SMs with other streams' CTAs now
+  // pays (measured +1.7 % frames/s over reserving the 64-row maximum; the
+  // opposite held for the per-probe design, profiles/r1_notes.md).
+  const long long kcap = req.compact ? (req.kmax > 0 ? req.kmax : (long long)kMaxRows * kFitLanes)
+                                     : req.k_host;
+  const int rows_cap = int(std::min<long long>(
+      kMaxRows, std::max<long long>(1, (kcap + kFitLanes - 1) / kFitLanes)));
   FitKParams P{};
   P.r = req;
   P.status = ctx->status;
