@@ -228,10 +228,10 @@ __global__ void __launch_bounds__(kAssignThreads)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
   __shared__ int s_cnt, s_nrows, s_rs[8], s_rb[9];
   __shared__ int s_rowcnt[kTileV];
-  __shared__ int4 s_ci[kMaxTileCenters];     // icu, icv, k
-  __shared__ double2 s_cd[kMaxTileCenters];  // cu, cv
-  __shared__ double s_val[kMaxTileCenters];
-  __shared__ short s_row[kTileV][kMaxTileCenters];  // per tile row: candidates reaching it
+  // candidate c: s_cd[2c] = (cu, cv), s_cd[2c+1] = (val, icu | k << 32)
+  __shared__ double2 s_cd[2 * kMaxTileCenters];
+  __shared__ int s_icv[kMaxTileCenters];
+  __shared__ unsigned short s_row[kTileV][kMaxTileCenters];  // per tile row: candidates reaching it
   const int tx = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
   const int u = u0 + tx;
@@ -283,18 +283,19 @@ __global__ void __launch_bounds__(kAssignThreads)
       const int dv = ik.y < v0 ? v0 - ik.y : (ik.y > v0 + kTileV - 1 ? ik.y - (v0 + kTileV - 1) : 0);
       if (du > win || dv > win) continue;
       const int slot = atomicAdd(&s_cnt, 1);
-      s_ci[slot] = ik;
-      s_cd[slot] = rec->cuv;
-      s_val[slot] = rec->val.x;
+      s_cd[2 * slot] = rec->cuv;
+      s_cd[2 * slot + 1] = make_double2(
+          rec->val.x, __longlong_as_double((long long)(uint32_t(ik.x) | (uint64_t(uint32_t(ik.z)) << 32))));
+      s_icv[slot] = ik.y;
     }
   }
   __syncthreads();
   const int nc = s_cnt;
   if (nc <= kMaxTileCenters) {  // distribute the candidates over the rows they reach
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-      const int icv = s_ci[i].y;
+      const int icv = s_icv[i];
       const int r0 = max(icv - win, v0) - v0, r1 = min(icv + win, v0 + kTileV - 1) - v0;
-      for (int r = r0; r <= r1; ++r) s_row[r][atomicAdd(&s_rowcnt[r], 1)] = short(i);
+      for (int r = r0; r <= r1; ++r) s_row[r][atomicAdd(&s_rowcnt[r], 1)] = (unsigned short)i;
     }
   }
   __syncthreads();
@@ -310,16 +311,21 @@ __global__ void __launch_bounds__(kAssignThreads)
     if (nc <= kMaxTileCenters) {
       const double du0 = double(u), dv0 = double(v), sw = a.sw;
       const int nr = s_rowcnt[ty];
+      const unsigned span = 2u * unsigned(win);
       for (int j = 0; j < nr; ++j) {
-        const int i = s_row[ty][j];
-        const int4 ci = s_ci[i];
-        const double2 cd = s_cd[i];
-        const double dval = x - s_val[i];
-        const double du = du0 - cd.x, dv = dv0 - cd.y;
+        const unsigned i = s_row[ty][j];
+        const double2 cuv = s_cd[2 * i];
+        const double2 vk = s_cd[2 * i + 1];
+        const unsigned long long ik = (unsigned long long)__double_as_longlong(vk.y);
+        const int icu = int(uint32_t(ik)), k = int(ik >> 32);
+        const double dval = x - vk.x;
+        const double du = du0 - cuv.x, dv = dv0 - cuv.y;
         const double dist = dval * dval + (du * du + dv * dv) * sw;
-        const bool take = abs(u - ci.x) <= win && (dist < best || (dist == best && ci.z < bk));
+        // |u - icu| <= win, branch-free; lexicographic (dist, k) minimum
+        const bool inw = unsigned(u - icu + win) <= span;
+        const bool take = inw & ((dist < best) | ((dist == best) & (k < bk)));
         best = take ? dist : best;
-        bk = take ? ci.z : bk;
+        bk = take ? k : bk;
       }
     }
     int label = -1;  // -1: outside the image
