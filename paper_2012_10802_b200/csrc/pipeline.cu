@@ -17,6 +17,8 @@
 #include "abi_util.hpp"
 #include "road.cuh"
 #include "seg.cuh"
+#include <cstdlib>
+
 #include "sgm.cuh"
 
 namespace rpdg {
@@ -132,8 +134,20 @@ FrameBuffers alloc_frame(rpd_ctx* ctx, int h, int w, int K) {
 }
 
 // Enqueues the device part of one frame (everything after the upload).
+// Debugging / cost attribution only (RPD_SKIP_STAGES bitmask, results are
+// garbage): 1 = road fits, 2 = SLIC + pooling + detection, 4 = detection,
+// 8 = bootstrap SGM, 16 = PT SGM.
+int skip_stages() {
+  static const int m = [] {
+    const char* e = std::getenv("RPD_SKIP_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const rpd_config& c) {
   cudaStream_t st = ctx->stream;
+  const int skip = skip_stages();
   const long long n = (long long)h * w;
   reset_status(ctx);
   ctx->agg_pass = 0;
@@ -154,13 +168,17 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
     launch_half_image(f.right, h, w, f.hr, st);
     rpd_config boot = c;
     boot.d_max = (c.d_max + 1) / 2;
-    match_pair_dev(ctx, f.hl, f.hr, bh, bw, f.flat, boot, boot.d_max, f.b_d0, f.b_d1, f.b_shifts);
+    if (!(skip & 8))
+      match_pair_dev(ctx, f.hl, f.hr, bh, bw, f.flat, boot, boot.d_max, f.b_d0, f.b_d1,
+                     f.b_shifts);
   } else {
     match_pair_dev(ctx, f.left, f.right, h, w, f.flat, c, c.d_max, f.b_d0, f.b_d1, f.b_shifts);
   }
   record_stage(ctx, 1);
   // pipeline.cpp:66-73 coarse road fit (a0 *= 2 when halved)
-  sample_observations_dev(ctx, f.b_d1, bh, bw, nullptr, kPipelineObsCap, f.obs, kWhereSampleBoot);
+  if (!(skip & 1))
+    sample_observations_dev(ctx, f.b_d1, bh, bw, nullptr, kPipelineObsCap, f.obs,
+                            kWhereSampleBoot);
   FitRequest fr;
   fr.mode = kFitRoad;
   fr.compact = true;
@@ -171,27 +189,41 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   fr.a0_scale = halve ? 2.0 : 1.0;
   fr.where = kWhereFitBoot;
   fr.out = f.coarse;
-  fit_dev(ctx, fr);
+  if (!(skip & 1)) fit_dev(ctx, fr);
   record_stage(ctx, 2);
   // pipeline.cpp:76 PT pass
-  match_pair_dev(ctx, f.left, f.right, h, w, &f.coarse->model, c, c.d_max_pt, f.d0, f.d1,
-                 f.shifts);
+  if (!(skip & 16))
+    match_pair_dev(ctx, f.left, f.right, h, w, &f.coarse->model, c, c.d_max_pt, f.d0, f.d1,
+                   f.shifts);
   record_stage(ctx, 3);
   // pipeline.cpp:81-86 refit
-  sample_observations_dev(ctx, f.d1, h, w, nullptr, kPipelineObsCap, f.obs, kWhereSamplePt);
+  if (!(skip & 1))
+    sample_observations_dev(ctx, f.d1, h, w, nullptr, kPipelineObsCap, f.obs, kWhereSamplePt);
   fr.a0_scale = 1.0;
   fr.where = kWhereFitPt;
   fr.out = f.fit;
-  fit_dev(ctx, fr);
+  if (!(skip & 1)) fit_dev(ctx, fr);
   record_stage(ctx, 4);
   // pipeline.cpp:89-91 disparity transformation
   RPD_CK(cudaMemsetAsync(f.clamped, 0, sizeof(unsigned long long), st));
   transform_disparity_dev(f.d1, h, w, &f.fit->model, c.delta_dt, f.d2, f.clamped, st);
   record_stage(ctx, 5);
   // pipeline.cpp:94-96 SLIC + pooling
+  if (skip & 2) {
+    f.sp.labels = f.labels;  // valid device buffers for the fetch
+    f.sp.count = f.n_potholes;
+    f.sp.centers = nullptr;
+    record_stage(ctx, 6);
+    record_stage(ctx, 7);
+    return;
+  }
   f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations);
   pool_superpixels_dev(ctx, f.d2, f.sp.labels, h, w, f.sp.k_seeds, f.d3);
   record_stage(ctx, 6);
+  if (skip & 4) {
+    record_stage(ctx, 7);
+    return;
+  }
   // pipeline.cpp:99-103 histogram, threshold, labelling
   const HistDev hd = build_histogram_dev(ctx, f.d2, h, w, c.hist_bin_width, c.tau_diag);
   find_threshold_dev(ctx, hd, c.hist_bin_width, c.delta_pd, c.tau_diag, f.thr,

@@ -221,10 +221,13 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 // are left for the fallback kernel, which adds their sums itself.
 constexpr int kTileU = 32, kTileV = 16, kMaxTileCenters = 384;
 constexpr int kAssignThreads = 256;
+#ifndef RPD_ASSIGN_MINB
+#define RPD_ASSIGN_MINB 6  // resident CTAs per SM the register budget targets
+#endif
 constexpr int kRowsPerWarp = kTileV / (kAssignThreads / 32);  // a warp owns rows w, w+8
 
 template <bool SUMS>
-__global__ void __launch_bounds__(kAssignThreads)
+__global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
   __shared__ int s_cnt, s_nrows, s_rs[8], s_rb[9];
   __shared__ int s_rowcnt[kTileV];
