@@ -28,7 +28,10 @@ namespace rpdg {
 namespace {
 
 constexpr int kNC = 32;      // chains per CTA
-constexpr int kDepth = 3;    // input ring depth (stages)
+#ifndef RPD_AGG_DEPTH
+#define RPD_AGG_DEPTH 3
+#endif
+constexpr int kDepth = RPD_AGG_DEPTH;  // input ring depth (stages)
 #ifndef RPD_AGG_RBASE
 #define RPD_AGG_RBASE 4      // steps per stage for <= 32 words per pixel
 #endif
@@ -43,6 +46,10 @@ constexpr int kDepth = 3;    // input ring depth (stages)
 #endif
 constexpr int kOutDepth = RPD_AGG_OUTDEPTH;
 constexpr int kRBase = RPD_AGG_RBASE;
+#ifndef RPD_AGG_RBASE_G1
+#define RPD_AGG_RBASE_G1 4  // steps per stage of the one-lane-per-chain kernels
+#endif
+constexpr int kRBaseG1 = RPD_AGG_RBASE_G1;
 constexpr int kStepUnroll = RPD_AGG_UNROLL;
 constexpr uint32_t kInf2 = 0x7FFF7FFFu;
 
@@ -143,7 +150,8 @@ __device__ __forceinline__ uint32_t min_pairs(const uint32_t (&x)[NPL]) {
 template <int WPL, int G>
 struct Geo {
   static constexpr int WPP = WPL * G;                  // words per pixel
-  static constexpr int R = WPP <= 32 ? kRBase : (WPP <= 64 ? (kRBase + 1) / 2 : 1);
+  static constexpr int RB = G == 1 ? kRBaseG1 : kRBase;
+  static constexpr int R = WPP <= 32 ? RB : (WPP <= 64 ? (RB + 1) / 2 : 1);
   static constexpr int ROW = kNC * WPP;                // words of one step (vert / diag)
   static constexpr int CWF = ROW < 256 ? ROW : 256;    // full chunk width
   static constexpr int NCH = (ROW + 255) / 256;        // chunks per row
