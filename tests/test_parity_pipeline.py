@@ -89,6 +89,48 @@ def test_fit_road_matches_oracle(gpu, oracle):
     assert m.phi == mo.phi
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_fit_road_moments_match_oracle(gpu, oracle, seed):
+    """Moment-based search + masked trimming: same angles, counts and values
+    as the oracle on varied inputs (integer pixel coordinates like the
+    pipeline's compact observations for even seeds, real-valued ones for odd
+    seeds), several noise levels and outlier fractions."""
+    rng = np.random.default_rng(300 + seed)
+    k = int(rng.integers(3000, 120000))
+    if seed % 2 == 0:
+        u = rng.integers(0, 1312, k).astype(np.float64)
+        v = rng.integers(0, 800, k).astype(np.float64)
+    else:
+        u = rng.uniform(0.0, 1311.0, k)
+        v = rng.uniform(0.0, 799.0, k)
+    phi = rng.uniform(-10.0, 10.0) * DEG
+    a0, a1 = rng.uniform(5.0, 40.0), rng.uniform(0.02, 0.2)
+    d = a0 + a1 * (v * math.cos(phi) - u * math.sin(phi)) + rng.normal(0, rng.uniform(0.01, 1.0), k)
+    nout = int(rng.uniform(0.0, 0.1) * k)
+    d[rng.choice(k, nout, replace=False)] -= rng.uniform(2.0, 8.0)
+    d = d.astype(np.float32).astype(np.float64)
+    g = gpu.fit_road(d, u, v, 0.261799, 1e-4)
+    o = oracle.fit_road(d, u, v, 0.261799, 1e-4)
+    assert g.model.phi == o.model.phi
+    assert g.used == o.used
+    assert rel_close(g.model.a0, o.model.a0, 1e-12)
+    assert rel_close(g.model.a1, o.model.a1, 1e-12)
+    assert rel_close(g.e0min, o.e0min, 1e-10)
+    assert abs(g.model.phi - phi) < 0.05 * DEG + 1e-4
+
+
+def test_fit_degenerate_search_raises(gpu, oracle):
+    """Every probe singular (all observations on one point): both raise."""
+    d = np.full(500, 12.0)
+    u = np.full(500, 40.0)
+    v = np.full(500, 30.0)
+    for ctx in (gpu, oracle):
+        with pytest.raises(DegenerateError):
+            ctx.estimate_roll(d, u, v, -0.2, 0.2, 1e-4)
+        with pytest.raises(DegenerateError):
+            ctx.fit_road(d, u, v, 0.2, 1e-4)
+
+
 def test_transform_disparity_bit_exact(gpu, oracle):
     rng = np.random.default_rng(5)
     d1 = rng.uniform(0, 80, (123, 157)).astype(np.float32)
