@@ -58,17 +58,25 @@ __device__ __forceinline__ bool hist_vector(const float* __restrict__ d2, int w,
 // meta: [0] n, [1] total, [2] excluded outside band, [3] lo key, [4] hi key
 __global__ void k_hist_range(const float* __restrict__ d2, int h, int w,
                              long long* __restrict__ meta) {
+  // rows strided over gridDim.y: one atomic triple per block (the three
+  // counters are single hot addresses)
   const int u = blockIdx.x * blockDim.x + threadIdx.x + 1;
-  const int v = blockIdx.y + 1;
-  double x = 0, y = 0;
-  const bool ok = u + 1 < w && v + 1 < h && hist_vector(d2, w, u, v, x, y);
-  const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
-  long long lo = ok ? min(ordered(x), ordered(y)) : 0x7FFFFFFFFFFFFFFFll;
-  long long hi = ok ? max(ordered(x), ordered(y)) : (long long)0x8000000000000000ull;
+  long long lo = 0x7FFFFFFFFFFFFFFFll, hi = (long long)0x8000000000000000ull;
+  unsigned long long cnt = 0;
+  for (int v = blockIdx.y + 1; v + 1 < h; v += gridDim.y) {
+    double x = 0, y = 0;
+    const bool ok = u + 1 < w && hist_vector(d2, w, u, v, x, y);
+    if (ok) {
+      lo = min(lo, min(ordered(x), ordered(y)));
+      hi = max(hi, max(ordered(x), ordered(y)));
+      ++cnt;
+    }
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, off));
     hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, off));
+    cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
   }
   __shared__ long long s_lo[32], s_hi[32];
   __shared__ unsigned long long s_cnt[32];
@@ -76,7 +84,7 @@ __global__ void k_hist_range(const float* __restrict__ d2, int h, int w,
   if (lane == 0) {
     s_lo[warp] = lo;
     s_hi[warp] = hi;
-    s_cnt[warp] = __popc(bal);
+    s_cnt[warp] = cnt;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -124,31 +132,33 @@ __global__ void k_hist_bin(const float* __restrict__ d2, int h, int w, double bw
                            const double* __restrict__ origin, long long* __restrict__ meta,
                            long long* __restrict__ band, int half) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x + 1;
-  const int v = blockIdx.y + 1;
   const long long n = meta[0];
-  double x = 0, y = 0;
-  bool ok = n > 0 && u + 1 < w && v + 1 < h && hist_vector(d2, w, u, v, x, y);
-  bool outside = false;
-  long long slot = -1;
-  if (ok) {
-    const double o = *origin;
-    long long i = (long long)floor((x - o) / bw), j = (long long)floor((y - o) / bw);
-    i = i < n - 1 ? i : n - 1;
-    j = j < n - 1 ? j : n - 1;
-    const long long dj = j - i;
-    if (dj < -half || dj > half)
-      outside = true;
-    else
-      slot = i * (2 * half + 1) + (dj + half);
+  const double o = *origin;
+  unsigned outside_cnt = 0;
+  for (int v = blockIdx.y + 1; v + 1 < h; v += gridDim.y) {
+    double x = 0, y = 0;
+    const bool ok = n > 0 && u + 1 < w && hist_vector(d2, w, u, v, x, y);
+    long long slot = -1;
+    if (ok) {
+      long long i = (long long)floor((x - o) / bw), j = (long long)floor((y - o) / bw);
+      i = i < n - 1 ? i : n - 1;
+      j = j < n - 1 ? j : n - 1;
+      const long long dj = j - i;
+      if (dj < -half || dj > half)
+        ++outside_cnt;
+      else
+        slot = i * (2 * half + 1) + (dj + half);
+    }
+    // neighbouring pixels mostly share a bin: one atomic per distinct bin per warp
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, slot);
+    if (slot >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&band[slot]),
+                (unsigned long long)__popc(peers));
   }
-  // neighbouring pixels mostly share a bin: one atomic per distinct bin per warp
-  const unsigned peers = __match_any_sync(0xFFFFFFFFu, slot);
-  if (slot >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&band[slot]),
-              (unsigned long long)__popc(peers));
-  const unsigned bal = __ballot_sync(0xFFFFFFFFu, outside);
-  if ((threadIdx.x & 31) == 0 && bal)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&meta[2]), (unsigned long long)__popc(bal));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) outside_cnt += __shfl_xor_sync(0xFFFFFFFFu, outside_cnt, off);
+  if ((threadIdx.x & 31) == 0 && outside_cnt)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&meta[2]), (unsigned long long)outside_cnt);
 }
 
 // Full n x n histogram -> band storage (ABI path), band = n - 1.
@@ -505,7 +515,9 @@ static void hist_range(rpd_ctx* ctx, const HistDev& hd, const float* d2, int h, 
   k_hist_init<<<1, 1, 0, st>>>(hd.meta);
   RPD_LAUNCH_CHECK();
   if (h >= 3 && w >= 3) {
-    k_hist_range<<<dim3(cdiv(w - 2, 128), h - 2), 128, 0, st>>>(d2, h, w, hd.meta);
+    const int gx = cdiv(w - 2, 128);
+    const int gy = std::max(1, std::min(h - 2, cdiv(ctx->sm_count * 8, gx)));
+    k_hist_range<<<dim3(gx, gy), 128, 0, st>>>(d2, h, w, hd.meta);
     RPD_LAUNCH_CHECK();
   }
   k_hist_setup<<<1, 1, 0, st>>>(hd.meta, bw, hd.origin, hd.cap_rows, ctx->status, where);
@@ -518,6 +530,8 @@ static void hist_bin(rpd_ctx* ctx, const HistDev& hd, const float* d2, int h, in
   k_hist_clear<<<ctx->sm_count * 4, 256, 0, st>>>(hd.bins, hd.meta, stride);
   RPD_LAUNCH_CHECK();
   if (h >= 3 && w >= 3) {
+    // one row per block (the band atomics are spread over bins; the single
+    // outside counter is aggregated per warp)
     k_hist_bin<<<dim3(cdiv(w - 2, 128), h - 2), 128, 0, st>>>(d2, h, w, bw, hd.origin, hd.meta,
                                                               hd.bins, hd.half);
     RPD_LAUNCH_CHECK();
