@@ -631,6 +631,7 @@ __global__ void k_wta(const __grid_constant__ WtaArgs a) {
 constexpr int kWtaPx = 128;
 constexpr int kWtaMaxWords = 36;  // lw <= 144 bytes (L <= 144)
 
+template <int P>  // path count (4 or 8): fully unrolled sums
 __global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ WtaArgs a) {
   extern __shared__ uint32_t sums[];  // [pixel][2*nw + 1] u16x2 pairs (odd stride: no conflicts)
   const int nw = a.lw / 4;
@@ -643,22 +644,21 @@ __global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ Wt
   // 16-byte loads: 8 paths x 16 B in flight per thread (tile bases are
   // 16-byte aligned: pitch and u0 * lw are multiples of 16)
   const int nvec = tile_words >> 2;
+  const float inv_nw = 1.0f / float(nw);
   for (int i4 = threadIdx.x; i4 < nvec; i4 += kWtaPx) {
-    uint4 x[8];
+    uint4 x[P];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < a.paths) x[r] = __ldg(reinterpret_cast<const uint4*>(a.path[r] + base) + i4);
-    int px = (4 * i4) / nw, j = 4 * i4 - px * nw;
+    for (int r = 0; r < P; ++r) x[r] = __ldg(reinterpret_cast<const uint4*>(a.path[r] + base) + i4);
+    // (4 i4) / nw exactly: (4 i4 + 0.5) / nw is >= 1/(2 nw) away from an integer
+    int px = int(__fmul_rn(float(4 * i4) + 0.5f, inv_nw)), j = 4 * i4 - px * nw;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint32_t s01 = 0, s23 = 0;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (r < a.paths) {
-          const uint32_t xe = e == 0 ? x[r].x : (e == 1 ? x[r].y : (e == 2 ? x[r].z : x[r].w));
-          s01 += __byte_perm(xe, 0u, 0x4140);
-          s23 += __byte_perm(xe, 0u, 0x4342);
-        }
+      for (int r = 0; r < P; ++r) {
+        const uint32_t xe = e == 0 ? x[r].x : (e == 1 ? x[r].y : (e == 2 ? x[r].z : x[r].w));
+        s01 += __byte_perm(xe, 0u, 0x4140);
+        s23 += __byte_perm(xe, 0u, 0x4342);
       }
       sums[px * stride + 2 * j] = s01;
       sums[px * stride + 2 * j + 1] = s23;
@@ -671,12 +671,10 @@ __global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ Wt
   for (int i = 4 * nvec + threadIdx.x; i < tile_words; i += kWtaPx) {
     uint32_t s01 = 0, s23 = 0;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (r < a.paths) {
-        const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a.path[r] + base) + i);
-        s01 += __byte_perm(x, 0u, 0x4140);
-        s23 += __byte_perm(x, 0u, 0x4342);
-      }
+    for (int r = 0; r < P; ++r) {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(a.path[r] + base) + i);
+      s01 += __byte_perm(x, 0u, 0x4140);
+      s23 += __byte_perm(x, 0u, 0x4342);
     }
     const int px = i / nw, j = i - px * nw;
     sums[px * stride + 2 * j] = s01;
@@ -686,21 +684,48 @@ __global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ Wt
   const int t = threadIdx.x;
   if (t >= npx) return;
   const long long p = (long long)row * a.w + u0 + t;
-  uint32_t minv = 0xFFFFFFFFu, last = 0, sbm1 = 0, sbp1 = 0;
+  uint32_t minv = 0xFFFFFFFFu, sbm1 = 0, sbp1 = 0;
   int best = -2, cnt = 0;
-  const uint32_t* my = sums + t * stride;
-  for (int j = 0; j < nw; ++j) {
-    if (4 * j >= a.levels) break;
-    const uint32_t s01 = my[2 * j], s23 = my[2 * j + 1];
-    const uint32_t sv[4] = {s01 & 0xFFFFu, s01 >> 16, s23 & 0xFFFFu, s23 >> 16};
+  const uint32_t* my = sums + t * stride;  // my[q] = exact u16 sums of levels (2q, 2q+1)
+  const int L = a.levels;
+  if (a.dump) {  // parity dumps: the reference's sequential scan, level by level
+    uint32_t last = 0;
+    for (int j = 0; j < nw; ++j) {
+      if (4 * j >= L) break;
+      const uint32_t s01 = my[2 * j], s23 = my[2 * j + 1];
+      const uint32_t sv[4] = {s01 & 0xFFFFu, s01 >> 16, s23 & 0xFFFFu, s23 >> 16};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int d = 4 * j + q;
-      if (d < a.levels) {
-        wta_visit(sv[q], d, minv, best, cnt, last, sbm1, sbp1);
-        if (a.dump) a.dump[p * a.levels + d] = float(sv[q]);
+      for (int q = 0; q < 4; ++q) {
+        const int d = 4 * j + q;
+        if (d < L) {
+          wta_visit(sv[q], d, minv, best, cnt, last, sbm1, sbp1);
+          a.dump[p * L + d] = float(sv[q]);
+        }
       }
     }
+  } else {
+    // Same result as the sequential scan (select_disparity, sgm.cpp:123-153):
+    // minv = minimum, best = its FIRST level, cnt = its multiplicity,
+    // sbm1 / sbp1 = the sums at best -+ 1 (0 / irrelevant at the ends).
+    const int np = (L + 1) >> 1;
+    const uint32_t hpad = (L & 1) ? 0xFFFF0000u : 0u;  // invalid high half of the last pair
+    uint32_t m2 = 0xFFFFFFFFu;
+    for (int q = 0; q < np; q += 2) {
+      const uint32_t v0 = my[q] | (q == np - 1 ? hpad : 0u);
+      const uint32_t v1 = q + 1 < np ? (my[q + 1] | (q + 1 == np - 1 ? hpad : 0u)) : 0xFFFFFFFFu;
+      m2 = __vimin3_u16x2(m2, v0, v1);
+    }
+    minv = min(m2 & 0xFFFFu, m2 >> 16);
+    best = -1;
+    for (int q = 0; q < np; ++q) {
+      const uint32_t v = my[q] | (q == np - 1 ? hpad : 0u);
+      const bool lo = (v & 0xFFFFu) == minv, hi = (v >> 16) == minv;
+      cnt += int(lo) + int(hi);
+      best = best >= 0 ? best : (lo ? 2 * q : (hi ? 2 * q + 1 : -1));
+    }
+    auto level = [&](int d) { return (my[d >> 1] >> (16 * (d & 1))) & 0xFFFFu; };
+    sbm1 = best > 0 ? level(best - 1) : 0u;
+    sbp1 = best + 1 < L ? level(best + 1) : 0u;
   }
   const int near = (best + 1 < a.levels && sbp1 == minv) ? 1 : 0;
   float r;
@@ -1031,7 +1056,10 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
       wa.dump = dump ? (vol == 0 ? dump->agg_left : dump->agg_right) : nullptr;
       if (L.lw / 4 <= kWtaMaxWords) {
         const int smem = kWtaPx * (2 * (L.lw / 4) + 1) * 4;
-        k_wta_tiled<<<dim3(cdiv(w, kWtaPx), h), kWtaPx, smem, st>>>(wa);
+        if (wa.paths == 8)
+          k_wta_tiled<8><<<dim3(cdiv(w, kWtaPx), h), kWtaPx, smem, st>>>(wa);
+        else
+          k_wta_tiled<4><<<dim3(cdiv(w, kWtaPx), h), kWtaPx, smem, st>>>(wa);
       } else {
         k_wta<<<cdiv(npix, 128), 128, 0, st>>>(wa);
       }
