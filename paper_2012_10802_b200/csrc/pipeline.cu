@@ -153,8 +153,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   ctx->agg_pass = 0;
   record_stage(ctx, 0);
   if (u8) {
-    launch_u8_to_f32(f.left8, f.left, n, st);
-    launch_u8_to_f32(f.right8, f.right, n, st);
+    launch_u8_to_f32(f.left8, f.left, n, st, f.right8, f.right);
   }
   k_flat_model<<<1, 1, 0, st>>>(f.flat);
   RPD_LAUNCH_CHECK();
@@ -164,8 +163,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   if (halve) {
     bh = h / 2;
     bw = w / 2;
-    launch_half_image(f.left, h, w, f.hl, st);
-    launch_half_image(f.right, h, w, f.hr, st);
+    launch_half_image(f.left, h, w, f.hl, st, f.right, f.hr);
     rpd_config boot = c;
     boot.d_max = (c.d_max + 1) / 2;
     if (!(skip & 8))

@@ -71,21 +71,28 @@ bool sgm_fast_path_ok(float l1, float l2, int window) {
 }
 
 // ------------------------------------------------------- image kernels ----
-__global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ out,
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ in0, float* __restrict__ out0,
+                            const uint8_t* __restrict__ in1, float* __restrict__ out1,
                             long long n) {
+  const uint8_t* __restrict__ in = blockIdx.y ? in1 : in0;  // blockIdx.y: which image
+  float* __restrict__ out = blockIdx.y ? out1 : out0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     out[i] = float(in[i]);
 }
 
-void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st) {
+void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st,
+                      const uint8_t* in1, float* out1) {
   const int blocks = std::min<long long>((n + 255) / 256, 148 * 16);
-  k_u8_to_f32<<<std::max(blocks, 1), 256, 0, st>>>(in, out, n);
+  k_u8_to_f32<<<dim3(std::max(blocks, 1), in1 ? 2 : 1), 256, 0, st>>>(in, out, in1, out1, n);
   RPD_LAUNCH_CHECK();
 }
 
 // half_image, pipeline.cpp:25-34: 0.25f * (((a + b) + c) + d)
-__global__ void k_half(const float* __restrict__ in, int h, int w, float* __restrict__ out) {
+__global__ void k_half(const float* __restrict__ in0, const float* __restrict__ in1, int h, int w,
+                       float* __restrict__ out0, float* __restrict__ out1) {
+  const float* __restrict__ in = blockIdx.z ? in1 : in0;  // blockIdx.z: which image
+  float* __restrict__ out = blockIdx.z ? out1 : out0;
   const int hh = h / 2, hw = w / 2;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
@@ -95,9 +102,10 @@ __global__ void k_half(const float* __restrict__ in, int h, int w, float* __rest
   out[size_t(v) * hw + u] = 0.25f * (r0[0] + r0[1] + r1[0] + r1[1]);
 }
 
-void launch_half_image(const float* in, int h, int w, float* out, cudaStream_t st) {
+void launch_half_image(const float* in, int h, int w, float* out, cudaStream_t st,
+                       const float* in1, float* out1) {
   if (h / 2 == 0 || w / 2 == 0) return;
-  k_half<<<dim3(cdiv(w / 2, 128), h / 2), 128, 0, st>>>(in, h, w, out);
+  k_half<<<dim3(cdiv(w / 2, 128), h / 2, in1 ? 2 : 1), 128, 0, st>>>(in, in1, h, w, out, out1);
   RPD_LAUNCH_CHECK();
 }
 
@@ -169,7 +177,11 @@ void launch_restore(const float* d0, const double* shifts, int h, int w, float* 
 // centre skipped, coordinates clamped.
 template <int R>
 __global__ void __launch_bounds__(128)
-    k_census(const float* __restrict__ img, int h, int w, uint64_t* __restrict__ out) {
+    k_census(const float* __restrict__ img0, const float* __restrict__ img1, int h, int w,
+             uint64_t* __restrict__ out0, uint64_t* __restrict__ out1) {
+  // blockIdx.z selects the image (both census transforms in one launch)
+  const float* __restrict__ img = blockIdx.z ? img1 : img0;
+  uint64_t* __restrict__ out = blockIdx.z ? out1 : out0;
   // the (2R+1) x (128+2R) window of this 128-pixel row segment, staged with
   // clamped coordinates (== the reference's clamped reads)
   constexpr int TW = 128 + 2 * R;
@@ -197,15 +209,20 @@ __global__ void __launch_bounds__(128)
   out[size_t(v) * w + u] = bits;
 }
 
-void launch_census(const float* img, int h, int w, int window, uint64_t* out, cudaStream_t st) {
-  const dim3 grid(cdiv(w, 128), h);
+void launch_census2(const float* img0, const float* img1, int h, int w, int window,
+                    uint64_t* out0, uint64_t* out1, cudaStream_t st) {
+  const dim3 grid(cdiv(w, 128), h, img1 ? 2 : 1);
   switch (window) {
-    case 3: k_census<1><<<grid, 128, 0, st>>>(img, h, w, out); break;
-    case 5: k_census<2><<<grid, 128, 0, st>>>(img, h, w, out); break;
-    case 7: k_census<3><<<grid, 128, 0, st>>>(img, h, w, out); break;
+    case 3: k_census<1><<<grid, 128, 0, st>>>(img0, img1, h, w, out0, out1); break;
+    case 5: k_census<2><<<grid, 128, 0, st>>>(img0, img1, h, w, out0, out1); break;
+    case 7: k_census<3><<<grid, 128, 0, st>>>(img0, img1, h, w, out0, out1); break;
     default: throw InvalidArg("census_cost_volume: window must be odd");
   }
   RPD_LAUNCH_CHECK();
+}
+
+void launch_census(const float* img, int h, int w, int window, uint64_t* out, cudaStream_t st) {
+  launch_census2(img, nullptr, h, w, window, out, nullptr, st);
 }
 
 // census_cost_volume, sgm.cpp:38-68, float output in the reference layout.
@@ -289,7 +306,10 @@ __global__ void __launch_bounds__(256)
     const uint8_t* ovd = s_ov + (u - d0);
     const CW* cld = s_cl + (u + d0);
     uint32_t wl, wr;
-    if (d0 + 3 < levels) {  // full word
+    if (d0 >= levels) {  // padding word
+      wl = 0xFFFFFFFFu;
+      wr = 0xFFFFFFFFu;
+    } else if (d0 + 3 < levels) {  // full word
       uint32_t cL[4], cR[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -946,8 +966,7 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
   launch_warp_right(right, shifts, h, w, warped, iv, st);
   uint64_t* cl = ctx->ws.get<uint64_t>("mp_census_l", npix);
   uint64_t* cr = ctx->ws.get<uint64_t>("mp_census_r", npix);
-  launch_census(left, h, w, window, cl, st);
-  launch_census(warped, h, w, window, cr, st);
+  launch_census2(left, warped, h, w, window, cl, cr, st);
   float* dl = ctx->ws.get<float>("mp_disp_l", npix);
   float* dr = ctx->ws.get<float>("mp_disp_r", npix);
   const dim3 rowgrid(cdiv(w, 128), h);

@@ -41,8 +41,10 @@ struct MatchDump {
 };
 
 // ---------------------------------------------------------------- kernels --
-void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st);
-void launch_half_image(const float* in, int h, int w, float* out, cudaStream_t st);
+void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st,
+                      const uint8_t* in1 = nullptr, float* out1 = nullptr);
+void launch_half_image(const float* in, int h, int w, float* out, cudaStream_t st,
+                       const float* in1 = nullptr, float* out1 = nullptr);
 void launch_row_shifts(const DevModel* model, int h, int w, double delta_pt, double* shifts,
                        cudaStream_t st);
 void launch_warp_right(const float* right, const double* shifts, int h, int w, float* out,
@@ -50,6 +52,8 @@ void launch_warp_right(const float* right, const double* shifts, int h, int w, f
 void launch_restore(const float* d0, const double* shifts, int h, int w, float* d1,
                     cudaStream_t st);
 void launch_census(const float* img, int h, int w, int window, uint64_t* out, cudaStream_t st);
+void launch_census2(const float* img0, const float* img1, int h, int w, int window,
+                    uint64_t* out0, uint64_t* out1, cudaStream_t st);
 // Float cost volume in the reference layout (census_cost_volume ABI).
 void launch_cost_f32(const uint64_t* cl, const uint64_t* cr, const uint8_t* in_view, int h, int w,
                      int levels, int window, float* costs, cudaStream_t st);
