@@ -292,6 +292,38 @@ rpd_status rpd_detect_potholes(rpd_ctx* ctx, const float* d3, const int32_t* sp_
                                int border_margin, int min_superpixels, int connectivity,
                                int32_t* out);
 
+/* ---- evaluation (evaluation.hpp) — SURVEY.md §8(f) row 1 ----------------- */
+typedef struct rpd_confusion {
+  int64_t n_tp, n_fp, n_fn, n_tn;
+} rpd_confusion;
+
+typedef struct rpd_pixel_report {
+  rpd_confusion counts;
+  double precision, recall, accuracy, fscore;
+  int32_t degenerate_precision; /* 0/0, reported as 0 */
+  int32_t degenerate_recall;
+} rpd_pixel_report;
+
+typedef struct rpd_instance_report {
+  int32_t correct, incorrect, misdetection;
+} rpd_instance_report;
+
+/* pep, evaluation.hpp:14-27: percentage of pixels valid in both maps with
+ * |est - gt| > eps.  RPD_EDEGENERATE when no pixel is valid in both. */
+rpd_status rpd_pep(rpd_ctx* ctx, const float* est, const float* gt, int h, int w, double eps,
+                   double* out);
+/* rmse, evaluation.hpp:29-42 (same validity rule and failure). */
+rpd_status rpd_rmse(rpd_ctx* ctx, const float* est, const float* gt, int h, int w, double* out);
+/* fscore, evaluation.hpp:63-66 (host arithmetic, no context). */
+double rpd_fscore(double precision, double recall);
+/* pixel_metrics, evaluation.hpp:69-89: nonzero = pothole in both maps. */
+rpd_status rpd_pixel_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t* gt_mask, int h,
+                             int w, rpd_pixel_report* out);
+/* instance_metrics, evaluation.hpp:97-149: greedy one-to-one matching by
+ * descending IoU (ties: lower prediction, then lower truth id). */
+rpd_status rpd_instance_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t* gt_instances,
+                                int h, int w, double iou_min, rpd_instance_report* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1483,4 +1483,118 @@ rpd_status rpd_detect_potholes(rpd_ctx* ctx, const float* d3, const int32_t* sp_
   });
 }
 
+// ---- evaluation.hpp:14-149, restated sequentially (raster order) ----------
+rpd_status rpd_pep(rpd_ctx* ctx, const float* est, const float* gt, int h, int w, double eps,
+                   double* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    long q = 0, bad = 0;
+    for (long i = 0; i < long(h) * w; ++i) {
+      if (!valid(est[i]) || !valid(gt[i])) continue;
+      ++q;
+      if (std::abs(static_cast<double>(est[i]) - gt[i]) > eps) ++bad;
+    }
+    if (q == 0) throw Degenerate("pep: no overlapping valid pixels");
+    *out = 100.0 * static_cast<double>(bad) / static_cast<double>(q);
+  });
+}
+
+rpd_status rpd_rmse(rpd_ctx* ctx, const float* est, const float* gt, int h, int w, double* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    long q = 0;
+    double sum = 0.0;
+    for (long i = 0; i < long(h) * w; ++i) {
+      if (!valid(est[i]) || !valid(gt[i])) continue;
+      ++q;
+      const double e = static_cast<double>(est[i]) - gt[i];
+      sum += e * e;
+    }
+    if (q == 0) throw Degenerate("rmse: no overlapping valid pixels");
+    *out = std::sqrt(sum / static_cast<double>(q));
+  });
+}
+
+double rpd_fscore(double precision, double recall) {
+  const double s = precision + recall;
+  return s > 0 ? 2.0 * precision * recall / s : 0.0;
+}
+
+rpd_status rpd_pixel_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t* gt_mask, int h,
+                             int w, rpd_pixel_report* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    rpd_pixel_report m{};
+    for (long i = 0; i < long(h) * w; ++i) {
+      const bool p = pred[i] != 0, g = gt_mask[i] != 0;
+      if (p && g) ++m.counts.n_tp;
+      else if (p) ++m.counts.n_fp;
+      else if (g) ++m.counts.n_fn;
+      else ++m.counts.n_tn;
+    }
+    const rpd_confusion& c = m.counts;
+    const long total = long(c.n_tp + c.n_fp + c.n_fn + c.n_tn);
+    m.degenerate_precision = c.n_tp + c.n_fp == 0;
+    m.degenerate_recall = c.n_tp + c.n_fn == 0;
+    m.precision = m.degenerate_precision ? 0.0 : static_cast<double>(c.n_tp) / double(c.n_tp + c.n_fp);
+    m.recall = m.degenerate_recall ? 0.0 : static_cast<double>(c.n_tp) / double(c.n_tp + c.n_fn);
+    m.accuracy = total > 0 ? static_cast<double>(c.n_tp + c.n_tn) / double(total) : 0.0;
+    m.fscore = rpd_fscore(m.precision, m.recall);
+    *out = m;
+  });
+}
+
+rpd_status rpd_instance_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t* gt, int h, int w,
+                                double iou_min, rpd_instance_report* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    const long n = long(h) * w;
+    int np = 0, ng = 0;
+    for (long i = 0; i < n; ++i) {
+      np = std::max(np, pred[i]);
+      ng = std::max(ng, gt[i]);
+    }
+    std::vector<long> area_p(size_t(np) + 1, 0), area_g(size_t(ng) + 1, 0);
+    std::vector<std::vector<long>> inter(size_t(np) + 1, std::vector<long>(size_t(ng) + 1, 0));
+    for (long i = 0; i < n; ++i) {
+      const int p = pred[i], g = gt[i];
+      if (p > 0) ++area_p[size_t(p)];
+      if (g > 0) ++area_g[size_t(g)];
+      if (p > 0 && g > 0) ++inter[size_t(p)][size_t(g)];
+    }
+    struct Pair {
+      double iou;
+      int p, g;
+    };
+    std::vector<Pair> pairs;
+    for (int p = 1; p <= np; ++p)
+      for (int g = 1; g <= ng; ++g) {
+        const long i = inter[size_t(p)][size_t(g)];
+        if (i == 0) continue;
+        pairs.push_back({static_cast<double>(i) /
+                             static_cast<double>(area_p[size_t(p)] + area_g[size_t(g)] - i),
+                         p, g});
+      }
+    std::sort(pairs.begin(), pairs.end(), [](const Pair& a, const Pair& b) {
+      if (a.iou != b.iou) return a.iou > b.iou;
+      if (a.p != b.p) return a.p < b.p;
+      return a.g < b.g;
+    });
+    std::vector<char> used_p(size_t(np) + 1, 0), used_g(size_t(ng) + 1, 0);
+    rpd_instance_report rep{0, 0, 0};
+    for (const auto& pr : pairs) {
+      if (pr.iou < iou_min) break;
+      if (used_p[size_t(pr.p)] || used_g[size_t(pr.g)]) continue;
+      used_p[size_t(pr.p)] = 1;
+      used_g[size_t(pr.g)] = 1;
+      ++rep.correct;
+    }
+    for (int p = 1; p <= np; ++p)
+      if (!used_p[size_t(p)]) ++rep.incorrect;
+    for (int g = 1; g <= ng; ++g)
+      if (!used_g[size_t(g)]) ++rep.misdetection;
+    *out = rep;
+  });
+}
+
 }  // extern "C"

@@ -103,6 +103,26 @@ class Threshold(C.Structure):
                 ("degenerate", C.c_int32)]
 
 
+class Confusion(C.Structure):
+    _fields_ = [("n_tp", C.c_int64), ("n_fp", C.c_int64), ("n_fn", C.c_int64),
+                ("n_tn", C.c_int64)]
+
+    def total(self) -> int:
+        return self.n_tp + self.n_fp + self.n_fn + self.n_tn
+
+
+class PixelReport(C.Structure):
+    """PixelMetrics, evaluation.hpp:51-59."""
+    _fields_ = [("counts", Confusion), ("precision", C.c_double), ("recall", C.c_double),
+                ("accuracy", C.c_double), ("fscore", C.c_double),
+                ("degenerate_precision", C.c_int32), ("degenerate_recall", C.c_int32)]
+
+
+class InstanceReport(C.Structure):
+    """InstanceReport, evaluation.hpp:91-95."""
+    _fields_ = [("correct", C.c_int32), ("incorrect", C.c_int32), ("misdetection", C.c_int32)]
+
+
 class DetectOut(C.Structure):
     _fields_ = [
         ("d0", C.POINTER(C.c_float)), ("d1", C.POINTER(C.c_float)),
@@ -230,6 +250,13 @@ _SIGS = {
     "rpd_connected_components": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp]),
     "rpd_detect_potholes": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, C.c_int,
                                       C.POINTER(Threshold), C.c_int, C.c_int, C.c_int, _vp]),
+    # evaluation.hpp
+    "rpd_pep": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_double)]),
+    "rpd_rmse": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "rpd_fscore": (C.c_double, [C.c_double, C.c_double]),
+    "rpd_pixel_metrics": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(PixelReport)]),
+    "rpd_instance_metrics": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_double,
+                                       C.POINTER(InstanceReport)]),
 }
 
 class Stats(C.Structure):
@@ -640,6 +667,46 @@ class Context:
         self._check(self.dll.rpd_detect_potholes(self.handle, _ptr(d3), _ptr(lab), sp_spacing,
                                                  h, w, C.byref(thr), border_margin,
                                                  min_superpixels, connectivity, _ptr(out)))
+        return out
+
+
+    # ---- evaluation.hpp:14-149 ---------------------------------------------
+    def _pair(self, a, b, conv):
+        a, b = conv(a), conv(b)
+        if a.shape != b.shape:
+            raise InvalidArgument("evaluation: dimension mismatch")
+        return a, b
+
+    def pep(self, est, gt, eps: float) -> float:
+        est, gt = self._pair(est, gt, _f32)
+        out = C.c_double()
+        self._check(self.dll.rpd_pep(self.handle, _ptr(est), _ptr(gt), est.shape[0],
+                                     est.shape[1], eps, C.byref(out)))
+        return out.value
+
+    def rmse(self, est, gt) -> float:
+        est, gt = self._pair(est, gt, _f32)
+        out = C.c_double()
+        self._check(self.dll.rpd_rmse(self.handle, _ptr(est), _ptr(gt), est.shape[0],
+                                      est.shape[1], C.byref(out)))
+        return out.value
+
+    def fscore(self, precision: float, recall: float) -> float:
+        return self.dll.rpd_fscore(precision, recall)
+
+    def pixel_metrics(self, pred, gt_mask) -> PixelReport:
+        pred, gt_mask = self._pair(pred, gt_mask, _i32)
+        out = PixelReport()
+        self._check(self.dll.rpd_pixel_metrics(self.handle, _ptr(pred), _ptr(gt_mask),
+                                               pred.shape[0], pred.shape[1], C.byref(out)))
+        return out
+
+    def instance_metrics(self, pred, gt_instances, iou_min: float = 0.5) -> InstanceReport:
+        pred, gt_instances = self._pair(pred, gt_instances, _i32)
+        out = InstanceReport()
+        self._check(self.dll.rpd_instance_metrics(self.handle, _ptr(pred), _ptr(gt_instances),
+                                                  pred.shape[0], pred.shape[1], iou_min,
+                                                  C.byref(out)))
         return out
 
 
