@@ -369,6 +369,35 @@ def gpu_arm(args, rank, world, local):
                              "kernel moves ~1/3 of them (u8 per-path outputs, no u16 sums)"},
         "clocks": clk,
     }
+    # ---- evaluation metrics of the frame (d1 vs the scene's
+    # ground-truth disparity, labels vs its pothole instances) through the
+    # C-ABI with host buffers, GPU vs the oracle on one host core
+    if rank == 0:
+        res = ctx.detect(scene.left, scene.right, cfg, want=("d1", "labels"))
+        gt_d = scene.gt_disparity.astype(np.float32)
+
+        def eval_all(c):
+            c.pep(res.d1, gt_d, 3.0)
+            c.rmse(res.d1, gt_d)
+            c.pixel_metrics(res.labels, scene.gt_mask)
+            return c.instance_metrics(res.labels, scene.gt_mask)
+
+        for _ in range(3):
+            eval_all(ctx)
+        t0 = time.perf_counter()
+        reps = 20
+        for _ in range(reps):
+            rep = eval_all(ctx)
+        gpu_eval_ms = (time.perf_counter() - t0) * 1e3 / reps
+        result["eval"] = {"metrics": "pep(eps=3) + rmse of d1, pixel + instance metrics of labels",
+                          "ms_per_frame_gpu_c_abi": round(gpu_eval_ms, 3),
+                          "instance_report": [rep.correct, rep.incorrect, rep.misdetection]}
+        if ORACLE_LIB.exists() and not args.no_cpu_baseline:
+            from paper_2012_10802_b200.api import Library as _Lib
+            octx = _Lib(str(ORACLE_LIB)).context()
+            t0 = time.perf_counter()
+            eval_all(octx)
+            result["eval"]["ms_per_frame_oracle_1core"] = round((time.perf_counter() - t0) * 1e3, 3)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = cpu_threads(args)
         fps, dt, frames = cpu_oracle_run(scene, PIPELINE[c] | {}, thr)
