@@ -324,6 +324,38 @@ rpd_status rpd_pixel_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t* g
 rpd_status rpd_instance_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t* gt_instances,
                                 int h, int w, double iou_min, rpd_instance_report* out);
 
+/* ---- 3-D reprojection (road_geometry.hpp:64-73) — SURVEY.md §8(f) row 2 --- */
+typedef struct rpd_stereo_rig {
+  double focal, baseline, cu, cv; /* types.hpp:25-30 */
+} rpd_stereo_rig;
+
+typedef struct rpd_point3 {
+  float x, y, z;
+} rpd_point3;
+
+/* rig_from_config, pipeline.hpp:46 (cu / cv < 0: image centre).  Host only. */
+rpd_stereo_rig rpd_rig_from_config(const rpd_config* cfg, int width, int height);
+/* reproject, road_geometry.hpp:65: Z = f b / d, X = (u - cu) Z / f,
+ * Y = (v - cv) Z / f over valid pixels with d > 0, in scan order.  *n receives
+ * the point count; RPD_ECAPACITY (and the first cap points) when n > cap. */
+rpd_status rpd_reproject(rpd_ctx* ctx, const float* d1, int h, int w, const rpd_stereo_rig* rig,
+                         rpd_point3* out, int64_t cap, int64_t* n);
+/* reproject_masked, road_geometry.hpp:67-68: only pixels with labels == label. */
+rpd_status rpd_reproject_masked(rpd_ctx* ctx, const float* d1, const int32_t* labels, int h,
+                                int w, int label, const rpd_stereo_rig* rig, rpd_point3* out,
+                                int64_t cap, int64_t* n);
+/* Every instance cloud at once (the CLI's loop over potholes 1..max_label,
+ * rpd_cli.cpp:99-104): instance k's points, in scan order, are
+ * out[offsets[k-1] .. offsets[k]); offsets has max_label + 1 entries. */
+rpd_status rpd_reproject_instances(rpd_ctx* ctx, const float* d1, const int32_t* labels, int h,
+                                   int w, int max_label, const rpd_stereo_rig* rig,
+                                   rpd_point3* out, int64_t cap, int64_t* offsets);
+/* closest_distance_error, road_geometry.hpp:72: RMS distance from each test
+ * point to its nearest truth point (exact brute force).  RPD_EINVAL when a
+ * cloud is empty. */
+rpd_status rpd_closest_distance_error(rpd_ctx* ctx, const rpd_point3* test, int64_t n_test,
+                                      const rpd_point3* truth, int64_t n_truth, double* out);
+
 #ifdef __cplusplus
 }
 #endif

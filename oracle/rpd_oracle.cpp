@@ -1073,12 +1073,20 @@ Obs to_obs(const double* d, const double* u, const double* v, int64_t k) {
   return o;
 }
 
+// caller buffer too small (RPD_ECAPACITY)
+struct Capacity : std::logic_error {
+  using std::logic_error::logic_error;
+};
+
 template <typename F>
 rpd_status guard(rpd_ctx* ctx, F&& f) {
   try {
     f();
     if (ctx) ctx->err.clear();
     return RPD_OK;
+  } catch (const Capacity& e) {
+    if (ctx) ctx->err = e.what();
+    return RPD_ECAPACITY;
   } catch (const std::invalid_argument& e) {
     if (ctx) ctx->err = e.what();
     return RPD_EINVAL;
@@ -1594,6 +1602,98 @@ rpd_status rpd_instance_metrics(rpd_ctx* ctx, const int32_t* pred, const int32_t
     for (int g = 1; g <= ng; ++g)
       if (!used_g[size_t(g)]) ++rep.misdetection;
     *out = rep;
+  });
+}
+
+// ---- road_geometry.cpp:153-188, restated sequentially ----------------------
+static std::vector<rpd_point3> reproject_seq(const float* d1, const int32_t* labels, int label,
+                                             int h, int w, const rpd_stereo_rig& rig) {
+  if (rig.focal <= 0 || rig.baseline <= 0) throw std::invalid_argument("reproject: bad rig");
+  std::vector<rpd_point3> cloud;
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      const long i = long(v) * w + u;
+      const float d = (labels && labels[i] != label) ? kInvalid : d1[i];
+      if (!valid(d) || d <= 0.0f) continue;
+      const double z = rig.focal * rig.baseline / d;
+      cloud.push_back({static_cast<float>((u - rig.cu) * z / rig.focal),
+                       static_cast<float>((v - rig.cv) * z / rig.focal), static_cast<float>(z)});
+    }
+  return cloud;
+}
+
+rpd_stereo_rig rpd_rig_from_config(const rpd_config* cfg, int width, int height) {
+  rpd_stereo_rig r{700.0, 0.12, 0.0, 0.0};
+  if (!cfg) return r;
+  r.focal = cfg->focal;
+  r.baseline = cfg->baseline;
+  r.cu = cfg->cu >= 0 ? cfg->cu : width / 2.0;
+  r.cv = cfg->cv >= 0 ? cfg->cv : height / 2.0;
+  return r;
+}
+
+static void put_cloud(const std::vector<rpd_point3>& c, rpd_point3* out, int64_t cap, int64_t* n) {
+  *n = int64_t(c.size());
+  const size_t k = std::min<size_t>(c.size(), size_t(std::max<int64_t>(cap, 0)));
+  if (k) std::memcpy(out, c.data(), sizeof(rpd_point3) * k);
+  if (int64_t(c.size()) > cap) throw Capacity("reproject: more points than cap");
+}
+
+rpd_status rpd_reproject(rpd_ctx* ctx, const float* d1, int h, int w, const rpd_stereo_rig* rig,
+                         rpd_point3* out, int64_t cap, int64_t* n) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (!rig) throw std::invalid_argument("reproject: null rig");
+    put_cloud(reproject_seq(d1, nullptr, 0, h, w, *rig), out, cap, n);
+  });
+}
+
+rpd_status rpd_reproject_masked(rpd_ctx* ctx, const float* d1, const int32_t* labels, int h,
+                                int w, int label, const rpd_stereo_rig* rig, rpd_point3* out,
+                                int64_t cap, int64_t* n) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (!rig) throw std::invalid_argument("reproject: null rig");
+    put_cloud(reproject_seq(d1, labels, label, h, w, *rig), out, cap, n);
+  });
+}
+
+rpd_status rpd_reproject_instances(rpd_ctx* ctx, const float* d1, const int32_t* labels, int h,
+                                   int w, int max_label, const rpd_stereo_rig* rig,
+                                   rpd_point3* out, int64_t cap, int64_t* offsets) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    if (!rig) throw std::invalid_argument("reproject: null rig");
+    if (max_label < 0) throw std::invalid_argument("reproject_instances: max_label < 0");
+    std::vector<rpd_point3> all;
+    offsets[0] = 0;
+    for (int k = 1; k <= max_label; ++k) {  // rpd_cli.cpp:99-104
+      const auto c = reproject_seq(d1, labels, k, h, w, *rig);
+      all.insert(all.end(), c.begin(), c.end());
+      offsets[k] = int64_t(all.size());
+    }
+    int64_t n = 0;
+    put_cloud(all, out, cap, &n);
+  });
+}
+
+rpd_status rpd_closest_distance_error(rpd_ctx* ctx, const rpd_point3* test, int64_t n_test,
+                                      const rpd_point3* truth, int64_t n_truth, double* out) {
+  return guard(ctx, [&] {
+    if (n_test <= 0 || n_truth <= 0)
+      throw std::invalid_argument("closest_distance_error: empty cloud");
+    double sum = 0.0;
+    for (int64_t i = 0; i < n_test; ++i) {
+      const rpd_point3& p = test[i];
+      double best = std::numeric_limits<double>::infinity();
+      for (int64_t j = 0; j < n_truth; ++j) {
+        const rpd_point3& g = truth[j];
+        const double dx = p.x - g.x, dy = p.y - g.y, dz = p.z - g.z;
+        best = std::min(best, dx * dx + dy * dy + dz * dz);
+      }
+      sum += best;
+    }
+    *out = std::sqrt(sum / static_cast<double>(n_test));
   });
 }
 

@@ -123,6 +123,16 @@ class InstanceReport(C.Structure):
     _fields_ = [("correct", C.c_int32), ("incorrect", C.c_int32), ("misdetection", C.c_int32)]
 
 
+class StereoRig(C.Structure):
+    """StereoRig, types.hpp:25-30."""
+    _fields_ = [("focal", C.c_double), ("baseline", C.c_double), ("cu", C.c_double),
+                ("cv", C.c_double)]
+
+
+class Point3(C.Structure):
+    _fields_ = [("x", C.c_float), ("y", C.c_float), ("z", C.c_float)]
+
+
 class DetectOut(C.Structure):
     _fields_ = [
         ("d0", C.POINTER(C.c_float)), ("d1", C.POINTER(C.c_float)),
@@ -257,6 +267,17 @@ _SIGS = {
     "rpd_pixel_metrics": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(PixelReport)]),
     "rpd_instance_metrics": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_double,
                                        C.POINTER(InstanceReport)]),
+    # road_geometry.hpp:64-73
+    "rpd_rig_from_config": (StereoRig, [C.POINTER(Config), C.c_int, C.c_int]),
+    "rpd_reproject": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.POINTER(StereoRig), _vp,
+                                C.c_int64, C.POINTER(C.c_int64)]),
+    "rpd_reproject_masked": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(StereoRig), _vp, C.c_int64,
+                                       C.POINTER(C.c_int64)]),
+    "rpd_reproject_instances": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(StereoRig), _vp, C.c_int64, _vp]),
+    "rpd_closest_distance_error": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64,
+                                             C.POINTER(C.c_double)]),
 }
 
 class Stats(C.Structure):
@@ -708,6 +729,50 @@ class Context:
                                                   pred.shape[0], pred.shape[1], iou_min,
                                                   C.byref(out)))
         return out
+
+
+    # ---- road_geometry.hpp:64-73 -------------------------------------------
+    def rig_from_config(self, cfg: Config, width: int, height: int) -> StereoRig:
+        return self.dll.rpd_rig_from_config(C.byref(cfg), width, height)
+
+    def reproject(self, d1, rig: StereoRig, labels=None, label: int = 0) -> np.ndarray:
+        """PointCloud as an (n, 3) float32 array (reproject / reproject_masked)."""
+        d1 = _f32(d1)
+        h, w = d1.shape
+        cap = h * w
+        out = np.empty((max(cap, 1), 3), np.float32)
+        n = C.c_int64()
+        if labels is None:
+            st = self.dll.rpd_reproject(self.handle, _ptr(d1), h, w, C.byref(rig), _ptr(out), cap,
+                                        C.byref(n))
+        else:
+            lab = _i32(labels)
+            if lab.shape != d1.shape:
+                raise InvalidArgument("reproject_masked: dimension mismatch")
+            st = self.dll.rpd_reproject_masked(self.handle, _ptr(d1), _ptr(lab), h, w, label,
+                                               C.byref(rig), _ptr(out), cap, C.byref(n))
+        self._check(st)
+        return out[:n.value].copy()
+
+    def reproject_instances(self, d1, labels, max_label: int, rig: StereoRig):
+        """[cloud of label 1, ..., cloud of label max_label]."""
+        d1, lab = _f32(d1), _i32(labels)
+        h, w = d1.shape
+        cap = h * w
+        out = np.empty((max(cap, 1), 3), np.float32)
+        off = np.zeros(max_label + 1, np.int64)
+        self._check(self.dll.rpd_reproject_instances(self.handle, _ptr(d1), _ptr(lab), h, w,
+                                                     max_label, C.byref(rig), _ptr(out), cap,
+                                                     _ptr(off)))
+        return [out[off[k - 1]:off[k]].copy() for k in range(1, max_label + 1)]
+
+    def closest_distance_error(self, test, truth) -> float:
+        t = np.ascontiguousarray(np.asarray(test, np.float32).reshape(-1, 3))
+        g = np.ascontiguousarray(np.asarray(truth, np.float32).reshape(-1, 3))
+        out = C.c_double()
+        self._check(self.dll.rpd_closest_distance_error(self.handle, _ptr(t), t.shape[0], _ptr(g),
+                                                        g.shape[0], C.byref(out)))
+        return out.value
 
 
 def model(a0=0.0, a1=0.0, phi=0.0) -> RoadModel:
