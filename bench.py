@@ -392,12 +392,29 @@ def gpu_arm(args, rank, world, local):
         result["eval"] = {"metrics": "pep(eps=3) + rmse of d1, pixel + instance metrics of labels",
                           "ms_per_frame_gpu_c_abi": round(gpu_eval_ms, 3),
                           "instance_report": [rep.correct, rep.incorrect, rep.misdetection]}
+        # every pothole's point cloud (rpd_cli.cpp:96-104)
+        rig = ctx.rig_from_config(cfg, w, h)
+        n_pot = int(res.labels.max())
+
+        def clouds(c):
+            return c.reproject_instances(res.d1, res.labels, n_pot, rig)
+        clouds(ctx)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            pts = clouds(ctx)
+        result["reproject"] = {"clouds": n_pot, "points": int(sum(len(p) for p in pts)),
+                               "ms_per_frame_gpu_c_abi":
+                                   round((time.perf_counter() - t0) * 1e3 / reps, 3)}
         if ORACLE_LIB.exists() and not args.no_cpu_baseline:
             from paper_2012_10802_b200.api import Library as _Lib
             octx = _Lib(str(ORACLE_LIB)).context()
             t0 = time.perf_counter()
             eval_all(octx)
             result["eval"]["ms_per_frame_oracle_1core"] = round((time.perf_counter() - t0) * 1e3, 3)
+            t0 = time.perf_counter()
+            clouds(octx)
+            result["reproject"]["ms_per_frame_oracle_1core"] = \
+                round((time.perf_counter() - t0) * 1e3, 3)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = cpu_threads(args)
         fps, dt, frames = cpu_oracle_run(scene, PIPELINE[c] | {}, thr)
