@@ -18,6 +18,8 @@
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
+#include <fstream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -368,6 +370,140 @@ inline LabelMap detect_potholes(const DisparityMap& d3, const SuperpixelMap& sp,
                                     d3.rows(), d3.cols(), &t, border_margin, min_superpixels,
                                     connectivity, out.ptr()));
   return out;
+}
+
+// ------------------------------------------------------------- evaluation --
+inline void check_same_shape(int h0, int w0, int h1, int w1, const char* what) {
+  if (h0 != h1 || w0 != w1) throw std::invalid_argument(std::string(what) + ": dimension mismatch");
+}
+inline double pep(const DisparityMap& est, const DisparityMap& gt, double eps) {  // :14
+  check_same_shape(est.rows(), est.cols(), gt.rows(), gt.cols(), "pep");
+  double out = 0.0;
+  detail::check(rpd_pep(detail::ctx(), est.ptr(), gt.ptr(), est.rows(), est.cols(), eps, &out));
+  return out;
+}
+inline double rmse(const DisparityMap& est, const DisparityMap& gt) {  // :29
+  check_same_shape(est.rows(), est.cols(), gt.rows(), gt.cols(), "rmse");
+  double out = 0.0;
+  detail::check(rpd_rmse(detail::ctx(), est.ptr(), gt.ptr(), est.rows(), est.cols(), &out));
+  return out;
+}
+struct ConfusionCounts {  // evaluation.hpp:44-47
+  long n_tp = 0, n_fp = 0, n_fn = 0, n_tn = 0;
+  long total() const { return n_tp + n_fp + n_fn + n_tn; }
+};
+struct PixelMetrics {  // evaluation.hpp:49-57
+  ConfusionCounts counts;
+  double precision = 0.0, recall = 0.0, accuracy = 0.0, fscore = 0.0;
+  bool degenerate_precision = false, degenerate_recall = false;
+};
+inline double fscore(double precision, double recall) { return rpd_fscore(precision, recall); }
+inline PixelMetrics pixel_metrics(const LabelMap& pred, const LabelMap& gt_mask) {  // :69
+  check_same_shape(pred.rows(), pred.cols(), gt_mask.rows(), gt_mask.cols(), "pixel_metrics");
+  rpd_pixel_report r{};
+  detail::check(rpd_pixel_metrics(detail::ctx(), pred.ptr(), gt_mask.ptr(), pred.rows(),
+                                   pred.cols(), &r));
+  PixelMetrics m;
+  m.counts = {long(r.counts.n_tp), long(r.counts.n_fp), long(r.counts.n_fn), long(r.counts.n_tn)};
+  m.precision = r.precision;
+  m.recall = r.recall;
+  m.accuracy = r.accuracy;
+  m.fscore = r.fscore;
+  m.degenerate_precision = r.degenerate_precision != 0;
+  m.degenerate_recall = r.degenerate_recall != 0;
+  return m;
+}
+struct InstanceReport {  // evaluation.hpp:91-95
+  int correct = 0, incorrect = 0, misdetection = 0;
+};
+inline InstanceReport instance_metrics(const LabelMap& pred, const LabelMap& gt_instances,
+                                       double iou_min = 0.5) {  // :97
+  check_same_shape(pred.rows(), pred.cols(), gt_instances.rows(), gt_instances.cols(),
+                   "instance_metrics");
+  rpd_instance_report r{};
+  detail::check(rpd_instance_metrics(detail::ctx(), pred.ptr(), gt_instances.ptr(), pred.rows(),
+                                     pred.cols(), iou_min, &r));
+  return InstanceReport{r.correct, r.incorrect, r.misdetection};
+}
+
+// ------------------------------------------------ 3-D reprojection + PLY --
+struct StereoRig {  // types.hpp:25-30
+  double focal = 700.0, baseline = 0.12, cu = 0.0, cv = 0.0;
+};
+struct Point3 {  // types.hpp:43-45
+  float x, y, z;
+};
+using PointCloud = std::vector<Point3>;
+inline StereoRig rig_from_config(const PipelineConfig& c, int width, int height) {
+  const rpd_stereo_rig r = rpd_rig_from_config(&c, width, height);
+  return StereoRig{r.focal, r.baseline, r.cu, r.cv};
+}
+inline PointCloud reproject_masked_impl(const DisparityMap& d1, const LabelMap* labels, int label,
+                                        const StereoRig& rig) {
+  const rpd_stereo_rig r{rig.focal, rig.baseline, rig.cu, rig.cv};
+  PointCloud cloud(size_t(std::max(1, d1.rows() * d1.cols())));
+  int64_t n = 0;
+  static_assert(sizeof(Point3) == sizeof(rpd_point3), "layout");
+  auto* out = reinterpret_cast<rpd_point3*>(cloud.data());
+  if (labels)
+    detail::check(rpd_reproject_masked(detail::ctx(), d1.ptr(), labels->ptr(), d1.rows(),
+                                       d1.cols(), label, &r, out, int64_t(cloud.size()), &n));
+  else
+    detail::check(rpd_reproject(detail::ctx(), d1.ptr(), d1.rows(), d1.cols(), &r, out,
+                                int64_t(cloud.size()), &n));
+  cloud.resize(size_t(n));
+  return cloud;
+}
+inline PointCloud reproject(const DisparityMap& d1, const StereoRig& rig) {  // :65
+  return reproject_masked_impl(d1, nullptr, 0, rig);
+}
+inline PointCloud reproject_masked(const DisparityMap& d1, const LabelMap& labels, int label,
+                                   const StereoRig& rig) {  // :67
+  check_same_shape(d1.rows(), d1.cols(), labels.rows(), labels.cols(), "reproject_masked");
+  return reproject_masked_impl(d1, &labels, label, rig);
+}
+inline double closest_distance_error(const PointCloud& test, const PointCloud& truth) {  // :72
+  double out = 0.0;
+  detail::check(rpd_closest_distance_error(
+      detail::ctx(), reinterpret_cast<const rpd_point3*>(test.data()), int64_t(test.size()),
+      reinterpret_cast<const rpd_point3*>(truth.data()), int64_t(truth.size()), &out));
+  return out;
+}
+inline void save_ply(const PointCloud& cloud, const std::string& path) {  // :190-197
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot write: " + path);
+  out << "ply\nformat ascii 1.0\nelement vertex " << cloud.size()
+      << "\nproperty float x\nproperty float y\nproperty float z\nend_header\n";
+  for (const auto& p : cloud) out << p.x << " " << p.y << " " << p.z << "\n";
+  if (!out) throw std::runtime_error("write failed: " + path);
+}
+inline PointCloud load_ply(const std::string& path) {  // :199-225
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("not found: " + path);
+  std::string line;
+  std::size_t n = 0;
+  bool header_done = false;
+  while (std::getline(in, line)) {
+    std::istringstream ss(line);
+    std::string tok;
+    ss >> tok;
+    if (tok == "element") {
+      std::string what;
+      ss >> what >> n;
+    } else if (tok == "end_header") {
+      header_done = true;
+      break;
+    }
+  }
+  if (!header_done) throw std::runtime_error("bad PLY header: " + path);
+  PointCloud cloud;
+  cloud.reserve(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    Point3 p;
+    if (!(in >> p.x >> p.y >> p.z)) throw std::runtime_error("truncated PLY: " + path);
+    cloud.push_back(p);
+  }
+  return cloud;
 }
 
 // --------------------------------------------------------------- pipeline --

@@ -81,6 +81,33 @@ int main() {
       std::printf("degenerate fit (acceptable for a planar-free pair): %s\n", e.what());
     }
   }
+  {  // test_evaluation.cpp:10-35 / :97-108 (pep, rmse, pixel metrics)
+    DisparityMap gt = DisparityMap::Constant(2, 5, 10.0f);
+    DisparityMap est = gt;
+    est(0, 0) = 13.5f;
+    est(0, 1) = 12.0f;
+    est(1, 0) = kInvalidDisparity;
+    gt(1, 1) = kInvalidDisparity;
+    CHECK(std::fabs(pep(est, gt, 2.0) - 100.0 / 8.0) < 1e-12);
+    DisparityMap g1 = DisparityMap::Constant(1, 4, 5.0f);
+    DisparityMap e1(1, 4);
+    e1(0, 0) = 5.0f; e1(0, 1) = 8.0f; e1(0, 2) = 1.0f; e1(0, 3) = kInvalidDisparity;
+    CHECK(std::fabs(rmse(e1, g1) - std::sqrt(25.0 / 3.0)) < 1e-12);
+    LabelMap pred(2, 4), gtm(2, 4);
+    const int pv[8] = {1, 1, 0, 0, 2, 0, 0, 0}, gv[8] = {1, 0, 1, 0, 1, 1, 0, 0};
+    for (int i = 0; i < 8; ++i) { pred(i / 4, i % 4) = pv[i]; gtm(i / 4, i % 4) = gv[i]; }
+    const PixelMetrics m = pixel_metrics(pred, gtm);
+    CHECK(m.counts.n_tp == 2 && m.counts.n_fp == 1 && m.counts.n_fn == 2 && m.counts.n_tn == 3);
+    CHECK(instance_metrics(pred, pred).correct == 2);
+  }
+  {  // test_road_geometry.cpp:209-225 (reproject)
+    StereoRig rig{700.0, 0.12, 320.0, 240.0};
+    DisparityMap d = DisparityMap::Constant(2, 2, kInvalidDisparity);
+    d(0, 0) = 7.0f;
+    PointCloud c = reproject(d, rig);
+    CHECK(c.size() == 1 && std::fabs(c[0].z - 12.0f) < 1e-5f);
+    CHECK(closest_distance_error(c, c) == 0.0);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
