@@ -356,6 +356,25 @@ rpd_status rpd_reproject_instances(rpd_ctx* ctx, const float* d1, const int32_t*
 rpd_status rpd_closest_distance_error(rpd_ctx* ctx, const rpd_point3* test, int64_t n_test,
                                       const rpd_point3* truth, int64_t n_truth, double* out);
 
+/* ---- raster encodings of the on-disk formats (image_io.cpp:190-339) —
+ * SURVEY.md §8(f) row 3.  The file codecs (PNG / PGM) are host-side
+ * (paper_2012_10802_b200/image_io.py); these are their per-pixel transforms. */
+/* save_disparity's KITTI encoding (:215-235): round(d * 256), 0 = invalid;
+ * RPD_EDEGENERATE ("disparity exceeds encoding range") outside [0, 65535]. */
+rpd_status rpd_encode_disparity_u16(rpd_ctx* ctx, const float* d, int h, int w, uint16_t* out);
+/* load_disparity (:202-213): s / 256.0f, 0 -> invalid. */
+rpd_status rpd_decode_disparity_u16(rpd_ctx* ctx, const uint16_t* s, int h, int w, float* out);
+/* save_labels (:245-259): RPD_EDEGENERATE outside [0, 65535]. */
+rpd_status rpd_encode_labels_u16(rpd_ctx* ctx, const int32_t* labels, int h, int w,
+                                 uint16_t* out);
+/* save_gray_image (:187-199): clamp(round(x), 0, 255). */
+rpd_status rpd_encode_gray_u8(rpd_ctx* ctx, const float* img, int h, int w, uint8_t* out);
+/* load_gray_image of an RGB raster (:176-181): 0.299 R + 0.587 G + 0.114 B (float). */
+rpd_status rpd_gray_from_rgb8(rpd_ctx* ctx, const uint8_t* rgb, int h, int w, float* out);
+/* save_overlay (:291-312): gray background, label k tinted with palette (k-1) mod 12. */
+rpd_status rpd_overlay_rgb8(rpd_ctx* ctx, const float* img, const int32_t* labels, int h, int w,
+                            uint8_t* rgb);
+
 #ifdef __cplusplus
 }
 #endif

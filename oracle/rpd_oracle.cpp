@@ -1697,4 +1697,84 @@ rpd_status rpd_closest_distance_error(rpd_ctx* ctx, const rpd_point3* test, int6
   });
 }
 
+// ---- image_io.cpp:171-339 per-pixel transforms, restated --------------------
+rpd_status rpd_encode_disparity_u16(rpd_ctx* ctx, const float* d, int h, int w, uint16_t* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    for (long i = 0; i < long(h) * w; ++i) {
+      std::uint16_t s = 0;
+      if (valid(d[i])) {
+        const double scaled = std::round(static_cast<double>(d[i]) * 256.0);
+        if (scaled < 0 || scaled > 65535) throw std::runtime_error("disparity exceeds encoding range");
+        s = static_cast<std::uint16_t>(scaled);
+      }
+      out[i] = s;
+    }
+  });
+}
+
+rpd_status rpd_decode_disparity_u16(rpd_ctx* ctx, const uint16_t* s, int h, int w, float* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    for (long i = 0; i < long(h) * w; ++i)
+      out[i] = s[i] == 0 ? kInvalid : static_cast<float>(s[i]) / 256.0f;
+  });
+}
+
+rpd_status rpd_encode_labels_u16(rpd_ctx* ctx, const int32_t* labels, int h, int w,
+                                 uint16_t* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    for (long i = 0; i < long(h) * w; ++i) {
+      const int k = labels[i];
+      if (k < 0 || k > 65535) throw std::runtime_error("label exceeds encoding range");
+      out[i] = static_cast<std::uint16_t>(k);
+    }
+  });
+}
+
+static unsigned char round_clamp_u8(float x) {
+  return static_cast<unsigned char>(std::clamp(std::round(x), 0.0f, 255.0f));
+}
+
+rpd_status rpd_encode_gray_u8(rpd_ctx* ctx, const float* img, int h, int w, uint8_t* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    for (long i = 0; i < long(h) * w; ++i) out[i] = round_clamp_u8(img[i]);
+  });
+}
+
+rpd_status rpd_gray_from_rgb8(rpd_ctx* ctx, const uint8_t* rgb, int h, int w, float* out) {
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    for (long i = 0; i < long(h) * w; ++i) {
+      const std::uint16_t r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+      out[i] = 0.299f * r + 0.587f * g + 0.114f * b;
+    }
+  });
+}
+
+rpd_status rpd_overlay_rgb8(rpd_ctx* ctx, const float* img, const int32_t* labels, int h, int w,
+                            uint8_t* rgb) {
+  static const unsigned char kPalette[12][3] = {
+      {230, 25, 75},  {60, 180, 75},  {255, 225, 25}, {0, 130, 200},  {245, 130, 48},
+      {145, 30, 180}, {70, 240, 240}, {240, 50, 230}, {210, 245, 60}, {250, 190, 190},
+      {0, 128, 128},  {170, 110, 40}};
+  return guard(ctx, [&] {
+    check_dims(h, w);
+    for (long i = 0; i < long(h) * w; ++i) {
+      const float gray = img[i];
+      const unsigned char g = round_clamp_u8(gray);
+      unsigned char c[3] = {g, g, g};
+      if (labels[i] > 0) {
+        const unsigned char* p = kPalette[(labels[i] - 1) % 12];
+        for (int ch = 0; ch < 3; ++ch) c[ch] = round_clamp_u8((gray + p[ch]) * 0.5f);
+      }
+      rgb[3 * i] = c[0];
+      rgb[3 * i + 1] = c[1];
+      rgb[3 * i + 2] = c[2];
+    }
+  });
+}
+
 }  // extern "C"

@@ -278,6 +278,13 @@ _SIGS = {
                                           C.POINTER(StereoRig), _vp, C.c_int64, _vp]),
     "rpd_closest_distance_error": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64,
                                              C.POINTER(C.c_double)]),
+    # image_io.cpp per-pixel transforms
+    "rpd_encode_disparity_u16": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "rpd_decode_disparity_u16": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "rpd_encode_labels_u16": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "rpd_encode_gray_u8": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "rpd_gray_from_rgb8": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
+    "rpd_overlay_rgb8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
 }
 
 class Stats(C.Structure):
@@ -773,6 +780,48 @@ class Context:
         self._check(self.dll.rpd_closest_distance_error(self.handle, _ptr(t), t.shape[0], _ptr(g),
                                                         g.shape[0], C.byref(out)))
         return out.value
+
+
+    # ---- image_io.cpp per-pixel transforms ---------------------------------
+    def encode_disparity_u16(self, d) -> np.ndarray:
+        d = _f32(d)
+        out = np.empty(d.shape, np.uint16)
+        self._check(self.dll.rpd_encode_disparity_u16(self.handle, _ptr(d), *d.shape, _ptr(out)))
+        return out
+
+    def decode_disparity_u16(self, s) -> np.ndarray:
+        s = np.ascontiguousarray(s, np.uint16)
+        out = np.empty(s.shape, np.float32)
+        self._check(self.dll.rpd_decode_disparity_u16(self.handle, _ptr(s), *s.shape, _ptr(out)))
+        return out
+
+    def encode_labels_u16(self, labels) -> np.ndarray:
+        lab = _i32(labels)
+        out = np.empty(lab.shape, np.uint16)
+        self._check(self.dll.rpd_encode_labels_u16(self.handle, _ptr(lab), *lab.shape, _ptr(out)))
+        return out
+
+    def encode_gray_u8(self, img) -> np.ndarray:
+        img = _f32(img)
+        out = np.empty(img.shape, np.uint8)
+        self._check(self.dll.rpd_encode_gray_u8(self.handle, _ptr(img), *img.shape, _ptr(out)))
+        return out
+
+    def gray_from_rgb8(self, rgb) -> np.ndarray:
+        rgb = np.ascontiguousarray(rgb, np.uint8)
+        h, w = rgb.shape[:2]
+        out = np.empty((h, w), np.float32)
+        self._check(self.dll.rpd_gray_from_rgb8(self.handle, _ptr(rgb), h, w, _ptr(out)))
+        return out
+
+    def overlay_rgb8(self, img, labels) -> np.ndarray:
+        img, lab = _f32(img), _i32(labels)
+        if img.shape != lab.shape:
+            raise DegenerateError("overlay: dimension mismatch")
+        out = np.empty(img.shape + (3,), np.uint8)
+        self._check(self.dll.rpd_overlay_rgb8(self.handle, _ptr(img), _ptr(lab), *img.shape,
+                                              _ptr(out)))
+        return out
 
 
 def model(a0=0.0, a1=0.0, phi=0.0) -> RoadModel:

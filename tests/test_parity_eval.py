@@ -65,3 +65,21 @@ def test_pipeline_outputs_against_scene_truth(gpu, oracle, cuda_lib):
     assert bytes(pa) == bytes(pb)
     ia, ib = gpu.instance_metrics(res.labels, sc.gt_mask), oracle.instance_metrics(res.labels, sc.gt_mask)
     assert (ia.correct, ia.incorrect, ia.misdetection) == (ib.correct, ib.incorrect, ib.misdetection)
+
+
+def test_image_io_transforms_match_oracle(gpu, oracle):
+    """image_io.cpp per-pixel transforms, bit-exact."""
+    rng = np.random.default_rng(42)
+    h, w = 600, 800
+    d = rng.uniform(0.0, 250.0, (h, w)).astype(np.float32)
+    d[rng.random((h, w)) < 0.1] = -1.0
+    assert np.array_equal(gpu.encode_disparity_u16(d), oracle.encode_disparity_u16(d))
+    s = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+    assert gpu.decode_disparity_u16(s).tobytes() == oracle.decode_disparity_u16(s).tobytes()
+    lab = rng.integers(0, 40, (h, w)).astype(np.int32)
+    assert np.array_equal(gpu.encode_labels_u16(lab), oracle.encode_labels_u16(lab))
+    img = rng.uniform(-20.0, 280.0, (h, w)).astype(np.float32)
+    assert np.array_equal(gpu.encode_gray_u8(img), oracle.encode_gray_u8(img))
+    rgb = rng.integers(0, 256, (h, w, 3)).astype(np.uint8)
+    assert gpu.gray_from_rgb8(rgb).tobytes() == oracle.gray_from_rgb8(rgb).tobytes()
+    assert np.array_equal(gpu.overlay_rgb8(img, lab), oracle.overlay_rgb8(img, lab))

@@ -9,7 +9,7 @@ out=../_lib/var_$name
 mkdir -p $out
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 obj=${src%.cu}.o
-nvcc $ARCH -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -I../../include $flags -c $src -o $out/$obj
+nvcc $ARCH -O3 -lineinfo --fmad=false -std=c++17 --extended-lambda -Xcompiler -fPIC -I../../include $flags -c $src -o $out/$obj
 objs=$(ls _obj/*.o | grep -v "/$obj")
 nvcc $ARCH -shared -cudart static -o $out/librpd_b200.so $objs $out/$obj
 rm $out/$obj
