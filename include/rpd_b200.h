@@ -180,6 +180,10 @@ rpd_status rpd_input_buffers_u8(rpd_ctx* ctx, int h, int w, uint8_t** d_left, ui
 rpd_status rpd_detect_async_u8(rpd_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right,
                                int h, int w, const rpd_config* cfg);
 rpd_status rpd_detect_fetch(rpd_ctx* ctx, rpd_detect_out* out);
+/* Same as rpd_detect_async_u8 for device-resident float32 images (e.g. the
+ * output of rpd_generate_scenes_device). */
+rpd_status rpd_detect_async(rpd_ctx* ctx, const float* d_left, const float* d_right, int h, int w,
+                            const rpd_config* cfg);
 
 /* Measurement extension.  With profiling enabled, CUDA events are recorded on
  * the context stream around every SGM path-aggregation launch (the dominant
@@ -374,6 +378,59 @@ rpd_status rpd_gray_from_rgb8(rpd_ctx* ctx, const uint8_t* rgb, int h, int w, fl
 /* save_overlay (:291-312): gray background, label k tinted with palette (k-1) mod 12. */
 rpd_status rpd_overlay_rgb8(rpd_ctx* ctx, const float* img, const int32_t* labels, int h, int w,
                             uint8_t* rgb);
+
+
+/* ---- synthetic scenes (synth.hpp:12-60, synth.cpp:94-196) — SURVEY.md
+ * §8(f) row 4.  The generator draws from the reference's random streams
+ * (std::mt19937 + libstdc++ distributions), so a scene equals the
+ * reference's for the same spec. */
+typedef struct rpd_pothole_spec {
+  double cu, cv; /* centre, px */
+  double ru, rv; /* radii, px */
+  double depth;  /* disparity deficit at the centre, px */
+} rpd_pothole_spec;
+
+typedef struct rpd_scene_spec {
+  int32_t width, height;
+  rpd_stereo_rig rig;
+  double a0, a1, phi_true;           /* true road line */
+  uint32_t texture_seed;
+  double noise_sigma;                /* additive intensity noise */
+  int32_t n_potholes;
+  const rpd_pothole_spec* potholes;  /* host array of n_potholes */
+} rpd_scene_spec;
+
+typedef struct rpd_batch_ranges {
+  double depth_min, depth_max;
+  double radius_min, radius_max;
+  double a0_min, a0_max;
+  double a1_min, a1_max;
+  double phi_abs_max;
+  double noise_sigma;
+  int32_t margin;
+} rpd_batch_ranges;
+
+/* SceneSpec / BatchRanges defaults (synth.hpp:20-30, 45-53).  Host only. */
+void rpd_scene_spec_default(rpd_scene_spec* spec);
+void rpd_batch_ranges_default(rpd_batch_ranges* ranges);
+/* The spec of scene `index` of scene_batch(count, base_seed, ranges)
+ * (synth.cpp:151-192): seed base_seed + index, 1-3 non-overlapping potholes
+ * written to potholes[0..2] and linked from spec->potholes.  Host only. */
+rpd_status rpd_scene_batch_spec(uint32_t base_seed, int32_t index, const rpd_batch_ranges* ranges,
+                                rpd_scene_spec* spec, rpd_pothole_spec potholes[3]);
+/* generate_scene, synth.hpp:43 / synth.cpp:94-149: H*W left, right, truth
+ * disparity and pothole mask (index + 1); NULL outputs are skipped.
+ * RPD_EINVAL on a bad pothole (depth <= 0, radius < 4), RPD_EDEGENERATE when
+ * the truth disparity goes negative. */
+rpd_status rpd_generate_scene(rpd_ctx* ctx, const rpd_scene_spec* spec, float* left,
+                              float* right, float* gt_disparity, int32_t* gt_mask);
+/* Streaming extension (product library only): `count` scenes of one size
+ * generated straight into device buffers of count*H*W elements each (scene b
+ * at offset b*H*W), in one batch of launches on the context stream; returns
+ * after the batch completes (errors as rpd_generate_scene). */
+rpd_status rpd_generate_scenes_device(rpd_ctx* ctx, int count, const rpd_scene_spec* specs,
+                                      float* d_left, float* d_right, float* d_gt,
+                                      int32_t* d_mask);
 
 #ifdef __cplusplus
 }

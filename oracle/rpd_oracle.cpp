@@ -34,6 +34,7 @@
 #include <deque>
 #include <limits>
 #include <map>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -1777,4 +1778,194 @@ rpd_status rpd_overlay_rgb8(rpd_ctx* ctx, const float* img, const int32_t* label
   });
 }
 
+// ---- synth.cpp:16-196 scene generator, restated sequentially -------------
+// std::mt19937 with libstdc++'s uniform_real_distribution / normal_distribution
+// (the streams the reference draws from); row-major float rasters.
 }  // extern "C"
+
+namespace {
+
+// value_noise (synth.cpp:16-38): one octave, bilinear over a random lattice.
+void add_value_noise(std::vector<float>& tex, int w, int h, int spacing, float amp,
+                     std::mt19937& rng) {
+  const int nu = w / spacing + 2, nv = h / spacing + 2;
+  std::vector<float> lat(static_cast<size_t>(nu) * nv);
+  std::uniform_real_distribution<float> uni(0.0f, 1.0f);
+  for (auto& x : lat) x = uni(rng);  // row j outer, column i inner
+  for (int v = 0; v < h; ++v) {
+    const double y = static_cast<double>(v) / spacing;
+    const int j = static_cast<int>(y);
+    const double ty = y - j;
+    for (int u = 0; u < w; ++u) {
+      const double x = static_cast<double>(u) / spacing;
+      const int i = static_cast<int>(x);
+      const double tx = x - i;
+      const double top = (1 - tx) * lat[size_t(j) * nu + i] + tx * lat[size_t(j) * nu + i + 1];
+      const double bot =
+          (1 - tx) * lat[size_t(j + 1) * nu + i] + tx * lat[size_t(j + 1) * nu + i + 1];
+      const float n = static_cast<float>((1 - ty) * top + ty * bot);
+      tex[size_t(v) * w + u] += amp * n;  // tex += amps[o] * value_noise (:65)
+    }
+  }
+}
+
+// binomial_smooth_5x5 (synth.cpp:40-58), clamped borders.
+std::vector<float> binomial5(const std::vector<float>& img, int w, int h) {
+  static const double k[5] = {1, 4, 6, 4, 1};
+  std::vector<float> tmp(img.size()), out(img.size());
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      double s = 0;
+      for (int i = -2; i <= 2; ++i) s += k[i + 2] * img[size_t(v) * w + std::clamp(u + i, 0, w - 1)];
+      tmp[size_t(v) * w + u] = static_cast<float>(s / 16.0);
+    }
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      double s = 0;
+      for (int i = -2; i <= 2; ++i) s += k[i + 2] * tmp[size_t(std::clamp(v + i, 0, h - 1)) * w + u];
+      out[size_t(v) * w + u] = static_cast<float>(s / 16.0);
+    }
+  return out;
+}
+
+// Linear interpolation along row v at column s, clamped (synth.cpp:74-91).
+template <typename T>
+double row_lerp(const T* row, int w, double s) {
+  s = std::clamp(s, 0.0, static_cast<double>(w - 1));
+  const int s0 = static_cast<int>(s);
+  const int s1 = std::min(s0 + 1, w - 1);
+  const double t = s - s0;
+  return (1 - t) * row[s0] + t * row[s1];
+}
+
+void oracle_scene(const rpd_scene_spec& sp, float* left, float* right, float* gt, int32_t* mask) {
+  const int w = sp.width, h = sp.height;
+  if (w <= 0 || h <= 0) throw std::invalid_argument("generate_scene: image dimensions must be positive");
+  for (int k = 0; k < sp.n_potholes; ++k) {
+    const rpd_pothole_spec& p = sp.potholes[k];
+    if (p.depth <= 0 || p.ru < 4 || p.rv < 4)
+      throw std::invalid_argument("generate_scene: bad pothole spec");
+  }
+  const size_t n = size_t(h) * w;
+  std::vector<float> g(n), l(n), r(n);
+  std::vector<int32_t> m(n, 0);
+  const double c = std::cos(sp.phi_true), s = std::sin(sp.phi_true);
+  for (int v = 0; v < h; ++v)
+    for (int u = 0; u < w; ++u) {
+      double d = sp.a0 + sp.a1 * (v * c - u * s);  // road_disparity_at (types.hpp:39-41)
+      for (int k = 0; k < sp.n_potholes; ++k) {
+        const rpd_pothole_spec& p = sp.potholes[k];
+        const double ru = (u - p.cu) / p.ru, rv = (v - p.cv) / p.rv;
+        const double r2 = ru * ru + rv * rv;
+        if (r2 < 1.0) {
+          d -= p.depth * (1.0 - r2);
+          m[size_t(v) * w + u] = k + 1;
+        }
+      }
+      if (d < 0) throw std::runtime_error("generate_scene: pothole depth drives disparity negative");
+      g[size_t(v) * w + u] = static_cast<float>(d);
+    }
+  // make_texture (synth.cpp:60-72)
+  std::mt19937 trng(sp.texture_seed);
+  std::vector<float> tex(n, 0.0f);
+  add_value_noise(tex, w, h, 64, 1.0f, trng);
+  add_value_noise(tex, w, h, 16, 0.5f, trng);
+  add_value_noise(tex, w, h, 4, 0.25f, trng);
+  tex = binomial5(tex, w, h);
+  const float lo = *std::min_element(tex.begin(), tex.end());
+  const float hi = *std::max_element(tex.begin(), tex.end());
+  const float scale = hi > lo ? 190.0f / (hi - lo) : 0.0f;
+  for (size_t i = 0; i < n; ++i) l[i] = hi > lo ? 30.0f + (tex[i] - lo) * scale : 125.0f;
+  // right view: fixed point u = x + d(v, u), 8 refinements (synth.cpp:126-137)
+  for (int v = 0; v < h; ++v) {
+    const float* grow = g.data() + size_t(v) * w;
+    const float* lrow = l.data() + size_t(v) * w;
+    for (int x = 0; x < w; ++x) {
+      double u = x + row_lerp(grow, w, x);
+      for (int it = 0; it < 8; ++it) u = x + row_lerp(grow, w, u);
+      r[size_t(v) * w + x] = static_cast<float>(row_lerp(lrow, w, u));
+    }
+  }
+  if (sp.noise_sigma > 0) {  // synth.cpp:139-146
+    std::mt19937 nrng(sp.texture_seed ^ 0x9e3779b9u);
+    std::normal_distribution<double> gauss(0.0, sp.noise_sigma);
+    for (size_t i = 0; i < n; ++i) {
+      l[i] = std::clamp(l[i] + static_cast<float>(gauss(nrng)), 0.0f, 255.0f);
+      r[i] = std::clamp(r[i] + static_cast<float>(gauss(nrng)), 0.0f, 255.0f);
+    }
+  }
+  if (left) std::memcpy(left, l.data(), sizeof(float) * n);
+  if (right) std::memcpy(right, r.data(), sizeof(float) * n);
+  if (gt) std::memcpy(gt, g.data(), sizeof(float) * n);
+  if (mask) std::memcpy(mask, m.data(), sizeof(int32_t) * n);
+}
+
+}  // namespace
+
+extern "C" {
+
+void rpd_scene_spec_default(rpd_scene_spec* s) {  // synth.hpp:20-30
+  *s = rpd_scene_spec{};
+  s->width = 640;
+  s->height = 480;
+  s->rig = rpd_stereo_rig{700.0, 0.12, 0.0, 0.0};
+  s->a0 = 5.0;
+  s->a1 = 0.08;
+  s->texture_seed = 1;
+}
+
+void rpd_batch_ranges_default(rpd_batch_ranges* r) {  // synth.hpp:45-53
+  *r = rpd_batch_ranges{1.5, 4.0, 22.0, 48.0, 4.0, 7.0, 0.07, 0.09, 0.035, 0.0, 40};
+}
+
+rpd_status rpd_scene_batch_spec(uint32_t base_seed, int32_t index, const rpd_batch_ranges* r,
+                                rpd_scene_spec* spec, rpd_pothole_spec potholes[3]) {
+  if (index < 0 || !r || !spec || !potholes) return RPD_EINVAL;
+  const uint32_t seed = base_seed + static_cast<uint32_t>(index);  // synth.cpp:157-191
+  std::mt19937 rng(seed * 2654435761u + 12345u);
+  std::uniform_real_distribution<double> uni(0.0, 1.0);
+  rpd_scene_spec_default(spec);
+  spec->texture_seed = seed;
+  spec->noise_sigma = r->noise_sigma;
+  spec->a0 = r->a0_min + (r->a0_max - r->a0_min) * uni(rng);
+  spec->a1 = r->a1_min + (r->a1_max - r->a1_min) * uni(rng);
+  spec->phi_true = r->phi_abs_max * (2.0 * uni(rng) - 1.0);
+  spec->rig.cu = spec->width / 2.0;
+  spec->rig.cv = spec->height / 2.0;
+  int placed = 0;
+  const int wanted = 1 + static_cast<int>(uni(rng) * 3.0) % 3;
+  for (int k = 0; k < wanted; ++k)
+    for (int attempt = 0; attempt < 100; ++attempt) {
+      rpd_pothole_spec p{};
+      p.ru = r->radius_min + (r->radius_max - r->radius_min) * uni(rng);
+      p.rv = r->radius_min + (r->radius_max - r->radius_min) * uni(rng);
+      p.depth = r->depth_min + (r->depth_max - r->depth_min) * uni(rng);
+      const double mu = r->margin + p.ru, mv = r->margin + p.rv;
+      p.cu = mu + (spec->width - 2 * mu) * uni(rng);
+      p.cv = mv + (spec->height - 2 * mv) * uni(rng);
+      bool clash = false;
+      for (int q = 0; q < placed; ++q) {
+        const double dx = p.cu - potholes[q].cu, dy = p.cv - potholes[q].cv;
+        const double sep = std::max(p.ru + potholes[q].ru, p.rv + potholes[q].rv) + 10.0;
+        clash |= dx * dx + dy * dy < sep * sep;
+      }
+      if (!clash) {
+        potholes[placed++] = p;
+        break;
+      }
+    }
+  spec->n_potholes = placed;
+  spec->potholes = potholes;
+  return RPD_OK;
+}
+
+rpd_status rpd_generate_scene(rpd_ctx* ctx, const rpd_scene_spec* spec, float* left,
+                              float* right, float* gt_disparity, int32_t* gt_mask) {
+  return guard(ctx, [&] {
+    if (!spec) throw std::invalid_argument("generate_scene: null spec");
+    oracle_scene(*spec, left, right, gt_disparity, gt_mask);
+  });
+}
+
+}  // extern "C"
+

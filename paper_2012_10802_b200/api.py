@@ -133,6 +133,30 @@ class Point3(C.Structure):
     _fields_ = [("x", C.c_float), ("y", C.c_float), ("z", C.c_float)]
 
 
+class PotholeSpecC(C.Structure):
+    """PotholeSpec, synth.hpp:12-18."""
+    _fields_ = [("cu", C.c_double), ("cv", C.c_double), ("ru", C.c_double), ("rv", C.c_double),
+                ("depth", C.c_double)]
+
+
+class SceneSpecC(C.Structure):
+    """SceneSpec, synth.hpp:20-30 (potholes as a pointer + count)."""
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("rig", StereoRig),
+                ("a0", C.c_double), ("a1", C.c_double), ("phi_true", C.c_double),
+                ("texture_seed", C.c_uint32), ("noise_sigma", C.c_double),
+                ("n_potholes", C.c_int32), ("potholes", C.POINTER(PotholeSpecC))]
+
+
+class BatchRangesC(C.Structure):
+    """BatchRanges, synth.hpp:45-53."""
+    _fields_ = [("depth_min", C.c_double), ("depth_max", C.c_double),
+                ("radius_min", C.c_double), ("radius_max", C.c_double),
+                ("a0_min", C.c_double), ("a0_max", C.c_double),
+                ("a1_min", C.c_double), ("a1_max", C.c_double),
+                ("phi_abs_max", C.c_double), ("noise_sigma", C.c_double),
+                ("margin", C.c_int32)]
+
+
 class DetectOut(C.Structure):
     _fields_ = [
         ("d0", C.POINTER(C.c_float)), ("d1", C.POINTER(C.c_float)),
@@ -285,6 +309,11 @@ _SIGS = {
     "rpd_encode_gray_u8": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
     "rpd_gray_from_rgb8": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp]),
     "rpd_overlay_rgb8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
+    "rpd_scene_spec_default": (None, [C.POINTER(SceneSpecC)]),
+    "rpd_batch_ranges_default": (None, [C.POINTER(BatchRangesC)]),
+    "rpd_scene_batch_spec": (C.c_int, [C.c_uint32, C.c_int32, C.POINTER(BatchRangesC),
+                                       C.POINTER(SceneSpecC), C.POINTER(PotholeSpecC)]),
+    "rpd_generate_scene": (C.c_int, [_vp, C.POINTER(SceneSpecC), _vp, _vp, _vp, _vp]),
 }
 
 class Stats(C.Structure):
@@ -297,6 +326,9 @@ _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
     "rpd_input_buffers_u8": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp), C.POINTER(_vp)]),
     "rpd_detect_async_u8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config)]),
     "rpd_detect_fetch": (C.c_int, [_vp, C.POINTER(DetectOut)]),
+    "rpd_detect_async": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config)]),
+    "rpd_generate_scenes_device": (C.c_int, [_vp, C.c_int, C.POINTER(SceneSpecC), _vp, _vp, _vp,
+                                             _vp]),
     "rpd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rpd_ctx_stats": (C.c_int, [_vp, C.POINTER(Stats)]),
     "rpd_debug_sincos": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
@@ -444,6 +476,10 @@ class Context:
     def detect_async_u8(self, d_left: int, d_right: int, h: int, w: int, cfg: Config):
         self._check(self.dll.rpd_detect_async_u8(self.handle, d_left, d_right, h, w,
                                                  C.byref(cfg)))
+
+    def detect_async(self, d_left: int, d_right: int, h: int, w: int, cfg: Config):
+        """Device-resident float32 images (e.g. from generate_scenes_device)."""
+        self._check(self.dll.rpd_detect_async(self.handle, d_left, d_right, h, w, C.byref(cfg)))
 
     def fetch(self, out: Optional[DetectOut] = None) -> DetectOut:
         out = out if out is not None else DetectOut()
@@ -822,6 +858,46 @@ class Context:
         self._check(self.dll.rpd_overlay_rgb8(self.handle, _ptr(img), _ptr(lab), *img.shape,
                                               _ptr(out)))
         return out
+
+    # ------------------------------------------- synth.hpp (§8(f) row 4) --
+    def generate_scene(self, spec):
+        """generate_scene (synth.cpp:94-149) -> (left, right, gt_disparity, gt_mask).
+        `spec` is a scenes.SceneSpec (or anything with its attributes)."""
+        cs, keep = scene_spec_c(spec)
+        h, w = cs.height, cs.width
+        left = np.empty((h, w), np.float32)
+        right = np.empty((h, w), np.float32)
+        gt = np.empty((h, w), np.float32)
+        mask = np.empty((h, w), np.int32)
+        self._check(self.dll.rpd_generate_scene(self.handle, C.byref(cs), _ptr(left), _ptr(right),
+                                                _ptr(gt), _ptr(mask)))
+        del keep
+        return left, right, gt, mask
+
+    def generate_scenes_device(self, specs, d_left: int, d_right: int, d_gt: int, d_mask: int):
+        """Streaming extension: len(specs) same-size scenes into device buffers."""
+        arr = (SceneSpecC * len(specs))()
+        keep = []
+        for i, sp in enumerate(specs):
+            arr[i], k = scene_spec_c(sp)
+            keep.append(k)
+        self._check(self.dll.rpd_generate_scenes_device(self.handle, len(specs), arr, d_left,
+                                                        d_right, d_gt, d_mask))
+
+
+def scene_spec_c(spec):
+    """ctypes SceneSpecC of a SceneSpec-like object; returns (struct, keepalive)."""
+    pots = list(getattr(spec, "potholes", []) or [])
+    parr = (PotholeSpecC * max(len(pots), 1))()
+    for i, p in enumerate(pots):
+        parr[i] = PotholeSpecC(p.cu, p.cv, p.ru, p.rv, p.depth)
+    rig = getattr(spec, "rig", None)
+    rig_c = StereoRig(rig.focal, rig.baseline, rig.cu, rig.cv) if rig is not None else \
+        StereoRig(700.0, 0.12, 0.0, 0.0)
+    cs = SceneSpecC(int(spec.width), int(spec.height), rig_c, float(spec.a0), float(spec.a1),
+                    float(spec.phi_true), int(spec.texture_seed) & 0xFFFFFFFF,
+                    float(spec.noise_sigma), len(pots), parr)
+    return cs, parr
 
 
 def model(a0=0.0, a1=0.0, phi=0.0) -> RoadModel:

@@ -411,6 +411,26 @@ rpd_status rpd_detect_async_u8(rpd_ctx* ctx, const uint8_t* d_left, const uint8_
   });
 }
 
+rpd_status rpd_detect_async(rpd_ctx* ctx, const float* d_left, const float* d_right, int h, int w,
+                            const rpd_config* cfg) {
+  return guard(ctx, [&] {
+    check_pipeline_args(cfg, h, w);
+    const size_t n = size_t(h) * w;
+    float* l = ctx->ws.get<float>("pl_left", n);
+    float* r = ctx->ws.get<float>("pl_right", n);
+    if (d_left != l)
+      RPD_CK(cudaMemcpyAsync(l, d_left, sizeof(float) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (d_right != r)
+      RPD_CK(cudaMemcpyAsync(r, d_right, sizeof(float) * n, cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    PipelineState& ps = state(ctx);
+    run_frame(ctx, h, w, false, *cfg, ps.last);
+    ps.have_last = true;
+    ps.last_h = h;
+    ps.last_w = w;
+  });
+}
+
 rpd_status rpd_detect_fetch(rpd_ctx* ctx, rpd_detect_out* out) {
   return guard(ctx, [&] {
     PipelineState& ps = state(ctx);
