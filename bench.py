@@ -405,9 +405,54 @@ def gpu_arm(args, rank, world, local):
         result["reproject"] = {"clouds": n_pot, "points": int(sum(len(p) for p in pts)),
                                "ms_per_frame_gpu_c_abi":
                                    round((time.perf_counter() - t0) * 1e3 / reps, 3)}
+        # the reference scene generator on the device — the
+        # acceptance batch scene_batch(20, 7100) (640 x 480), without and with
+        # noise, generated straight into HBM; then generate -> detect streamed
+        # with no host image traffic
+        import torch
+        from paper_2012_10802_b200.scenes import BatchRanges, batch_spec
+        nb = 20
+        sb = {}
+        for sigma in (0.0, 2.0):
+            specs = [batch_spec(ctx.lib, 7100, i, BatchRanges(noise_sigma=sigma)) for i in range(nb)]
+            sh, sw = specs[0].height, specs[0].width
+            dv = torch.device("cuda", 0)
+            bl = torch.empty((nb, sh, sw), dtype=torch.float32, device=dv)
+            br, bg = torch.empty_like(bl), torch.empty_like(bl)
+            bm = torch.empty((nb, sh, sw), dtype=torch.int32, device=dv)
+            torch.cuda.synchronize()
+            for _ in range(2):
+                ctx.generate_scenes_device(specs, bl.data_ptr(), br.data_ptr(), bg.data_ptr(),
+                                           bm.data_ptr())
+            reps = 5
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                ctx.generate_scenes_device(specs, bl.data_ptr(), br.data_ptr(), bg.data_ptr(),
+                                           bm.data_ptr())
+            sb["noise%g" % sigma] = round(nb * reps / (time.perf_counter() - t0), 1)
+        acfg = ctx.lib.default_config(delta_pd=0.48, superpixels=2400)
+        per = sh * sw * 4
+        for i in range(2):
+            ctx.detect_async(bl.data_ptr() + i * per, br.data_ptr() + i * per, sh, sw, acfg)
+            ctx.fetch()
+        t0 = time.perf_counter()
+        ctx.generate_scenes_device(specs, bl.data_ptr(), br.data_ptr(), bg.data_ptr(),
+                                   bm.data_ptr())
+        for i in range(nb):
+            ctx.detect_async(bl.data_ptr() + i * per, br.data_ptr() + i * per, sh, sw, acfg)
+        ctx.fetch()
+        stream_fps = nb / (time.perf_counter() - t0)
+        result["scenes"] = {"batch": "scene_batch(20, 7100), 640x480 (acceptance.cpp:221)",
+                            "scenes_per_s_gpu": sb["noise0"],
+                            "scenes_per_s_gpu_noise2": sb["noise2"],
+                            "generate_detect_stream_frames_per_s": round(stream_fps, 1)}
         if ORACLE_LIB.exists() and not args.no_cpu_baseline:
             from paper_2012_10802_b200.api import Library as _Lib
             octx = _Lib(str(ORACLE_LIB)).context()
+            t0 = time.perf_counter()
+            octx.generate_scene(specs[0])
+            result["scenes"]["scenes_per_s_oracle_1core_noise2"] = \
+                round(1.0 / (time.perf_counter() - t0), 2)
             t0 = time.perf_counter()
             eval_all(octx)
             result["eval"]["ms_per_frame_oracle_1core"] = round((time.perf_counter() - t0) * 1e3, 3)

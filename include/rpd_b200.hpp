@@ -506,6 +506,88 @@ inline PointCloud load_ply(const std::string& path) {  // :199-225
   return cloud;
 }
 
+// -------------------------------------------------- synthetic scenes --
+struct PotholeSpec {  // synth.hpp:12-18
+  double cu = 0.0, cv = 0.0, ru = 10.0, rv = 10.0, depth = 2.0;
+};
+struct SceneSpec {  // synth.hpp:20-30
+  int width = 640;
+  int height = 480;
+  StereoRig rig;
+  double a0 = 5.0;
+  double a1 = 0.08;
+  double phi_true = 0.0;
+  std::vector<PotholeSpec> potholes;
+  std::uint32_t texture_seed = 1;
+  double noise_sigma = 0.0;
+};
+struct SceneTruth {  // synth.hpp:32-38
+  GrayImage left, right;
+  DisparityMap gt_disparity;
+  LabelMap gt_mask;
+  SceneSpec spec;
+};
+struct BatchRanges {  // synth.hpp:45-53
+  double depth_min = 1.5, depth_max = 4.0;
+  double radius_min = 22.0, radius_max = 48.0;
+  double a0_min = 4.0, a0_max = 7.0;
+  double a1_min = 0.07, a1_max = 0.09;
+  double phi_abs_max = 0.035;
+  double noise_sigma = 0.0;
+  int margin = 40;
+};
+inline SceneTruth generate_scene(const SceneSpec& spec) {  // synth.hpp:43
+  std::vector<rpd_pothole_spec> pots;
+  for (const auto& p : spec.potholes) pots.push_back({p.cu, p.cv, p.ru, p.rv, p.depth});
+  rpd_scene_spec c{};
+  c.width = spec.width;
+  c.height = spec.height;
+  c.rig = rpd_stereo_rig{spec.rig.focal, spec.rig.baseline, spec.rig.cu, spec.rig.cv};
+  c.a0 = spec.a0;
+  c.a1 = spec.a1;
+  c.phi_true = spec.phi_true;
+  c.texture_seed = spec.texture_seed;
+  c.noise_sigma = spec.noise_sigma;
+  c.n_potholes = int(pots.size());
+  c.potholes = pots.data();
+  SceneTruth t;
+  const int h = std::max(spec.height, 0), w = std::max(spec.width, 0);
+  t.left = GrayImage(h, w);
+  t.right = GrayImage(h, w);
+  t.gt_disparity = DisparityMap(h, w);
+  t.gt_mask = LabelMap(h, w);
+  detail::check(rpd_generate_scene(detail::ctx(), &c, t.left.ptr(), t.right.ptr(),
+                                   t.gt_disparity.ptr(), t.gt_mask.ptr()));
+  t.spec = spec;
+  return t;
+}
+inline std::vector<SceneTruth> scene_batch(int count, std::uint32_t base_seed,
+                                           const BatchRanges& r = {}) {  // synth.hpp:56-57
+  if (count < 1) throw std::invalid_argument("scene_batch: count must be >= 1");
+  const rpd_batch_ranges rc{r.depth_min, r.depth_max, r.radius_min, r.radius_max, r.a0_min,
+                            r.a0_max,    r.a1_min,    r.a1_max,     r.phi_abs_max, r.noise_sigma,
+                            r.margin};
+  std::vector<SceneTruth> out;
+  for (int i = 0; i < count; ++i) {
+    rpd_scene_spec c{};
+    rpd_pothole_spec pots[3];
+    detail::check(rpd_scene_batch_spec(base_seed, i, &rc, &c, pots));
+    SceneSpec s;
+    s.width = c.width;
+    s.height = c.height;
+    s.rig = StereoRig{c.rig.focal, c.rig.baseline, c.rig.cu, c.rig.cv};
+    s.a0 = c.a0;
+    s.a1 = c.a1;
+    s.phi_true = c.phi_true;
+    s.texture_seed = c.texture_seed;
+    s.noise_sigma = c.noise_sigma;
+    for (int k = 0; k < c.n_potholes; ++k)
+      s.potholes.push_back({pots[k].cu, pots[k].cv, pots[k].ru, pots[k].rv, pots[k].depth});
+    out.push_back(generate_scene(s));
+  }
+  return out;
+}
+
 // --------------------------------------------------------------- pipeline --
 struct StageTime {  // pipeline.hpp:21-24
   std::string name;

@@ -65,70 +65,137 @@ Lattice lattice_of(int w, int h) {
 constexpr int kMtThreads = 640;
 constexpr int kRing = 2048;  // > 1078 + 620: the oldest word a round reads plus one round
 
-// blockIdx.y = 0: lattice stream -> lattice[scene][0..total) (uniform floats);
-// blockIdx.y = 1: noise stream -> pairs[scene][0..need) (accepted polar (x, y)).
+// The serial part: one CTA per (scene, stream) runs mt19937 in rounds of 620
+// words with a single barrier per round (t[m] = twist(x[m], x[m+1]) is
+// recomputed from the ring instead of stored).  The ring is mapped twice
+// (word n at n mod 2048 and n mod 2048 + 2048), so every read x[n - c] is the
+// thread's slot minus a constant: no index arithmetic in the loop.
+// blockIdx.y = 0: the lattice stream -> lattice[scene][0..total) as uniform
+// floats; blockIdx.y = 1: the noise stream -> its first `nwords` tempered
+// outputs, consumed in parallel by k_polar_count / k_polar_scatter.
 __global__ void __launch_bounds__(kMtThreads) k_mt_streams(const DevScene* scenes, int total,
-                                                           float* lattice, double2* pairs,
-                                                           long long need) {
+                                                           float* lattice, uint32_t* words,
+                                                           int nwords) {
   const DevScene s = scenes[blockIdx.x];
   const bool noise = blockIdx.y == 1;
   if (noise && !(s.sigma > 0)) return;
-  __shared__ uint32_t X[kRing], T[kRing];
-  __shared__ int wcnt[kMtThreads / 32];
-  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  __shared__ uint32_t X[2 * kRing];
+  const int i = threadIdx.x;
   if (i == 0) {
     uint32_t v = noise ? (s.seed ^ 0x9e3779b9u) : s.seed;
-    X[0] = v;
-    for (uint32_t k = 1; k < 624; ++k) X[k] = v = mt_seed_next(v, k);
+    X[0] = X[kRing] = v;
+    for (uint32_t k = 1; k < 624; ++k) X[k] = X[kRing + k] = v = mt_seed_next(v, k);
   }
   __syncthreads();
-  if (i < 623) T[i] = mt_twist(X[i], X[i + 1]);
-  __syncthreads();
-  auto xs = [&](long long k) { return X[k & (kRing - 1)]; };
-  auto ts = [&](long long k) { return T[k & (kRing - 1)]; };
+  const int limit = noise ? nwords : total;
   float* lat = lattice + (size_t)blockIdx.x * total;
-  double2* pr = pairs + (size_t)blockIdx.x * need;
-  long long accepted = 0;
-  for (long long base = 624;; base += kMtRound) {
-    const long long n = base + i;
-    const bool live = i < kMtRound;
-    uint32_t xn = 0;
+  uint32_t* wo = words + (size_t)blockIdx.x * nwords;
+  const bool live = i < kMtRound;
+  int slot = (624 + i) & (kRing - 1);  // n mod 2048 of this thread's word
+  for (int base = 624;; base += kMtRound) {
+    const int n = base + i;
     if (live) {
-      xn = mt_word(n, xs, ts);
-      X[n & (kRing - 1)] = xn;
+      const uint32_t* h = X + kRing + slot;  // h[-c] = x[n - c]
+      auto xs = [&](int k) { return h[k - n]; };
+      auto ts = [&](int k) { return mt_twist(h[k - n], h[k + 1 - n]); };
+      const uint32_t xn = mt_word(n, xs, ts);
+      X[slot] = xn;
+      X[slot + kRing] = xn;
+      const int j = n - 624;  // output index
+      if (j < limit) {
+        const uint32_t o = mt_temper(xn);
+        if (noise)
+          wo[j] = o;
+        else
+          lat[j] = canonical_f32(o);
+      }
     }
+    slot = (slot + kMtRound) & (kRing - 1);
     __syncthreads();
-    if (live) T[(n - 1) & (kRing - 1)] = mt_twist(X[(n - 1) & (kRing - 1)], xn);
-    const uint32_t o = mt_temper(xn);
-    const long long j = n - 624;  // output index
-    if (!noise) {
-      if (live && j < total) lat[j] = canonical_f32(o);
-      __syncthreads();
-      if (base - 624 + kMtRound >= total) break;
-      continue;
-    }
-    const uint32_t o1 = __shfl_down_sync(0xffffffffu, o, 1);
-    const uint32_t o2 = __shfl_down_sync(0xffffffffu, o, 2);
-    const uint32_t o3 = __shfl_down_sync(0xffffffffu, o, 3);
-    double px = 0, py = 0;
-    const bool acc = live && (i & 3) == 0 && polar_attempt(o, o1, o2, o3, px, py);
-    const unsigned bal = __ballot_sync(0xffffffffu, acc);
-    if (lane == 0) wcnt[warp] = __popc(bal);
-    __syncthreads();
-    int before = 0, round_total = 0;
-#pragma unroll
-    for (int w = 0; w < kMtThreads / 32; ++w) {
-      const int c = wcnt[w];
-      round_total += c;
-      before += w < warp ? c : 0;
-    }
-    if (acc) {
-      const long long k = accepted + before + __popc(bal & ((1u << lane) - 1u));
-      if (k < need) pr[k] = make_double2(px, py);
-    }
-    accepted += round_total;
-    if (accepted >= need) break;
+    if (base - 624 + kMtRound >= limit) break;
   }
+}
+
+// Noise stream, parallel part: polar attempts (4 words each) accepted in
+// order; pixel k takes the k-th accepted attempt (left = y m, right = x m).
+constexpr int kPolarThreads = 256, kPolarPerThread = 4;
+constexpr int kPolarPerBlock = kPolarThreads * kPolarPerThread;
+
+__device__ __forceinline__ int polar_flags(const uint32_t* w, long long a0, long long attempts,
+                                           double* px, double* py) {
+  int mask = 0;
+#pragma unroll
+  for (int q = 0; q < kPolarPerThread; ++q) {
+    const long long a = a0 + q;
+    if (a >= attempts) break;
+    const uint4 o = reinterpret_cast<const uint4*>(w)[a];
+    if (polar_attempt(o.x, o.y, o.z, o.w, px[q], py[q])) mask |= 1 << q;
+  }
+  return mask;
+}
+
+__global__ void __launch_bounds__(kPolarThreads) k_polar_count(const DevScene* scenes,
+                                                               const uint32_t* words,
+                                                               long long nwords, int* counts) {
+  const int b = blockIdx.y;
+  if (!(scenes[b].sigma > 0)) return;
+  const long long attempts = nwords / 4;
+  const long long a0 = (long long)blockIdx.x * kPolarPerBlock + threadIdx.x * kPolarPerThread;
+  double px[kPolarPerThread], py[kPolarPerThread];
+  int c = __popc(polar_flags(words + (size_t)b * nwords, a0, attempts, px, py));
+  for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  __shared__ int wsum[kPolarThreads / 32];
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < kPolarThreads / 32; ++k) t += wsum[k];
+    counts[(size_t)b * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kPolarThreads) k_polar_scatter(
+    const DevScene* scenes, const uint32_t* words, long long nwords, const int* counts,
+    double2* pairs, long long need, int* exhausted) {
+  const int b = blockIdx.y;
+  if (!(scenes[b].sigma > 0)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ long long s_red[kPolarThreads / 32];
+  __shared__ int s_scan[kPolarThreads / 32];
+  // accepted attempts before this block
+  const int* cnt = counts + (size_t)b * gridDim.x;
+  long long before = 0;
+  for (int k = tid; k < (int)blockIdx.x; k += kPolarThreads) before += cnt[k];
+  for (int off = 16; off; off >>= 1) before += __shfl_xor_sync(0xffffffffu, before, off);
+  if (lane == 0) s_red[warp] = before;
+  const long long attempts = nwords / 4;
+  const long long a0 = (long long)blockIdx.x * kPolarPerBlock + tid * kPolarPerThread;
+  double px[kPolarPerThread], py[kPolarPerThread];
+  const int mask = polar_flags(words + (size_t)b * nwords, a0, attempts, px, py);
+  const int c = __popc(mask);
+  int incl = c;  // warp inclusive scan
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) s_scan[warp] = incl;
+  __syncthreads();
+  long long base = 0;
+  int wbase = 0;
+  for (int k = 0; k < kPolarThreads / 32; ++k) {
+    base += s_red[k];
+    wbase += k < warp ? s_scan[k] : 0;
+  }
+  long long k = base + wbase + incl - c;
+  double2* pr = pairs + (size_t)b * need;
+#pragma unroll
+  for (int q = 0; q < kPolarPerThread; ++q)
+    if (mask & (1 << q)) {
+      if (k < need) pr[k] = make_double2(px[q], py[q]);
+      ++k;
+    }
+  if (blockIdx.x == gridDim.x - 1 && tid == kPolarThreads - 1 && k < need)
+    atomicOr(exhausted, 1);  // the drawn words held fewer than `need` accepted attempts
 }
 
 // Ground truth (synth.cpp:103-121): gt disparity, mask, negativity flag.
@@ -344,6 +411,18 @@ void enqueue_scenes(rpd_ctx* ctx, int count, const rpd_scene_spec* specs, float*
   float* lattice = ctx->ws.get<float>("syn_lattice", size_t(count) * L.total);
   const long long need = any_noise ? per : 0;
   double2* pairs = ctx->ws.get<double2>("syn_pairs", size_t(count) * std::max<long long>(need, 1));
+  // attempts drawn: need / (pi/4) + 2% + 4096 (the shortfall is > 20 sigma away;
+  // k_polar_scatter flags it), rounded up to whole polar blocks
+  const long long attempts =
+      any_noise ? ((long long)(need / 0.7853981633974483 * 1.02) + 4096 + kPolarPerBlock - 1) /
+                      kPolarPerBlock * kPolarPerBlock
+                : 0;
+  const long long nwords = 4 * attempts;
+  if (nwords + 624 + kMtRound > 0x7fffffffLL || (long long)L.total > 0x7fffffffLL)
+    throw InvalidArg("generate_scene: image too large for the noise stream");
+  const int polar_blocks = int(attempts / kPolarPerBlock);
+  uint32_t* words = ctx->ws.get<uint32_t>("syn_words", size_t(count) * std::max<long long>(nwords, 1));
+  int* pcounts = ctx->ws.get<int>("syn_pcounts", size_t(count) * std::max(polar_blocks, 1));
   float* smooth = ctx->ws.get<float>("syn_smooth", size_t(count) * per);
   // one pinned staging block: scene table | pothole list | min/max seeds
   const size_t scene_bytes = sizeof(DevScene) * hs.size();
@@ -363,11 +442,19 @@ void enqueue_scenes(rpd_ctx* ctx, int count, const rpd_scene_spec* specs, float*
   const DevScene* dsc = reinterpret_cast<const DevScene*>(dstage);
   const DevPothole* dpot = reinterpret_cast<const DevPothole*>(dstage + scene_bytes);
   unsigned* minmax = reinterpret_cast<unsigned*>(dstage + scene_bytes + pot_bytes);
-  RPD_CK(cudaMemsetAsync(d_negative, 0, sizeof(int) * size_t(count), ctx->stream));
+  RPD_CK(cudaMemsetAsync(d_negative, 0, sizeof(int) * size_t(count + 1), ctx->stream));
 
   k_mt_streams<<<dim3(count, any_noise ? 2 : 1), kMtThreads, 0, ctx->stream>>>(
-      dsc, L.total, lattice, pairs, need);
+      dsc, L.total, lattice, words, int(nwords));
   RPD_LAUNCH_CHECK();
+  if (any_noise) {
+    k_polar_count<<<dim3(polar_blocks, count), kPolarThreads, 0, ctx->stream>>>(dsc, words, nwords,
+                                                                                pcounts);
+    RPD_LAUNCH_CHECK();
+    k_polar_scatter<<<dim3(polar_blocks, count), kPolarThreads, 0, ctx->stream>>>(
+        dsc, words, nwords, pcounts, pairs, need, d_negative + count);
+    RPD_LAUNCH_CHECK();
+  }
   const int px_blocks = int(std::min<long long>((per + 255) / 256, 1024));
   k_truth<<<dim3(px_blocks, count), 256, 0, ctx->stream>>>(dsc, dpot, h, w, d_gt, d_mask,
                                                           d_negative);
@@ -457,11 +544,12 @@ rpd_status rpd_generate_scene(rpd_ctx* ctx, const rpd_scene_spec* spec, float* l
     float* dr = ctx->ws.get<float>("syn_right", n);
     float* dg = ctx->ws.get<float>("syn_gt", n);
     int32_t* dm = ctx->ws.get<int32_t>("syn_mask", n);
-    int* neg = ctx->ws.get<int>("syn_neg", 1);
+    int* neg = ctx->ws.get<int>("syn_neg", 2);
     enqueue_scenes(ctx, 1, spec, dl, dr, dg, dm, neg);
-    int hneg = 0;
-    download(ctx, &hneg, neg, sizeof(int));
-    if (hneg) throw Degenerate("generate_scene: pothole depth drives disparity negative");
+    int hneg[2] = {0, 0};
+    download(ctx, hneg, neg, sizeof(hneg));
+    if (hneg[0]) throw Degenerate("generate_scene: pothole depth drives disparity negative");
+    if (hneg[1]) throw CudaFail("generate_scene: noise stream exhausted");
     if (left) download(ctx, left, dl, sizeof(float) * n);
     if (right) download(ctx, right, dr, sizeof(float) * n);
     if (gt_disparity) download(ctx, gt_disparity, dg, sizeof(float) * n);
@@ -476,10 +564,11 @@ rpd_status rpd_generate_scenes_device(rpd_ctx* ctx, int count, const rpd_scene_s
     if (count < 1 || !specs) throw InvalidArg("generate_scenes: count must be >= 1");
     if (!d_left || !d_right || !d_gt || !d_mask)
       throw InvalidArg("generate_scenes: null device buffer");
-    int* neg = ctx->ws.get<int>("syn_negs", size_t(count));
+    int* neg = ctx->ws.get<int>("syn_negs", size_t(count) + 1);
     enqueue_scenes(ctx, count, specs, d_left, d_right, d_gt, d_mask, neg);
-    int* hneg = static_cast<int*>(ctx->pinned.get(sizeof(int) * size_t(count)));
-    download(ctx, hneg, neg, sizeof(int) * size_t(count));
+    int* hneg = static_cast<int*>(ctx->pinned.get(sizeof(int) * (size_t(count) + 1)));
+    download(ctx, hneg, neg, sizeof(int) * (size_t(count) + 1));
+    if (hneg[count]) throw CudaFail("generate_scene: noise stream exhausted");
     for (int b = 0; b < count; ++b)
       if (hneg[b])
         throw Degenerate("generate_scene: pothole depth drives disparity negative (scene " +

@@ -17,6 +17,11 @@
 #else
 #define RPD_HD inline
 #endif
+#ifdef __CUDA_ARCH__
+#define RPD_UNROLL _Pragma("unroll")
+#else
+#define RPD_UNROLL
+#endif
 
 namespace rpd_synth {
 
@@ -41,8 +46,8 @@ RPD_HD uint32_t mt_twist(uint32_t xm, uint32_t xm1) {
 // nearest in-round dependency is x[n-623] through t[n-624]; 620 keeps rounds
 // aligned to the 4 draws of a polar attempt).  x(i) / t(i) read the history.
 constexpr int kMtRound = 620;
-template <class XF, class TF>
-RPD_HD uint32_t mt_word(long long n, XF x, TF t) {
+template <class I, class XF, class TF>
+RPD_HD uint32_t mt_word(I n, XF x, TF t) {
   if (n < 851) return x(n - 227) ^ t(n - 624);
   if (n < 1078) return x(n - 454) ^ t(n - 851) ^ t(n - 624);
   return x(n - 681) ^ t(n - 1078) ^ t(n - 851) ^ t(n - 624);
@@ -120,13 +125,6 @@ RPD_HD Dd dd_div(Dd a, Dd b) {
   const double q2 = r.hi / b.hi;
   return dd_fast_two_sum(q1, q2);
 }
-// 1 / (2k + 1) as a double-double.
-RPD_HD Dd dd_recip_odd(int k) {
-  const double d = 2.0 * k + 1.0;
-  const double h = 1.0 / d;
-  return {h, fma(-h, d, 1.0) / d};
-}
-
 RPD_HD double log_dd(double r2) {
   // r2 = m 2^e with m in [sqrt(1/2), sqrt(2))
   int e = 0;
@@ -140,11 +138,27 @@ RPD_HD double log_dd(double r2) {
   const Dd den = dd_two_sum(m, 1.0);
   const Dd s = dd_div(num, den);
   const Dd s2 = dd_mul(s, s);
-  // P(s2) = sum_k s2^k / (2k+1): tail k >= 6 in double, head in double-double
-  double tail = 1.0 / 45.0;
-  for (int k = 21; k >= 6; --k) tail = tail * s2.hi + 1.0 / (2.0 * k + 1.0);
+  // P(s2) = sum_k s2^k / (2k+1): tail k = 22..6 in double, head k = 5..0 in
+  // double-double (coefficients: 1/(2k+1) correctly rounded, plus the residual)
+  const double tail_c[17] = {
+      0.022222222222222223, 0.023255813953488372, 0.024390243902439025, 0.02564102564102564,
+      0.02702702702702703, 0.02857142857142857, 0.030303030303030304, 0.03225806451612903,
+      0.034482758620689655, 0.037037037037037035, 0.04, 0.043478260869565216,
+      0.047619047619047616, 0.05263157894736842, 0.058823529411764705, 0.06666666666666667,
+      0.07692307692307693};
+  double tail = tail_c[0];
+RPD_UNROLL
+  for (int k = 1; k < 17; ++k) tail = tail * s2.hi + tail_c[k];
+  const Dd head_c[6] = {
+      {0.09090909090909091, -2.523234146875356e-18},
+      {0.1111111111111111, 6.1679056923619804e-18},
+      {0.14285714285714285, 7.93016446160826e-18},
+      {0.2, -1.1102230246251566e-17},
+      {0.3333333333333333, 1.850371707708594e-17},
+      {1.0, 0.0}};
   Dd p = {tail, 0.0};
-  for (int k = 5; k >= 0; --k) p = dd_add(dd_mul(p, s2), dd_recip_odd(k));
+RPD_UNROLL
+  for (int k = 0; k < 6; ++k) p = dd_add(dd_mul(p, s2), head_c[k]);
   Dd lm = dd_mul(s, p);
   lm.hi *= 2.0;
   lm.lo *= 2.0;

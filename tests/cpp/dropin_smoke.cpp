@@ -108,6 +108,20 @@ int main() {
     CHECK(c.size() == 1 && std::fabs(c[0].z - 12.0f) < 1e-5f);
     CHECK(closest_distance_error(c, c) == 0.0);
   }
+  {  // test_synth.cpp:46-61, 131-147
+    SceneSpec spec;
+    spec.width = 160;
+    spec.height = 120;
+    spec.texture_seed = 42;
+    spec.potholes.push_back({80.0, 60.0, 18.0, 12.0, 3.0});
+    SceneTruth sc = generate_scene(spec);
+    CHECK(sc.gt_mask(60, 80) == 1 && sc.gt_mask(60, 100) == 0);
+    CHECK(std::fabs(sc.gt_disparity(60, 80) - (road_disparity_at({5.0, 0.08, 0.0}, 80, 60) - 3.0)) <
+          1e-5);
+    std::vector<SceneTruth> batch = scene_batch(2, 900);
+    CHECK(batch.size() == 2 && !batch[0].spec.potholes.empty());
+    CHECK(batch[1].left.rows() == 480 && batch[1].left.cols() == 640);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
