@@ -762,6 +762,208 @@ __global__ void __launch_bounds__(kWtaPx) k_wta_tiled(const __grid_constant__ Wt
   a.disp[p] = r;
 }
 
+// Bulk WTA: both reference volumes of a pass in one launch (blockIdx.z), the
+// words per pixel NW a compile-time constant.  An elected thread copies the P
+// per-path row segments of the CTA's TP-pixel tile into shared memory with
+// one-dimensional bulk async copies (cp.async.bulk, mbarrier completion: the
+// whole tile is in flight at once, no load instructions), then every thread
+// owns one pixel: its P x NW words are summed into 2*NW exact u16x2 level
+// pairs in registers and select_disparity's rules are applied with packed
+// min / compare instructions.  Identical results to k_wta_tiled (parity
+// dumps keep that kernel).
+namespace {
+
+__device__ __forceinline__ uint32_t wta_smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int NW>
+struct WtaGeo {
+  static constexpr int TP = NW <= 9 ? 128 : 64;                 // pixels per CTA
+  static constexpr int V = NW % 4 == 0 ? 4 : (NW % 2 == 0 ? 2 : 1);  // words per LDS
+  static constexpr int NP = 2 * NW;                              // u16x2 level pairs
+};
+
+}  // namespace
+
+struct WtaBulkArgs {
+  const uint8_t* path[2][8];
+  float* disp[2];
+  int w;
+  size_t pitch;
+  int lw, levels;
+};
+
+template <int P, int NW>
+__global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_constant__ WtaBulkArgs a) {
+  using GE = WtaGeo<NW>;
+  constexpr int TP = GE::TP, V = GE::V, NP = GE::NP;
+  extern __shared__ __align__(16) uint32_t tile[];  // [P][TP * NW] words
+  __shared__ __align__(8) uint64_t bar;
+  const int vol = blockIdx.z;
+  const int row = blockIdx.y;
+  const int u0 = blockIdx.x * TP;
+  const int npx = min(TP, a.w - u0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wta_smem_addr(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // row segments start 16-byte aligned (pitch and u0 * lw are multiples of
+    // 16); the size is rounded up to 16 inside the row pitch
+    const uint32_t bytes = uint32_t(npx * NW * 4 + 15) & ~15u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wta_smem_addr(&bar)),
+                 "r"(bytes * P)
+                 : "memory");
+    const size_t off = size_t(row) * a.pitch + size_t(u0) * (NW * 4);
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              wta_smem_addr(tile + r * (TP * NW))),
+          "l"(a.path[vol][r] + off), "r"(bytes), "r"(wta_smem_addr(&bar))
+          : "memory");
+  }
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WTA_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WTA_WAIT_%=;\n"
+      "}\n" ::"r"(wta_smem_addr(&bar))
+      : "memory");
+  const int t = threadIdx.x;
+  if (t >= npx) return;
+  // exact per-level sums over the P paths, two levels per u16x2 word
+  uint32_t s[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) s[q] = 0u;
+#pragma unroll
+  for (int r = 0; r < P; r += 2) {
+    const uint32_t* pa = tile + r * (TP * NW) + t * NW;
+    const uint32_t* pb = pa + TP * NW;
+#pragma unroll
+    for (int j = 0; j < NW; j += V) {
+      uint32_t xa[V], xb[V];
+      if constexpr (V == 4) {
+        const uint4 ua = *reinterpret_cast<const uint4*>(pa + j);
+        const uint4 ub = *reinterpret_cast<const uint4*>(pb + j);
+        xa[0] = ua.x; xa[1] = ua.y; xa[2] = ua.z; xa[3] = ua.w;
+        xb[0] = ub.x; xb[1] = ub.y; xb[2] = ub.z; xb[3] = ub.w;
+      } else if constexpr (V == 2) {
+        const uint2 ua = *reinterpret_cast<const uint2*>(pa + j);
+        const uint2 ub = *reinterpret_cast<const uint2*>(pb + j);
+        xa[0] = ua.x; xa[1] = ua.y;
+        xb[0] = ub.x; xb[1] = ub.y;
+      } else {
+        xa[0] = pa[j];
+        xb[0] = pb[j];
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const int q = 2 * (j + e);
+        s[q] = s[q] + __byte_perm(xa[e], 0u, 0x4140) + __byte_perm(xb[e], 0u, 0x4140);
+        s[q + 1] = s[q + 1] + __byte_perm(xa[e], 0u, 0x4342) + __byte_perm(xb[e], 0u, 0x4342);
+      }
+    }
+  }
+  // select_disparity (sgm.cpp:123-153): minimum, its FIRST level, its
+  // multiplicity and the sums at best -+ 1, over the levels < L only
+  const int L = a.levels;
+  const int np = (L + 1) >> 1;
+  const uint32_t hpad = (L & 1) ? 0xFFFF0000u : 0u;  // invalid high half of the last pair
+#pragma unroll
+  for (int q = 0; q < NP; ++q) s[q] = q < np ? (s[q] | (q == np - 1 ? hpad : 0u)) : 0xFFFFFFFFu;
+  uint32_t m2 = 0xFFFFFFFFu;
+#pragma unroll
+  for (int q = 0; q < NP; q += 2) m2 = __vimin3_u16x2(m2, s[q], q + 1 < NP ? s[q + 1] : 0xFFFFFFFFu);
+  const uint32_t minv = min(m2 & 0xFFFFu, m2 >> 16);
+  const uint32_t mx2 = minv * 0x10001u;
+  int cnt = 0, bq = 0, bh = 0;
+#pragma unroll
+  for (int q = NP - 1; q >= 0; --q) {  // descending: the last hit is the first level
+    const uint32_t eq = __vcmpeq2(s[q], mx2);
+    cnt += __popc(eq);
+    if (eq) {
+      bq = q;
+      bh = (eq & 1u) ^ 1u;
+    }
+  }
+  cnt >>= 4;
+  const int best = 2 * bq + bh;
+  uint32_t sbm1 = 0u, sbp1 = 0u;
+  const int qm = (best - 1) >> 1, qp = (best + 1) >> 1;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    if (q == qm) sbm1 = s[q];
+    if (q == qp) sbp1 = s[q];
+  }
+  sbm1 = best > 0 ? ((sbm1 >> (16 * ((best - 1) & 1))) & 0xFFFFu) : 0u;
+  sbp1 = best + 1 < L ? ((sbp1 >> (16 * ((best + 1) & 1))) & 0xFFFFu) : 0u;
+  const int near = (best + 1 < L && sbp1 == minv) ? 1 : 0;
+  float res;
+  if (cnt - 1 - near > 0) {
+    res = kInvalid;
+  } else {
+    res = float(best);
+    if (best > 0 && best < L - 1) {
+      const float cm = float(sbm1), cb = float(minv), cp = float(sbp1);
+      const float denom = cm + cp - 2.0f * cb;
+      if (denom > 0.0f) res += (cm - cp) / (2.0f * denom);
+    }
+  }
+  a.disp[vol][(long long)row * a.w + u0 + t] = res;
+}
+
+namespace {
+using WtaBulkKernel = void (*)(WtaBulkArgs);
+struct WtaBulkInfo {
+  WtaBulkKernel fn = nullptr;
+  int tp = 0;
+  int smem = 0;
+};
+
+template <int P, int NW>
+WtaBulkInfo wta_bulk_info() {
+  return WtaBulkInfo{k_wta_bulk<P, NW>, WtaGeo<NW>::TP, P * WtaGeo<NW>::TP * NW * 4};
+}
+
+template <int P>
+WtaBulkInfo wta_bulk_pick(int nw) {
+  switch (nw) {
+    case 1: return wta_bulk_info<P, 1>();
+    case 2: return wta_bulk_info<P, 2>();
+    case 3: return wta_bulk_info<P, 3>();
+    case 4: return wta_bulk_info<P, 4>();
+    case 5: return wta_bulk_info<P, 5>();
+    case 6: return wta_bulk_info<P, 6>();
+    case 7: return wta_bulk_info<P, 7>();
+    case 8: return wta_bulk_info<P, 8>();
+    case 9: return wta_bulk_info<P, 9>();
+    case 20: return wta_bulk_info<P, 20>();
+    case 24: return wta_bulk_info<P, 24>();
+    case 28: return wta_bulk_info<P, 28>();
+    case 32: return wta_bulk_info<P, 32>();
+    case 36: return wta_bulk_info<P, 36>();
+    default: return WtaBulkInfo{};
+  }
+}
+
+// Both volumes of a pass; false when the layout has no bulk instantiation.
+bool launch_wta_bulk(const WtaBulkArgs& wa, int paths, int h, int w, cudaStream_t st) {
+  if (std::getenv("RPD_WTA_TILED")) return false;  // A/B: the previous two-launch WTA
+  const int nw = wa.lw / 4;
+  const WtaBulkInfo ki = paths == 8 ? wta_bulk_pick<8>(nw) : (paths == 4 ? wta_bulk_pick<4>(nw)
+                                                                          : WtaBulkInfo{});
+  if (!ki.fn) return false;
+  RPD_CK(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ki.smem));
+  ki.fn<<<dim3(cdiv(w, ki.tp), h, 2), ki.tp, ki.smem, st>>>(wa);
+  RPD_LAUNCH_CHECK();
+  return true;
+}
+}  // namespace
+
 // ------------------------------------------- LR check + post filters ----
 // consistency_filter (sgm.cpp:155-170), flat raw cost curve (:200-212),
 // best sample out of view (:216-222), restore_disparity (perspective.hpp:69-80).
@@ -1062,7 +1264,20 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
       ctx->agg_cells[pass] = cells;
       ctx->agg_pass = pass + 1;
     }
-    for (int vol = 0; vol < 2; ++vol) {
+    bool wta_done = false;
+    if (!dump) {
+      WtaBulkArgs wb{};
+      for (int vol = 0; vol < 2; ++vol)
+        for (int r = 0; r < paths; ++r) wb.path[vol][r] = pathbuf + size_t(vol * paths + r) * vb;
+      wb.disp[0] = dl;
+      wb.disp[1] = dr;
+      wb.w = w;
+      wb.pitch = L.pitch;
+      wb.lw = L.lw;
+      wb.levels = levels;
+      wta_done = launch_wta_bulk(wb, paths, h, w, st);
+    }
+    for (int vol = 0; vol < 2 && !wta_done; ++vol) {
       WtaArgs wa{};
       for (int r = 0; r < paths; ++r) wa.path[r] = pathbuf + size_t(vol * paths + r) * vb;
       wa.paths = paths;
