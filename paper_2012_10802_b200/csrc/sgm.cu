@@ -369,6 +369,134 @@ __global__ void k_cost_u8_flat(const uint64_t* __restrict__ cl, const uint64_t* 
   }
 }
 
+// Pixel-major cost volumes for census windows of <= 24 bits (3x3, 5x5) and a
+// compile-time word count NW.  One CTA per image row; each staged census entry
+// carries its own override: {word | ov << 24, ov ? ~0 : 0} with ov set for
+// out-of-row pixels (and, on the right view, out-of-view ones), so a cost is
+// LDS.64 + LOP3 ((a ^ e) | m) + POPC + IMNMX: an overridden entry counts 32
+// bits, clamped to maxc exactly as the reference substitutes it (a valid
+// count never exceeds maxc).  A thread owns one pixel and all its levels, the
+// row chunk's words are staged in shared memory and written back coalesced.
+template <int NW>
+__global__ void __launch_bounds__(256)
+    k_cost_px(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
+              const uint8_t* __restrict__ iv, int w, int levels, size_t pitch_words,
+              uint32_t maxc, uint32_t* __restrict__ vol_l, uint32_t* __restrict__ vol_r) {
+  constexpr int TPX = 256;
+  constexpr int PAD = 4 * NW;  // every stored level, padding ones included, reads in range
+  constexpr int V = NW % 4 == 0 ? 4 : (NW % 2 == 0 ? 2 : 1);  // words per shared store
+  extern __shared__ __align__(16) uint32_t csx[];
+  const int W = w + 2 * PAD;
+  uint2* s_r = reinterpret_cast<uint2*>(csx) + PAD;          // right-view entries, x in [-PAD, w+PAD)
+  uint2* s_l = reinterpret_cast<uint2*>(csx) + W + PAD;      // left-view entries
+  uint32_t* o_l = csx + 4 * W;                               // [TPX * NW] words per volume
+  uint32_t* o_r = o_l + TPX * NW;
+  const int v = blockIdx.x;
+  const long long row = (long long)v * w;
+  for (int x = int(threadIdx.x) - PAD; x < w + PAD; x += blockDim.x) {
+    const bool in = x >= 0 && x < w;
+    const uint32_t a = in ? uint32_t(cl[row + x]) : 0u;
+    const uint32_t b = in ? uint32_t(cr[row + x]) : 0u;
+    const bool ovr = !in || !iv[row + x];
+    s_r[x] = ovr ? make_uint2(b | 0xFF000000u, 0xFFFFFFFFu) : make_uint2(b, 0u);
+    s_l[x] = in ? make_uint2(a, 0u) : make_uint2(0xFF000000u, 0xFFFFFFFFu);
+  }
+  __syncthreads();
+  uint32_t* gl = vol_l + size_t(v) * pitch_words;
+  uint32_t* gr = vol_r + size_t(v) * pitch_words;
+  for (int u0 = 0; u0 < w; u0 += TPX) {
+    const int npx = min(TPX, w - u0);
+    const int t = threadIdx.x;
+    if (t < npx) {
+      const int u = u0 + t;
+      const uint32_t a = s_l[u].x;        // left census of u (in row: no override)
+      const uint2 eb = s_r[u];
+      const uint32_t b = eb.x & 0xFFFFFFu;
+      const bool ovu = eb.y != 0u;        // right reference: own pixel out of view -> all maxc
+      const uint2* pr = s_r + u;
+      const uint2* pl = s_l + u;
+#pragma unroll
+      for (int j0 = 0; j0 < NW; j0 += V) {
+        uint32_t bl[V], br[V];
+#pragma unroll
+        for (int jj = 0; jj < V; ++jj) {
+          const int j = j0 + jj;
+          uint32_t cL[4], cR[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int d = 4 * j + q;
+            const uint2 e = pr[-d];
+            const uint2 f = pl[d];
+            cL[q] = min(uint32_t(__popc((a ^ e.x) | e.y)), maxc);
+            cR[q] = min(uint32_t(__popc((f.x ^ b) | f.y)), maxc);
+          }
+          uint32_t wl = __byte_perm(__byte_perm(cL[0], cL[1], 0x0040),
+                                    __byte_perm(cL[2], cL[3], 0x0040), 0x5410);
+          uint32_t wr = __byte_perm(__byte_perm(cR[0], cR[1], 0x0040),
+                                    __byte_perm(cR[2], cR[3], 0x0040), 0x5410);
+          if (ovu) wr = maxc * 0x01010101u;
+          if (4 * j + 3 >= levels) {  // padding levels (the last words only)
+            const int k = levels - 4 * j;  // valid bytes in this word, <= 3
+            const uint32_t keep = k <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * k));
+            wl = (wl & keep) | ~keep;
+            wr = (wr & keep) | ~keep;
+          }
+          bl[jj] = wl;
+          br[jj] = wr;
+        }
+        if constexpr (V == 4) {
+          *reinterpret_cast<uint4*>(o_l + t * NW + j0) = make_uint4(bl[0], bl[1], bl[2], bl[3]);
+          *reinterpret_cast<uint4*>(o_r + t * NW + j0) = make_uint4(br[0], br[1], br[2], br[3]);
+        } else if constexpr (V == 2) {
+          *reinterpret_cast<uint2*>(o_l + t * NW + j0) = make_uint2(bl[0], bl[1]);
+          *reinterpret_cast<uint2*>(o_r + t * NW + j0) = make_uint2(br[0], br[1]);
+        } else {
+          o_l[t * NW + j0] = bl[0];
+          o_r[t * NW + j0] = br[0];
+        }
+      }
+    }
+    __syncthreads();
+    const int nwords = npx * NW;
+    uint32_t* dl = gl + size_t(u0) * NW;
+    uint32_t* dr = gr + size_t(u0) * NW;
+    const int nvec = nwords >> 2;  // u0 * NW * 4 bytes and the pitch are 16-byte multiples
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+      reinterpret_cast<uint4*>(dl)[i] = reinterpret_cast<const uint4*>(o_l)[i];
+      reinterpret_cast<uint4*>(dr)[i] = reinterpret_cast<const uint4*>(o_r)[i];
+    }
+    for (int i = 4 * nvec + threadIdx.x; i < nwords; i += blockDim.x) {
+      dl[i] = o_l[i];
+      dr[i] = o_r[i];
+    }
+    __syncthreads();
+  }
+}
+
+namespace {
+using CostPxKernel = void (*)(const uint64_t*, const uint64_t*, const uint8_t*, int, int, size_t,
+                              uint32_t, uint32_t*, uint32_t*);
+CostPxKernel cost_px_pick(int nw) {
+  switch (nw) {
+    case 1: return k_cost_px<1>;
+    case 2: return k_cost_px<2>;
+    case 3: return k_cost_px<3>;
+    case 4: return k_cost_px<4>;
+    case 5: return k_cost_px<5>;
+    case 6: return k_cost_px<6>;
+    case 7: return k_cost_px<7>;
+    case 8: return k_cost_px<8>;
+    case 9: return k_cost_px<9>;
+    case 20: return k_cost_px<20>;
+    case 24: return k_cost_px<24>;
+    case 28: return k_cost_px<28>;
+    case 32: return k_cost_px<32>;
+    case 36: return k_cost_px<36>;
+    default: return nullptr;
+  }
+}
+}  // namespace
+
 // u8 volume (row pitch, pixel stride lw) -> float reference layout (parity dumps only).
 __global__ void k_u8vol_to_f32(const uint8_t* __restrict__ vol, int w, long long npix,
                                size_t pitch, int lw, int levels, float* __restrict__ out) {
@@ -1210,7 +1338,15 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     {
       const bool narrow = window * window - 1 <= 32;
       const int smem = (w + 2 * levels) * (narrow ? 9 : 17);
-      if (smem <= 200 * 1024) {
+      const CostPxKernel pxfn = window <= 5 ? cost_px_pick(nw) : nullptr;
+      const int pxsmem = (w + 8 * nw) * 16 + 2 * 256 * nw * 4;
+      if (pxfn && pxsmem <= 200 * 1024 && !std::getenv("RPD_COST_ROWS")) {
+        if (pxsmem > 48 * 1024)
+          RPD_CK(cudaFuncSetAttribute(pxfn, cudaFuncAttributeMaxDynamicSharedMemorySize, pxsmem));
+        pxfn<<<h, 256, pxsmem, st>>>(cl, cr, iv, w, levels, L.pitch / 4, uint32_t(window * window - 1),
+                                     reinterpret_cast<uint32_t*>(vol_l),
+                                     reinterpret_cast<uint32_t*>(vol_r));
+      } else if (smem <= 200 * 1024) {
         auto* kfn = narrow ? k_cost_u8<uint32_t> : k_cost_u8<uint64_t>;
         if (smem > 48 * 1024)
           RPD_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
