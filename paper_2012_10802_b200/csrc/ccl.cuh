@@ -270,6 +270,40 @@ __device__ __forceinline__ Acc128 to_fixed(float x, int* inexact) {
   return r;
 }
 
+// Warp run sum of `x` (per contiguous key run, see run_info) added to the
+// run's AccSum by its head lane.  Fast path when every participating value is
+// 0 or has an exponent field in [110, 140] (2^-17 <= |x| < 2^14): then x * 2^40
+// is an exact int64 below 2^54 and a run of <= 32 of them stays below 2^59, so
+// the run is summed in one 64-bit word and lands in the accumulator as
+// s * 2^60 (a1 and a2 words; its a0 part is zero).  Otherwise the 128-bit
+// fixed-point path.  Both give the same exact total.
+__device__ __forceinline__ void run_add_value(AccSum* sx, int key, bool active, float x,
+                                              const RunInfo& ri, int* inexact) {
+  const uint32_t b = __float_as_uint(x);
+  const int e = int((b >> 23) & 0xFFu);
+  const bool zero = !active || (b << 1) == 0u;
+  const bool fast = zero || (e >= 110 && e <= 140);
+  if (__all_sync(0xFFFFFFFFu, fast)) {
+    long long v = 0;
+    if (!zero) {
+      v = (long long)((b & 0x7FFFFFu) | 0x800000u) << (e - 110);
+      if (b >> 31) v = -v;
+    }
+    v = run_sum(v, ri);
+    if (ri.head) {
+      const unsigned long long a1 = ((unsigned long long)v << 60) >> 32;
+      if (a1) atomicAdd(&sx[key].a1, a1);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sx[key].a2), (unsigned long long)(v >> 4));
+    }
+  } else {
+    int bad = 0;
+    Acc128 ax = active ? to_fixed(x, &bad) : Acc128{0ull, 0ll};
+    if (bad) atomicOr(inexact, 1);
+    ax = run_sum(ax, ri);
+    if (ri.head) red_add_acc(&sx[key], ax);
+  }
+}
+
 // Correctly rounded double of (a * 2^-100).
 __device__ __forceinline__ double fixed_to_double(Acc128 a) {
   const bool neg = a.hi < 0;

@@ -219,7 +219,8 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 // and — when SUMS — the pixel's (1, u, v, value) is added to its label's sums
 // with warp run aggregation (a warp is one tile row).  Pixels without a window
 // are left for the fallback kernel, which adds their sums itself.
-constexpr int kTileU = 32, kTileV = 16, kMaxTileCenters = 384;
+constexpr int kTileU = 32, kTileV = 16, kMaxTileCenters = 192;
+constexpr int kRowCap = 40;  // candidate records per tile row (more: per-pixel bucket walk)
 constexpr int kAssignThreads = 256;
 #ifndef RPD_ASSIGN_MINB
 #define RPD_ASSIGN_MINB 6  // resident CTAs per SM the register budget targets
@@ -234,7 +235,8 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   // candidate c: s_cd[2c] = (cu, cv), s_cd[2c+1] = (val, icu | k << 32)
   __shared__ double2 s_cd[2 * kMaxTileCenters];
   __shared__ int s_icv[kMaxTileCenters];
-  __shared__ unsigned short s_row[kTileV][kMaxTileCenters];  // per tile row: candidates reaching it
+  // per tile row, the candidates whose window reaches it: {cu, (v - cv)^2}, {val, icu | k << 32}
+  __shared__ double2 s_rec[kTileV][2 * kRowCap];
   const int tx = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
   const int u = u0 + tx;
@@ -293,15 +295,31 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     }
   }
   __syncthreads();
-  const int nc = s_cnt;
-  if (nc <= kMaxTileCenters) {  // distribute the candidates over the rows they reach
+  int nc = s_cnt;
+  if (nc <= kMaxTileCenters) {
+    // distribute the candidates over the rows they reach, with the row's
+    // (v - cv)^2 precomputed (the reference's dv * dv, segmentation.cpp:48)
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
       const int icv = s_icv[i];
       const int r0 = max(icv - win, v0) - v0, r1 = min(icv + win, v0 + kTileV - 1) - v0;
-      for (int r = r0; r <= r1; ++r) s_row[r][atomicAdd(&s_rowcnt[r], 1)] = (unsigned short)i;
+      const double2 cuv = s_cd[2 * i], vk = s_cd[2 * i + 1];
+      for (int r = r0; r <= r1; ++r) {
+        const int slot = atomicAdd(&s_rowcnt[r], 1);
+        if (slot < kRowCap) {
+          const double dv = double(v0 + r) - cuv.y;
+          s_rec[r][2 * slot] = make_double2(cuv.x, dv * dv);
+          s_rec[r][2 * slot + 1] = vk;
+        }
+      }
     }
   }
   __syncthreads();
+  if (nc <= kMaxTileCenters) {  // a row list overflowed: per-pixel bucket walk for the tile
+    bool over = false;
+#pragma unroll
+    for (int r = 0; r < kTileV; ++r) over |= s_rowcnt[r] > kRowCap;
+    if (over) nc = kMaxTileCenters + 1;
+  }
 #pragma unroll
   for (int q = 0; q < kRowsPerWarp; ++q) {
     const int ty = wid + 8 * q;
@@ -312,18 +330,17 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     double best = __longlong_as_double(0x7FF0000000000000ll);
     int bk = -1;
     if (nc <= kMaxTileCenters) {
-      const double du0 = double(u), dv0 = double(v), sw = a.sw;
+      const double du0 = double(u), sw = a.sw;
       const int nr = s_rowcnt[ty];
       const unsigned span = 2u * unsigned(win);
       for (int j = 0; j < nr; ++j) {
-        const unsigned i = s_row[ty][j];
-        const double2 cuv = s_cd[2 * i];
-        const double2 vk = s_cd[2 * i + 1];
+        const double2 cd = s_rec[ty][2 * j];      // cu, (v - cv)^2
+        const double2 vk = s_rec[ty][2 * j + 1];  // val, icu | k << 32
         const unsigned long long ik = (unsigned long long)__double_as_longlong(vk.y);
         const int icu = int(uint32_t(ik)), k = int(ik >> 32);
         const double dval = x - vk.x;
-        const double du = du0 - cuv.x, dv = dv0 - cuv.y;
-        const double dist = dval * dval + (du * du + dv * dv) * sw;
+        const double du = du0 - cd.x;
+        const double dist = dval * dval + (du * du + cd.y) * sw;
         // |u - icu| <= win, branch-free; lexicographic (dist, k) minimum
         const bool inw = unsigned(u - icu + win) <= span;
         const bool take = inw & ((dist < best) | ((dist == best) & (k < bk)));
@@ -348,10 +365,7 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     if (SUMS) {
       const int key = label > 0 ? label : -1;
       const RunInfo ri = run_info(key);
-      int bad = 0;
-      Acc128 ax = key > 0 ? to_fixed(xf[q], &bad) : Acc128{0ull, 0ll};
-      if (bad) atomicOr(a.inexact, 1);
-      ax = run_sum(ax, ri);
+      run_add_value(s.sx, key, key > 0, xf[q], ri, a.inexact);
       // a run is a contiguous pixel segment of one row: count and coordinate
       // sums follow from its bounds
       const int cnt = ri.end - tx + 1;
@@ -359,7 +373,6 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
       const long long sv = (long long)cnt * v;
       if (ri.head) {
         atomicAdd(&s.n[key], cnt);
-        red_add_acc(&s.sx[key], ax);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
       }
@@ -430,11 +443,8 @@ __global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __re
       if (l >= 0 && l <= max_label && (!valid_only || x != kInvalid)) key = l;
     }
     const RunInfo ri = run_info(key);
-    int bad = 0;
-    Acc128 ax = key >= 0 ? to_fixed(x, &bad) : Acc128{0ull, 0ll};
-    if (bad) atomicOr(inexact, 1);
+    run_add_value(s.sx, key, key >= 0, x, ri, inexact);
     const int cnt = run_sum(key >= 0 ? 1 : 0, ri);
-    ax = run_sum(ax, ri);
     long long su = 0, sv = 0;
     if (coords) {
       su = run_sum(key >= 0 ? (long long)(p % w) : 0ll, ri);
@@ -442,7 +452,6 @@ __global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __re
     }
     if (ri.head) {
       atomicAdd(&s.n[key], cnt);
-      red_add_acc(&s.sx[key], ax);
       if (coords) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
