@@ -219,13 +219,19 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 // and — when SUMS — the pixel's (1, u, v, value) is added to its label's sums
 // with warp run aggregation (a warp is one tile row).  Pixels without a window
 // are left for the fallback kernel, which adds their sums itself.
-constexpr int kTileU = 32, kTileV = 16, kMaxTileCenters = 192;
-constexpr int kRowCap = 40;  // candidate records per tile row (more: per-pixel bucket walk)
+#ifndef RPD_ASSIGN_TILEV
+#define RPD_ASSIGN_TILEV 32
+#endif
+#ifndef RPD_ASSIGN_ROWCAP
+#define RPD_ASSIGN_ROWCAP 24
+#endif
+constexpr int kTileU = 32, kTileV = RPD_ASSIGN_TILEV, kMaxTileCenters = 192;
+constexpr int kRowCap = RPD_ASSIGN_ROWCAP;  // candidate records per tile row (more: per-pixel bucket walk)
 constexpr int kAssignThreads = 256;
 #ifndef RPD_ASSIGN_MINB
 #define RPD_ASSIGN_MINB 6  // resident CTAs per SM the register budget targets
 #endif
-constexpr int kRowsPerWarp = kTileV / (kAssignThreads / 32);  // a warp owns rows w, w+8
+constexpr int kRowsPerWarp = kTileV / (kAssignThreads / 32);  // a warp owns rows w, w+8, ...
 
 template <bool SUMS>
 __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
