@@ -18,6 +18,7 @@
 // C_R(v,u,d) = C_L(v,u+d,d) is generated directly from the census words.
 
 #include <cfloat>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 
@@ -174,44 +175,55 @@ void launch_restore(const float* d0, const double* shifts, int h, int w, float* 
 }
 
 // census_transform, sgm.cpp:13-34: MSB-first bits over the row-major window,
-// centre skipped, coordinates clamped.
+// centre skipped, coordinates clamped.  A CTA computes a 128 x kCensusRows
+// block; the (rows + 2R) x (128 + 2R) window is staged once with clamped
+// coordinates (== the reference's clamped reads) and each thread walks a
+// column of the block.  Windows of <= 32 bits accumulate in 32-bit words.
+constexpr int kCensusRows = 8;
 template <int R>
 __global__ void __launch_bounds__(128)
     k_census(const float* __restrict__ img0, const float* __restrict__ img1, int h, int w,
              uint64_t* __restrict__ out0, uint64_t* __restrict__ out1) {
+  using Bits = typename std::conditional<((2 * R + 1) * (2 * R + 1) - 1 <= 32), uint32_t,
+                                         uint64_t>::type;
   // blockIdx.z selects the image (both census transforms in one launch)
   const float* __restrict__ img = blockIdx.z ? img1 : img0;
   uint64_t* __restrict__ out = blockIdx.z ? out1 : out0;
-  // the (2R+1) x (128+2R) window of this 128-pixel row segment, staged with
-  // clamped coordinates (== the reference's clamped reads)
   constexpr int TW = 128 + 2 * R;
-  __shared__ float tile[2 * R + 1][TW];
+  constexpr int TH = kCensusRows + 2 * R;
+  __shared__ float tile[TH][TW];
   const int u0 = blockIdx.x * 128;
-  const int v = blockIdx.y;
-  for (int i = threadIdx.x; i < (2 * R + 1) * TW; i += 128) {
-    const int r = i / TW, c = i - r * TW;
-    const int vv = min(max(v + r - R, 0), h - 1), uu = min(max(u0 + c - R, 0), w - 1);
-    tile[r][c] = img[size_t(vv) * w + uu];
+  const int v0 = blockIdx.y * kCensusRows;
+  for (int r = 0; r < TH; ++r) {
+    const int vv = min(max(v0 + r - R, 0), h - 1);
+    const float* src = img + size_t(vv) * w;
+    for (int c = threadIdx.x; c < TW; c += 128) tile[r][c] = src[min(max(u0 + c - R, 0), w - 1)];
   }
   __syncthreads();
   const int u = u0 + threadIdx.x;
   if (u >= w) return;
-  const float c = tile[R][threadIdx.x + R];
-  uint64_t bits = 0;
+  const int t = threadIdx.x + R;
+#pragma unroll 2
+  for (int y = 0; y < kCensusRows; ++y) {
+    const int v = v0 + y;
+    if (v >= h) break;
+    const float c = tile[y + R][t];
+    Bits bits = 0;
 #pragma unroll
-  for (int dv = -R; dv <= R; ++dv) {
+    for (int dv = -R; dv <= R; ++dv) {
 #pragma unroll
-    for (int du = -R; du <= R; ++du) {
-      if (dv == 0 && du == 0) continue;
-      bits = (bits << 1) | (tile[dv + R][threadIdx.x + R + du] < c ? 1ull : 0ull);
+      for (int du = -R; du <= R; ++du) {
+        if (dv == 0 && du == 0) continue;
+        bits = (bits << 1) | (tile[y + R + dv][t + du] < c ? Bits(1) : Bits(0));
+      }
     }
+    out[size_t(v) * w + u] = uint64_t(bits);
   }
-  out[size_t(v) * w + u] = bits;
 }
 
 void launch_census2(const float* img0, const float* img1, int h, int w, int window,
                     uint64_t* out0, uint64_t* out1, cudaStream_t st) {
-  const dim3 grid(cdiv(w, 128), h, img1 ? 2 : 1);
+  const dim3 grid(cdiv(w, 128), cdiv(h, kCensusRows), img1 ? 2 : 1);
   switch (window) {
     case 3: k_census<1><<<grid, 128, 0, st>>>(img0, img1, h, w, out0, out1); break;
     case 5: k_census<2><<<grid, 128, 0, st>>>(img0, img1, h, w, out0, out1); break;
