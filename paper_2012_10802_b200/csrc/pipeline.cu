@@ -144,10 +144,21 @@ int skip_stages() {
   }();
   return m;
 }
+// Marginal-cost attribution (RPD_DUP_STAGES, same bits): the stage is enqueued
+// twice (idempotent: same inputs, same outputs), so the throughput drop is
+// the stage's cost in the concurrent regime.
+int dup_stages() {
+  static const int m = [] {
+    const char* e = std::getenv("RPD_DUP_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
 
 void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const rpd_config& c) {
   cudaStream_t st = ctx->stream;
   const int skip = skip_stages();
+  const int dup = dup_stages();
   const long long n = (long long)h * w;
   reset_status(ctx);
   ctx->agg_pass = 0;
@@ -166,7 +177,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
     launch_half_image(f.left, h, w, f.hl, st, f.right, f.hr);
     rpd_config boot = c;
     boot.d_max = (c.d_max + 1) / 2;
-    if (!(skip & 8))
+    for (int rep = 0; rep < ((dup & 8) ? 2 : 1) && !(skip & 8); ++rep)
       match_pair_dev(ctx, f.hl, f.hr, bh, bw, f.flat, boot, boot.d_max, f.b_d0, f.b_d1,
                      f.b_shifts);
   } else {
@@ -190,7 +201,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   if (!(skip & 1)) fit_dev(ctx, fr);
   record_stage(ctx, 2);
   // pipeline.cpp:76 PT pass
-  if (!(skip & 16))
+  for (int rep = 0; rep < ((dup & 16) ? 2 : 1) && !(skip & 16); ++rep)
     match_pair_dev(ctx, f.left, f.right, h, w, &f.coarse->model, c, c.d_max_pt, f.d0, f.d1,
                    f.shifts);
   record_stage(ctx, 3);
@@ -201,6 +212,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   fr.where = kWhereFitPt;
   fr.out = f.fit;
   if (!(skip & 1)) fit_dev(ctx, fr);
+  if (dup & 1) fit_dev(ctx, fr);
   record_stage(ctx, 4);
   // pipeline.cpp:89-91 disparity transformation
   RPD_CK(cudaMemsetAsync(f.clamped, 0, sizeof(unsigned long long), st));
@@ -216,6 +228,7 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
     return;
   }
   f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations);
+  if (dup & 2) f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations);
   pool_superpixels_dev(ctx, f.d2, f.sp.labels, h, w, f.sp.k_seeds, f.d3);
   record_stage(ctx, 6);
   if (skip & 4) {
@@ -226,8 +239,9 @@ void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const r
   const HistDev hd = build_histogram_dev(ctx, f.d2, h, w, c.hist_bin_width, c.tau_diag);
   find_threshold_dev(ctx, hd, c.hist_bin_width, c.delta_pd, c.tau_diag, f.thr,
                      kWhereThresholdEmpty);
-  detect_potholes_dev(ctx, f.d3, f.sp.labels, f.sp.spacing, h, w, f.thr, c.border_margin,
-                      c.min_superpixels, c.connectivity, f.labels, f.n_potholes);
+  for (int rep = 0; rep < ((dup & 4) ? 2 : 1); ++rep)
+    detect_potholes_dev(ctx, f.d3, f.sp.labels, f.sp.spacing, h, w, f.thr, c.border_margin,
+                        c.min_superpixels, c.connectivity, f.labels, f.n_potholes);
   record_stage(ctx, 7);
 }
 
