@@ -1020,27 +1020,30 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
   for (int q = 0; q < NP; q += 2) m2 = __vimin3_u16x2(m2, s[q], q + 1 < NP ? s[q + 1] : 0xFFFFFFFFu);
   const uint32_t minv = min(m2 & 0xFFFFu, m2 >> 16);
   const uint32_t mx2 = minv * 0x10001u;
-  int cnt = 0, bq = 0, bh = 0;
+  // per pair: e = min(s - min, 1) per half (no borrow: s >= min in both
+  // halves), i.e. 0 where a level attains the minimum, 1 elsewhere
+  int ne = 0, bq = 0, bh = 0;
 #pragma unroll
   for (int q = NP - 1; q >= 0; --q) {  // descending: the last hit is the first level
-    const uint32_t eq = __vcmpeq2(s[q], mx2);
-    cnt += __popc(eq);
-    if (eq) {
+    const uint32_t e = __vminu2(s[q] - mx2, 0x00010001u);
+    ne += __popc(e);
+    if (e != 0x00010001u) {
       bq = q;
-      bh = (eq & 1u) ^ 1u;
+      bh = int(e & 1u);
     }
   }
-  cnt >>= 4;
+  const int cnt = 2 * NP - ne;
   const int best = 2 * bq + bh;
-  uint32_t sbm1 = 0u, sbp1 = 0u;
-  const int qm = (best - 1) >> 1, qp = (best + 1) >> 1;
+  // the sums at best -+ 1 through shared memory: this thread's own words of
+  // paths 0 and 1 (2 * NW = NP words, read by nobody else) take its pairs
+  uint32_t* own0 = tile + t * NW;
+  uint32_t* own1 = own0 + TP * NW;
 #pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    if (q == qm) sbm1 = s[q];
-    if (q == qp) sbp1 = s[q];
-  }
-  sbm1 = best > 0 ? ((sbm1 >> (16 * ((best - 1) & 1))) & 0xFFFFu) : 0u;
-  sbp1 = best + 1 < L ? ((sbp1 >> (16 * ((best + 1) & 1))) & 0xFFFFu) : 0u;
+  for (int q = 0; q < NP; ++q) (q < NW ? own0[q] : own1[q - NW]) = s[q];
+  auto pair_at = [&](int q) { return q < NW ? own0[q] : own1[q - NW]; };
+  const int qm = (best - 1) >> 1, qp = (best + 1) >> 1;
+  const uint32_t sbm1 = best > 0 ? ((pair_at(qm) >> (16 * ((best - 1) & 1))) & 0xFFFFu) : 0u;
+  const uint32_t sbp1 = best + 1 < L ? ((pair_at(qp) >> (16 * ((best + 1) & 1))) & 0xFFFFu) : 0u;
   const int near = (best + 1 < L && sbp1 == minv) ? 1 : 0;
   float res;
   if (cnt - 1 - near > 0) {

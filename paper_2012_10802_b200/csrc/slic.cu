@@ -321,9 +321,8 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   }
   __syncthreads();
   if (nc <= kMaxTileCenters) {  // a row list overflowed: per-pixel bucket walk for the tile
-    bool over = false;
-#pragma unroll
-    for (int r = 0; r < kTileV; ++r) over |= s_rowcnt[r] > kRowCap;
+    static_assert(kTileV <= 32, "one lane per tile row");
+    const bool over = __any_sync(0xFFFFFFFFu, tx < kTileV && s_rowcnt[tx] > kRowCap);
     if (over) nc = kMaxTileCenters + 1;
   }
 #pragma unroll
