@@ -176,17 +176,37 @@ struct TileAddr {
   static constexpr bool kChunked =
       (TYPE == kVert && GE::NCH > 1) || (TYPE == kDiag && GE::DNCH > 1);
   static constexpr int kStride = TYPE == kHoriz ? GE::WPP : (TYPE == kVert ? GE::ROW : GE::DROW);
+  // word-offset shifts of diagonal rows are 0 whenever a pixel is a whole
+  // number of 16-byte groups: the chunked offsets are then step-invariant
+  static constexpr bool kNoShift = TYPE != kDiag || GE::WPP % 4 == 0;
+  static constexpr bool kPre = kChunked && kNoShift;
   int base;
+  int off[kPre ? WPL : 1], str[kPre ? WPL : 1];
   __device__ __forceinline__ void init(int t, int g) {
     base = (TYPE == kHoriz) ? t * (GE::R * GE::WPP) + g * WPL : t * GE::WPP + g * WPL;
+    if constexpr (kPre) {
+      const int last = TYPE == kVert ? GE::NCH - 1 : GE::DNCH - 1;
+      const int cwl = TYPE == kVert ? GE::CWL : GE::DCWL;
+#pragma unroll
+      for (int q = 0; q < WPL; ++q) {
+        const int wd = base + q, ch = wd >> 8;
+        off[q] = ch * (256 * GE::R) + (wd & 255);
+        str[q] = ch == last ? cwl : 256;
+      }
+    }
   }
   __device__ __forceinline__ int at(int q, int rr, int shift) const {
-    if (!kChunked) return base + shift + q + rr * kStride;
-    const int wd = base + shift + q;
-    const int ch = wd >> 8;
-    const int last = TYPE == kVert ? GE::NCH - 1 : GE::DNCH - 1;
-    const int cwl = TYPE == kVert ? GE::CWL : GE::DCWL;
-    return ch * (256 * GE::R) + rr * (ch == last ? cwl : 256) + (wd & 255);
+    if constexpr (!kChunked) {
+      return base + shift + q + rr * kStride;
+    } else if constexpr (kPre) {
+      return off[q] + rr * str[q];
+    } else {
+      const int wd = base + shift + q;
+      const int ch = wd >> 8;
+      const int last = TYPE == kVert ? GE::NCH - 1 : GE::DNCH - 1;
+      const int cwl = TYPE == kVert ? GE::CWL : GE::DCWL;
+      return ch * (256 * GE::R) + rr * (ch == last ? cwl : 256) + (wd & 255);
+    }
   }
 };
 
