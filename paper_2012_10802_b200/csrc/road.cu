@@ -368,127 +368,133 @@ __device__ __forceinline__ void fit_get(const FitState& F, int m, double& d, dou
 template <int NV, bool DDV>
 __device__ void grid_sum(FitState& F, double (&x)[NV]) {
   static_assert(NV <= kMaxNV && (!DDV || NV % 2 == 0), "values");
+  // Every step below runs element by element (one double, or one
+  // double-double when DDV): the per-element trees are those of the
+  // all-elements formulation, but only one element's temporaries are live
+  // (the register footprint sets how many other CTAs share the fit's SMs).
+  constexpr int ST = DDV ? 2 : 1;
   FitShared& S = *F.S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned flag = ++F.calls;
   unsigned long long* part =
       F.P->part + size_t(flag & 1u) * (kPartReplicas * kFitCtas * kMaxNV * 2);
   const unsigned long long ftag = (unsigned long long)flag << 32;
-  auto plus = [](double (&a)[NV], const double (&b)[NV]) {
+  // a[0..ST) += b[0..ST)
+  auto plus = [](double* a, const double* b) {
     if (DDV) {
-#pragma unroll
-      for (int q = 0; q < NV; q += 2) {
-        const DD r = dd_add(DD{a[q], a[q + 1]}, DD{b[q], b[q + 1]});
-        a[q] = r.hi;
-        a[q + 1] = r.lo;
-      }
+      const DD r = dd_add(DD{a[0], a[1]}, DD{b[0], b[1]});
+      a[0] = r.hi;
+      a[1] = r.lo;
     } else {
-#pragma unroll
-      for (int q = 0; q < NV; ++q) a[q] += b[q];
+      a[0] += b[0];
     }
   };
   fit_tr(F, 3);
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    double o[NV];
+  for (int q = 0; q < NV; q += ST) {
 #pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] = __shfl_down_sync(0xFFFFFFFFu, x[q], off);
-    plus(x, o);
+    for (int off = 1; off < 32; off <<= 1) {
+      double o[ST];
+#pragma unroll
+      for (int c = 0; c < ST; ++c) o[c] = __shfl_down_sync(0xFFFFFFFFu, x[q + c], off);
+      plus(&x[q], o);
+    }
   }
   if (lane == 0)
 #pragma unroll
     for (int q = 0; q < NV; ++q) S.warp_part[warp][q] = x[q];
   __syncthreads();
-  if (threadIdx.x < 32) {  // one warp publishes the CTA partial
-    double p[kFitSweepWarps][NV];
+  if (threadIdx.x < NV) {  // thread q publishes value q of the CTA partial
+    const int q = threadIdx.x;
+    const int e = q - q % ST;
+    double p[kFitSweepWarps][ST];
 #pragma unroll
     for (int r = 0; r < kFitSweepWarps; ++r)
 #pragma unroll
-      for (int q = 0; q < NV; ++q) p[r][q] = S.warp_part[r][q];
+      for (int c = 0; c < ST; ++c) p[r][c] = S.warp_part[r][e + c];
 #pragma unroll
     for (int width = 1; width < kFitSweepWarps; width *= 2)
 #pragma unroll
       for (int j = 0; j < kFitSweepWarps; j += 2 * width) plus(p[j], p[j + width]);
-    if (threadIdx.x < NV) {
-      const int q = threadIdx.x;
-      double val = p[0][0];
+    const double val = p[0][q - e];
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(val);
+    const unsigned long long w0 = ftag | (bits & 0xFFFFFFFFull), w1 = ftag | (bits >> 32);
 #pragma unroll
-      for (int qq = 1; qq < NV; ++qq)
-        if (qq == q) val = p[0][qq];
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(val);
-      const unsigned long long w0 = ftag | (bits & 0xFFFFFFFFull), w1 = ftag | (bits >> 32);
-#pragma unroll
-      for (int rep = 0; rep < kPartReplicas; ++rep) {
-        unsigned long long* dst = part + ((size_t(rep) * kFitCtas + blockIdx.x) * kMaxNV + q) * 2;
-        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
-                     : "memory");
-      }
+    for (int rep = 0; rep < kPartReplicas; ++rep) {
+      unsigned long long* dst = part + ((size_t(rep) * kFitCtas + blockIdx.x) * kMaxNV + q) * 2;
+      asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
+                   : "memory");
     }
   }
   fit_tr(F, 4);
   // combine the kFitCtas partials: thread j holds pair (2j, 2j+1)
   constexpr int kPairs = kFitCtas / 2;
   if (threadIdx.x < kPairs) {
-    double y[NV];
     const unsigned long long* src =
         part + (size_t(blockIdx.x % kPartReplicas) * kFitCtas + 2 * threadIdx.x) * kMaxNV * 2;
     unsigned spins = 0;
-    while (true) {
-      unsigned long long w[2][NV][2];
+    constexpr int kW = kPairs < 32 ? kPairs : 32;
+#pragma unroll 1
+    for (int q = 0; q < NV; q += ST) {
+      double y[ST], b[ST];
+      while (true) {  // element q of both partials, polled until the call's flag shows
+        unsigned long long w[2][ST][2];
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int q = 0; q < NV; ++q)
-          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
-                       : "=l"(w[c][q][0]), "=l"(w[c][q][1])
-                       : "l"(src + (c * kMaxNV + q) * 2)
-                       : "memory");
-      bool ready = true;
+          for (int t = 0; t < ST; ++t)
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                         : "=l"(w[c][t][0]), "=l"(w[c][t][1])
+                         : "l"(src + (c * kMaxNV + q + t) * 2)
+                         : "memory");
+        bool ready = true;
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int q = 0; q < NV; ++q)
-          ready &= (w[c][q][0] >> 32) == flag && (w[c][q][1] >> 32) == flag;
-      if (ready) {
-        double b[NV];
+          for (int t = 0; t < ST; ++t)
+            ready &= (w[c][t][0] >> 32) == flag && (w[c][t][1] >> 32) == flag;
+        if (ready) {
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          y[q] = __longlong_as_double(
-              (long long)((w[0][q][0] & 0xFFFFFFFFull) | (w[0][q][1] << 32)));
-          b[q] = __longlong_as_double(
-              (long long)((w[1][q][0] & 0xFFFFFFFFull) | (w[1][q][1] << 32)));
+          for (int t = 0; t < ST; ++t) {
+            y[t] = __longlong_as_double(
+                (long long)((w[0][t][0] & 0xFFFFFFFFull) | (w[0][t][1] << 32)));
+            b[t] = __longlong_as_double(
+                (long long)((w[1][t][0] & 0xFFFFFFFFull) | (w[1][t][1] << 32)));
+          }
+          break;
         }
-        plus(y, b);
-        break;
+        if (++spins > kSpinLimit) __trap();
       }
-      if (++spins > kSpinLimit) __trap();
+      plus(y, b);
+#pragma unroll
+      for (int off = 1; off < kW; off <<= 1) {
+        double o[ST];
+#pragma unroll
+        for (int t = 0; t < ST; ++t) o[t] = __shfl_down_sync(0xFFFFFFFFu, y[t], off);
+        plus(y, o);
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int t = 0; t < ST; ++t) S.red[warp][q + t] = y[t];
     }
     fit_tr(F, 41);
-    constexpr int kW = kPairs < 32 ? kPairs : 32;
-#pragma unroll
-    for (int off = 1; off < kW; off <<= 1) {
-      double o[NV];
-#pragma unroll
-      for (int q = 0; q < NV; ++q) o[q] = __shfl_down_sync(0xFFFFFFFFu, y[q], off);
-      plus(y, o);
-    }
-    if (lane == 0)
-#pragma unroll
-      for (int q = 0; q < NV; ++q) S.red[warp][q] = y[q];
   }
   __syncthreads();
   constexpr int kRW = (kPairs + 31) / 32;
-  double p[kRW][NV];
 #pragma unroll
-  for (int r = 0; r < kRW; ++r)
+  for (int q = 0; q < NV; q += ST) {
+    double p[kRW][ST];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) p[r][q] = S.red[r][q];
+    for (int r = 0; r < kRW; ++r)
 #pragma unroll
-  for (int width = 1; width < kRW; width *= 2)
+      for (int t = 0; t < ST; ++t) p[r][t] = S.red[r][q + t];
 #pragma unroll
-    for (int j = 0; j < kRW; j += 2 * width) plus(p[j], p[j + width]);
+    for (int width = 1; width < kRW; width *= 2)
 #pragma unroll
-  for (int q = 0; q < NV; ++q) x[q] = p[0][q];
+      for (int j = 0; j < kRW; j += 2 * width) plus(p[j], p[j + width]);
+#pragma unroll
+    for (int t = 0; t < ST; ++t) x[q + t] = p[0][t];
+  }
   __syncthreads();  // S.red / S.warp_part reusable
   fit_tr(F, 5);
 }
@@ -742,7 +748,10 @@ __device__ void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok)
   }
 }
 
-__global__ void __launch_bounds__(kFitThreads, 1) k_fit(const __grid_constant__ FitKParams P) {
+#ifndef RPD_FIT_MINB
+#define RPD_FIT_MINB 8  // 128 registers: the fit shares its SMs with other streams (+1.5 % frames/s over 1)
+#endif
+__global__ void __launch_bounds__(kFitThreads, RPD_FIT_MINB) k_fit(const __grid_constant__ FitKParams P) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FitShared S;
   const FitRequest& R = P.r;
