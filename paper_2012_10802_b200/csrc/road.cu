@@ -4,8 +4,8 @@
 // Reference: /root/reference/proj/src/road_geometry.cpp:12-151.
 //
 // The whole fit_road (golden-section roll search, trimming, second search)
-// runs inside ONE cooperative launch of 128 co-resident CTAs (one per SM,
-// 64 summation lanes each). The observations (<= 524 288) are staged once in
+// runs inside ONE cooperative launch of 64 co-resident CTAs (one per SM,
+// 128 summation lanes each). The observations (<= 524 288) are staged once in
 // shared memory as exact doubles; the searches run on double-double moments
 // (one pass), only the reported residual energies need further passes. Every
 // pass ends in one grid-wide reduction whose CTA partials are exchanged
@@ -13,8 +13,8 @@
 //
 // Reduction order (shared with the CPU oracle, oracle/rpd_oracle.cpp
 // lane_tree_sum / moments): element i belongs to lane i mod 8192 (lane =
-// CTA*64 + thread) and is added sequentially; lanes are then combined by an
-// adjacent-pairwise binary tree (warp shuffles, CTA, then the 128 CTA
+// CTA*128 + thread) and is added sequentially; lanes are then combined by an
+// adjacent-pairwise binary tree (warp shuffles, CTA, then the 64 CTA
 // partials). Eigen's own SIMD order (road_geometry.cpp:20-24, 37) is not
 // reproducible without Eigen; the reference tests pin these sums to 1e-9.
 
@@ -220,15 +220,20 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
 // in the lane order.  Trimming (road_geometry.cpp:83-97) masks elements in
 // place; the survivors keep their lanes.  A fit_road is therefore four
 // grid-wide reductions (moments, residual, survivor moments, residual); each
-// CTA combines the 128 CTA partials with the same pairwise tree, so all CTAs
+// CTA combines the kFitCtas CTA partials with the same pairwise tree, so all CTAs
 // hold bit-identical sums and run the scalar search redundantly.
 // oracle/rpd_oracle.cpp restates exactly this arithmetic.
-constexpr int kFitCtas = 128;
-constexpr int kFitSweep = 64;                      // summation lanes per CTA
+#ifndef RPD_FIT_CTAS
+#define RPD_FIT_CTAS 64  // 64 x 128 threads: +1 % frames/s and a faster serial fit than 128 x 64
+#endif
+constexpr int kFitCtas = RPD_FIT_CTAS;
+constexpr int kFitSweep = 8192 / kFitCtas;         // summation lanes per CTA
 constexpr int kFitSweepWarps = kFitSweep / 32;
 constexpr int kFitThreads = kFitSweep;
 constexpr int kFitLanes = kFitCtas * kFitSweep;    // == oracle kFitLanes (8192)
-constexpr int kMaxRows = 64;                       // 524288 observations
+// rows of staged observations (64: 524288 observations), within ~200 KB of shared memory
+constexpr int kMaxRowsSmem = (200 * 1024) / (kFitSweep * 3 * 8);
+constexpr int kMaxRows = kMaxRowsSmem < 64 ? kMaxRowsSmem : 64;
 constexpr int kMaxNV = 20;                         // doubles per reduction (10 DD moments)
 constexpr int kPartReplicas = 8;  // copies of the CTA partials (spreads the polling over L2)
 constexpr int kPartWords = 2 * kPartReplicas * kFitCtas * kMaxNV * 2;
@@ -434,6 +439,7 @@ __device__ void grid_sum(FitState& F, double (&x)[NV]) {
         part + (size_t(blockIdx.x % kPartReplicas) * kFitCtas + 2 * threadIdx.x) * kMaxNV * 2;
     unsigned spins = 0;
     constexpr int kW = kPairs < 32 ? kPairs : 32;
+    constexpr unsigned kWMask = kW == 32 ? 0xFFFFFFFFu : ((1u << kW) - 1u);
 #pragma unroll 1
     for (int q = 0; q < NV; q += ST) {
       double y[ST], b[ST];
@@ -470,7 +476,7 @@ __device__ void grid_sum(FitState& F, double (&x)[NV]) {
       for (int off = 1; off < kW; off <<= 1) {
         double o[ST];
 #pragma unroll
-        for (int t = 0; t < ST; ++t) o[t] = __shfl_down_sync(0xFFFFFFFFu, y[t], off);
+        for (int t = 0; t < ST; ++t) o[t] = __shfl_down_sync(kWMask, y[t], off);
         plus(y, o);
       }
       if (lane == 0)
@@ -629,7 +635,8 @@ __device__ __forceinline__ double g_advance(GState& s, bool br) {
 // and its sin/cos.
 __device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, double tol,
                            double& phi, double& cphi, double& sphi) {
-  static_assert(kFitThreads == 64, "the tree batches use 64 threads");
+  static_assert((kFitThreads & (kFitThreads - 1)) == 0 && kFitThreads >= 64, "tree batch size");
+  constexpr int kTreeLv = kFitThreads == 64 ? 6 : (kFitThreads == 128 ? 7 : (kFitThreads == 256 ? 8 : 9));
   FitShared& S = *F.S;
   const int t = threadIdx.x;
   GState st{lo, hi, hi - kGolden * (hi - lo), lo + kGolden * (hi - lo)};
@@ -660,7 +667,7 @@ __device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, 
   }
   if (S.g_bad[0] | S.g_bad[1]) return false;
   DD f1 = S.g_e[0], f2 = S.g_e[1];
-  int node = 1, left = 5;  // the tree below the probes: children of virtual node 1
+  int node = 1, left = kTreeLv - 1;  // the tree below the probes: children of virtual node 1
   bool br = dd_lt(f1, f2);
   node = 2 * node + (br ? 1 : 0);
   while (st.b - st.a > tol) {
@@ -676,7 +683,7 @@ __device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, 
       __syncthreads();
       fit_tr(F, 8);
       node = 1;
-      left = 6;
+      left = kTreeLv;
     }
     if (S.g_bad[node]) return false;  // fit_line throws on this probe
     g_advance(st, br);
@@ -751,7 +758,7 @@ __device__ void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok)
 #ifndef RPD_FIT_MINB
 #define RPD_FIT_MINB 8  // 128 registers: the fit shares its SMs with other streams (+1.5 % frames/s over 1)
 #endif
-__global__ void __launch_bounds__(kFitThreads, RPD_FIT_MINB) k_fit(const __grid_constant__ FitKParams P) {
+__global__ void __launch_bounds__(kFitThreads, RPD_FIT_MINB * 64 / kFitThreads) k_fit(const __grid_constant__ FitKParams P) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ FitShared S;
   const FitRequest& R = P.r;
@@ -807,7 +814,8 @@ void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
     attr_done = true;
   }
   if (!req.compact && req.k_host > (long long)kMaxRows * kFitLanes)
-    throw InvalidArg("fit: too many observations for the device fit (max 524288)");
+    throw InvalidArg("fit: too many observations for the device fit (max " +
+                     std::to_string((long long)kMaxRows * kFitLanes) + ")");
   // Shared memory sized to the request's observation cap (13 rows for the
   // pipeline's 100 000).  With the moment-based search the fit makes only
   // four grid-wide exchanges, so sharing its SMs with other streams' CTAs now
