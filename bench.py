@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2, help="BASELINE config index (1-5)")
     ap.add_argument("--cpu-threads", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=8,
+    ap.add_argument("--streams", type=int, default=16,
                     help="concurrent pipeline contexts (one CUDA stream each) per GPU")
     ap.add_argument("--frames", type=int, default=0,
                     help="frames per step per GPU (0 = 2 x streams)")

@@ -19,10 +19,23 @@ __device__ __forceinline__ int uf_find(const int* parent, int p) {
   return p;
 }
 
+// find with path halving in global memory (benign races: a write only
+// re-points a node to one of its ancestors)
+__device__ __forceinline__ int uf_find_halve(int* parent, int p) {
+  int q = __ldcg(parent + p);
+  while (q != p) {
+    const int r = __ldcg(parent + q);
+    if (r != q) parent[p] = r;
+    p = q;
+    q = r;
+  }
+  return p;
+}
+
 __device__ __forceinline__ void uf_union(int* parent, int a, int b) {
   while (true) {
-    a = uf_find(parent, a);
-    b = uf_find(parent, b);
+    a = uf_find_halve(parent, a);
+    b = uf_find_halve(parent, b);
     if (a == b) return;
     if (a < b) {
       const int t = a;
@@ -95,7 +108,10 @@ __global__ void __launch_bounds__(kTileW* kTileH)
   const int i = threadIdx.x;
   const bool fg = in && pr.fg(p);
   lab[i] = fg ? i : -1;
-  __syncthreads();
+  if (!__syncthreads_or(fg)) {  // all-background tile (most of a pothole mask)
+    if (in) parent[p] = -1;
+    return;
+  }
   if (fg) {
     if (tx > 0 && u - 1 < w && pr.same(p, p - 1)) uf_union_s(lab, i, i - 1);
     if (ty > 0) {
@@ -118,21 +134,71 @@ __global__ void __launch_bounds__(kTileW* kTileH)
   }
 }
 
+// Cross-tile unions.  Threads cover only the tile-border pixels: every pixel
+// of each tile's top row (part A), then the left / right columns of the other
+// rows (part B); each does the unions whose neighbour lies in another tile.
+// One warp per tile, tiles in raster order (the order the unions reach the
+// shared roots keeps the trees shallow): pass 0 = the tile's top row, pass 1 =
+// its left (lanes 0-14) and right (lanes 15-29) columns below the top row.
+constexpr int kBorderWarps = 8;
 template <typename Pred>
-__global__ void k_uf_border(Pred pr, int h, int w, int conn8, int* parent) {
-  const int tx = threadIdx.x % kTileW, ty = threadIdx.x / kTileW;
-  const int u = blockIdx.x * kTileW + tx, v = blockIdx.y * kTileH + ty;
-  if (u >= w || v >= h) return;
-  const bool left = tx == 0, top = ty == 0, right = tx == kTileW - 1;
-  if (!(left || top || right)) return;
-  const int p = v * w + u;
-  if (!pr.fg(p)) return;
-  if (left && u > 0 && pr.same(p, p - 1)) uf_union(parent, p, p - 1);
-  if (v > 0) {
-    if (top && pr.same(p, p - w)) uf_union(parent, p, p - w);
-    if (conn8) {
-      if ((top || left) && u > 0 && pr.same(p, p - w - 1)) uf_union(parent, p, p - w - 1);
-      if ((top || right) && u + 1 < w && pr.same(p, p - w + 1)) uf_union(parent, p, p - w + 1);
+__global__ void __launch_bounds__(32 * kBorderWarps)
+    k_uf_border(Pred pr, int h, int w, int conn8, int* parent) {
+  const int ncol = (w + kTileW - 1) / kTileW, nrow = (h + kTileH - 1) / kTileH;
+  const int tile = blockIdx.x * kBorderWarps + int(threadIdx.x >> 5);
+  if (tile >= ncol * nrow) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int u0 = (tile % ncol) * kTileW, v0 = (tile / ncol) * kTileH;
+  for (int pass = 0; pass < 2; ++pass) {
+    int u, v;
+    if (pass == 0) {
+      u = u0 + lane;
+      v = v0;
+    } else {
+      u = lane < kTileH - 1 ? u0 : u0 + kTileW - 1;
+      v = v0 + 1 + (lane < kTileH - 1 ? lane : lane - (kTileH - 1));
+    }
+    bool act = u < w && v < h && (pass == 0 || lane < 2 * (kTileH - 1));
+    const int tx = u % kTileW;
+    const bool left = tx == 0, top = v % kTileH == 0, right = tx == kTileW - 1;
+    const int p = v * w + u;
+    act = act && pr.fg(p);
+    int q[4];
+    bool need[4];
+    q[0] = p - 1;
+    q[1] = p - w;
+    q[2] = p - w - 1;
+    q[3] = p - w + 1;
+    need[0] = act && left && u > 0 && pr.same(p, p - 1);
+    need[1] = act && v > 0 && top && pr.same(p, p - w);
+    need[2] = act && v > 0 && conn8 && (top || left) && u > 0 && pr.same(p, p - w - 1);
+    need[3] = act && v > 0 && conn8 && (top || right) && u + 1 < w && pr.same(p, p - w + 1);
+    // A union is skipped when an earlier direction of this pixel or any
+    // direction of the previous lane's pixel joins the same pair of current
+    // ancestors: that union links the same two sets (ancestors never leave a
+    // set), so the result is unchanged and the shared roots see fewer atomics.
+    const int rp = act ? __ldcg(parent + p) : -1;
+    unsigned long long key[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int rq = need[d] ? __ldcg(parent + q[d]) : -2;
+      const unsigned lo = unsigned(min(rp, rq)), hi = unsigned(max(rp, rq));
+      key[d] = need[d] ? ((unsigned long long)lo << 32 | hi) : ~0ull - d;
+    }
+    unsigned long long prev[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) prev[d] = __shfl_up_sync(0xFFFFFFFFu, key[d], 1);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (!need[d] || (key[d] >> 32) == (key[d] & 0xFFFFFFFFull)) continue;
+      bool dup = false;
+#pragma unroll
+      for (int e = 0; e < d; ++e) dup |= key[e] == key[d];
+      if (lane > 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dup |= prev[e] == key[d];
+      }
+      if (!dup) uf_union(parent, p, q[d]);
     }
   }
 }
@@ -144,7 +210,8 @@ void uf_label(Pred pr, int h, int w, int conn8, int* parent, int sm_count, cudaS
   const dim3 tiles(cdiv(w, kTileW), cdiv(h, kTileH));
   k_uf_local<<<tiles, kTileW * kTileH, 0, st>>>(pr, h, w, conn8, parent);
   RPD_LAUNCH_CHECK();
-  k_uf_border<<<tiles, kTileW * kTileH, 0, st>>>(pr, h, w, conn8, parent);
+  k_uf_border<<<cdiv(tiles.x * tiles.y, kBorderWarps), 32 * kBorderWarps, 0, st>>>(pr, h, w, conn8,
+                                                                                   parent);
   RPD_LAUNCH_CHECK();
   k_uf_flatten<<<std::max(blocks, 1), 256, 0, st>>>(h, w, parent);
   RPD_LAUNCH_CHECK();
