@@ -53,11 +53,13 @@ struct SameLabel {  // SLIC pieces: equal superpixel label (all pixels foregroun
   const int32_t* lab;
   __device__ bool fg(int) const { return true; }
   __device__ bool same(int p, int q) const { return lab[p] == lab[q]; }
+  __device__ int key(int p) const { return lab[p]; }  // class of a foreground pixel
 };
 struct SameMask {  // binary mask components
   const int32_t* mask;
   __device__ bool fg(int p) const { return mask[p] != 0; }
   __device__ bool same(int p, int q) const { return mask[q] != 0; }
+  __device__ int key(int) const { return 0; }
 };
 
 __global__ void k_uf_flatten(int h, int w, int* parent);
@@ -96,10 +98,17 @@ __device__ __forceinline__ void uf_union_s(int* lab, int a, int b) {
   }
 }
 
+// A warp is one tile row (kTileW == 32): each same-class run of the row is
+// linked to its first pixel directly (ballot of run starts), so only the
+// links to the row above need unions, and a union is skipped when an earlier
+// direction of this pixel or the previous lane joins the same pair of
+// current ancestors (the pair's sets are then already linked).
 template <typename Pred>
 __global__ void __launch_bounds__(kTileW* kTileH)
     k_uf_local(Pred pr, int h, int w, int conn8, int* __restrict__ parent) {
+  static_assert(kTileW == 32, "a warp is one tile row");
   __shared__ int lab[kTileW * kTileH];
+  __shared__ int cls[kTileW * kTileH];
   const int tx = threadIdx.x % kTileW, ty = threadIdx.x / kTileW;
   const int u0 = blockIdx.x * kTileW, v0 = blockIdx.y * kTileH;
   const int u = u0 + tx, v = v0 + ty;
@@ -107,20 +116,49 @@ __global__ void __launch_bounds__(kTileW* kTileH)
   const int p = v * w + u;
   const int i = threadIdx.x;
   const bool fg = in && pr.fg(p);
-  lab[i] = fg ? i : -1;
+  const int key = fg ? pr.key(p) : 0;
+  const int kl = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+  const bool fgl = __shfl_up_sync(0xFFFFFFFFu, fg, 1);
+  const unsigned starts = __ballot_sync(0xFFFFFFFFu, fg && (tx == 0 || !fgl || kl != key));
+  const int head = 31 - __clz(starts & (0xFFFFFFFFu >> (31 - tx)));
+  lab[i] = fg ? ty * kTileW + head : -1;
+  cls[i] = key;
   if (!__syncthreads_or(fg)) {  // all-background tile (most of a pothole mask)
     if (in) parent[p] = -1;
     return;
   }
-  if (fg) {
-    if (tx > 0 && u - 1 < w && pr.same(p, p - 1)) uf_union_s(lab, i, i - 1);
-    if (ty > 0) {
-      if (pr.same(p, p - w)) uf_union_s(lab, i, i - kTileW);
-      if (conn8) {
-        if (tx > 0 && pr.same(p, p - w - 1)) uf_union_s(lab, i, i - kTileW - 1);
-        if (tx + 1 < kTileW && u + 1 < w && pr.same(p, p - w + 1))
-          uf_union_s(lab, i, i - kTileW + 1);
+  if (ty > 0) {  // warp-uniform
+    // directions: N, NW, NE (8-connectivity); the W link is the run
+    bool need[3];
+    int j[3];
+    j[0] = i - kTileW;
+    j[1] = i - kTileW - 1;
+    j[2] = i - kTileW + 1;
+    need[0] = fg && lab[j[0]] >= 0 && cls[j[0]] == key;
+    need[1] = fg && conn8 && tx > 0 && lab[j[1]] >= 0 && cls[j[1]] == key;
+    need[2] = fg && conn8 && tx + 1 < kTileW && lab[j[2]] >= 0 && cls[j[2]] == key;
+    const int ra = fg ? lab[i] : 0;
+    unsigned long long pk[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int rb = need[d] ? lab[j[d]] : 0;
+      const unsigned lo = unsigned(min(ra, rb)), hi = unsigned(max(ra, rb));
+      pk[d] = need[d] ? ((unsigned long long)lo << 32 | hi) : ~0ull - d;
+    }
+    unsigned long long pv[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) pv[d] = __shfl_up_sync(0xFFFFFFFFu, pk[d], 1);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (!need[d] || (pk[d] >> 32) == (pk[d] & 0xFFFFFFFFull)) continue;
+      bool dup = false;
+#pragma unroll
+      for (int e = 0; e < d; ++e) dup |= pk[e] == pk[d];
+      if (tx > 0) {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) dup |= pv[e] == pk[d];
       }
+      if (!dup) uf_union_s(lab, i, j[d]);
     }
   }
   __syncthreads();
