@@ -82,8 +82,36 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ in0, float* __restrict__
     out[i] = float(in[i]);
 }
 
+// 16 pixels per thread: one 16-byte load, four 16-byte stores (n16 = n / 16
+// groups; 16-byte aligned buffers), the remainder by the first threads.
+__global__ void k_u8_to_f32_v16(const uint8_t* __restrict__ in0, float* __restrict__ out0,
+                                const uint8_t* __restrict__ in1, float* __restrict__ out1,
+                                int n16, int rem) {
+  const uint8_t* __restrict__ in = blockIdx.y ? in1 : in0;
+  float* __restrict__ out = blockIdx.y ? out1 : out0;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n16) {
+    const uint4 b = reinterpret_cast<const uint4*>(in)[i];
+    const uint32_t wd[4] = {b.x, b.y, b.z, b.w};
+    float4* o = reinterpret_cast<float4*>(out) + 4 * size_t(i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      o[k] = make_float4(float(wd[k] & 0xFFu), float((wd[k] >> 8) & 0xFFu),
+                         float((wd[k] >> 16) & 0xFFu), float(wd[k] >> 24));
+  }
+  if (i < rem) out[16 * size_t(n16) + i] = float(in[16 * size_t(n16) + i]);
+}
+
 void launch_u8_to_f32(const uint8_t* in, float* out, long long n, cudaStream_t st,
                       const uint8_t* in1, float* out1) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  if (n < (1ll << 34) && al16(in) && al16(out) && (!in1 || (al16(in1) && al16(out1)))) {
+    const int n16 = int(n / 16), rem = int(n % 16);
+    const int blocks = std::max(1, cdiv(std::max(n16, rem), 256));
+    k_u8_to_f32_v16<<<dim3(blocks, in1 ? 2 : 1), 256, 0, st>>>(in, out, in1, out1, n16, rem);
+    RPD_LAUNCH_CHECK();
+    return;
+  }
   const int blocks = std::min<long long>((n + 255) / 256, 148 * 16);
   k_u8_to_f32<<<dim3(std::max(blocks, 1), in1 ? 2 : 1), 256, 0, st>>>(in, out, in1, out1, n);
   RPD_LAUNCH_CHECK();
@@ -934,7 +962,9 @@ struct WtaBulkArgs {
   int lw, levels;
 };
 
-template <int P, int NW>
+// LV > 0: the level count is a compile-time constant (the pipeline's passes),
+// so the padding masks and the loops over the level pairs fold away.
+template <int P, int NW, int LV>
 __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_constant__ WtaBulkArgs a) {
   using GE = WtaGeo<NW>;
   constexpr int TP = GE::TP, V = GE::V, NP = GE::NP;
@@ -979,12 +1009,14 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
   uint32_t s[NP];
 #pragma unroll
   for (int q = 0; q < NP; ++q) s[q] = 0u;
+  constexpr int NPS = LV > 0 ? (LV + 1) / 2 : NP;  // pairs that can hold levels < L
 #pragma unroll
   for (int r = 0; r < P; r += 2) {
     const uint32_t* pa = tile + r * (TP * NW) + t * NW;
     const uint32_t* pb = pa + TP * NW;
 #pragma unroll
     for (int j = 0; j < NW; j += V) {
+      if (2 * j >= NPS) break;  // words of padding levels only
       uint32_t xa[V], xb[V];
       if constexpr (V == 4) {
         const uint4 ua = *reinterpret_cast<const uint4*>(pa + j);
@@ -1003,28 +1035,31 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         const int q = 2 * (j + e);
-        s[q] = s[q] + __byte_perm(xa[e], 0u, 0x4140) + __byte_perm(xb[e], 0u, 0x4140);
-        s[q + 1] = s[q + 1] + __byte_perm(xa[e], 0u, 0x4342) + __byte_perm(xb[e], 0u, 0x4342);
+        if (q < NPS)
+          s[q] = s[q] + __byte_perm(xa[e], 0u, 0x4140) + __byte_perm(xb[e], 0u, 0x4140);
+        if (q + 1 < NPS)
+          s[q + 1] = s[q + 1] + __byte_perm(xa[e], 0u, 0x4342) + __byte_perm(xb[e], 0u, 0x4342);
       }
     }
   }
   // select_disparity (sgm.cpp:123-153): minimum, its FIRST level, its
   // multiplicity and the sums at best -+ 1, over the levels < L only
-  const int L = a.levels;
+  const int L = LV > 0 ? LV : a.levels;
   const int np = (L + 1) >> 1;
   const uint32_t hpad = (L & 1) ? 0xFFFF0000u : 0u;  // invalid high half of the last pair
+  constexpr int NPE = NPS;
 #pragma unroll
-  for (int q = 0; q < NP; ++q) s[q] = q < np ? (s[q] | (q == np - 1 ? hpad : 0u)) : 0xFFFFFFFFu;
+  for (int q = 0; q < NPE; ++q) s[q] = q < np ? (s[q] | (q == np - 1 ? hpad : 0u)) : 0xFFFFFFFFu;
   uint32_t m2 = 0xFFFFFFFFu;
 #pragma unroll
-  for (int q = 0; q < NP; q += 2) m2 = __vimin3_u16x2(m2, s[q], q + 1 < NP ? s[q + 1] : 0xFFFFFFFFu);
+  for (int q = 0; q < NPE; q += 2) m2 = __vimin3_u16x2(m2, s[q], q + 1 < NPE ? s[q + 1] : 0xFFFFFFFFu);
   const uint32_t minv = min(m2 & 0xFFFFu, m2 >> 16);
   const uint32_t mx2 = minv * 0x10001u;
   // per pair: e = min(s - min, 1) per half (no borrow: s >= min in both
   // halves), i.e. 0 where a level attains the minimum, 1 elsewhere
   int ne = 0, bq = 0, bh = 0;
 #pragma unroll
-  for (int q = NP - 1; q >= 0; --q) {  // descending: the last hit is the first level
+  for (int q = NPE - 1; q >= 0; --q) {  // descending: the last hit is the first level
     const uint32_t e = __vminu2(s[q] - mx2, 0x00010001u);
     ne += __popc(e);
     if (e != 0x00010001u) {
@@ -1032,7 +1067,7 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
       bh = int(e & 1u);
     }
   }
-  const int cnt = 2 * NP - ne;
+  const int cnt = 2 * NPE - ne;
   const int best = 2 * bq + bh;
   // the sums at best -+ 1 through shared memory: this thread's own words of
   // paths 0 and 1 (2 * NW = NP words, read by nobody else) take its pairs
@@ -1067,13 +1102,19 @@ struct WtaBulkInfo {
   int smem = 0;
 };
 
-template <int P, int NW>
+template <int P, int NW, int LV = 0>
 WtaBulkInfo wta_bulk_info() {
-  return WtaBulkInfo{k_wta_bulk<P, NW>, WtaGeo<NW>::TP, P * WtaGeo<NW>::TP * NW * 4};
+  return WtaBulkInfo{k_wta_bulk<P, NW, LV>, WtaGeo<NW>::TP, P * WtaGeo<NW>::TP * NW * 4};
 }
 
 template <int P>
-WtaBulkInfo wta_bulk_pick(int nw) {
+WtaBulkInfo wta_bulk_pick(int nw, int levels) {
+  // compile-time level counts of the pipeline's passes: PT (d_max_pt = 16)
+  // and the bootstrap of D = 64 / 128 / 256, in their sgm_layout word counts
+  if (nw == 5 && levels == 17) return wta_bulk_info<P, 5, 17>();
+  if (nw == 9 && levels == 33) return wta_bulk_info<P, 9, 33>();
+  if (nw == 20 && levels == 65) return wta_bulk_info<P, 20, 65>();
+  if (nw == 36 && levels == 129) return wta_bulk_info<P, 36, 129>();
   switch (nw) {
     case 1: return wta_bulk_info<P, 1>();
     case 2: return wta_bulk_info<P, 2>();
@@ -1097,8 +1138,9 @@ WtaBulkInfo wta_bulk_pick(int nw) {
 bool launch_wta_bulk(const WtaBulkArgs& wa, int paths, int h, int w, cudaStream_t st) {
   if (std::getenv("RPD_WTA_TILED")) return false;  // A/B: the previous two-launch WTA
   const int nw = wa.lw / 4;
-  const WtaBulkInfo ki = paths == 8 ? wta_bulk_pick<8>(nw) : (paths == 4 ? wta_bulk_pick<4>(nw)
-                                                                          : WtaBulkInfo{});
+  const WtaBulkInfo ki = paths == 8   ? wta_bulk_pick<8>(nw, wa.levels)
+                         : paths == 4 ? wta_bulk_pick<4>(nw, wa.levels)
+                                      : WtaBulkInfo{};
   if (!ki.fn) return false;
   RPD_CK(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ki.smem));
   ki.fn<<<dim3(cdiv(w, ki.tp), h, 2), ki.tp, ki.smem, st>>>(wa);
