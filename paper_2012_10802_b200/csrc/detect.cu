@@ -19,6 +19,7 @@
 //    counted with an open-addressing hash set of (root, superpixel) pairs.
 
 #include <cfloat>
+#include <cmath>
 
 #include <cub/cub.cuh>
 
@@ -128,7 +129,9 @@ __global__ void k_hist_clear(long long* __restrict__ band, const long long* __re
     band[i] = 0;
 }
 
-__global__ void k_hist_bin(const float* __restrict__ d2, int h, int w, double bw,
+// inv_bw != 0: bw is a power of two and (x - o) / bw == (x - o) * inv_bw
+// exactly (both are the correctly rounded value of the same real number).
+__global__ void k_hist_bin(const float* __restrict__ d2, int h, int w, double bw, double inv_bw,
                            const double* __restrict__ origin, long long* __restrict__ meta,
                            long long* __restrict__ band, int half) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x + 1;
@@ -140,7 +143,9 @@ __global__ void k_hist_bin(const float* __restrict__ d2, int h, int w, double bw
     const bool ok = n > 0 && u + 1 < w && hist_vector(d2, w, u, v, x, y);
     long long slot = -1;
     if (ok) {
-      long long i = (long long)floor((x - o) / bw), j = (long long)floor((y - o) / bw);
+      const double qx = inv_bw != 0.0 ? (x - o) * inv_bw : (x - o) / bw;
+      const double qy = inv_bw != 0.0 ? (y - o) * inv_bw : (y - o) / bw;
+      long long i = (long long)floor(qx), j = (long long)floor(qy);
       i = i < n - 1 ? i : n - 1;
       j = j < n - 1 ? j : n - 1;
       const long long dj = j - i;
@@ -532,8 +537,10 @@ static void hist_bin(rpd_ctx* ctx, const HistDev& hd, const float* d2, int h, in
   if (h >= 3 && w >= 3) {
     // one row per block (the band atomics are spread over bins; the single
     // outside counter is aggregated per warp)
-    k_hist_bin<<<dim3(cdiv(w - 2, 128), h - 2), 128, 0, st>>>(d2, h, w, bw, hd.origin, hd.meta,
-                                                              hd.bins, hd.half);
+    int ex = 0;
+    const double inv = (bw > 0.0 && std::frexp(bw, &ex) == 0.5) ? 1.0 / bw : 0.0;
+    k_hist_bin<<<dim3(cdiv(w - 2, 128), h - 2), 128, 0, st>>>(d2, h, w, bw, inv, hd.origin,
+                                                              hd.meta, hd.bins, hd.half);
     RPD_LAUNCH_CHECK();
   }
 }

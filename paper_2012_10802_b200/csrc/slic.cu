@@ -674,17 +674,20 @@ __global__ void k_centers_out(Centers c, const CenterSums s, const int* __restri
 }
 
 // pool_superpixels tail: D3(p) = float(sum / n) of its label or invalid.
-__global__ void k_pool_write(const int32_t* __restrict__ labels, CenterSums s, long long n,
-                             int max_label, float* __restrict__ d3) {
+// Pooled value per label (pool_superpixels, segmentation.cpp:236-246), once per label.
+__global__ void k_pool_values(CenterSums s, int max_label, float* __restrict__ val) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l > max_label) return;
+  const int c = s.n[l];
+  val[l] = c > 0 ? float(fixed_to_double(acc_value(s.sx[l])) / double(c)) : kInvalid;
+}
+
+__global__ void k_pool_write(const int32_t* __restrict__ labels, const float* __restrict__ val,
+                             long long n, int max_label, float* __restrict__ d3) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
        p += (long long)gridDim.x * blockDim.x) {
     const int l = labels[p];
-    float r = kInvalid;
-    if (l >= 0 && l <= max_label) {
-      const int c = s.n[l];
-      if (c > 0) r = float(fixed_to_double(acc_value(s.sx[l])) / double(c));
-    }
-    d3[p] = r;
+    d3[p] = (l >= 0 && l <= max_label) ? val[l] : kInvalid;
   }
 }
 
@@ -845,7 +848,10 @@ void pool_superpixels_dev(rpd_ctx* ctx, const float* d2, const int32_t* labels, 
   RPD_CK(cudaMemsetAsync(s.sx, 0, sizeof(AccSum) * (max_count + 1), st));
   k_label_sums<<<gblocks, 256, 0, st>>>(d2, labels, h, w, max_count, true, false, s, inexact);
   RPD_LAUNCH_CHECK();
-  k_pool_write<<<gblocks, 256, 0, st>>>(labels, s, n, max_count, d3);
+  float* val = ctx->ws.get<float>("pool_val", max_count + 1);
+  k_pool_values<<<cdiv(max_count + 1, 256), 256, 0, st>>>(s, max_count, val);
+  RPD_LAUNCH_CHECK();
+  k_pool_write<<<gblocks, 256, 0, st>>>(labels, val, n, max_count, d3);
   RPD_LAUNCH_CHECK();
 }
 
