@@ -231,21 +231,35 @@ __global__ void __launch_bounds__(128)
   const int u = u0 + threadIdx.x;
   if (u >= w) return;
   const int t = threadIdx.x + R;
-#pragma unroll 2
+  // The thread's column of windows slides down the rows: each step loads one
+  // new window row.  A bit is the sign of (neighbour - centre): for finite
+  // floats a - b < 0 exactly when a < b (a difference of distinct floats is
+  // never zero), and one funnel shift appends it.
+  constexpr int K = 2 * R + 1;
+  float win[K][K];
+#pragma unroll
+  for (int r = 0; r < K - 1; ++r)
+#pragma unroll
+    for (int k = 0; k < K; ++k) win[r][k] = tile[r][t - R + k];
+#pragma unroll
   for (int y = 0; y < kCensusRows; ++y) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) win[(y + K - 1) % K][k] = tile[y + K - 1][t - R + k];
     const int v = v0 + y;
     if (v >= h) break;
-    const float c = tile[y + R][t];
-    Bits bits = 0;
+    const float c = win[(y + R) % K][R];
+    uint32_t lo = 0, hi = 0;  // bits, most significant first (64-bit windows use both)
 #pragma unroll
-    for (int dv = -R; dv <= R; ++dv) {
+    for (int dv = 0; dv < K; ++dv) {
 #pragma unroll
-      for (int du = -R; du <= R; ++du) {
-        if (dv == 0 && du == 0) continue;
-        bits = (bits << 1) | (tile[y + R + dv][t + du] < c ? Bits(1) : Bits(0));
+      for (int du = 0; du < K; ++du) {
+        if (dv == R && du == R) continue;
+        const uint32_t sg = __float_as_uint(__fsub_rn(win[(y + dv) % K][du], c));
+        if (sizeof(Bits) == 8) hi = __funnelshift_l(lo, hi, 1);
+        lo = __funnelshift_l(sg, lo, 1);
       }
     }
-    out[size_t(v) * w + u] = uint64_t(bits);
+    out[size_t(v) * w + u] = sizeof(Bits) == 8 ? ((uint64_t(hi) << 32) | lo) : uint64_t(lo);
   }
 }
 
