@@ -431,7 +431,9 @@ __global__ void k_cost_u8_flat(const uint64_t* __restrict__ cl, const uint64_t* 
 // bits, clamped to maxc exactly as the reference substitutes it (a valid
 // count never exceeds maxc).  A thread owns one pixel and all its levels, the
 // row chunk's words are staged in shared memory and written back coalesced.
-template <int NW>
+// LV > 0: compile-time level count (the pipeline's passes): words that hold
+// only padding levels are stored as 0xFF bytes without computing costs.
+template <int NW, int LV = 0>
 __global__ void __launch_bounds__(256)
     k_cost_px(const uint64_t* __restrict__ cl, const uint64_t* __restrict__ cr,
               const uint8_t* __restrict__ iv, int w, int levels, size_t pitch_words,
@@ -475,6 +477,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int jj = 0; jj < V; ++jj) {
           const int j = j0 + jj;
+          if (LV > 0 && 4 * j >= LV) {  // padding word
+            bl[jj] = br[jj] = 0xFFFFFFFFu;
+            continue;
+          }
           uint32_t cL[4], cR[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -489,8 +495,9 @@ __global__ void __launch_bounds__(256)
           uint32_t wr = __byte_perm(__byte_perm(cR[0], cR[1], 0x0040),
                                     __byte_perm(cR[2], cR[3], 0x0040), 0x5410);
           if (ovu) wr = maxc * 0x01010101u;
-          if (4 * j + 3 >= levels) {  // padding levels (the last words only)
-            const int k = levels - 4 * j;  // valid bytes in this word, <= 3
+          const int nlev = LV > 0 ? LV : levels;
+          if (4 * j + 3 >= nlev) {  // padding levels (the last words only)
+            const int k = nlev - 4 * j;  // valid bytes in this word, <= 3
             const uint32_t keep = k <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * k));
             wl = (wl & keep) | ~keep;
             wr = (wr & keep) | ~keep;
@@ -530,7 +537,12 @@ __global__ void __launch_bounds__(256)
 namespace {
 using CostPxKernel = void (*)(const uint64_t*, const uint64_t*, const uint8_t*, int, int, size_t,
                               uint32_t, uint32_t*, uint32_t*);
-CostPxKernel cost_px_pick(int nw) {
+CostPxKernel cost_px_pick(int nw, int levels) {
+  // compile-time level counts of the pipeline's passes (as wta_bulk_pick)
+  if (nw == 5 && levels == 17) return k_cost_px<5, 17>;
+  if (nw == 9 && levels == 33) return k_cost_px<9, 33>;
+  if (nw == 20 && levels == 65) return k_cost_px<20, 65>;
+  if (nw == 36 && levels == 129) return k_cost_px<36, 129>;
   switch (nw) {
     case 1: return k_cost_px<1>;
     case 2: return k_cost_px<2>;
@@ -1409,7 +1421,7 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     {
       const bool narrow = window * window - 1 <= 32;
       const int smem = (w + 2 * levels) * (narrow ? 9 : 17);
-      const CostPxKernel pxfn = window <= 5 ? cost_px_pick(nw) : nullptr;
+      const CostPxKernel pxfn = window <= 5 ? cost_px_pick(nw, levels) : nullptr;
       const int pxsmem = (w + 8 * nw) * 16 + 2 * 256 * nw * 4;
       if (pxfn && pxsmem <= 200 * 1024 && !std::getenv("RPD_COST_ROWS")) {
         if (pxsmem > 48 * 1024)
