@@ -297,6 +297,22 @@ __device__ __forceinline__ RunInfo run_info(int key) {
   return r;
 }
 
+// As run_info, but a lane with brk set also starts a new run (row starts:
+// a run then lies in one image row, so its count and coordinate sums follow
+// from its bounds).
+__device__ __forceinline__ RunInfo run_info_brk(int key, bool brk) {
+  const int lane = threadIdx.x & 31;
+  const int nxt = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+  const int prv = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+  const unsigned brks = __ballot_sync(0xFFFFFFFFu, brk);
+  const bool tail = lane == 31 || nxt != key || ((brks >> (lane + 1)) & 1u);
+  const unsigned tails = __ballot_sync(0xFFFFFFFFu, tail);
+  RunInfo r;
+  r.end = lane + __ffs(tails >> lane) - 1;
+  r.head = key >= 0 && (lane == 0 || prv != key || brk);
+  return r;
+}
+
 template <typename T>
 __device__ __forceinline__ T run_sum(T x, const RunInfo& ri) {
   const int lane = threadIdx.x & 31;

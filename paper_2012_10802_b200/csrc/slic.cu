@@ -447,14 +447,19 @@ __global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __re
       x = vals[p];
       if (l >= 0 && l <= max_label && (!valid_only || x != kInvalid)) key = l;
     }
-    const RunInfo ri = run_info(key);
-    run_add_value(s.sx, key, key >= 0, x, ri, inexact);
-    const int cnt = run_sum(key >= 0 ? 1 : 0, ri);
-    long long su = 0, sv = 0;
-    if (coords) {
-      su = run_sum(key >= 0 ? (long long)(p % w) : 0ll, ri);
-      sv = run_sum(key >= 0 ? (long long)(p / w) : 0ll, ri);
+    // (v, u) of this lane from one division per warp
+    const long long pw = p0 + (threadIdx.x & ~31u);
+    int v = int(pw / w), u = int(pw - (long long)v * w) + int(threadIdx.x & 31);
+    while (u >= w) {
+      u -= w;
+      ++v;
     }
+    const RunInfo ri = run_info_brk(key, u == 0);
+    run_add_value(s.sx, key, key >= 0, x, ri, inexact);
+    // runs lie in one row: count and coordinate sums from the run bounds
+    const int cnt = ri.end - int(threadIdx.x & 31) + 1;
+    const long long su = (long long)cnt * u + (long long)cnt * (cnt - 1) / 2;
+    const long long sv = (long long)cnt * v;
     if (ri.head) {
       atomicAdd(&s.n[key], cnt);
       if (coords) {
@@ -500,8 +505,7 @@ __global__ void k_piece_sizes(const int* __restrict__ parent, long long n, int* 
     const long long p = p0 + threadIdx.x;
     const int key = p < n ? parent[p] : -1;
     const RunInfo ri = run_info(key);
-    const int c = run_sum(key >= 0 ? 1 : 0, ri);
-    if (ri.head) atomicAdd(&size[key], c);
+    if (ri.head) atomicAdd(&size[key], ri.end - int(threadIdx.x & 31) + 1);  // run length
   }
 }
 
@@ -531,24 +535,21 @@ __global__ void k_orphans(const int* __restrict__ parent, int32_t* __restrict__ 
 }
 
 // Level-0 frontier: kept pixels with an orphan neighbour, in scan order.
+// Orphans are rare, so the flags (zeroed beforehand) are set from the orphan
+// side: each orphan marks its kept 8-neighbours (plain stores of 1).
 __global__ void k_frontier_flags(const int32_t* __restrict__ labels, int h, int w,
                                  int* __restrict__ flags) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
   if (u >= w) return;
   const size_t p = size_t(v) * w + u;
-  int f = 0;
-  if (labels[p] != 0) {
-    for (int i = 0; i < 8; ++i) {
-      const int nu = u + c_du[i], nv = v + c_dv[i];
-      if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
-      if (labels[size_t(nv) * w + nu] == 0) {
-        f = 1;
-        break;
-      }
-    }
+  if (labels[p] != 0) return;
+  for (int i = 0; i < 8; ++i) {
+    const int nu = u + c_du[i], nv = v + c_dv[i];
+    if (nu < 0 || nu >= w || nv < 0 || nv >= h) continue;
+    const size_t q = size_t(nv) * w + nu;
+    if (labels[q] != 0) flags[q] = 1;
   }
-  flags[p] = f;
 }
 
 __global__ void k_scatter_flagged(const int* __restrict__ flags, const int* __restrict__ pos,
@@ -794,6 +795,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_LAUNCH_CHECK();
   k_orphans<<<gblocks, 256, 0, st>>>(parent, labels, best, n, claim);
   RPD_LAUNCH_CHECK();
+  RPD_CK(cudaMemsetAsync(flags, 0, sizeof(int) * n, st));
   k_frontier_flags<<<rowgrid, 128, 0, st>>>(labels, h, w, flags);
   RPD_LAUNCH_CHECK();
   scan_flags(ctx, flags, pos, n, "front");
