@@ -395,21 +395,32 @@ __global__ void __launch_bounds__(kThrThreads) k_threshold(const __grid_constant
 }
 
 // ------------------------------------------------------------ labelling ----
+// Elementwise passes take four pixels per thread (one 16-byte access per
+// array; workspace buffers are 256-byte aligned), launched with ew4_blocks(n).
 __global__ void k_root_flags(const int* __restrict__ parent, const unsigned char* __restrict__ keep,
                              long long n, int* __restrict__ flags) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x)
-    flags[p] = (parent[p] == p && (!keep || keep[p])) ? 1 : 0;
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 r = *reinterpret_cast<const int4*>(parent + p0);
+    const uchar4 k = keep ? *reinterpret_cast<const uchar4*>(keep + p0) : make_uchar4(1, 1, 1, 1);
+    *reinterpret_cast<int4*>(flags + p0) =
+        make_int4(r.x == p0 && k.x, r.y == p0 + 1 && k.y, r.z == p0 + 2 && k.z, r.w == p0 + 3 && k.w);
+    return;
+  }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) flags[p] = (parent[p] == p && (!keep || keep[p])) ? 1 : 0;
 }
 
 __global__ void k_root_relabel(const int* __restrict__ parent,
                                const unsigned char* __restrict__ keep,
                                const int* __restrict__ rank, long long n, int32_t* __restrict__ out) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int r = parent[p];
-    out[p] = (r >= 0 && (!keep || keep[r])) ? rank[r] + 1 : 0;
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  auto lab = [&](int r) { return (r >= 0 && (!keep || keep[r])) ? rank[r] + 1 : 0; };
+  if (p0 + 3 < n && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+    const int4 r = *reinterpret_cast<const int4*>(parent + p0);
+    *reinterpret_cast<int4*>(out + p0) = make_int4(lab(r.x), lab(r.y), lab(r.z), lab(r.w));
+    return;
   }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) out[p] = lab(parent[p]);
 }
 
 __global__ void k_total_from_scan(const int* __restrict__ flags, const int* __restrict__ pos,
@@ -420,11 +431,14 @@ __global__ void k_total_from_scan(const int* __restrict__ flags, const int* __re
 __global__ void k_detect_mask(const float* __restrict__ d3, long long n,
                               const rpd_threshold* __restrict__ thr, int32_t* __restrict__ mask) {
   const double ts = thr->t_s;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    const float x = d3[p];
-    mask[p] = (x != kInvalid && double(x) < ts) ? 1 : 0;
+  auto in = [&](float x) { return (x != kInvalid && double(x) < ts) ? 1 : 0; };
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n && (reinterpret_cast<uintptr_t>(d3) & 15u) == 0) {
+    const float4 x = *reinterpret_cast<const float4*>(d3 + p0);
+    *reinterpret_cast<int4*>(mask + p0) = make_int4(in(x.x), in(x.y), in(x.z), in(x.w));
+    return;
   }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) mask[p] = in(d3[p]);
 }
 
 constexpr unsigned long long kEmpty = 0xFFFFFFFFFFFFFFFFull;
@@ -439,9 +453,9 @@ __global__ void k_detect_stats(const int* __restrict__ parent, const int32_t* __
        p0 += (long long)gridDim.x * blockDim.x) {
     const long long p = p0 + threadIdx.x;
     const int r = p < n ? parent[p] : -1;
+    if (!__any_sync(0xFFFFFFFFu, r >= 0)) continue;  // all background (most of the mask)
     const RunInfo ri = run_info(r);
-    const int c = run_sum(r >= 0 ? 1 : 0, ri);
-    if (ri.head) atomicAdd(&area[r], c);
+    if (ri.head) atomicAdd(&area[r], ri.end - int(threadIdx.x & 31) + 1);  // run length
     if (r >= 0) {
       const int u = int(p % w), v = int(p / w);
       if (u < margin || u >= w - margin || v < margin || v >= h - margin) border[r] = 1;
@@ -640,10 +654,10 @@ void connected_components_dev(rpd_ctx* ctx, const int32_t* mask, int h, int w, i
   int* flags = ctx->ws.get<int>("ccl_flags", n);
   int* pos = ctx->ws.get<int>("ccl_pos", n);
   uf_label(SameMask{mask}, h, w, connectivity == 4 ? 0 : 1, parent, ctx->sm_count, st);
-  k_root_flags<<<gblocks, 256, 0, st>>>(parent, nullptr, n, flags);
+  k_root_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, nullptr, n, flags);
   RPD_LAUNCH_CHECK();
   scan_flags_d(ctx, flags, pos, n, "ccl");
-  k_root_relabel<<<gblocks, 256, 0, st>>>(parent, nullptr, pos, n, out);
+  k_root_relabel<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, nullptr, pos, n, out);
   RPD_LAUNCH_CHECK();
 }
 
@@ -665,7 +679,7 @@ void detect_potholes_dev(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels
   unsigned long long tsize = 1024;
   while (tsize < 2ull * (unsigned long long)n) tsize <<= 1;
   unsigned long long* table = ctx->ws.get<unsigned long long>("det_table", tsize);
-  k_detect_mask<<<gblocks, 256, 0, st>>>(d3, n, thr_dev, mask);
+  k_detect_mask<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(d3, n, thr_dev, mask);
   RPD_LAUNCH_CHECK();
   uf_label(SameMask{mask}, h, w, connectivity == 4 ? 0 : 1, parent, ctx->sm_count, st);
   RPD_CK(cudaMemsetAsync(area, 0, sizeof(int) * n, st));
@@ -680,10 +694,10 @@ void detect_potholes_dev(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels
   k_detect_keep<<<gblocks, 256, 0, st>>>(parent, area, border, nsp, n, min_area, min_superpixels,
                                          keep);
   RPD_LAUNCH_CHECK();
-  k_root_flags<<<gblocks, 256, 0, st>>>(parent, keep, n, flags);
+  k_root_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, keep, n, flags);
   RPD_LAUNCH_CHECK();
   scan_flags_d(ctx, flags, pos, n, "det");
-  k_root_relabel<<<gblocks, 256, 0, st>>>(parent, keep, pos, n, out);
+  k_root_relabel<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, keep, pos, n, out);
   RPD_LAUNCH_CHECK();
   if (n_out) {
     k_total_from_scan<<<1, 1, 0, st>>>(flags, pos, n, n_out);

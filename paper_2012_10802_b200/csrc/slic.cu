@@ -54,12 +54,17 @@ struct CenterSums {
 };
 
 // values_or_zero, segmentation.cpp:13-19
+// Elementwise passes below take four pixels per thread (16-byte accesses;
+// workspace buffers are 256-byte aligned), launched with max(1, cdiv(n, 1024)).
 __global__ void k_values_or_zero(const float* __restrict__ d2, long long n, float* __restrict__ vals) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float x = d2[i];
-    vals[i] = x != kInvalid ? x : 0.0f;
+  auto z = [](float x) { return x != kInvalid ? x : 0.0f; };
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n && (reinterpret_cast<uintptr_t>(d2) & 15u) == 0) {
+    const float4 x = *reinterpret_cast<const float4*>(d2 + p0);
+    *reinterpret_cast<float4*>(vals + p0) = make_float4(z(x.x), z(x.y), z(x.z), z(x.w));
+    return;
   }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) vals[p] = z(d2[p]);
 }
 
 // gradient_at, segmentation.cpp:22-28 (float difference, squared in double)
@@ -525,11 +530,22 @@ __global__ void k_main_piece(const int* __restrict__ parent, const int32_t* __re
 __global__ void k_orphans(const int* __restrict__ parent, int32_t* __restrict__ labels,
                           const unsigned long long* __restrict__ best, long long n,
                           int* __restrict__ claim) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int l = labels[p];
+  auto keep = [&](int l, long long p, int par) {
     const long long root = (long long)(0xFFFFFFFFull - (best[l] & 0xFFFFFFFFull));
-    if (parent[p] != root) labels[p] = 0;
+    return par == root ? l : 0;
+  };
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 l = *reinterpret_cast<const int4*>(labels + p0);
+    const int4 r = *reinterpret_cast<const int4*>(parent + p0);
+    *reinterpret_cast<int4*>(labels + p0) =
+        make_int4(keep(l.x, p0, r.x), keep(l.y, p0 + 1, r.y), keep(l.z, p0 + 2, r.z),
+                  keep(l.w, p0 + 3, r.w));
+    *reinterpret_cast<int4*>(claim + p0) = make_int4(0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF);
+    return;
+  }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) {
+    labels[p] = keep(labels[p], p, parent[p]);
     claim[p] = 0x7FFFFFFF;
   }
 }
@@ -640,16 +656,28 @@ __global__ void k_label_minidx(const int32_t* __restrict__ labels, long long n,
 
 __global__ void k_first_flags(const int32_t* __restrict__ labels, const int* __restrict__ minidx,
                               long long n, int* __restrict__ flags) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x)
-    flags[p] = minidx[labels[p]] == int(p) ? 1 : 0;
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 l = *reinterpret_cast<const int4*>(labels + p0);
+    const int q = int(p0);
+    *reinterpret_cast<int4*>(flags + p0) =
+        make_int4(minidx[l.x] == q, minidx[l.y] == q + 1, minidx[l.z] == q + 2, minidx[l.w] == q + 3);
+    return;
+  }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) flags[p] = minidx[labels[p]] == int(p) ? 1 : 0;
 }
 
 __global__ void k_relabel(int32_t* __restrict__ labels, const int* __restrict__ minidx,
                           const int* __restrict__ rank, long long n) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x)
-    labels[p] = rank[minidx[labels[p]]] + 1;
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 l = *reinterpret_cast<const int4*>(labels + p0);
+    *reinterpret_cast<int4*>(labels + p0) =
+        make_int4(rank[minidx[l.x]] + 1, rank[minidx[l.y]] + 1, rank[minidx[l.z]] + 1,
+                  rank[minidx[l.w]] + 1);
+    return;
+  }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) labels[p] = rank[minidx[labels[p]]] + 1;
 }
 
 __global__ void k_count_from_scan(const int* __restrict__ flags, const int* __restrict__ pos,
@@ -736,7 +764,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   int* orphan_count = ctx->ws.get<int>("slic_orphan_count", 2);
   int* inexact = orphan_count + 1;
 
-  k_values_or_zero<<<gblocks, 256, 0, st>>>(d2, n, vals);
+  k_values_or_zero<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(d2, n, vals);
   RPD_LAUNCH_CHECK();
   k_seeds<<<cdiv(K, 128), 128, 0, st>>>(vals, h, w, nu, nv, su, sv, c);
   RPD_LAUNCH_CHECK();
@@ -793,7 +821,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_LAUNCH_CHECK();
   k_main_piece<<<gblocks, 256, 0, st>>>(parent, labels, psize, n, best);
   RPD_LAUNCH_CHECK();
-  k_orphans<<<gblocks, 256, 0, st>>>(parent, labels, best, n, claim);
+  k_orphans<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, labels, best, n, claim);
   RPD_LAUNCH_CHECK();
   RPD_CK(cudaMemsetAsync(flags, 0, sizeof(int) * n, st));
   k_frontier_flags<<<rowgrid, 128, 0, st>>>(labels, h, w, flags);
@@ -811,12 +839,12 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_LAUNCH_CHECK();
   k_label_minidx<<<gblocks, 256, 0, st>>>(labels, n, minidx);
   RPD_LAUNCH_CHECK();
-  k_first_flags<<<gblocks, 256, 0, st>>>(labels, minidx, n, flags);
+  k_first_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(labels, minidx, n, flags);
   RPD_LAUNCH_CHECK();
   scan_flags(ctx, flags, pos, n, "first");
   k_count_from_scan<<<1, 1, 0, st>>>(flags, pos, n, count);
   RPD_LAUNCH_CHECK();
-  k_relabel<<<gblocks, 256, 0, st>>>(labels, minidx, pos, n);
+  k_relabel<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(labels, minidx, pos, n);
   RPD_LAUNCH_CHECK();
   // final update_centers over the compacted labels (centres start at zero)
   RPD_CK(cudaMemsetAsync(c.cu, 0, sizeof(double) * K, st));
