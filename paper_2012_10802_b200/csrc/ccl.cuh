@@ -242,16 +242,15 @@ __global__ void __launch_bounds__(32 * kBorderWarps)
 }
 
 template <typename Pred>
-void uf_label(Pred pr, int h, int w, int conn8, int* parent, int sm_count, cudaStream_t st) {
+void uf_label(Pred pr, int h, int w, int conn8, int* parent, int /*sm_count*/, cudaStream_t st) {
   const long long n = (long long)h * w;
-  const int blocks = int(std::min<long long>((n + 255) / 256, sm_count * 16));
   const dim3 tiles(cdiv(w, kTileW), cdiv(h, kTileH));
   k_uf_local<<<tiles, kTileW * kTileH, 0, st>>>(pr, h, w, conn8, parent);
   RPD_LAUNCH_CHECK();
   k_uf_border<<<cdiv(tiles.x * tiles.y, kBorderWarps), 32 * kBorderWarps, 0, st>>>(pr, h, w, conn8,
                                                                                    parent);
   RPD_LAUNCH_CHECK();
-  k_uf_flatten<<<std::max(blocks, 1), 256, 0, st>>>(h, w, parent);
+  k_uf_flatten<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(h, w, parent);
   RPD_LAUNCH_CHECK();
 }
 

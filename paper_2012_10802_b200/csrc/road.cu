@@ -137,21 +137,46 @@ struct RoiPred {
 
 __global__ void k_sample_flags(const float* __restrict__ d1, int h, int w, RoiPred r,
                                int* __restrict__ flags) {
+  // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
   const long long n = (long long)h * w;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int u = int(p % w), v = int(p / w);
-    flags[p] = (u >= r.u0 && u < r.u1 && v >= r.v0 && v < r.v1 && d1[p] != kInvalid) ? 1 : 0;
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 >= n) return;
+  int v = int(p0 / w), u = int(p0 - (long long)v * w);
+  int f[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long p = p0 + k;
+    f[k] = (p < n && u >= r.u0 && u < r.u1 && v >= r.v0 && v < r.v1 && d1[p] != kInvalid) ? 1 : 0;
+    if (++u == w) {
+      u = 0;
+      ++v;
+    }
+  }
+  if (p0 + 3 < n) {
+    *reinterpret_cast<int4*>(flags + p0) = make_int4(f[0], f[1], f[2], f[3]);
+  } else {
+    for (int k = 0; p0 + k < n; ++k) flags[p0 + k] = f[k];
   }
 }
 
 __global__ void k_sample_scatter(const int* __restrict__ flags, const int* __restrict__ pos,
                                  long long n, int* __restrict__ list, int* __restrict__ total) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    if (flags[p]) list[pos[p]] = int(p);
-    if (p == n - 1) *total = pos[p] + flags[p];
+  // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 f = *reinterpret_cast<const int4*>(flags + p0);
+    if (f.x | f.y | f.z | f.w) {
+      const int4 q = *reinterpret_cast<const int4*>(pos + p0);
+      if (f.x) list[q.x] = int(p0);
+      if (f.y) list[q.y] = int(p0 + 1);
+      if (f.z) list[q.z] = int(p0 + 2);
+      if (f.w) list[q.w] = int(p0 + 3);
+    }
+  } else {
+    for (long long p = p0; p < n; ++p)
+      if (flags[p]) list[pos[p]] = int(p);
   }
+  if (p0 <= n - 1 && n - 1 < p0 + 4) *total = pos[n - 1] + flags[n - 1];
 }
 
 // road_geometry.cpp:119-133: k = min(n, cap); obs_i = valid[floor(i*n/k)].
@@ -187,15 +212,14 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
   int* pos = ctx->ws.get<int>("so_pos", n);
   int* list = ctx->ws.get<int>("so_list", n);
   int* total = ctx->ws.get<int>("so_total", 1);
-  const int blocks = int(std::min<long long>((n + 255) / 256, ctx->sm_count * 16));
-  k_sample_flags<<<blocks, 256, 0, st>>>(d1, h, w, r, flags);
+  k_sample_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(d1, h, w, r, flags);
   RPD_LAUNCH_CHECK();
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flags, pos, int(n), st);
   void* tmp = ctx->ws.get<uint8_t>("so_cub", tmp_bytes);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flags, pos, int(n), st);
   RPD_LAUNCH_CHECK();
-  k_sample_scatter<<<blocks, 256, 0, st>>>(flags, pos, n, list, total);
+  k_sample_scatter<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(flags, pos, n, list, total);
   RPD_LAUNCH_CHECK();
   const long long gmax = std::min<long long>(cap, n);
   k_sample_gather<<<std::max(1, cdiv(gmax, 256)), 256, 0, st>>>(

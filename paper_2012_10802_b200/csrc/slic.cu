@@ -23,12 +23,22 @@
 
 namespace rpdg {
 
+// four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
 __global__ void k_uf_flatten(int h, int w, int* parent) {
   const long long n = (long long)h * w;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    if (parent[p] >= 0) parent[p] = uf_find(parent, int(p));
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    int4 r = *reinterpret_cast<const int4*>(parent + p0);
+    // a pixel whose parent is itself or a root keeps it
+    if (r.x >= 0) r.x = uf_find(parent, r.x);
+    if (r.y >= 0) r.y = uf_find(parent, r.y);
+    if (r.z >= 0) r.z = uf_find(parent, r.z);
+    if (r.w >= 0) r.w = uf_find(parent, r.w);
+    *reinterpret_cast<int4*>(parent + p0) = r;
+    return;
   }
+  for (long long p = p0; p < n; ++p)
+    if (parent[p] >= 0) parent[p] = uf_find(parent, int(p));
 }
 
 namespace {
@@ -570,11 +580,22 @@ __global__ void k_frontier_flags(const int32_t* __restrict__ labels, int h, int 
 
 __global__ void k_scatter_flagged(const int* __restrict__ flags, const int* __restrict__ pos,
                                   long long n, int* __restrict__ list, int* __restrict__ total) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    if (flags[p]) list[pos[p]] = int(p);
-    if (p == n - 1) *total = pos[p] + flags[p];
+  // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 f = *reinterpret_cast<const int4*>(flags + p0);
+    if (f.x | f.y | f.z | f.w) {
+      const int4 q = *reinterpret_cast<const int4*>(pos + p0);
+      if (f.x) list[q.x] = int(p0);
+      if (f.y) list[q.y] = int(p0 + 1);
+      if (f.z) list[q.z] = int(p0 + 2);
+      if (f.w) list[q.w] = int(p0 + 3);
+    }
+  } else {
+    for (long long p = p0; p < n; ++p)
+      if (flags[p]) list[pos[p]] = int(p);
   }
+  if (p0 <= n - 1 && n - 1 < p0 + 4) *total = pos[n - 1] + flags[n - 1];
 }
 
 // Ordered multi-source BFS (single CTA), segmentation.cpp:145-165.
@@ -713,11 +734,15 @@ __global__ void k_pool_values(CenterSums s, int max_label, float* __restrict__ v
 
 __global__ void k_pool_write(const int32_t* __restrict__ labels, const float* __restrict__ val,
                              long long n, int max_label, float* __restrict__ d3) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int l = labels[p];
-    d3[p] = (l >= 0 && l <= max_label) ? val[l] : kInvalid;
+  auto pv = [&](int l) { return (l >= 0 && l <= max_label) ? val[l] : kInvalid; };
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n && (reinterpret_cast<uintptr_t>(d3) & 15u) == 0 &&
+      (reinterpret_cast<uintptr_t>(labels) & 15u) == 0) {
+    const int4 l = *reinterpret_cast<const int4*>(labels + p0);
+    *reinterpret_cast<float4*>(d3 + p0) = make_float4(pv(l.x), pv(l.y), pv(l.z), pv(l.w));
+    return;
   }
+  for (long long p = p0; p < min(n, p0 + 4); ++p) d3[p] = pv(labels[p]);
 }
 
 }  // namespace
@@ -827,7 +852,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   k_frontier_flags<<<rowgrid, 128, 0, st>>>(labels, h, w, flags);
   RPD_LAUNCH_CHECK();
   scan_flags(ctx, flags, pos, n, "front");
-  k_scatter_flagged<<<gblocks, 256, 0, st>>>(flags, pos, n, qa, n0);
+  k_scatter_flagged<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(flags, pos, n, qa, n0);
   RPD_LAUNCH_CHECK();
   k_bfs<<<1, kBfsThreads, 0, st>>>(labels, h, w, claim, qa, qb, n0);
   RPD_LAUNCH_CHECK();
@@ -881,7 +906,7 @@ void pool_superpixels_dev(rpd_ctx* ctx, const float* d2, const int32_t* labels, 
   float* val = ctx->ws.get<float>("pool_val", max_count + 1);
   k_pool_values<<<cdiv(max_count + 1, 256), 256, 0, st>>>(s, max_count, val);
   RPD_LAUNCH_CHECK();
-  k_pool_write<<<gblocks, 256, 0, st>>>(labels, val, n, max_count, d3);
+  k_pool_write<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(labels, val, n, max_count, d3);
   RPD_LAUNCH_CHECK();
 }
 
