@@ -486,11 +486,21 @@ __global__ void k_detect_keep(const int* __restrict__ parent, const int* __restr
                               const unsigned char* __restrict__ border, const int* __restrict__ nsp,
                               long long n, long long min_area, int min_sp,
                               unsigned char* __restrict__ keep) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    if (parent[p] != p) continue;
+  // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
+  auto root = [&](long long p) {
     keep[p] = (!border[p] && (long long)area[p] >= min_area && nsp[p] >= min_sp) ? 1 : 0;
+  };
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 r = *reinterpret_cast<const int4*>(parent + p0);
+    if (r.x == p0) root(p0);
+    if (r.y == p0 + 1) root(p0 + 1);
+    if (r.z == p0 + 2) root(p0 + 2);
+    if (r.w == p0 + 3) root(p0 + 3);
+    return;
   }
+  for (long long p = p0; p < n; ++p)
+    if (parent[p] == p) root(p);
 }
 
 }  // namespace
@@ -648,8 +658,6 @@ void connected_components_dev(rpd_ctx* ctx, const int32_t* mask, int h, int w, i
                               int32_t* out) {
   cudaStream_t st = ctx->stream;
   const long long n = (long long)h * w;
-  const int gblocks = int(std::max<long long>(1, std::min<long long>((n + 255) / 256,
-                                                                      ctx->sm_count * 16)));
   int* parent = ctx->ws.get<int>("ccl_parent", n);
   int* flags = ctx->ws.get<int>("ccl_flags", n);
   int* pos = ctx->ws.get<int>("ccl_pos", n);
@@ -691,7 +699,7 @@ void detect_potholes_dev(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels
                                           table, tsize - 1, nsp);
   RPD_LAUNCH_CHECK();
   const long long min_area = (long long)(spacing * spacing);  // segmentation.cpp:418
-  k_detect_keep<<<gblocks, 256, 0, st>>>(parent, area, border, nsp, n, min_area, min_superpixels,
+  k_detect_keep<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, area, border, nsp, n, min_area, min_superpixels,
                                          keep);
   RPD_LAUNCH_CHECK();
   k_root_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, keep, n, flags);

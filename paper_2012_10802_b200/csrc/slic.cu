@@ -528,13 +528,23 @@ __global__ void k_piece_sizes(const int* __restrict__ parent, long long n, int* 
 __global__ void k_main_piece(const int* __restrict__ parent, const int32_t* __restrict__ labels,
                              const int* __restrict__ size, long long n,
                              unsigned long long* __restrict__ best) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
-       p += (long long)gridDim.x * blockDim.x) {
-    if (parent[p] != p) continue;
+  // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
+  auto root = [&](long long p) {
     const unsigned long long key =
         ((unsigned long long)(unsigned)size[p] << 32) | (0xFFFFFFFFull - (unsigned long long)p);
     atomicMax(&best[labels[p]], key);
+  };
+  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 + 3 < n) {
+    const int4 r = *reinterpret_cast<const int4*>(parent + p0);
+    if (r.x == p0) root(p0);
+    if (r.y == p0 + 1) root(p0 + 1);
+    if (r.z == p0 + 2) root(p0 + 2);
+    if (r.w == p0 + 3) root(p0 + 3);
+    return;
   }
+  for (long long p = p0; p < n; ++p)
+    if (parent[p] == p) root(p);
 }
 
 __global__ void k_orphans(const int* __restrict__ parent, int32_t* __restrict__ labels,
@@ -844,7 +854,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_CK(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * (K + 1), st));
   k_piece_sizes<<<gblocks, 256, 0, st>>>(parent, n, psize);
   RPD_LAUNCH_CHECK();
-  k_main_piece<<<gblocks, 256, 0, st>>>(parent, labels, psize, n, best);
+  k_main_piece<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, labels, psize, n, best);
   RPD_LAUNCH_CHECK();
   k_orphans<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, labels, best, n, claim);
   RPD_LAUNCH_CHECK();
