@@ -6,8 +6,8 @@
 // u16x2 level pairs) of the chain's current pixel in registers.  An elected
 // thread streams the raw cost tiles of the next R steps into a DEPTH-deep
 // shared-memory ring with cp.async.bulk.tensor (completion on mbarriers), and
-// writes the per-path u8 results back with TMA stores from a double-buffered
-// output tile, so the compute threads only touch shared memory.
+// writes the per-path u8 results back with TMA stores from an output tile
+// (RPD_AGG_OUTDEPTH deep), so the compute threads only touch shared memory.
 //
 // Chains: horizontal = image rows, vertical = columns, diagonal = the W+H-1
 // non-wrapping diagonals u = k + du*s; tiles that stick out of the image are
@@ -42,7 +42,7 @@ constexpr int kDepth = RPD_AGG_DEPTH;  // input ring depth (stages)
 #define RPD_AGG_REC 2  // recurrence form: 0 = 2x add-min + min, 1 = min3 + add-min, 2 = min3 + add + min3
 #endif
 #ifndef RPD_AGG_OUTDEPTH
-#define RPD_AGG_OUTDEPTH 2  // output tiles in flight (TMA stores not yet read)
+#define RPD_AGG_OUTDEPTH 1  // output tiles in flight (TMA stores not yet read); 1: less smem, +1 % concurrent
 #endif
 constexpr int kOutDepth = RPD_AGG_OUTDEPTH;
 constexpr int kRBase = RPD_AGG_RBASE;
