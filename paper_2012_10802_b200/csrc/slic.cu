@@ -823,10 +823,10 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
       k_assign_tile<false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
     RPD_LAUNCH_CHECK();
     if (sums)
-      k_assign_fallback<true><<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
+      k_assign_fallback<true><<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list,
                                                                   orphan_count, vals, s, inexact);
     else
-      k_assign_fallback<false><<<ctx->sm_count * 4, 256, 0, st>>>(w, c, K, labels, orphan_list,
+      k_assign_fallback<false><<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list,
                                                                    orphan_count, vals, s, inexact);
     RPD_LAUNCH_CHECK();
   };
