@@ -563,8 +563,10 @@ static void hist_bin(rpd_ctx* ctx, const HistDev& hd, const float* d2, int h, in
     // outside counter is aggregated per warp)
     int ex = 0;
     const double inv = (bw > 0.0 && std::frexp(bw, &ex) == 0.5) ? 1.0 / bw : 0.0;
-    k_hist_bin<<<dim3(cdiv(w - 2, 128), h - 2), 128, 0, st>>>(d2, h, w, bw, inv, hd.origin,
-                                                              hd.meta, hd.bins, hd.half);
+    // rows strided over gridDim.y (about 4 rows per block)
+    const int gy = std::max(1, cdiv(h - 2, 4));
+    k_hist_bin<<<dim3(cdiv(w - 2, 128), gy), 128, 0, st>>>(d2, h, w, bw, inv, hd.origin, hd.meta,
+                                                           hd.bins, hd.half);
     RPD_LAUNCH_CHECK();
   }
 }
