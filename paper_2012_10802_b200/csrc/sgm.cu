@@ -1185,41 +1185,42 @@ __global__ void k_post(const float* __restrict__ dl, const float* __restrict__ d
                        int w, int levels, double thr, float* __restrict__ d0,
                        float* __restrict__ d1) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
   if (u >= w) return;
-  const size_t i = size_t(v) * w + u;
-  const size_t coff = size_t(v) * crow + size_t(u) * cstride;  // element offset of the cost curve
-  const size_t row = size_t(v) * w;
-  float d = dl[i];
-  if (d != kInvalid) {
-    const int ur = u - int(lroundf(d));
-    if (ur < 0 || ur >= w) {
-      d = kInvalid;
-    } else {
-      const float x = dr[row + ur];
-      if (x == kInvalid || double(fabsf(d - x)) > thr) d = kInvalid;
+  for (int v = blockIdx.y; v < h; v += gridDim.y) {  // rows strided over gridDim.y
+    const size_t i = size_t(v) * w + u;
+    const size_t coff = size_t(v) * crow + size_t(u) * cstride;  // element offset of the cost curve
+    const size_t row = size_t(v) * w;
+    float d = dl[i];
+    if (d != kInvalid) {
+      const int ur = u - int(lroundf(d));
+      if (ur < 0 || ur >= w) {
+        d = kInvalid;
+      } else {
+        const float x = dr[row + ur];
+        if (x == kInvalid || double(fabsf(d - x)) > thr) d = kInvalid;
+      }
     }
-  }
-  if (d != kInvalid) {
-    float lo = FLT_MAX, hi = -FLT_MAX;
-    const CostT* c = cost + coff;
-    for (int k = 0; k < levels; ++k) {
-      const int ur = u - k;
-      if (ur < 0) break;
-      if (!iv[row + ur]) continue;
-      const float x = float(c[k]);
-      lo = (x < lo) ? x : lo;
-      hi = (hi < x) ? x : hi;
-      if (lo < hi) break;
+    if (d != kInvalid) {
+      float lo = FLT_MAX, hi = -FLT_MAX;
+      const CostT* c = cost + coff;
+      for (int k = 0; k < levels; ++k) {
+        const int ur = u - k;
+        if (ur < 0) break;
+        if (!iv[row + ur]) continue;
+        const float x = float(c[k]);
+        lo = (x < lo) ? x : lo;
+        hi = (hi < x) ? x : hi;
+        if (lo < hi) break;
+      }
+      if (hi <= lo) d = kInvalid;
     }
-    if (hi <= lo) d = kInvalid;
+    if (d != kInvalid) {
+      const int ur = u - int(lroundf(d));
+      if (ur < 0 || !iv[row + ur]) d = kInvalid;
+    }
+    d0[i] = d;
+    d1[i] = (d != kInvalid) ? d + float(shifts[v]) : d;
   }
-  if (d != kInvalid) {
-    const int ur = u - int(lroundf(d));
-    if (ur < 0 || !iv[row + ur]) d = kInvalid;
-  }
-  d0[i] = d;
-  d1[i] = (d != kInvalid) ? d + float(shifts[v]) : d;
 }
 
 // ------------------------------------------------------ generic float path --
@@ -1382,7 +1383,7 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
   launch_census2(left, warped, h, w, window, cl, cr, st);
   float* dl = ctx->ws.get<float>("mp_disp_l", npix);
   float* dr = ctx->ws.get<float>("mp_disp_r", npix);
-  const dim3 rowgrid(cdiv(w, 128), h);
+  const dim3 rowgrid(cdiv(w, 128), std::max(1, cdiv(h, 4)));  // k_post strides rows over gridDim.y
   int32_t dirs[16];
   const int paths = cfg.sgm_paths == 4 ? 4 : 8;
   const int eight[16] = {1, 0, -1, 0, 0, 1, 0, -1, 1, 1, -1, 1, 1, -1, -1, -1};
