@@ -875,30 +875,33 @@ __global__ void k_transform(const float* __restrict__ d1, int h, int w,
                             const DevModel* __restrict__ model, double delta,
                             float* __restrict__ d2, unsigned long long* __restrict__ clamped) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
-  bool clamp = false;
-  if (u < w) {
-    const size_t i = size_t(v) * w + u;
-    const float x = d1[i];
-    if (x != kInvalid) {
-      const DevModel m = *model;
-      double y = double(x) - road_at(m, double(u), double(v)) + delta;
-      if (y < 0) {
-        y = 0;
-        clamp = true;
+  unsigned nclamp = 0;
+  for (int v = blockIdx.y; v < h; v += gridDim.y) {  // rows strided over gridDim.y
+    bool clamp = false;
+    if (u < w) {
+      const size_t i = size_t(v) * w + u;
+      const float x = d1[i];
+      if (x != kInvalid) {
+        const DevModel m = *model;
+        double y = double(x) - road_at(m, double(u), double(v)) + delta;
+        if (y < 0) {
+          y = 0;
+          clamp = true;
+        }
+        d2[i] = float(y);
+      } else {
+        d2[i] = x;
       }
-      d2[i] = float(y);
-    } else {
-      d2[i] = x;
     }
+    nclamp += __popc(__ballot_sync(0xFFFFFFFFu, clamp));
   }
-  const unsigned bal = __ballot_sync(0xFFFFFFFFu, clamp);
-  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(clamped, (unsigned long long)__popc(bal));
+  if ((threadIdx.x & 31) == 0 && nclamp) atomicAdd(clamped, (unsigned long long)nclamp);
 }
 
 void transform_disparity_dev(const float* d1, int h, int w, const DevModel* model, double delta_dt,
                              float* d2, unsigned long long* clamped, cudaStream_t st) {
-  k_transform<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(d1, h, w, model, delta_dt, d2, clamped);
+  k_transform<<<dim3(cdiv(w, 128), std::max(1, cdiv(h, 4))), 128, 0, st>>>(d1, h, w, model,
+                                                                           delta_dt, d2, clamped);
   RPD_LAUNCH_CHECK();
 }
 

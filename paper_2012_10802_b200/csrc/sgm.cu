@@ -162,26 +162,28 @@ void launch_row_shifts(const DevModel* model, int h, int w, double delta_pt, dou
 __global__ void k_warp(const float* __restrict__ right, const double* __restrict__ shifts, int h,
                        int w, float* __restrict__ out, uint8_t* __restrict__ iv) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
   if (u >= w) return;
-  const size_t i = size_t(v) * w + u;
-  const double s = double(u) - shifts[v];
-  if (s < 0.0 || s > double(w - 1)) {
-    out[i] = 0.0f;
-    iv[i] = 0;
-    return;
+  for (int v = blockIdx.y; v < h; v += gridDim.y) {  // rows strided over gridDim.y
+    const size_t i = size_t(v) * w + u;
+    const double s = double(u) - shifts[v];
+    if (s < 0.0 || s > double(w - 1)) {
+      out[i] = 0.0f;
+      iv[i] = 0;
+      continue;
+    }
+    const int s0 = int(floor(s));
+    const int s1 = min(s0 + 1, w - 1);
+    const double t = s - double(s0);
+    const float* row = right + size_t(v) * w;
+    out[i] = float((1.0 - t) * double(row[s0]) + t * double(row[s1]));
+    iv[i] = 1;
   }
-  const int s0 = int(floor(s));
-  const int s1 = min(s0 + 1, w - 1);
-  const double t = s - double(s0);
-  const float* row = right + size_t(v) * w;
-  out[i] = float((1.0 - t) * double(row[s0]) + t * double(row[s1]));
-  iv[i] = 1;
 }
 
 void launch_warp_right(const float* right, const double* shifts, int h, int w, float* out,
                        uint8_t* in_view, cudaStream_t st) {
-  k_warp<<<dim3(cdiv(w, 128), h), 128, 0, st>>>(right, shifts, h, w, out, in_view);
+  k_warp<<<dim3(cdiv(w, 128), std::max(1, cdiv(h, 4))), 128, 0, st>>>(right, shifts, h, w, out,
+                                                                       in_view);
   RPD_LAUNCH_CHECK();
 }
 
