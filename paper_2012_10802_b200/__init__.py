@@ -25,7 +25,7 @@ _loaded = None
 def load_library(path: str | os.PathLike | None = None) -> Library:
     """Load the sm_100a CUDA library.  Fails loudly when it is absent."""
     global _loaded
-    p = Path(path) if path else Path(os.environ.get("RPD_B200_LIB", CUDA_LIB))
+    p = Path(path) if path else CUDA_LIB
     if _loaded is not None and Path(_loaded.path) == p:
         return _loaded
     if not p.exists():

@@ -48,6 +48,16 @@ class CapacityError(RpdError):
     pass
 
 
+class MissingSymbol(RpdError, NotImplementedError):
+    """The bound library does not export this entry point."""
+
+
+def _missing(path, name):
+    def call(*_a, **_k):
+        raise MissingSymbol(f"{path} does not export {name}")
+    return call
+
+
 # ------------------------------------------------------------------ structs --
 class RoadModel(C.Structure):
     _fields_ = [("a0", C.c_double), ("a1", C.c_double), ("phi", C.c_double)]
@@ -346,7 +356,15 @@ class Library:
     def __init__(self, path: str):
         self.path = str(path)
         self.dll = C.CDLL(self.path)
+        # The product and the restated oracle export every symbol; the literal
+        # reference wrapper (oracle/_ref) only the hot-path subset — calls to
+        # a missing one raise MissingSymbol.
+        self.missing = set()
         for name, (res, args) in _SIGS.items():
+            if not hasattr(self.dll, name):
+                self.missing.add(name)
+                setattr(self.dll, name, _missing(self.path, name))
+                continue
             fn = getattr(self.dll, name)
             fn.restype = res
             fn.argtypes = args

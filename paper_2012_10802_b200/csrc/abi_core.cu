@@ -13,7 +13,7 @@ namespace rpdg {
 
 bool rpd_sync_debug() {
   static const bool on = [] {
-    const char* e = std::getenv("RPD_SYNC_DEBUG");
+    const char* e = debug_knob("RPD_SYNC_DEBUG");
     return e && e[0] == '1';
   }();
   return on;

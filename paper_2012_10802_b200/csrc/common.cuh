@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -45,7 +46,20 @@ struct Capacity : std::runtime_error {
       throw ::rpdg::CudaFail(std::string(#x) + ": " + cudaGetErrorString(e_));       \
   } while (0)
 
-// RPD_SYNC_DEBUG=1 in the environment synchronises after every launch and
+// Debug / A-B switches (RPD_SKIP_STAGES, RPD_TMA_TYPES, ...) are read from the
+// environment only in a build with -DRPD_DEBUG_KNOBS (`make DEBUG_KNOBS=1`).
+// The product library ignores the environment entirely, so a caller's
+// environment can never change its outputs.
+inline const char* debug_knob(const char* name) {
+#ifdef RPD_DEBUG_KNOBS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+// RPD_SYNC_DEBUG=1 in the environment (debug-knob builds) synchronises after every launch and
 // names the failing call site (debugging only; never set in timed runs).
 bool rpd_sync_debug();
 #define RPD_LAUNCH_CHECK()                                                                 \

@@ -139,7 +139,7 @@ FrameBuffers alloc_frame(rpd_ctx* ctx, int h, int w, int K) {
 // 8 = bootstrap SGM, 16 = PT SGM.
 int skip_stages() {
   static const int m = [] {
-    const char* e = std::getenv("RPD_SKIP_STAGES");
+    const char* e = debug_knob("RPD_SKIP_STAGES");
     return e ? std::atoi(e) : 0;
   }();
   return m;
@@ -149,7 +149,7 @@ int skip_stages() {
 // the stage's cost in the concurrent regime.
 int dup_stages() {
   static const int m = [] {
-    const char* e = std::getenv("RPD_DUP_STAGES");
+    const char* e = debug_knob("RPD_DUP_STAGES");
     return e ? std::atoi(e) : 0;
   }();
   return m;

@@ -23,6 +23,9 @@
 
 #include <cub/cub.cuh>
 
+#include <mutex>
+#include <vector>
+
 #include "road.cuh"
 
 
@@ -826,16 +829,23 @@ __global__ void __launch_bounds__(kFitThreads, RPD_FIT_MINB * 64 / kFitThreads) 
 }
 
 void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                fit_dyn_smem(kMaxRows)));
-    int per_sm = 0;
-    RPD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit, kFitThreads,
-                                                         fit_dyn_smem(kMaxRows)));
-    if (per_sm * ctx->sm_count < kFitCtas)
-      throw CudaFail("fit: device cannot co-schedule the fit grid");
-    attr_done = true;
+  // Function attributes are per device: one setup per device, thread-safe
+  // (contexts on several devices and host threads share this code).
+  static std::mutex attr_mu;
+  static std::vector<char> attr_done;
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if ((int)attr_done.size() <= ctx->device) attr_done.resize(ctx->device + 1, 0);
+    if (!attr_done[ctx->device]) {
+      RPD_CK(cudaFuncSetAttribute(k_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  fit_dyn_smem(kMaxRows)));
+      int per_sm = 0;
+      RPD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit, kFitThreads,
+                                                           fit_dyn_smem(kMaxRows)));
+      if (per_sm * ctx->sm_count < kFitCtas)
+        throw CudaFail("fit: device cannot co-schedule the fit grid");
+      attr_done[ctx->device] = 1;
+    }
   }
   if (!req.compact && req.k_host > (long long)kMaxRows * kFitLanes)
     throw InvalidArg("fit: too many observations for the device fit (max " +
@@ -853,7 +863,7 @@ void fit_dev(rpd_ctx* ctx, const FitRequest& req) {
   P.r = req;
   P.status = ctx->status;
   P.rows_cap = rows_cap;
-  static const bool trace = getenv("RPD_FIT_TRACE") != nullptr;
+  static const bool trace = debug_knob("RPD_FIT_TRACE") != nullptr;
   P.trace = trace ? 1 : 0;
   P.part = ctx->ws.get<unsigned long long>("fit_part", kPartWords);
   RPD_CK(cudaMemsetAsync(P.part, 0, sizeof(unsigned long long) * kPartWords, ctx->stream));

@@ -42,7 +42,7 @@ SgmLayout sgm_layout(int h, int w, int levels, int paths) {
   L.paths = paths;
   // tuning overrides "G,WPL" (RPD_SGM_LAYOUT_SMALL for <= 36 levels, _BIG otherwise)
   auto env_layout = [&](const char* name, int& G, int& wpl) {
-    const char* e = std::getenv(name);
+    const char* e = debug_knob(name);
     int g = 0, wp = 0;
     if (e && std::sscanf(e, "%d,%d", &g, &wp) == 2 && g >= 1 && wp >= 1 && 4 * g * wp >= levels) {
       G = g;
@@ -1164,7 +1164,7 @@ WtaBulkInfo wta_bulk_pick(int nw, int levels) {
 
 // Both volumes of a pass; false when the layout has no bulk instantiation.
 bool launch_wta_bulk(const WtaBulkArgs& wa, int paths, int h, int w, cudaStream_t st) {
-  if (std::getenv("RPD_WTA_TILED")) return false;  // A/B: the previous two-launch WTA
+  if (debug_knob("RPD_WTA_TILED")) return false;  // A/B: the previous two-launch WTA
   const int nw = wa.lw / 4;
   const WtaBulkInfo ki = paths == 8   ? wta_bulk_pick<8>(nw, wa.levels)
                          : paths == 4 ? wta_bulk_pick<4>(nw, wa.levels)
@@ -1426,7 +1426,7 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
       const int smem = (w + 2 * levels) * (narrow ? 9 : 17);
       const CostPxKernel pxfn = window <= 5 ? cost_px_pick(nw, levels) : nullptr;
       const int pxsmem = (w + 8 * nw) * 16 + 2 * 256 * nw * 4;
-      if (pxfn && pxsmem <= 200 * 1024 && !std::getenv("RPD_COST_ROWS")) {
+      if (pxfn && pxsmem <= 200 * 1024 && !debug_knob("RPD_COST_ROWS")) {
         if (pxsmem > 48 * 1024)
           RPD_CK(cudaFuncSetAttribute(pxfn, cudaFuncAttributeMaxDynamicSharedMemorySize, pxsmem));
         pxfn<<<h, 256, pxsmem, st>>>(cl, cr, iv, w, levels, L.pitch / 4, uint32_t(window * window - 1),

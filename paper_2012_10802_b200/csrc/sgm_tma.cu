@@ -607,7 +607,7 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
   args.pitch = L.pitch;
   args.vol_bytes = L.vol_bytes();
   {
-    const char* e = std::getenv("RPD_TMA_DBG");
+    const char* e = debug_knob("RPD_TMA_DBG");
     args.dbg = e ? std::atoi(e) : 0;
   }
   const int R = ki.R;
@@ -622,7 +622,7 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
   args.path_df = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwf, 1);
   args.path_dl = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwl, 1);
   int blocks = 0;
-  const char* dbg = std::getenv("RPD_TMA_TYPES");  // debugging: bitmask of job types to run
+  const char* dbg = debug_knob("RPD_TMA_TYPES");  // debugging: bitmask of job types to run
   const int type_mask = dbg ? std::atoi(dbg) : 7;
   for (int vol = 0; vol < 2; ++vol)
     for (int r = 0; r < paths_n; ++r) {

@@ -20,6 +20,10 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 ORACLE_LIB = ROOT / "oracle" / "_build" / "librpd_oracle.so"
+# The literal reference (untouched /root/reference sources + Eigen shim,
+# oracle/Makefile).  Built here; the prebuilt .so travels to the GPU box.
+REF_LIB = ROOT / "oracle" / "_ref" / "librpd_ref.so"
+REF_SRC = Path("/root/reference/proj/src/sgm.cpp")
 
 
 def pytest_configure(config):
@@ -35,7 +39,7 @@ def pytest_configure(config):
 
 
 def _ensure_oracle():
-    if not ORACLE_LIB.exists():
+    if not ORACLE_LIB.exists() or (REF_SRC.exists() and not REF_LIB.exists()):
         subprocess.run(["make", "-C", str(ROOT / "oracle")], check=True,
                        stdout=subprocess.DEVNULL)
     return ORACLE_LIB
@@ -52,6 +56,35 @@ def oracle(oracle_lib):
     return oracle_lib.context()
 
 
+def have_ref() -> bool:
+    _ensure_oracle()
+    return REF_LIB.exists()
+
+
+@pytest.fixture(scope="session")
+def ref_lib():
+    from paper_2012_10802_b200.api import Library
+    if not have_ref():
+        pytest.skip("literal reference not built (needs /root/reference)")
+    return Library(str(REF_LIB))
+
+
+@pytest.fixture(scope="session")
+def ref(ref_lib):
+    return ref_lib.context()
+
+
+@pytest.hookimpl(hookwrapper=True)
+def pytest_pyfunc_call(pyfuncitem):
+    """A test that reaches an entry point the bound library does not export
+    (the literal reference wraps only the hot path) is skipped, not failed."""
+    from paper_2012_10802_b200.api import MissingSymbol
+    outcome = yield
+    exc = outcome.excinfo
+    if exc is not None and issubclass(exc[0], MissingSymbol):
+        outcome.force_exception(pytest.skip.Exception(str(exc[1]), _use_item_location=True))
+
+
 @pytest.fixture(scope="session")
 def cuda_lib():
     import paper_2012_10802_b200 as pkg
@@ -63,10 +96,14 @@ def gpu(cuda_lib):
     return cuda_lib.context(0)
 
 
-@pytest.fixture(params=["oracle", pytest.param("cuda", marks=pytest.mark.gpu)])
+@pytest.fixture(params=["oracle", "reference", pytest.param("cuda", marks=pytest.mark.gpu)])
 def ctx(request):
+    """Known-answer tests run against the restated oracle, the literal
+    reference build and the CUDA product."""
     if request.param == "oracle":
         return request.getfixturevalue("oracle")
+    if request.param == "reference":
+        return request.getfixturevalue("ref")
     return request.getfixturevalue("gpu")
 
 
