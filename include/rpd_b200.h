@@ -22,6 +22,8 @@
  * Two shared libraries export this exact symbol set:
  *   paper_2012_10802_b200/_lib/librpd_b200.so   — the product (sm_100a CUDA)
  *   oracle/_build/librpd_oracle.so               — CPU restatement, TEST ONLY
+ * and oracle/_ref/librpd_ref.so (TEST ONLY) exports the hot-path subset over
+ * the literal reference sources (oracle/ref_abi.cpp).
  */
 #ifndef RPD_B200_H
 #define RPD_B200_H
@@ -197,7 +199,13 @@ typedef struct rpd_stats {
   double sgm_agg_ms[2];         /* device duration of each aggregation launch */
   double sgm_agg_alg_bytes[2];  /* 2*(5P-2)*cells: u8 cost read + u16 sum read/write */
   double sgm_cells[2];          /* H*W*L of the pass */
+  int32_t last_agg_kernel;      /* aggregation implementation of the context's last
+                                   match_pair / aggregate_costs: RPD_AGG_* */
 } rpd_stats;
+#define RPD_AGG_NONE 0
+#define RPD_AGG_F32 1    /* generic float kernels (non-integral penalties, other directions) */
+#define RPD_AGG_U8_TMA 2 /* production k_aggregate_tma (u8 paths, u16x2 DPX recurrence) */
+#define RPD_AGG_U8 3     /* production u8 kernel without TMA staging (layouts TMA cannot map) */
 rpd_status rpd_ctx_set_profiling(rpd_ctx* ctx, int enable);
 rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out);
 
@@ -213,6 +221,22 @@ rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* rig
                                const rpd_road_model* model, const rpd_config* cfg, int d_max,
                                float* cost, float* agg_left, float* agg_right, float* disp_left,
                                float* disp_right);
+
+/* Same, with the right-reference cost volume swap_reference(cost)
+ * (sgm.cpp:112-121, sgm.cpp:193) as well: the product generates it directly
+ * from the census words inside the cost kernel, so this is the production
+ * volume the right-reference aggregation consumed.  NULL members skip. */
+typedef struct rpd_sgm_dump {
+  float* cost;        /* census_cost_volume, H*W*(d_max+1) */
+  float* cost_right;  /* swap_reference(cost) */
+  float* agg_left;    /* aggregate_costs(cost) */
+  float* agg_right;   /* aggregate_costs(swap_reference(cost)) */
+  float* disp_left;   /* select_disparity(agg_left), H*W */
+  float* disp_right;  /* select_disparity(agg_right) */
+} rpd_sgm_dump;
+rpd_status rpd_match_pair_dump_ex(rpd_ctx* ctx, const float* left, const float* right, int h,
+                                  int w, const rpd_road_model* model, const rpd_config* cfg,
+                                  int d_max, const rpd_sgm_dump* out);
 
 /* ---- perspective transformation (perspective.hpp) ----------------------- */
 /* compute_row_shifts, perspective.hpp:23-35; shifts: H doubles. */
@@ -231,7 +255,12 @@ rpd_status rpd_restore_disparity(rpd_ctx* ctx, const float* d0, int h, int w,
 rpd_status rpd_census_cost_volume(rpd_ctx* ctx, const float* left, const float* right_warped,
                                   int h, int w, int d_max, int window,
                                   const uint8_t* right_in_view, float* costs);
-/* aggregate_costs, sgm.hpp:56; dirs: ndirs (du,dv) pairs. */
+/* aggregate_costs, sgm.hpp:56; dirs: ndirs (du,dv) pairs.  The product runs
+ * the production u8 aggregation kernels (RPD_AGG_U8_TMA) whenever their
+ * result is provably the reference's: integral costs and penalties,
+ * 1 <= lambda1 <= lambda2, max(cost) + lambda2 <= 255, and the direction set
+ * equal to the first 4 or all 8 of kEightDirections; otherwise the generic
+ * float kernels (RPD_AGG_F32). */
 rpd_status rpd_aggregate_costs(rpd_ctx* ctx, const float* costs, int h, int w, int d_max,
                                const int32_t* dirs, int ndirs, float lambda1, float lambda2,
                                float* aggregated);

@@ -488,6 +488,18 @@ rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* rig
                                const rpd_road_model* m, const rpd_config* cfg, int d_max,
                                float* cost, float* agg_left, float* agg_right, float* disp_left,
                                float* disp_right) {
+  const rpd_sgm_dump d{cost, nullptr, agg_left, agg_right, disp_left, disp_right};
+  return rpd_match_pair_dump_ex(ctx, left, right, h, w, m, cfg, d_max, &d);
+}
+
+rpd_status rpd_match_pair_dump_ex(rpd_ctx* ctx, const float* left, const float* right, int h,
+                                  int w, const rpd_road_model* m, const rpd_config* cfg,
+                                  int d_max, const rpd_sgm_dump* out) {
+  float* cost = out->cost;
+  float* agg_left = out->agg_left;
+  float* agg_right = out->agg_right;
+  float* disp_left = out->disp_left;
+  float* disp_right = out->disp_right;
   return guard(ctx, [&] {  // the intermediates of sgm.cpp:179-194, same calls
     check_dims(h, w);
     const rpd::PipelineConfig c = to_config(*cfg);
@@ -498,8 +510,10 @@ rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* rig
     const rpd::CostVolume raw = rpd::census_cost_volume(to_raster<float>(left, h, w), wr.image,
                                                         d_max, c.census_window, &wr.in_view);
     const rpd::CostVolume al = rpd::aggregate_costs(raw, params);
-    const rpd::CostVolume ar = rpd::aggregate_costs(rpd::swap_reference(raw), params);
+    const rpd::CostVolume cr = rpd::swap_reference(raw);
+    const rpd::CostVolume ar = rpd::aggregate_costs(cr, params);
     put_volume(cost, raw);
+    put_volume(out->cost_right, cr);
     put_volume(agg_left, al);
     put_volume(agg_right, ar);
     put(disp_left, rpd::select_disparity(al));

@@ -1363,6 +1363,23 @@ rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* rig
   });
 }
 
+rpd_status rpd_match_pair_dump_ex(rpd_ctx* ctx, const float* left, const float* right, int h,
+                                  int w, const rpd_road_model* m, const rpd_config* cfg,
+                                  int d_max, const rpd_sgm_dump* out) {
+  const rpd_status st = rpd_match_pair_dump(ctx, left, right, h, w, m, cfg, d_max, out->cost,
+                                            out->agg_left, out->agg_right, out->disp_left,
+                                            out->disp_right);
+  if (st != RPD_OK || !out->cost_right) return st;
+  return guard(ctx, [&] {  // swap_reference of the same census volume (sgm.cpp:193)
+    const Shifts t = row_shifts({m->a0, m->a1, m->phi}, w, h, cfg->delta_pt);
+    const Warped wr = warp(to_gray(right, h, w), t);
+    const Volume raw =
+        cost_volume(to_gray(left, h, w), wr.img, d_max, cfg->census_window, &wr.in_view);
+    const Volume cr = swap_ref(raw);
+    std::memcpy(out->cost_right, cr.c.data(), sizeof(float) * cr.c.size());
+  });
+}
+
 rpd_status rpd_sample_observations(rpd_ctx* ctx, const float* d1, int h, int w,
                                    const rpd_rect_roi* roi, int64_t cap, double* d, double* u,
                                    double* v, int64_t* count) {

@@ -329,7 +329,17 @@ _SIGS = {
 class Stats(C.Structure):
     _fields_ = [("kernels_last_frame", C.c_int32), ("graph_replayed", C.c_int32),
                 ("sgm_passes", C.c_int32), ("sgm_agg_ms", C.c_double * 2),
-                ("sgm_agg_alg_bytes", C.c_double * 2), ("sgm_cells", C.c_double * 2)]
+                ("sgm_agg_alg_bytes", C.c_double * 2), ("sgm_cells", C.c_double * 2),
+                ("last_agg_kernel", C.c_int32)]
+
+
+AGG_KERNELS = {0: "none", 1: "f32", 2: "u8_tma", 3: "u8"}  # RPD_AGG_*
+
+
+class SgmDump(C.Structure):
+    """rpd_sgm_dump (rpd_match_pair_dump_ex)."""
+    _fields_ = [("cost", _vp), ("cost_right", _vp), ("agg_left", _vp), ("agg_right", _vp),
+                ("disp_left", _vp), ("disp_right", _vp)]
 
 
 _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
@@ -345,6 +355,10 @@ _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
 }
 _SIGS["rpd_match_pair_dump"] = (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
                                           C.POINTER(Config), C.c_int, _vp, _vp, _vp, _vp, _vp])
+
+_SIGS["rpd_match_pair_dump_ex"] = (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int,
+                                             C.POINTER(RoadModel), C.POINTER(Config), C.c_int,
+                                             C.POINTER(SgmDump)])
 
 ABI_SYMBOLS = tuple(_SIGS)
 EXTENSION_SYMBOLS = tuple(_EXT_SIGS)
@@ -631,6 +645,21 @@ class Context:
                                                  *[_ptr(v) for v in vols],
                                                  *[_ptr(m) for m in maps]))
         return (*vols, *maps)
+
+    def match_pair_dump_ex(self, left, right, model: RoadModel, cfg: Config, d_max: int):
+        """match_pair intermediates incl. the right-reference costs, as a dict:
+        cost, cost_right, agg_left, agg_right (H x W x L), disp_left, disp_right."""
+        left = _f32(left)
+        right = _f32(right)
+        h, w = left.shape
+        res = {k: np.empty((h, w, d_max + 1), np.float32)
+               for k in ("cost", "cost_right", "agg_left", "agg_right")}
+        res.update({k: np.empty((h, w), np.float32) for k in ("disp_left", "disp_right")})
+        d = SgmDump(**{k: v.ctypes.data for k, v in res.items()})
+        self._check(self.dll.rpd_match_pair_dump_ex(self.handle, _ptr(left), _ptr(right), h, w,
+                                                    C.byref(model), C.byref(cfg), d_max,
+                                                    C.byref(d)))
+        return res
 
     # ------------------------------------------------------- road geometry --
     def sample_observations(self, d1, roi: Optional[RectRoi] = None, cap: int = 100000):

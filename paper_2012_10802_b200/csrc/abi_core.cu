@@ -127,6 +127,7 @@ rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out) {
     rpd_stats s{};
     s.kernels_last_frame = ctx->kernels_last_frame;
     s.graph_replayed = ctx->graph_replayed;
+    s.last_agg_kernel = ctx->last_agg_kernel;
     s.sgm_passes = ctx->profile ? ctx->agg_pass : 0;
     for (int i = 0; i < s.sgm_passes; ++i) {
       float ms = 0;
@@ -223,9 +224,16 @@ rpd_status rpd_aggregate_costs(rpd_ctx* ctx, const float* costs, int h, int w, i
     check_dims(h, w);
     if (d_max < 0 || ndirs < 0) throw InvalidArg("aggregate_costs: bad dimensions");
     const size_t cells = size_t(h) * w * size_t(d_max + 1);
+    int paths = 0;
+    const bool u8 = aggregate_u8_eligible(costs, cells, d_max + 1, dirs, ndirs, l1, l2, &paths);
     const float* c = upload(ctx, "abi_vol0", costs, cells);
     float* o = ctx->ws.get<float>("abi_vol1", cells);
-    aggregate_f32(ctx, c, h, w, d_max + 1, dirs, ndirs, l1, l2, o);
+    if (u8) {
+      aggregate_u8_dev(ctx, c, h, w, d_max + 1, paths, l1, l2, o);
+    } else {
+      aggregate_f32(ctx, c, h, w, d_max + 1, dirs, ndirs, l1, l2, o);
+      ctx->last_agg_kernel = kAggF32;
+    }
     download(ctx, agg, o, sizeof(float) * cells);
   });
 }
@@ -293,6 +301,19 @@ rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* rig
                                const rpd_road_model* model, const rpd_config* cfg, int d_max,
                                float* cost, float* agg_left, float* agg_right, float* disp_left,
                                float* disp_right) {
+  const rpd_sgm_dump d{cost, nullptr, agg_left, agg_right, disp_left, disp_right};
+  return rpd_match_pair_dump_ex(ctx, left, right, h, w, model, cfg, d_max, &d);
+}
+
+rpd_status rpd_match_pair_dump_ex(rpd_ctx* ctx, const float* left, const float* right, int h,
+                                  int w, const rpd_road_model* model, const rpd_config* cfg,
+                                  int d_max, const rpd_sgm_dump* out) {
+  float* cost = out->cost;
+  float* cost_right = out->cost_right;
+  float* agg_left = out->agg_left;
+  float* agg_right = out->agg_right;
+  float* disp_left = out->disp_left;
+  float* disp_right = out->disp_right;
   return guard(ctx, [&] {
     check_dims(h, w);
     if (cfg->sgm_paths != 4 && cfg->sgm_paths != 8)
@@ -308,12 +329,14 @@ rpd_status rpd_match_pair_dump(rpd_ctx* ctx, const float* left, const float* rig
     double* s = ctx->ws.get<double>("abi_shifts", h);
     MatchDump dump;
     dump.cost = cost ? ctx->ws.get<float>("abi_dump_cost", cells) : nullptr;
+    dump.cost_right = cost_right ? ctx->ws.get<float>("abi_dump_costr", cells) : nullptr;
     dump.agg_left = agg_left ? ctx->ws.get<float>("abi_dump_aggl", cells) : nullptr;
     dump.agg_right = agg_right ? ctx->ws.get<float>("abi_dump_aggr", cells) : nullptr;
     dump.disp_left = disp_left ? ctx->ws.get<float>("abi_dump_dl", n) : nullptr;
     dump.disp_right = disp_right ? ctx->ws.get<float>("abi_dump_dr", n) : nullptr;
     match_pair_dev(ctx, l, r, h, w, m, *cfg, d_max, o0, o1, s, &dump);
     if (cost) download(ctx, cost, dump.cost, sizeof(float) * cells);
+    if (cost_right) download(ctx, cost_right, dump.cost_right, sizeof(float) * cells);
     if (agg_left) download(ctx, agg_left, dump.agg_left, sizeof(float) * cells);
     if (agg_right) download(ctx, agg_right, dump.agg_right, sizeof(float) * cells);
     if (disp_left) download(ctx, disp_left, dump.disp_left, sizeof(float) * n);

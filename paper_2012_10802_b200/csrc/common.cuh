@@ -199,6 +199,7 @@ struct rpd_ctx {
   double agg_cells[2] = {0, 0};
   int kernels_last_frame = 0;
   int graph_replayed = 0;
+  int last_agg_kernel = 0;  // rpdg::AggImpl of the last aggregation
 };
 
 namespace rpdg {

@@ -577,6 +577,20 @@ __global__ void k_u8vol_to_f32(const uint8_t* __restrict__ vol, int w, long long
   }
 }
 
+// Float reference layout -> u8 volume (row pitch, pixel stride lw), levels
+// >= L padded with 0xFF like the cost kernels (aggregate_costs ABI route).
+__global__ void k_f32_to_u8vol(const float* __restrict__ in, int w, long long npix, size_t pitch,
+                               int lw, int levels, uint8_t* __restrict__ vol) {
+  const long long n = npix * lw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / lw;
+    const int d = int(i % lw);
+    vol[size_t(p / w) * pitch + size_t(p % w) * lw + d] =
+        d < levels ? uint8_t(in[p * levels + d]) : uint8_t(0xFF);
+  }
+}
+
 // ------------------------------------------------------ path aggregation --
 struct AggJob {
   const uint8_t* cost;
@@ -1393,6 +1407,7 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
 
   if (!sgm_fast_path_ok(l1, l2, window) || levels > kMaxFastLevels) {
     // generic float path (non-integral or very large penalties)
+    ctx->last_agg_kernel = kAggF32;
     float* cost = ctx->ws.get<float>("mp_cost_f32", size_t(npix) * levels);
     float* costr = ctx->ws.get<float>("mp_costr_f32", size_t(npix) * levels);
     float* agg = ctx->ws.get<float>("mp_agg_f32", size_t(npix) * levels);
@@ -1403,6 +1418,9 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
                              cudaMemcpyDeviceToDevice, st));
     select_disparity_f32(agg, h, w, levels, dl, st);
     swap_reference_f32(ctx, cost, h, w, levels, costr);
+    if (dump && dump->cost_right)
+      RPD_CK(cudaMemcpyAsync(dump->cost_right, costr, sizeof(float) * npix * levels,
+                             cudaMemcpyDeviceToDevice, st));
     aggregate_f32(ctx, costr, h, w, levels, dirs, paths, l1, l2, agg);
     if (dump && dump->agg_right)
       RPD_CK(cudaMemcpyAsync(dump->agg_right, agg, sizeof(float) * npix * levels,
@@ -1454,7 +1472,9 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
     if (prof) record_event(ctx, ctx->agg_ev[pass][0]);
     if (sgm_tma_supported(L)) {
       launch_aggregate_tma(ctx, L, vol_l, pathbuf, dirs, paths, p1, p2);
+      ctx->last_agg_kernel = kAggU8Tma;
     } else {
+      ctx->last_agg_kernel = kAggU8;
       AggArgs args{};
       args.h = h;
       args.w = w;
@@ -1521,10 +1541,14 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
       }
       RPD_LAUNCH_CHECK();
     }
-    if (dump && dump->cost) {
+    if (dump && (dump->cost || dump->cost_right)) {
       const long long n = npix * levels;
-      k_u8vol_to_f32<<<int(std::min<long long>((n + 255) / 256, 148 * 32)), 256, 0, st>>>(
-          vol_l, w, npix, L.pitch, L.lw, levels, dump->cost);
+      const int nb = int(std::min<long long>((n + 255) / 256, 148 * 32));
+      if (dump->cost)
+        k_u8vol_to_f32<<<nb, 256, 0, st>>>(vol_l, w, npix, L.pitch, L.lw, levels, dump->cost);
+      if (dump->cost_right)  // the right-reference volume the cost kernel generated
+        k_u8vol_to_f32<<<nb, 256, 0, st>>>(vol_r, w, npix, L.pitch, L.lw, levels,
+                                           dump->cost_right);
       RPD_LAUNCH_CHECK();
     }
     k_post<uint8_t><<<rowgrid, 128, 0, st>>>(dl, dr, vol_l, L.lw, L.pitch, iv, shifts, h, w,
@@ -1537,6 +1561,104 @@ void match_pair_dev(rpd_ctx* ctx, const float* left, const float* right, int h, 
   if (dump && dump->disp_right)
     RPD_CK(cudaMemcpyAsync(dump->disp_right, dr, sizeof(float) * npix, cudaMemcpyDeviceToDevice,
                            st));
+}
+
+
+// ------------------------------------------- aggregate_costs, u8 route ----
+bool aggregate_u8_eligible(const float* costs, size_t cells, int levels, const int32_t* dirs,
+                           int ndirs, float l1, float l2, int* paths) {
+  if (!(l1 >= 1.0f && l2 >= l1 && l1 == std::floor(l1) && l2 == std::floor(l2)))
+    return false;
+  if (levels > kMaxFastLevels) return false;
+  // direction set = first 4 or all 8 of kEightDirections (sum order is
+  // irrelevant: every partial sum is an exact integer)
+  const int eight[16] = {1, 0, -1, 0, 0, 1, 0, -1, 1, 1, -1, 1, 1, -1, -1, -1};
+  if (ndirs != 4 && ndirs != 8) return false;
+  bool seen[8] = {};
+  for (int i = 0; i < ndirs; ++i) {
+    int k = 0;
+    while (k < ndirs && !(eight[2 * k] == dirs[2 * i] && eight[2 * k + 1] == dirs[2 * i + 1])) ++k;
+    if (k == ndirs || seen[k]) return false;
+    seen[k] = true;
+  }
+  float mx = 0.0f;
+  for (size_t i = 0; i < cells; ++i) {
+    const float c = costs[i];
+    if (!(c >= 0.0f) || c != std::floor(c)) return false;
+    mx = std::max(mx, c);
+  }
+  if (mx + l2 > 255.0f) return false;  // every path value fits u8
+  *paths = ndirs;
+  return true;
+}
+
+void aggregate_u8_dev(rpd_ctx* ctx, const float* costs, int h, int w, int levels, int paths,
+                      float l1, float l2, float* out) {
+  cudaStream_t st = ctx->stream;
+  const long long npix = (long long)h * w;
+  const SgmLayout L = sgm_layout(h, w, levels, paths);
+  const size_t vb = L.vol_bytes();
+  uint8_t* vol = ctx->ws.get<uint8_t>("ag_vols", 2 * vb);  // TMA maps span two planes
+  uint8_t* pathbuf = ctx->ws.get<uint8_t>("ag_paths", vb * paths);
+  float* disp = ctx->ws.get<float>("ag_disp", npix);
+  {
+    const long long n = npix * L.lw;
+    k_f32_to_u8vol<<<int(std::min<long long>((n + 255) / 256, 148 * 32)), 256, 0, st>>>(
+        costs, w, npix, L.pitch, L.lw, levels, vol);
+    RPD_LAUNCH_CHECK();
+  }
+  const int eight[16] = {1, 0, -1, 0, 0, 1, 0, -1, 1, 1, -1, 1, 1, -1, -1, -1};
+  int32_t dirs[16];
+  for (int i = 0; i < 2 * paths; ++i) dirs[i] = eight[i];
+  const uint32_t p1 = uint32_t(l1), p2 = uint32_t(l2);
+  if (sgm_tma_supported(L)) {
+    launch_aggregate_tma(ctx, L, vol, pathbuf, dirs, paths, p1, p2, /*nvols=*/1);
+    ctx->last_agg_kernel = kAggU8Tma;
+  } else {
+    AggArgs args{};
+    args.h = h;
+    args.w = w;
+    args.lw = L.lw;
+    args.pitch = L.pitch;
+    args.p1x2 = p1 | (p1 << 16);
+    args.p2x2 = p2 | (p2 << 16);
+    const int cpb = kAggThreads / L.G;
+    int blocks = 0;
+    for (int r = 0; r < paths; ++r) {
+      AggJob& J = args.job[args.njobs++];
+      J.cost = vol;
+      J.out = pathbuf + size_t(r) * vb;
+      J.du = dirs[2 * r];
+      J.dv = dirs[2 * r + 1];
+      J.nchains = (J.dv == 0) ? h : w;
+      J.block0 = blocks;
+      blocks += cdiv(J.nchains, cpb);
+    }
+    agg_kernel(L.wpl, L.G)<<<blocks, kAggThreads, 0, st>>>(args);
+    RPD_LAUNCH_CHECK();
+    ctx->last_agg_kernel = kAggU8;
+  }
+  // exact u16 sums over the paths, written in the reference float layout
+  WtaArgs wa{};
+  for (int r = 0; r < paths; ++r) wa.path[r] = pathbuf + size_t(r) * vb;
+  wa.paths = paths;
+  wa.npix = npix;
+  wa.w = w;
+  wa.pitch = L.pitch;
+  wa.lw = L.lw;
+  wa.levels = levels;
+  wa.disp = disp;
+  wa.dump = out;
+  if (L.lw / 4 <= kWtaMaxWords) {
+    const int smem = kWtaPx * (2 * (L.lw / 4) + 1) * 4;
+    if (paths == 8)
+      k_wta_tiled<8><<<dim3(cdiv(w, kWtaPx), h), kWtaPx, smem, st>>>(wa);
+    else
+      k_wta_tiled<4><<<dim3(cdiv(w, kWtaPx), h), kWtaPx, smem, st>>>(wa);
+  } else {
+    k_wta<<<cdiv(npix, 128), 128, 0, st>>>(wa);
+  }
+  RPD_LAUNCH_CHECK();
 }
 
 }  // namespace rpdg

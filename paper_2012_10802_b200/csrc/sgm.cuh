@@ -22,8 +22,25 @@ SgmLayout sgm_layout(int h, int w, int levels, int paths);
 // (sgm_tma.cu).  vol_lr: left- then right-reference u8 cost volumes;
 // paths: 2P per-path u8 output volumes, each vol_bytes() apart.
 bool sgm_tma_supported(const SgmLayout& L);
+// nvols = 1 aggregates only the first (left-reference) volume.
 void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uint8_t* paths,
-                          const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2);
+                          const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2,
+                          int nvols = 2);
+
+// Which aggregation implementation the last match_pair / aggregate_costs of
+// a context ran (rpd_stats.last_agg_kernel).
+enum AggImpl { kAggNone = 0, kAggF32 = 1, kAggU8Tma = 2, kAggU8 = 3 };
+
+// aggregate_costs (sgm.cpp:70-110) through the production u8 kernels
+// (k_aggregate_tma + the WTA's exact u16 sums) — the ABI entry takes this
+// route whenever the result is provably identical to the float recursion:
+// integral costs and penalties with max(cost) + lambda2 <= 255, and the
+// direction set equal to the first 4 or all 8 of kEightDirections.  Returns
+// false (nothing launched) when the volume does not qualify.
+bool aggregate_u8_eligible(const float* costs_host, size_t cells, int levels,
+                           const int32_t* dirs, int ndirs, float l1, float l2, int* paths);
+void aggregate_u8_dev(rpd_ctx* ctx, const float* costs, int h, int w, int levels, int paths,
+                      float l1, float l2, float* out);
 
 // Whether the integer u8/u16x2 path reproduces the reference's float
 // arithmetic bit-exactly for these penalties (integral lambdas and
@@ -38,6 +55,7 @@ struct MatchDump {
   float* agg_right = nullptr;  // aggregate_costs(swap_reference(cost))
   float* disp_left = nullptr;  // select_disparity(agg_left)
   float* disp_right = nullptr; // select_disparity(agg_right)
+  float* cost_right = nullptr; // swap_reference(cost)
 };
 
 // ---------------------------------------------------------------- kernels --

@@ -594,7 +594,8 @@ bool sgm_tma_supported(const SgmLayout& L) {
 
 // Launches the aggregation of all 2P (volume, direction) jobs of one pass.
 void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uint8_t* paths,
-                          const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2) {
+                          const int32_t* dirs, int paths_n, uint32_t p1, uint32_t p2,
+                          int nvols) {
   const KernelInfo ki = pick(L.wpl, L.G, L.levels);
   const int wpp = L.lw / 4;
   const int words_row = L.w * wpp;
@@ -624,7 +625,7 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
   int blocks = 0;
   const char* dbg = debug_knob("RPD_TMA_TYPES");  // debugging: bitmask of job types to run
   const int type_mask = dbg ? std::atoi(dbg) : 7;
-  for (int vol = 0; vol < 2; ++vol)
+  for (int vol = 0; vol < nvols; ++vol)
     for (int r = 0; r < paths_n; ++r) {
       const int du = dirs[2 * r], dv = dirs[2 * r + 1];
       const int ty = dv == 0 ? kHoriz : (du == 0 ? kVert : kDiag);

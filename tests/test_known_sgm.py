@@ -13,7 +13,7 @@ import sys
 import numpy as np
 import pytest
 
-from paper_2012_10802_b200.api import EIGHT_DIRECTIONS, InvalidArgument, model
+from paper_2012_10802_b200.api import AGG_KERNELS, EIGHT_DIRECTIONS, InvalidArgument, model
 from conftest import mt_textured
 
 
@@ -43,6 +43,34 @@ def dp_oracle_aggregate(raw, l1, l2, directions):
                 for d in range(n):
                     total[v, u, d] = np.float32(total[v, u, d] + np.float32(agg(v, u, d)))
     return total
+
+
+def scan_aggregate(raw, l1, l2, directions):
+    """Vectorised scan-order restatement of aggregate_costs (sgm.cpp:70-110)
+    in float64 (every value an exact integer here), for volumes too large for
+    the memoised recursion."""
+    h, w, n = raw.shape
+    raw = raw.astype(np.float64)
+    total = np.zeros_like(raw)
+    for du, dv in directions:
+        lr = np.empty_like(raw)
+        vs = range(h) if dv >= 0 else range(h - 1, -1, -1)
+        us = list(range(w)) if du >= 0 else list(range(w - 1, -1, -1))
+        for v in vs:
+            for u in us:
+                pv, pu = v - dv, u - du
+                if pv < 0 or pv >= h or pu < 0 or pu >= w:
+                    lr[v, u] = raw[v, u]
+                    continue
+                prev = lr[pv, pu]
+                m = prev.min()
+                best = prev.copy()
+                best[1:] = np.minimum(best[1:], prev[:-1] + l1)
+                best[:-1] = np.minimum(best[:-1], prev[1:] + l1)
+                best = np.minimum(best, m + l2)
+                lr[v, u] = raw[v, u] + best - m
+        total += lr
+    return total.astype(np.float32)
 
 
 def random_volume(w, h, d_max, seed, cost_max=40):
@@ -103,7 +131,30 @@ def test_acceptance_check1_random_volumes_equal_dp_oracle(ctx):
         w, h, dm = int(rng.integers(2, 17)), int(rng.integers(2, 17)), int(rng.integers(1, 9))
         vol = rng.integers(0, 61, size=(h, w, dm + 1)).astype(np.float32)
         agg = ctx.aggregate_costs(vol, 7.0, 21.0)
+        if ctx.lib.has_streaming:  # the product: these volumes take the production kernel
+            assert AGG_KERNELS[ctx.stats().last_agg_kernel] == "u8_tma"
         exp = dp_oracle_aggregate(vol, 7.0, 21.0, EIGHT_DIRECTIONS)
+        assert np.array_equal(agg, exp)
+
+
+@pytest.mark.parametrize("paths", [4, 8])
+def test_acceptance_volumes_production_kernel_both_path_counts(ctx, paths):
+    """acceptance.cpp:78-102's volumes with the 4- and 8-path direction sets
+    (costs 0..60, lambda 7/21 fit the production u8 kernel) plus level counts
+    up to the pipeline's (17, 33, 65, 129) on wider rasters."""
+    rng = np.random.default_rng(2002 + paths)
+    dirs = EIGHT_DIRECTIONS[:paths]
+    shapes = [(int(rng.integers(2, 17)), int(rng.integers(2, 17)), int(rng.integers(1, 9)))
+              for _ in range(12)] + [(3, 40, 16), (4, 33, 32), (2, 70, 64), (2, 140, 128)]
+    for w, h, dm in shapes:
+        vol = rng.integers(0, 61, size=(h, w, dm + 1)).astype(np.float32)
+        agg = ctx.aggregate_costs(vol, 7.0, 21.0, dirs)
+        if ctx.lib.has_streaming:
+            assert AGG_KERNELS[ctx.stats().last_agg_kernel] == "u8_tma"
+        exp = dp_oracle_aggregate(vol, 7.0, 21.0, dirs) if dm < 20 else None
+        if exp is None:  # the DP oracle recursion is too slow here: scan oracle
+            from test_known_sgm import scan_aggregate
+            exp = scan_aggregate(vol, 7.0, 21.0, dirs)
         assert np.array_equal(agg, exp)
 
 
