@@ -182,6 +182,16 @@ rpd_status rpd_input_buffers_u8(rpd_ctx* ctx, int h, int w, uint8_t** d_left, ui
 rpd_status rpd_detect_async_u8(rpd_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right,
                                int h, int w, const rpd_config* cfg);
 rpd_status rpd_detect_fetch(rpd_ctx* ctx, rpd_detect_out* out);
+/* Streaming from host memory (BASELINE config 5's pinned double-buffered
+ * upload): enqueues the H2D copy of the pair and the frame on the context
+ * stream and returns.  The copy is asynchronous when left/right are pinned
+ * (rpd_host_alloc); they must stay unchanged until rpd_detect_fetch returns,
+ * so a caller alternates two slots and fills the next while a frame runs. */
+rpd_status rpd_detect_async_host_u8(rpd_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                                    int h, int w, const rpd_config* cfg);
+/* Page-locked host memory for the streaming buffers (cudaHostAlloc). */
+rpd_status rpd_host_alloc(size_t bytes, void** out);
+void rpd_host_free(void* p);
 /* Same as rpd_detect_async_u8 for device-resident float32 images (e.g. the
  * output of rpd_generate_scenes_device). */
 rpd_status rpd_detect_async(rpd_ctx* ctx, const float* d_left, const float* d_right, int h, int w,

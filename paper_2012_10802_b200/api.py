@@ -349,6 +349,9 @@ _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
     "rpd_detect_async": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config)]),
     "rpd_generate_scenes_device": (C.c_int, [_vp, C.c_int, C.POINTER(SceneSpecC), _vp, _vp, _vp,
                                              _vp]),
+    "rpd_detect_async_host_u8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(Config)]),
+    "rpd_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "rpd_host_free": (None, [_vp]),
     "rpd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rpd_ctx_stats": (C.c_int, [_vp, C.POINTER(Stats)]),
     "rpd_debug_sincos": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
@@ -390,6 +393,20 @@ class Library:
                 fn.argtypes = args
         if self.dll.rpd_abi_version() != 1:
             raise RpdError(f"{path}: unexpected ABI version")
+
+    def pinned_empty(self, shape, dtype):
+        """numpy array over page-locked host memory (rpd_host_alloc); freed
+        when the array is garbage collected."""
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        p = _vp()
+        if self.dll.rpd_host_alloc(nbytes, C.byref(p)) != RPD_OK:
+            raise MemoryError("rpd_host_alloc failed")
+        buf = (C.c_uint8 * max(nbytes, 1)).from_address(p.value)
+        arr = np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
+        import weakref
+        weakref.finalize(buf, self.dll.rpd_host_free, p.value)
+        return arr
 
     def default_config(self, **overrides) -> Config:
         cfg = Config()
@@ -508,6 +525,11 @@ class Context:
     def detect_async_u8(self, d_left: int, d_right: int, h: int, w: int, cfg: Config):
         self._check(self.dll.rpd_detect_async_u8(self.handle, d_left, d_right, h, w,
                                                  C.byref(cfg)))
+
+    def detect_async_host_u8(self, left_ptr: int, right_ptr: int, h: int, w: int, cfg: Config):
+        """Enqueue H2D (async from pinned memory) + the frame; fetch() completes it."""
+        self._check(self.dll.rpd_detect_async_host_u8(self.handle, left_ptr, right_ptr, h, w,
+                                                      C.byref(cfg)))
 
     def detect_async(self, d_left: int, d_right: int, h: int, w: int, cfg: Config):
         """Device-resident float32 images (e.g. from generate_scenes_device)."""

@@ -445,6 +445,39 @@ rpd_status rpd_detect_async(rpd_ctx* ctx, const float* d_left, const float* d_ri
   });
 }
 
+rpd_status rpd_detect_async_host_u8(rpd_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                                    int h, int w, const rpd_config* cfg) {
+  return guard(ctx, [&] {
+    check_pipeline_args(cfg, h, w);
+    const size_t n = size_t(h) * w;
+    uint8_t* l = ctx->ws.get<uint8_t>("pl_left8", n);
+    uint8_t* r = ctx->ws.get<uint8_t>("pl_right8", n);
+    // asynchronous (DMA) when the host buffers are pinned (rpd_host_alloc)
+    RPD_CK(cudaMemcpyAsync(l, left, n, cudaMemcpyHostToDevice, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(r, right, n, cudaMemcpyHostToDevice, ctx->stream));
+    PipelineState& ps = state(ctx);
+    run_frame(ctx, h, w, true, *cfg, ps.last);
+    ps.have_last = true;
+    ps.last_h = h;
+    ps.last_w = w;
+  });
+}
+
+rpd_status rpd_host_alloc(size_t bytes, void** out) {
+  if (!out) return RPD_EINVAL;
+  *out = nullptr;
+  if (cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return RPD_ENOMEM;
+  }
+  return RPD_OK;
+}
+
+void rpd_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 rpd_status rpd_detect_fetch(rpd_ctx* ctx, rpd_detect_out* out) {
   return guard(ctx, [&] {
     PipelineState& ps = state(ctx);

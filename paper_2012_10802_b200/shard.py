@@ -13,6 +13,7 @@ std::async threads on the CPU (rpd_cli.cpp:293-302).
 """
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 import threading
 import time
@@ -52,7 +53,15 @@ def summarize(frame: int, res) -> FrameSummary:
 
 
 class StreamingRunner:
-    """Processes frames with `n_streams` concurrent contexts of one library."""
+    """Processes frames with `n_streams` concurrent contexts of one library.
+
+    With the CUDA library every worker thread owns a context (its own CUDA
+    stream) and two pinned host slots (rpd_host_alloc): while frame k runs on
+    the device — its H2D copy enqueued asynchronously from slot k % 2 — the
+    thread builds frame k + 1 into the other slot, then fetches k's outputs
+    into pinned result buffers (BASELINE config 5: "pinned double-buffered
+    host upload").  Libraries without the streaming extension (the CPU
+    oracle) run plain synchronous detect calls per thread."""
 
     def __init__(self, lib, device: int = 0, n_streams: int = 2):
         self.lib = lib
@@ -65,20 +74,57 @@ class StreamingRunner:
         next_idx = [0]
         lock = threading.Lock()
 
-        def worker(ctx):
+        def take():
+            with lock:
+                i = next_idx[0]
+                next_idx[0] += 1
+            return i if i < len(frame_ids) else None
+
+        def worker_sync(ctx):
+            while (i := take()) is not None:
+                left, right = make_frame(frame_ids[i])
+                out[i] = summarize(frame_ids[i], ctx.detect(left, right, cfg, want=want))
+
+        def worker_pinned(ctx):
+            from .api import DetectOut, Threshold  # noqa: F401
+            slots, outs = None, None
+            i = take()
+            if i is None:
+                return
+            left, right = make_frame(frame_ids[i])
+            h, w = left.shape
+            slots = [(self.lib.pinned_empty((h, w), np.uint8),
+                      self.lib.pinned_empty((h, w), np.uint8)) for _ in range(2)]
+            labels = self.lib.pinned_empty((h, w), np.int32)
+            o = DetectOut()
+            o.labels = labels.ctypes.data_as(C.POINTER(C.c_int32))
+            cur = 0
+            slots[cur][0][...] = left
+            slots[cur][1][...] = right
+            ctx.detect_async_host_u8(slots[cur][0].ctypes.data, slots[cur][1].ctypes.data, h, w,
+                                     cfg)
             while True:
-                with lock:
-                    i = next_idx[0]
-                    next_idx[0] += 1
-                if i >= len(frame_ids):
+                j = take()
+                if j is not None:  # build the next frame while this one runs
+                    nl, nr = make_frame(frame_ids[j])
+                    slots[1 - cur][0][...] = nl
+                    slots[1 - cur][1][...] = nr
+                ctx.fetch(o)
+                out[i] = _summary_from_out(frame_ids[i], o, labels)
+                if j is None:
                     return
-                try:
-                    left, right = make_frame(frame_ids[i])
-                    res = ctx.detect(left, right, cfg, want=want)
-                    out[i] = summarize(frame_ids[i], res)
-                except Exception as e:  # surfaced after join
-                    errors.append(e)
-                    return
+                i, cur = j, 1 - cur
+                ctx.detect_async_host_u8(slots[cur][0].ctypes.data, slots[cur][1].ctypes.data,
+                                         h, w, cfg)
+
+        pinned = getattr(self.lib, "has_streaming", False) and "rpd_detect_async_host_u8" \
+            not in getattr(self.lib, "missing", ())
+
+        def worker(ctx):
+            try:
+                (worker_pinned if pinned else worker_sync)(ctx)
+            except Exception as e:  # surfaced after join
+                errors.append(e)
 
         threads = [threading.Thread(target=worker, args=(c,)) for c in self.ctxs]
         for t in threads:
@@ -88,6 +134,14 @@ class StreamingRunner:
         if errors:
             raise errors[0]
         return [s for s in out if s is not None]
+
+
+def _summary_from_out(frame: int, o, labels) -> FrameSummary:
+    from .api import STAGE_NAMES
+    sha = hashlib.sha1(np.ascontiguousarray(labels).tobytes()).hexdigest()
+    m = o.fit.model
+    return FrameSummary(frame, int(o.n_potholes), sha, (m.a0, m.a1, m.phi),
+                        dict(zip(STAGE_NAMES, list(o.stage_ms))))
 
 
 def run_sharded(lib, make_frame: Callable[[int], tuple], cfg, n_frames: int, rank: int,

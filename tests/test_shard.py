@@ -70,3 +70,24 @@ def test_two_rank_gloo_matches_single_process(tmp_path, oracle_lib):
     single, _ = run_sharded(oracle_lib, _make_frame, cfg, 6, 0, 1, n_streams=1)
     assert [m[0] for m in multi] == list(range(6))
     assert multi == [[s.frame, s.n_potholes, s.labels_sha1] for s in single]
+
+
+def test_bench_gpus2_spawns_sharded_ranks():
+    """`bench.py --gpus 2` without a torchrun environment spawns one process
+    per rank (gloo + the oracle backend here), shards the config-5 frame
+    stream round-robin and reports the whole-job numbers with n_gpus = 2."""
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--backend", "oracle",
+         "--config", "5", "--steps", "1", "--warmup", "0", "--streams", "2", "--frames", "2",
+         "--pool", "2"], capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+    res = json.loads(line)
+    assert res["n_gpus"] == 2
+    assert res["frame_ids_per_rank"] == [[0, 2], [1, 3]]  # round-robin shard of cfg5
+    assert res["frames_processed"] == 4
+    assert "round-robin" in res["config"]["workload"]
