@@ -64,11 +64,12 @@ void run(const char* name, const char* sass, double cell_ops_per_lane_op, bool l
   cudaMemcpy(&c0, cyc, sizeof(c0), cudaMemcpyDeviceToHost);
   const double lane_ops = double(blocks) * threads * iters * kChains;
   const double s = ms * 1e-3;
-  // CTA 0's clock64 span over its own run approximates the SM clock
-  const int waves = blocks / (148 * 8);  // 8 resident 256-thread CTAs per SM
-  const double clk_hz = double(c0) * waves / s;
+  (void)c0;
+  int khz = 0;
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);  // max SM clock
+  const double clk_hz = double(khz) * 1e3;
   printf("  \"%s\": {\"sass\": \"%s\", \"lane_ops_per_s\": %.4e, \"warp_inst_per_clk_per_sm\": %.3f, "
-         "\"cell_ops_per_lane_op\": %.0f, \"cell_ops_per_s\": %.4e, \"sm_clock_mhz_est\": %.0f}%s\n",
+         "\"cell_ops_per_lane_op\": %.0f, \"cell_ops_per_s\": %.4e, \"sm_clock_mhz\": %.0f}%s\n",
          name, sass, lane_ops / s, lane_ops / 32.0 / s / clk_hz / 148.0, cell_ops_per_lane_op,
          lane_ops * cell_ops_per_lane_op / s, clk_hz / 1e6, last ? "" : ",");
   cudaFree(d);
