@@ -39,7 +39,9 @@ constexpr int kDepth = RPD_AGG_DEPTH;  // input ring depth (stages)
 #define RPD_AGG_UNROLL 4     // unrolled steps of the inner loop (code size vs ILP)
 #endif
 #ifndef RPD_AGG_REC
-#define RPD_AGG_REC 2  // recurrence form: 0 = 2x add-min + min, 1 = min3 + add-min, 2 = min3 + add + min3
+// recurrence form: 0 = 2x add-min + min, 1 = min3 + add-min, 2 = min3 + add + min3,
+// 3 = normalised state (n = L - min L, see chain_step_norm)
+#define RPD_AGG_REC 3
 #endif
 #ifndef RPD_AGG_OUTDEPTH
 #define RPD_AGG_OUTDEPTH 1  // output tiles in flight (TMA stores not yet read); 1: less smem, +1 % concurrent
@@ -72,6 +74,7 @@ struct TmaArgs {
   int njobs;
   int h, w;
   uint32_t p1x2, p2x2;
+  uint32_t one;  // 1 at run time: keeps `x * one + y` an IMAD (FMA pipe) instead of an ALU add
   uint8_t* path_base;  // diagonal jobs store directly
   size_t pitch, vol_bytes;
   int dbg;  // debugging early-exit level (RPD_TMA_DBG), 0 in production
@@ -245,11 +248,72 @@ struct ChainState {
   uint32_t prev[NPAIR];
   uint32_t mnx2;
   __device__ __forceinline__ void reset() {
+#if RPD_AGG_REC == 3
+    // normalised state: n = 0 gives cur = raw + min(0, P1, P2) = raw exactly
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) prev[q] = 0u;
+    mnx2 = 0u;
+#else
 #pragma unroll
     for (int q = 0; q < NPAIR; ++q) prev[q] = kInf2;
     mnx2 = kInf2;
+#endif
   }
 };
+
+__device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t y) {
+  uint32_t r;  // x * one + y on the FMA pipe (one == 1 at run time)
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(y));
+  return r;
+}
+
+// Normalised recurrence (RPD_AGG_REC 3).  With n(d) = L_prev(d) - min L_prev
+// (>= 0, exact integers) sgm.cpp:95-104 reads
+//   cur(d) = raw(d) + min(n(d), min(n(d-1), n(d+1), P2 - P1) + P1)
+//   n'(d)  = cur(d) - min cur
+// (= raw + min(L, L(d+-1) + P1, min L + P2) - min L).  Per u16x2 level pair:
+// PRMT (n(d+1)), VIMNMX3, VIADDMNMX and the raw-byte PRMT on the ALU pipe,
+// the two adds as IMADs on the FMA pipe (co-issued; tools/pipe_probe.cu).
+// A chain (re)start is n = 0: cur = raw + min(0, P1, P2) = raw.  Padding
+// levels (raw 0xFF) stay >= 255 - min and never win (L <= 255 - P1 + ...,
+// sgm_fast_path_ok).
+template <int WPL, int G, int NPAIR>
+__device__ __forceinline__ void chain_step_norm(ChainState<NPAIR>& cs, const uint32_t (&w8)[WPL],
+                                                uint32_t p1x2, uint32_t c21x2, uint32_t one,
+                                                int g, unsigned gmask, uint32_t (&packed)[WPL]) {
+  uint32_t lo_nb = kInf2, hi_nb = kInf2;
+  if (G > 1) {
+    const uint32_t up = __shfl_up_sync(gmask, cs.prev[NPAIR - 1], 1, G);
+    const uint32_t dn = __shfl_down_sync(gmask, cs.prev[0], 1, G);
+    if (g > 0) lo_nb = up;
+    if (g < G - 1) hi_nb = dn;
+  }
+  uint32_t cur[NPAIR];
+  uint32_t qprev = __byte_perm(lo_nb, cs.prev[0], 0x5432);
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) {
+    const uint32_t nxt = (q + 1 < NPAIR) ? cs.prev[q + 1] : hi_nb;
+    const uint32_t qn = __byte_perm(cs.prev[q], nxt, 0x5432);  // n(d+1) of both halves
+    const uint32_t a = __vimin3_u16x2(qprev, qn, c21x2);
+    const uint32_t tt = __viaddmin_u16x2(a, p1x2, cs.prev[q]);
+    const uint32_t raw = __byte_perm(w8[q / 2], 0u, (q & 1) ? 0x4342 : 0x4140);
+    cur[q] = imad_add(tt, one, raw);
+    qprev = qn;
+  }
+#pragma unroll
+  for (int q = 0; q < WPL; ++q)
+    packed[q] =
+        __byte_perm(cur[2 * q], (2 * q + 1 < NPAIR) ? cur[2 * q + 1] : 0xFFFFFFFFu, 0x6420);
+  const uint32_t m2 = min_pairs3<NPAIR>(cur);
+  uint32_t m = min(m2 & 0xFFFFu, m2 >> 16);
+  if (G > 1) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(gmask, m, off, G));
+  }
+  const uint32_t negm = 0u - m * 0x10001u;  // per-half exact: cur >= m
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) cs.prev[q] = imad_add(cur[q], one, negm);
+}
 
 // One recurrence step on packed u16x2 level pairs; returns the packed u8
 // words of the new costs in `packed` and updates the state.
@@ -417,7 +481,7 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
 
   TileAddr<TYPE, WPL, G> ad;
   ad.init(t, g);
-  const uint32_t p1x2 = a.p1x2, p2x2 = a.p2x2;
+  const uint32_t p1x2 = a.p1x2, p2x2 = a.p2x2, one = a.one;
   ChainState<NPAIR> cs;
   cs.reset();
   uint8_t* const pbase = a.path_base + size_t(zp) * a.vol_bytes + size_t(g * WPL) * 4;
@@ -447,7 +511,11 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
       for (int q = 0; q < WPL; ++q) w8[q] = inb[ad.at(q, rr, shift)];
       uint32_t packed[WPL];
       if (check && s < s_begin) continue;  // padding step: state stays INF
+#if RPD_AGG_REC == 3
+      chain_step_norm<WPL, G, NPAIR>(cs, w8, p1x2, p2x2 - p1x2, one, g, gmask, packed);
+#else
       chain_step<WPL, G, NPAIR>(cs, w8, p1x2, p2x2, g, gmask, packed);
+#endif
       if (TYPE == kDiag) {
         if (unsigned(col) < unsigned(w) && s < s_end) {
           const int vrow = dv > 0 ? s : h - 1 - s;
@@ -604,6 +672,7 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
   args.w = L.w;
   args.p1x2 = p1 | (p1 << 16);
   args.p2x2 = p2 | (p2 << 16);
+  args.one = 1u;
   args.path_base = paths;
   args.pitch = L.pitch;
   args.vol_bytes = L.vol_bytes();
