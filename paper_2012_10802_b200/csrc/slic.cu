@@ -320,17 +320,19 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   if (nc <= kMaxTileCenters) {
     // distribute the candidates over the rows they reach, with the row's
     // (v - cv)^2 precomputed (the reference's dv * dv, segmentation.cpp:48)
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    // one (candidate, row) item per thread: lane = tile row, so a warp's
+    // counter atomics never collide and every thread has work
+    static_assert(kTileV == 32, "item decomposition assumes 32 tile rows");
+    for (int t = threadIdx.x; t < nc * kTileV; t += blockDim.x) {
+      const int i = t >> 5, r = t & 31;
       const int icv = s_icv[i];
-      const int r0 = max(icv - win, v0) - v0, r1 = min(icv + win, v0 + kTileV - 1) - v0;
-      const double2 cuv = s_cd[2 * i], vk = s_cd[2 * i + 1];
-      for (int r = r0; r <= r1; ++r) {
-        const int slot = atomicAdd(&s_rowcnt[r], 1);
-        if (slot < kRowCap) {
-          const double dv = double(v0 + r) - cuv.y;
-          s_rec[r][2 * slot] = make_double2(cuv.x, dv * dv);
-          s_rec[r][2 * slot + 1] = vk;
-        }
+      if (r < max(icv - win, v0) - v0 || r > min(icv + win, v0 + kTileV - 1) - v0) continue;
+      const double2 cuv = s_cd[2 * i];
+      const int slot = atomicAdd(&s_rowcnt[r], 1);
+      if (slot < kRowCap) {
+        const double dv = double(v0 + r) - cuv.y;
+        s_rec[r][2 * slot] = make_double2(cuv.x, dv * dv);
+        s_rec[r][2 * slot + 1] = s_cd[2 * i + 1];
       }
     }
   }

@@ -2,8 +2,8 @@
 # ab_var.sh V1 V2 ... : bench each paper_2012_10802_b200/_lib/var_V (2 runs each, interleaved)
 for rep in 1 2; do
   for v in "$@"; do
-    RPD_B200_LIB=paper_2012_10802_b200/_lib/var_$v/librpd_b200.so timeout 120 \
-      python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/ab_${v}_$rep.log 2>&1
+    timeout 120 python bench.py --lib paper_2012_10802_b200/_lib/var_$v/librpd_b200.so \
+      --steps 20 --warmup 5 --no-cpu-baseline --no-extras > gpurun_out/ab_${v}_$rep.log 2>&1
   done
 done
 for v in "$@"; do
