@@ -219,6 +219,17 @@ typedef struct rpd_stats {
 rpd_status rpd_ctx_set_profiling(rpd_ctx* ctx, int enable);
 rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out);
 
+/* Checked-build hook (make DEBUG_KNOBS=1 -> _lib_dbg/): every workspace
+ * buffer is allocated at its exact size followed by a 4 KiB guard zone of
+ * 0xA5 bytes; this reports how many guard bytes were overwritten (and the
+ * first buffer's name).  The product build returns *corrupted = -1.
+ * (compute-sanitizer is closed on the GPU pool; this is the out-of-bounds
+ * write check that replaces memcheck.) */
+rpd_status rpd_debug_guard_check(rpd_ctx* ctx, long long* corrupted, char* first, int cap);
+/* Checked build: writes one byte just past a fresh `bytes`-sized workspace
+ * buffer (proves the guard check fires).  RPD_EINVAL in the product. */
+rpd_status rpd_debug_guard_selftest(rpd_ctx* ctx, size_t bytes);
+
 /* Test hook: the device's roll-angle sin/cos (double-double, correctly
  * rounded with overwhelming probability) for n angles. */
 rpd_status rpd_debug_sincos(rpd_ctx* ctx, const double* x, int n, double* s, double* c);

@@ -355,6 +355,8 @@ _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
     "rpd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rpd_ctx_stats": (C.c_int, [_vp, C.POINTER(Stats)]),
     "rpd_debug_sincos": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+    "rpd_debug_guard_check": (C.c_int, [_vp, C.POINTER(C.c_longlong), C.c_char_p, C.c_int]),
+    "rpd_debug_guard_selftest": (C.c_int, [_vp, C.c_size_t]),
 }
 _SIGS["rpd_match_pair_dump"] = (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(RoadModel),
                                           C.POINTER(Config), C.c_int, _vp, _vp, _vp, _vp, _vp])
@@ -546,6 +548,13 @@ class Context:
         c = np.empty_like(x)
         self._check(self.dll.rpd_debug_sincos(self.handle, _ptr(x), x.shape[0], _ptr(s), _ptr(c)))
         return s, c
+
+    def guard_check(self):
+        """(corrupted guard bytes, first buffer) — checked build only (-1 otherwise)."""
+        n = C.c_longlong(0)
+        buf = C.create_string_buffer(128)
+        self._check(self.dll.rpd_debug_guard_check(self.handle, C.byref(n), buf, 128))
+        return n.value, buf.value.decode()
 
     def set_profiling(self, enable: bool):
         self._check(self.dll.rpd_ctx_set_profiling(self.handle, 1 if enable else 0))

@@ -121,6 +121,37 @@ rpd_status rpd_ctx_set_profiling(rpd_ctx* ctx, int enable) {
   return guard(ctx, [&] { ctx->profile = enable != 0; });
 }
 
+namespace {
+__global__ void k_poke(unsigned char* p, size_t off) { p[off] = 0; }
+}  // namespace
+
+// Self-test of the guard mechanism (checked build): writes one byte just past
+// a fresh workspace buffer; rpd_debug_guard_check must then report it.
+rpd_status rpd_debug_guard_selftest(rpd_ctx* ctx, size_t bytes) {
+  return guard(ctx, [&] {
+#ifdef RPD_DEBUG_KNOBS
+    unsigned char* p = ctx->ws.get<unsigned char>("guard_selftest", bytes);
+    k_poke<<<1, 1, 0, ctx->stream>>>(p, bytes);
+    RPD_LAUNCH_CHECK();
+#else
+    (void)bytes;
+    throw InvalidArg("guard self-test: checked build only");
+#endif
+  });
+}
+
+rpd_status rpd_debug_guard_check(rpd_ctx* ctx, long long* corrupted, char* first, int cap) {
+  return guard(ctx, [&] {
+    RPD_CK(cudaStreamSynchronize(ctx->stream));
+    std::string who;
+    *corrupted = ctx->ws.check_guards(&who);
+    if (first && cap > 0) {
+      std::strncpy(first, who.c_str(), size_t(cap - 1));
+      first[cap - 1] = 0;
+    }
+  });
+}
+
 rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out) {
   return guard(ctx, [&] {
     RPD_CK(cudaStreamSynchronize(ctx->stream));

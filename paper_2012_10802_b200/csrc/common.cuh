@@ -136,12 +136,23 @@ class Workspace {
       if (b.p) RPD_CK(cudaFree(b.p));
       b.p = nullptr;
       b.bytes = 0;
+#ifdef RPD_DEBUG_KNOBS
+      // checked build: no headroom, a guard zone right after the requested
+      // bytes that rpd_debug_guard_check verifies
+      const size_t want = bytes;
+      const size_t alloc = want + kGuardBytes;
+#else
       const size_t want = bytes + bytes / 8;  // headroom for small shape drift
-      if (cudaMalloc(&b.p, want) != cudaSuccess) {
+      const size_t alloc = want;
+#endif
+      if (cudaMalloc(&b.p, alloc) != cudaSuccess) {
         cudaGetLastError();
-        throw CudaFail("device allocation of " + std::to_string(want) + " bytes failed (" +
+        throw CudaFail("device allocation of " + std::to_string(alloc) + " bytes failed (" +
                        name + ")");
       }
+#ifdef RPD_DEBUG_KNOBS
+      RPD_CK(cudaMemset(static_cast<char*>(b.p) + want, kGuardByte, kGuardBytes));
+#endif
       b.bytes = want;
       ++generation_;
     }
@@ -149,7 +160,30 @@ class Workspace {
   }
   unsigned generation() const { return generation_; }
 
+  // Checked build: number of guard bytes overwritten (first offender in *who).
+  long long check_guards(std::string* who) const {
+#ifdef RPD_DEBUG_KNOBS
+    long long bad = 0;
+    std::vector<unsigned char> h(kGuardBytes);
+    for (const auto& kv : bufs_) {
+      if (!kv.second.p) continue;
+      RPD_CK(cudaMemcpy(h.data(), static_cast<const char*>(kv.second.p) + kv.second.bytes,
+                        kGuardBytes, cudaMemcpyDeviceToHost));
+      long long n = 0;
+      for (unsigned char c : h) n += c != kGuardByte;
+      if (n && who && who->empty()) *who = kv.first;
+      bad += n;
+    }
+    return bad;
+#else
+    (void)who;
+    return -1;
+#endif
+  }
+
  private:
+  static constexpr size_t kGuardBytes = 4096;
+  static constexpr unsigned char kGuardByte = 0xA5;
   struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
