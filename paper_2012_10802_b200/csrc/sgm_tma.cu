@@ -27,9 +27,13 @@ namespace rpdg {
 
 namespace {
 
-constexpr int kNC = 32;      // chains per CTA
+#ifndef RPD_AGG_NC1
+#define RPD_AGG_NC1 32  // chains (= threads) per CTA of the one-lane-per-chain kernels
+#endif
+// chains per CTA: one warp of chains; G == 1 kernels may take several warps
+__host__ __device__ constexpr int nc_of(int G) { return G == 1 ? RPD_AGG_NC1 : 32; }
 #ifndef RPD_AGG_DEPTH
-#define RPD_AGG_DEPTH 3
+#define RPD_AGG_DEPTH 2
 #endif
 constexpr int kDepth = RPD_AGG_DEPTH;  // input ring depth (stages)
 #ifndef RPD_AGG_RBASE
@@ -155,7 +159,8 @@ struct Geo {
   static constexpr int WPP = WPL * G;                  // words per pixel
   static constexpr int RB = G == 1 ? kRBaseG1 : kRBase;
   static constexpr int R = WPP <= 32 ? RB : (WPP <= 64 ? (RB + 1) / 2 : 1);
-  static constexpr int ROW = kNC * WPP;                // words of one step (vert / diag)
+  static constexpr int NC = nc_of(G);                  // chains per CTA
+  static constexpr int ROW = NC * WPP;                 // words of one step (vert / diag)
   static constexpr int CWF = ROW < 256 ? ROW : 256;    // full chunk width
   static constexpr int NCH = (ROW + 255) / 256;        // chunks per row
   static constexpr int CWL = ROW - (NCH - 1) * 256;    // last chunk width
@@ -167,7 +172,7 @@ struct Geo {
   static constexpr int DNCH = (DROW + 255) / 256;
   static constexpr int DCWL = DROW - (DNCH - 1) * 256;
   static constexpr int STAGE_IN = R * DROW;            // words per input stage
-  static constexpr int THREADS = kNC * G;
+  static constexpr int THREADS = NC * G;
 };
 
 // Shared-memory word offsets of this thread's pixel words inside a tile.
@@ -397,6 +402,7 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
   const unsigned gmask =
       G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
 
+  constexpr int kNC = GE::NC;
   const int c0 = cta * kNC;  // first chain of this CTA (row / column / diagonal offset)
   const int nsteps = TYPE == kHoriz ? w : h;
   // Steps are "virtual": horizontal / vertical tiles are aligned to multiples
@@ -681,6 +687,7 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
     args.dbg = e ? std::atoi(e) : 0;
   }
   const int R = ki.R;
+  const int kNC = nc_of(L.G);
   args.cost_h = make_map(vol_lr, words_row, L.h, 2, L.pitch, R * wpp, kNC);
   args.cost_vf = make_map(vol_lr, words_row, L.h, 2, L.pitch, ki.cwf, R);
   args.cost_vl = make_map(vol_lr, words_row, L.h, 2, L.pitch, ki.cwl, R);
