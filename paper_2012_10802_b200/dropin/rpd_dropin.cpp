@@ -1,16 +1,18 @@
-// dropin_rpd.cpp — the reference's C++ API (`namespace rpd`, declared by the
-// UNTOUCHED /root/reference/proj/include/rpd/*.hpp) implemented on the B200
-// library's C-ABI (include/rpd_b200.h -> paper_2012_10802_b200/_lib/librpd_b200.so).
+// rpd_dropin.cpp — the reference's C++ API (`namespace rpd`, declared by the
+// reference's own include/rpd/*.hpp, compiled against them unchanged)
+// implemented on the B200 library's C-ABI (include/rpd_b200.h ->
+// paper_2012_10802_b200/_lib/librpd_b200.so).
 //
-// Linking this object instead of the reference's src/*.cpp is the drop-in:
-// the reference's own test files and acceptance gate, compiled unmodified,
-// then exercise the CUDA kernels (tests/cpp/refsuite/Makefile, gpu_* binaries;
-// tests/test_reference_suite.py).  Every hot-path function below forwards to
-// one C-ABI entry point; rasters are the reference's Eigen row-major arrays
-// (oracle/ref_shim stands in for Eigen), whose data() is the C-ABI layout.
+// The drop-in for C++ callers of the reference: compile this file against the
+// reference headers and Eigen, and link it with -lrpd_b200 INSTEAD OF the
+// reference's src/{sgm,road_geometry,segmentation,pipeline,config,synth}.cpp
+// (INTEGRATION.md §A).  The reference's own test files and acceptance gate,
+// compiled unmodified, then run on the CUDA kernels (tests/cpp/refsuite,
+// tests/test_reference_suite.py; there oracle/ref_shim stands in for Eigen).
+// Every hot-path function below forwards to one C-ABI entry point; rasters
+// are the reference's Eigen row-major arrays, whose data() is the C-ABI layout.
 // Status codes map back onto the reference's exception types.  The header-
 // only functions of perspective.hpp / evaluation.hpp stay the reference's.
-// Test infrastructure: this file is not part of the product library.
 
 #include <cstring>
 #include <fstream>

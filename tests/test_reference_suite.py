@@ -5,7 +5,7 @@ acceptance gate (acceptance.cpp), compiled UNMODIFIED (tests/cpp/refsuite):
   * lit_*  against the literal reference build (untouched src/*.cpp + the
            Eigen subset in oracle/ref_shim): pins the shims themselves;
   * gpu_*  against the B200 library through the reference-API adapter
-           (tests/cpp/refsuite/dropin_rpd.cpp -> librpd_b200.so): the drop-in
+           (paper_2012_10802_b200/dropin/rpd_dropin.cpp -> librpd_b200.so): the drop-in
            proof — the reference's own known answers, exact DP / QR /
            flood-fill / 2-means oracles and acceptance checks 1-8 on the CUDA
            kernels.
