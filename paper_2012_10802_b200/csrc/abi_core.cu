@@ -54,6 +54,10 @@ void sync_and_check(rpd_ctx* ctx) {
   RPD_CK(cudaMemcpyAsync(&h, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
                          ctx->stream));
   RPD_CK(cudaStreamSynchronize(ctx->stream));
+  check_status(h);
+}
+
+void check_status(const DevStatus& h) {
   if (h.code == RPD_EDEGENERATE) throw Degenerate(status_message(h.where));
   if (h.code == RPD_EINVAL) throw InvalidArg(status_message(h.where));
   if (h.code == RPD_ENOMEM) throw CudaFail(status_message(h.where));

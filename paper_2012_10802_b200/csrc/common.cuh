@@ -242,6 +242,7 @@ namespace rpdg {
 void reset_status(rpd_ctx* ctx);
 // Synchronises the stream and throws the recorded device status, if any.
 void sync_and_check(rpd_ctx* ctx);
+void check_status(const DevStatus& h);  // throws the status' exception
 DevModel host_model(const rpd_road_model& m);  // cos/sin on the host (glibc)
 void pipeline_forget(rpd_ctx* ctx);           // releases captured graphs
 // Records `ev` on ctx->stream; inside a stream capture it becomes an external

@@ -51,7 +51,31 @@ struct FrameBuffers {
   DevModel* flat;
   ObsBuffers obs;
   SlicOut sp;
+  struct FrameScalars* scal;  // every scalar output + the status, one D2H copy
 };
+
+// The frame's scalar results gathered on the device at the end of the graph,
+// so rpd_detect_fetch reads them (and the status word) with ONE small copy
+// instead of seven.
+struct FrameScalars {
+  FitOut coarse, fit;
+  rpd_threshold thr;
+  unsigned long long clamped;
+  int count, npot;
+  DevStatus status;
+};
+
+__global__ void k_gather_scalars(const FitOut* coarse, const FitOut* fit, const rpd_threshold* thr,
+                                 const unsigned long long* clamped, const int* count,
+                                 const int* npot, const DevStatus* status, FrameScalars* out) {
+  out->coarse = *coarse;
+  out->fit = *fit;
+  out->thr = *thr;
+  out->clamped = *clamped;
+  out->count = *count;
+  out->npot = *npot;
+  out->status = *status;
+}
 
 struct GraphKey {
   int h, w, u8, profile;
@@ -105,6 +129,7 @@ FrameBuffers alloc_frame(rpd_ctx* ctx, int h, int w, int K) {
   const size_t hn = size_t(h / 2) * (w / 2);
   FrameBuffers f{};
   Workspace& ws = ctx->ws;
+  f.scal = ws.get<FrameScalars>("pl_scalars", 1);
   f.left = ws.get<float>("pl_left", n);
   f.right = ws.get<float>("pl_right", n);
   f.left8 = ws.get<uint8_t>("pl_left8", n);
@@ -155,7 +180,18 @@ int dup_stages() {
   return m;
 }
 
+void enqueue_frame_body(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8,
+                        const rpd_config& c);
+
 void enqueue_frame(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8, const rpd_config& c) {
+  enqueue_frame_body(ctx, f, h, w, u8, c);
+  k_gather_scalars<<<1, 1, 0, ctx->stream>>>(f.coarse, f.fit, f.thr, f.clamped, f.sp.count,
+                                             f.n_potholes, ctx->status, f.scal);
+  RPD_LAUNCH_CHECK();
+}
+
+void enqueue_frame_body(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8,
+                        const rpd_config& c) {
   cudaStream_t st = ctx->stream;
   const int skip = skip_stages();
   const int dup = dup_stages();
@@ -316,20 +352,10 @@ void fetch(rpd_ctx* ctx, const FrameBuffers& f, int h, int w, rpd_detect_out* ou
   d2h(out->d3, f.d3, sizeof(float) * n);
   d2h(out->labels, f.labels, sizeof(int32_t) * n);
   d2h(out->sp_labels, f.sp.labels, sizeof(int32_t) * n);
-  struct Scalars {
-    FitOut coarse, fit;
-    rpd_threshold thr;
-    unsigned long long clamped;
-    int count, npot;
-  };
-  Scalars* hs = static_cast<Scalars*>(ctx->pinned.get(sizeof(Scalars)));
-  d2h(&hs->coarse, f.coarse, sizeof(FitOut));
-  d2h(&hs->fit, f.fit, sizeof(FitOut));
-  d2h(&hs->thr, f.thr, sizeof(rpd_threshold));
-  d2h(&hs->clamped, f.clamped, sizeof(unsigned long long));
-  d2h(&hs->count, f.sp.count, sizeof(int));
-  d2h(&hs->npot, f.n_potholes, sizeof(int));
-  sync_and_check(ctx);
+  FrameScalars* hs = static_cast<FrameScalars*>(ctx->pinned.get(sizeof(FrameScalars)));
+  RPD_CK(cudaMemcpyAsync(hs, f.scal, sizeof(FrameScalars), cudaMemcpyDeviceToHost, st));
+  RPD_CK(cudaStreamSynchronize(st));
+  check_status(hs->status);
   const int count = hs->count;
   if (out->centers && out->centers_cap > 0 && count > 0) {
     const int m = std::min(out->centers_cap, count);

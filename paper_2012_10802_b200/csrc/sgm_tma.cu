@@ -701,10 +701,17 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
   int blocks = 0;
   const char* dbg = debug_knob("RPD_TMA_TYPES");  // debugging: bitmask of job types to run
   const int type_mask = dbg ? std::atoi(dbg) : 7;
+#ifndef RPD_AGG_ORDER
+#define RPD_AGG_ORDER 1
+#endif
+  // Block order = dispatch order: the long horizontal chains (W steps) first,
+  // so they start on empty SMs; the shorter vertical / diagonal jobs fill in.
+  for (int pass = 0; pass < (RPD_AGG_ORDER ? 3 : 1); ++pass)
   for (int vol = 0; vol < nvols; ++vol)
     for (int r = 0; r < paths_n; ++r) {
       const int du = dirs[2 * r], dv = dirs[2 * r + 1];
       const int ty = dv == 0 ? kHoriz : (du == 0 ? kVert : kDiag);
+      if (RPD_AGG_ORDER && ty != pass) continue;
       if (!((type_mask >> ty) & 1)) continue;
       TmaJob& J = args.job[args.njobs++];
       J.vol = vol;
