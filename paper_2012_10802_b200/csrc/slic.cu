@@ -116,20 +116,39 @@ struct __align__(16) CRec {
   double2 val;   // val, 0
 };
 
-// Single-CTA counting sort of the centres into the bucket grid.
-constexpr int kBucketThreads = 1024;
-constexpr int kBucketItems = 8;  // supports up to 8192 buckets (32 KB smem)
-constexpr int kMaxBuckets = kBucketThreads * kBucketItems;
+// Centre grid for the assignment: bucket (bx, by) of side B holds up to
+// kBucketCap centre records in a fixed-capacity slot array, filled with one
+// atomic per centre (order inside a bucket is irrelevant: the assignment keeps
+// the lexicographic (dist, k) minimum).  A bucket that overflows sets the
+// round's overflow flag; the assignment then falls back to a brute-force scan
+// of every centre.  Counts and flags are double-buffered by round parity: the
+// round-r kernel fills buffer r & 1 and clears buffer (r + 1) & 1 for the next
+// round (its previous user, the round r - 1 assignment, is complete).
+constexpr int kBucketCap = 8;
 
-__global__ void __launch_bounds__(kBucketThreads)
-    k_buckets(Centers c, int K, int w, int h, int B, int nbx, int nby, int* __restrict__ cell_start,
-              int* __restrict__ cell_items, CRec* __restrict__ recs, CenterSums s, int finalize) {
-  using Scan = cub::BlockScan<int, kBucketThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int cnt[kMaxBuckets];
-  const int nb = nbx * nby;
-  if (finalize) {  // update_centers tail (segmentation.cpp:88-92) of the previous assignment
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+struct CenterGrid {
+  int B, nbx, nby;
+  int* count[2];  // per bucket
+  int* ovf[2];    // one flag
+  CRec* rec;      // nb * kBucketCap
+};
+
+// update_centers tail (segmentation.cpp:88-92) of the previous assignment's
+// sums when `finalize`, then lround positions (assign_pixels' window centres,
+// :38-41) and the bucket insert.  Also zeroes the orphan counter of the round.
+__global__ void k_centers(Centers c, int K, CenterSums s, int finalize, CenterGrid g, int cur,
+                          int* __restrict__ orphan_count) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthreads = gridDim.x * blockDim.x;
+  const int nb = g.nbx * g.nby;
+  int* cnt_next = g.count[cur ^ 1];
+  for (int b = tid; b < nb; b += nthreads) cnt_next[b] = 0;
+  if (tid == 0) {
+    *g.ovf[cur ^ 1] = 0;
+    *orphan_count = 0;
+  }
+  for (int k = tid; k < K; k += nthreads) {
+    if (finalize) {
       const int l = k + 1;
       const int n = s.n[l];
       if (n > 0) {
@@ -143,53 +162,27 @@ __global__ void __launch_bounds__(kBucketThreads)
       s.sv[l] = 0;
       s.sx[l] = AccSum{0ull, 0ull, 0ll, 0ll};
     }
-    __syncthreads();
-  }
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    const int iu = int(lround(c.cu[k])), iv = int(lround(c.cv[k]));
+    const double cu = c.cu[k], cv = c.cv[k];
+    const int iu = int(lround(cu)), iv = int(lround(cv));
     c.icu[k] = iu;
     c.icv[k] = iv;
-    const int bx = min(max(iu, 0) / B, nbx - 1), by = min(max(iv, 0) / B, nby - 1);
-    atomicAdd(&cnt[by * nbx + bx], 1);
-  }
-  __syncthreads();
-  int items[kBucketItems];
-#pragma unroll
-  for (int q = 0; q < kBucketItems; ++q) {
-    const int b = threadIdx.x * kBucketItems + q;
-    items[q] = b < nb ? cnt[b] : 0;
-  }
-  int total;
-  Scan(tmp).ExclusiveSum(items, items, total);
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < kBucketItems; ++q) {
-    const int b = threadIdx.x * kBucketItems + q;
-    if (b < nb) {
-      cell_start[b] = items[q];
-      cnt[b] = items[q];  // becomes the scatter cursor
-    }
-  }
-  if (threadIdx.x == 0) cell_start[nb] = total;
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    const int iu = c.icu[k], iv = c.icv[k];
-    const int bx = min(max(iu, 0) / B, nbx - 1), by = min(max(iv, 0) / B, nby - 1);
-    const int pos = atomicAdd(&cnt[by * nbx + bx], 1);
-    cell_items[pos] = k;
-    recs[pos] = CRec{make_int4(iu, iv, k, 0), make_double2(c.cu[k], c.cv[k]),
-                     make_double2(c.val[k], 0.0)};
+    const int bx = min(max(iu, 0) / g.B, g.nbx - 1), by = min(max(iv, 0) / g.B, g.nby - 1);
+    const int b = by * g.nbx + bx;
+    const int slot = atomicAdd(&g.count[cur][b], 1);
+    if (slot < kBucketCap)
+      g.rec[size_t(b) * kBucketCap + slot] =
+          CRec{make_int4(iu, iv, k, 0), make_double2(cu, cv), make_double2(c.val[k], 0.0)};
+    else
+      *g.ovf[cur] = 1;
   }
 }
 
 struct AssignArgs {
   const float* vals;
-  int h, w;
+  int h, w, K;
   Centers c;
-  const int* cell_start;
-  const int* cell_items;
+  const int* bcount;  // this round's bucket counts
+  const int* ovf;     // this round's bucket overflow flag
   const CRec* recs;
   int B, nbx, nby, win;
   double sw;
@@ -197,33 +190,25 @@ struct AssignArgs {
   int* orphan_list;
   int* orphan_count;
   int* inexact;
+  int force_walk;  // checked build only (RPD_SLIC_FORCE_WALK): exercise the brute-force path
 };
 
 // assign_pixels, segmentation.cpp:30-57 (windowed part) for one pixel by
-// walking the bucket grid; used when a tile's candidate list overflows.
+// scanning every centre; used when a tile's candidate list or a bucket
+// overflows (pathological centre pile-ups).
 __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, double x) {
-  const int bx0 = u - a.win < 0 ? 0 : (u - a.win) / a.B;
-  const int bx1 = min(a.nbx - 1, (u + a.win) / a.B);
-  const int by0 = v - a.win < 0 ? 0 : (v - a.win) / a.B;
-  const int by1 = min(a.nby - 1, (v + a.win) / a.B);
   double best = __longlong_as_double(0x7FF0000000000000ll);
   int bk = -1;
-  for (int by = by0; by <= by1; ++by)
-    for (int bx = bx0; bx <= bx1; ++bx) {
-      const int b = by * a.nbx + bx;
-      const int e = a.cell_start[b + 1];
-      for (int idx = a.cell_start[b]; idx < e; ++idx) {
-        const int k = a.cell_items[idx];
-        if (abs(u - a.c.icu[k]) > a.win || abs(v - a.c.icv[k]) > a.win) continue;
-        const double dval = x - a.c.val[k];
-        const double du = double(u) - a.c.cu[k], dv = double(v) - a.c.cv[k];
-        const double dist = dval * dval + (du * du + dv * dv) * a.sw;
-        if (dist < best || (dist == best && k < bk)) {
-          best = dist;
-          bk = k;
-        }
-      }
+  for (int k = 0; k < a.K; ++k) {
+    if (abs(u - a.c.icu[k]) > a.win || abs(v - a.c.icv[k]) > a.win) continue;
+    const double dval = x - a.c.val[k];
+    const double du = double(u) - a.c.cu[k], dv = double(v) - a.c.cv[k];
+    const double dist = dval * dval + (du * du + dv * dv) * a.sw;
+    if (dist < best || (dist == best && k < bk)) {
+      best = dist;
+      bk = k;
     }
+  }
   return bk;
 }
 
@@ -270,53 +255,36 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     xf[q] = (u < a.w && v < a.h) ? a.vals[size_t(v) * a.w + u] : 0.0f;
   }
   if (threadIdx.x < kTileV) s_rowcnt[threadIdx.x] = 0;
-  // bucket range of the tile +- win; each bucket row's centres are one
-  // contiguous range of the bucket-ordered records
-  if (threadIdx.x < 32) {
-    const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
-    const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
-    const int nrows = min(a.nby - 1, (v0 + kTileV - 1 + win) / a.B) - by0 + 1;
-    if (tx < min(nrows, 8)) {
-      const int bx1 = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B);
-      const int r0 = (by0 + tx) * a.nbx;
-      const int st = a.cell_start[r0 + bx0];
-      s_rs[tx] = st;
-      s_rb[tx + 1] = a.cell_start[r0 + bx1 + 1] - st;
-    }
-    if (tx == 0) {
-      s_cnt = 0;
-      s_nrows = nrows;
-    }
-  }
+  if (threadIdx.x == 0) s_cnt = 0;
+  const bool walk_all = a.force_walk || *a.ovf != 0;  // a bucket overflowed this round
+  // bucket range of the tile +- win
+  const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
+  const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
+  const int nbxr = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B) - bx0 + 1;
+  const int nbyr = min(a.nby - 1, (v0 + kTileV - 1 + win) / a.B) - by0 + 1;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    s_rb[0] = 0;
-    for (int r = 0; r < min(s_nrows, 8); ++r) s_rb[r + 1] += s_rb[r];
-  }
-  __syncthreads();
-  const int nrows = s_nrows;
-  const int ntot = nrows <= 8 ? s_rb[nrows] : (kMaxTileCenters + 1);
-  if (ntot > kMaxTileCenters) {
-    if (threadIdx.x == 0) s_cnt = kMaxTileCenters + 1;  // per-pixel bucket walk below
-  } else {
-    for (int t = threadIdx.x; t < ntot; t += blockDim.x) {
-      int r = 0;
-      while (t >= s_rb[r + 1]) ++r;
-      const CRec* rec = a.recs + s_rs[r] + (t - s_rb[r]);
+  if (!walk_all) {
+    // one (bucket, slot) item per thread; keep the centres whose window
+    // reaches the tile
+    for (int t = threadIdx.x; t < nbxr * nbyr * kBucketCap; t += blockDim.x) {
+      const int bl = t / kBucketCap, slot = t % kBucketCap;
+      const int b = (by0 + bl / nbxr) * a.nbx + bx0 + bl % nbxr;
+      if (slot >= a.bcount[b]) continue;
+      const CRec* rec = a.recs + size_t(b) * kBucketCap + slot;
       const int4 ik = rec->ik;
-      // keep only centres whose window reaches the tile
       const int du = ik.x < u0 ? u0 - ik.x : (ik.x > u0 + kTileU - 1 ? ik.x - (u0 + kTileU - 1) : 0);
       const int dv = ik.y < v0 ? v0 - ik.y : (ik.y > v0 + kTileV - 1 ? ik.y - (v0 + kTileV - 1) : 0);
       if (du > win || dv > win) continue;
-      const int slot = atomicAdd(&s_cnt, 1);
-      s_cd[2 * slot] = rec->cuv;
-      s_cd[2 * slot + 1] = make_double2(
+      const int slotc = atomicAdd(&s_cnt, 1);
+      if (slotc >= kMaxTileCenters) continue;  // tile overflow: per-pixel scan below
+      s_cd[2 * slotc] = rec->cuv;
+      s_cd[2 * slotc + 1] = make_double2(
           rec->val.x, __longlong_as_double((long long)(uint32_t(ik.x) | (uint64_t(uint32_t(ik.z)) << 32))));
-      s_icv[slot] = ik.y;
+      s_icv[slotc] = ik.y;
     }
   }
   __syncthreads();
-  int nc = s_cnt;
+  int nc = walk_all ? kMaxTileCenters + 1 : s_cnt;
   if (nc <= kMaxTileCenters) {
     // distribute the candidates over the rows they reach, with the row's
     // (v - cv)^2 precomputed (the reference's dv * dv, segmentation.cpp:48)
@@ -783,9 +751,9 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   const double su = double(w) / nu, sv = double(h) / nv;
   const int win = int(std::ceil(S));
   const double sw = m * m / (S * S);
-  int B = std::max(win, 1);
-  while ((long long)cdiv(w, B) * cdiv(h, B) > kMaxBuckets) B *= 2;
+  const int B = std::max(win, 1);
   const int nbx = cdiv(w, B), nby = cdiv(h, B);
+  const int nb = nbx * nby;
 
   float* vals = ctx->ws.get<float>("slic_vals", n);
   int32_t* labels = ctx->ws.get<int32_t>("slic_labels", n);
@@ -794,9 +762,9 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
             ctx->ws.get<int>("slic_icv", K)};
   CenterSums s{ctx->ws.get<int>("slic_n", K + 1), ctx->ws.get<long long>("slic_su", K + 1),
                ctx->ws.get<long long>("slic_sv", K + 1), ctx->ws.get<AccSum>("slic_sx", K + 1)};
-  int* cell_start = ctx->ws.get<int>("slic_cell_start", nbx * nby + 1);
-  int* cell_items = ctx->ws.get<int>("slic_cell_items", K);
-  CRec* recs = ctx->ws.get<CRec>("slic_recs", K);
+  int* gridbuf = ctx->ws.get<int>("slic_grid_counts", 2 * size_t(nb) + 2);
+  CenterGrid grid{B, nbx, nby, {gridbuf, gridbuf + nb}, {gridbuf + 2 * nb, gridbuf + 2 * nb + 1},
+                  ctx->ws.get<CRec>("slic_recs", size_t(nb) * kBucketCap)};
   int* orphan_list = ctx->ws.get<int>("slic_orphans", n);
   int* orphan_count = ctx->ws.get<int>("slic_orphan_count", 2);
   int* inexact = orphan_count + 1;
@@ -808,17 +776,24 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   k_zero_sums<<<cdiv(K + 1, 256), 256, 0, st>>>(s, K + 1);
   RPD_LAUNCH_CHECK();
   RPD_CK(cudaMemsetAsync(orphan_count, 0, 2 * sizeof(int), st));
+  // round 0's bucket counts and overflow flag start at zero
+  RPD_CK(cudaMemsetAsync(gridbuf, 0, sizeof(int) * nb, st));
+  RPD_CK(cudaMemsetAsync(grid.ovf[0], 0, sizeof(int), st));
 
-  AssignArgs aa{vals, h, w, c, cell_start, cell_items, recs, B, nbx, nby, win, sw, labels,
-                orphan_list, orphan_count, inexact};
+  AssignArgs aa{vals, h, w, K, c, nullptr, nullptr, grid.rec, B, nbx, nby, win, sw, labels,
+                orphan_list, orphan_count, inexact,
+                debug_knob("RPD_SLIC_FORCE_WALK") != nullptr ? 1 : 0};
   const dim3 tgrid(cdiv(w, kTileU), cdiv(h, kTileV));
-  // One round = bucket build (finalising the previous round's sums first) +
+  const int cblocks = cdiv(std::max(K, nb), 256);
+  int round = 0;
+  // One round = centre grid (finalising the previous round's sums first) +
   // assignment that accumulates the sums the next round needs.
   auto assign = [&](bool finalize, bool sums) {
-    k_buckets<<<1, kBucketThreads, 0, st>>>(c, K, w, h, B, nbx, nby, cell_start, cell_items, recs, s,
-                                            finalize ? 1 : 0);
+    const int cur = round++ & 1;
+    k_centers<<<cblocks, 256, 0, st>>>(c, K, s, finalize ? 1 : 0, grid, cur, orphan_count);
     RPD_LAUNCH_CHECK();
-    RPD_CK(cudaMemsetAsync(orphan_count, 0, sizeof(int), st));
+    aa.bcount = grid.count[cur];
+    aa.ovf = grid.ovf[cur];
     if (sums)
       k_assign_tile<true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
     else

@@ -102,3 +102,32 @@ def test_concurrent_contexts_deterministic(cuda_lib):
     for t in ths:
         t.join()
     assert not errors, errors[:5]
+
+
+def test_slic_brute_force_walk_matches_oracle(dbg_lib, oracle):
+    """The assignment's brute-force path (taken when a centre bucket or a
+    tile's candidate list overflows) forced on every tile of the checked
+    build: labels and centres equal the oracle's."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path[:0] = [%r, %r]
+from paper_2012_10802_b200.api import Library
+g = Library(%r).context(0)
+o = Library(%r).context()
+rng = np.random.default_rng(5)
+d2 = (30 + rng.normal(0, 2, (120, 170))).astype(np.float32)
+d2[rng.random(d2.shape) < 0.1] = -1
+a = g.slic(d2, 150, 8.0, 5)
+b = o.slic(d2, 150, 8.0, 5)
+assert np.array_equal(a[0], b[0]), "labels"
+assert a[2] == b[2] and np.array_equal(a[1], b[1]), "centres"
+print("walk ok")
+''' % (str(DBG_LIB.parents[2]), str(DBG_LIB.parents[2] / "tests"), str(DBG_LIB),
+       str(DBG_LIB.parents[2] / "oracle" / "_build" / "librpd_oracle.so"))
+    env = dict(os.environ, RPD_SLIC_FORCE_WALK="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "walk ok" in out.stdout, out.stderr[-2000:]
