@@ -211,6 +211,10 @@ typedef struct rpd_stats {
   double sgm_cells[2];          /* H*W*L of the pass */
   int32_t last_agg_kernel;      /* aggregation implementation of the context's last
                                    match_pair / aggregate_costs: RPD_AGG_* */
+  int32_t agg_segmented_ctas;   /* last aggregation launch: CTAs that run a chain segment
+                                   after the first (long H / V chains are cut) */
+  int64_t agg_segment_reruns;   /* cumulative: segments whose warm-up state differed from
+                                   the predecessor's and that were recomputed */
 } rpd_stats;
 #define RPD_AGG_NONE 0
 #define RPD_AGG_F32 1    /* generic float kernels (non-integral penalties, other directions) */

@@ -163,6 +163,12 @@ rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out) {
     s.kernels_last_frame = ctx->kernels_last_frame;
     s.graph_replayed = ctx->graph_replayed;
     s.last_agg_kernel = ctx->last_agg_kernel;
+    s.agg_segmented_ctas = ctx->agg_segmented_ctas;
+    if (ctx->agg_reruns) {
+      unsigned long long n = 0;
+      RPD_CK(cudaMemcpy(&n, ctx->agg_reruns, sizeof(n), cudaMemcpyDeviceToHost));
+      s.agg_segment_reruns = (int64_t)n;
+    }
     s.sgm_passes = ctx->profile ? ctx->agg_pass : 0;
     for (int i = 0; i < s.sgm_passes; ++i) {
       float ms = 0;

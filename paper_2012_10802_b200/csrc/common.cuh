@@ -234,6 +234,10 @@ struct rpd_ctx {
   int kernels_last_frame = 0;
   int graph_replayed = 0;
   int last_agg_kernel = 0;  // rpdg::AggImpl of the last aggregation
+  void* agg_flags_zeroed = nullptr;  // segmented aggregation: flag buffer known to be zero
+  int agg_flags_words = 0;
+  int agg_segmented_ctas = 0;                  // last aggregation launch
+  unsigned long long* agg_reruns = nullptr;    // device counter (workspace)
 };
 
 namespace rpdg {

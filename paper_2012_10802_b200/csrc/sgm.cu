@@ -34,6 +34,9 @@ namespace {
 constexpr int kMaxFastLevels = 576;
 }
 
+#ifndef RPD_SGM_WIDE_G1
+#define RPD_SGM_WIDE_G1 0  // 1: one lane per chain up to 68 levels (measured 1.4x slower bootstrap)
+#endif
 SgmLayout sgm_layout(int h, int w, int levels, int paths) {
   SgmLayout L;
   L.h = h;
@@ -53,6 +56,12 @@ SgmLayout sgm_layout(int h, int w, int levels, int paths) {
     L.G = 1;
     L.wpl = (levels + 3) / 4;
     env_layout("RPD_SGM_LAYOUT_SMALL", L.G, L.wpl);
+  } else if (levels <= 4 * kWplG1Max && RPD_SGM_WIDE_G1) {
+    // one lane per chain up to 68 levels (the D = 128 bootstrap's 65): no
+    // shuffles on the step's dependency chain, 17 words per pixel instead of 20
+    L.G = 1;
+    L.wpl = kWplG1Max;
+    env_layout("RPD_SGM_LAYOUT_BIG", L.G, L.wpl);
   } else {
     int G = 4;  // 4 lanes per chain: 2x the warps of G = 2
     while (4 * 9 * G < levels) G *= 2;
@@ -544,6 +553,7 @@ CostPxKernel cost_px_pick(int nw, int levels) {
   if (nw == 5 && levels == 17) return k_cost_px<5, 17>;
   if (nw == 9 && levels == 33) return k_cost_px<9, 33>;
   if (nw == 20 && levels == 65) return k_cost_px<20, 65>;
+  if (nw == 17 && levels == 65) return k_cost_px<17, 65>;
   if (nw == 36 && levels == 129) return k_cost_px<36, 129>;
   switch (nw) {
     case 1: return k_cost_px<1>;
@@ -555,6 +565,7 @@ CostPxKernel cost_px_pick(int nw, int levels) {
     case 7: return k_cost_px<7>;
     case 8: return k_cost_px<8>;
     case 9: return k_cost_px<9>;
+    case 17: return k_cost_px<17>;
     case 20: return k_cost_px<20>;
     case 24: return k_cost_px<24>;
     case 28: return k_cost_px<28>;
@@ -1156,6 +1167,7 @@ WtaBulkInfo wta_bulk_pick(int nw, int levels) {
   if (nw == 5 && levels == 17) return wta_bulk_info<P, 5, 17>();
   if (nw == 9 && levels == 33) return wta_bulk_info<P, 9, 33>();
   if (nw == 20 && levels == 65) return wta_bulk_info<P, 20, 65>();
+  if (nw == 17 && levels == 65) return wta_bulk_info<P, 17, 65>();
   if (nw == 36 && levels == 129) return wta_bulk_info<P, 36, 129>();
   switch (nw) {
     case 1: return wta_bulk_info<P, 1>();
@@ -1167,6 +1179,7 @@ WtaBulkInfo wta_bulk_pick(int nw, int levels) {
     case 7: return wta_bulk_info<P, 7>();
     case 8: return wta_bulk_info<P, 8>();
     case 9: return wta_bulk_info<P, 9>();
+    case 17: return wta_bulk_info<P, 17>();
     case 20: return wta_bulk_info<P, 20>();
     case 24: return wta_bulk_info<P, 24>();
     case 28: return wta_bulk_info<P, 28>();

@@ -17,6 +17,7 @@ struct SgmLayout {
   size_t vol_bytes() const { return pitch * size_t(h); }
 };
 SgmLayout sgm_layout(int h, int w, int levels, int paths);
+constexpr int kWplG1Max = 17;  // widest one-lane-per-chain layout (68 levels)
 
 // TMA-staged aggregation of all 2P (volume, direction) chains of one pass
 // (sgm_tma.cu).  vol_lr: left- then right-reference u8 cost volumes;

@@ -69,6 +69,8 @@ struct TmaJob {
   int kmin;     // diagonal: first chain index (u = k + du*s)
   int nchains;
   int block0;
+  int nseg;     // H / V: CTAs (segments) per chain group along the scan (1 = unsplit)
+  int slot0;    // first segment-boundary slot of this job in the exchange area
 };
 
 struct TmaArgs {
@@ -82,6 +84,13 @@ struct TmaArgs {
   uint8_t* path_base;  // diagonal jobs store directly
   size_t pitch, vol_bytes;
   int dbg;  // debugging early-exit level (RPD_TMA_DBG), 0 in production
+  // Segmented chains (see agg_body): boundary states and flags, CTA tickets.
+  uint32_t* seg_state;  // per boundary slot: true state, then the warm-up guess
+  uint32_t* seg_flag;   // per boundary slot: 1 = predecessor's true state published
+  unsigned* ticket;     // dynamic CTA order (start order = logical block index)
+  unsigned long long* reruns;  // count of recomputed segments (rpd_stats)
+  int seg_words;        // words of one state image (NPAIR * THREADS)
+  int warm_stages;      // warm-up stages of a segment before its first stored stage
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -391,7 +400,7 @@ __device__ __forceinline__ void chain_step(ChainState<NPAIR>& cs, const uint32_t
 // One job type, fully specialised.  NPAIR <= 2*WPL level pairs are computed
 // per lane; a trailing all-padding pair (odd L with G == 1) is skipped.
 template <int TYPE, int WPL, int G, int NPAIR>
-__device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int cta,
+__device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int cta, int cta_seg,
                                          uint32_t* in_ring, uint32_t* out_ring, uint64_t* full) {
   using GE = Geo<WPL, G>;
   constexpr int R = GE::R;
@@ -478,13 +487,6 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
     return uint32_t(rows) * uint32_t(GE::DROW) * 4u;
   };
 
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kDepth && st < nstage; ++st) {
-      mbar_expect_tx(&full[st], stage_bytes(st));
-      tile_ops(st, true, in_ring + st * GE::STAGE_IN, &full[st]);
-    }
-  }
-
   TileAddr<TYPE, WPL, G> ad;
   ad.init(t, g);
   const uint32_t p1x2 = a.p1x2, p2x2 = a.p2x2, one = a.one;
@@ -492,63 +494,148 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
   cs.reset();
   uint8_t* const pbase = a.path_base + size_t(zp) * a.vol_bytes + size_t(g * WPL) * 4;
 
-  for (int st = 0; st < nstage; ++st) {
-    const int slot = st % kDepth;
-    mbar_wait(&full[slot], uint32_t(st / kDepth) & 1u);
-    const uint32_t* inb = in_ring + slot * GE::STAGE_IN;
-    uint32_t* outb = out_ring + (st % kOutDepth) * GE::STAGE;
-    const int s0 = stage_base + st * R;
-    // only the first tile of a backward H/V scan holds padding steps
-    const bool check = TYPE != kDiag && s0 < s_begin;
-#pragma unroll(kStepUnroll)
-    for (int r = 0; r < R; ++r) {
-      const int s = s0 + r;
-      const int rr = (TYPE != kDiag && backward) ? R - 1 - r : r;
-      int shift = 0, col = 0;
-      if (TYPE == kDiag) {
-        const int cbase = kbase + du * s;
-        shift = (cbase * GE::WPP) & 3;
-        col = cbase + t;
-        const bool has_pred = s > 0 && unsigned(col - du) < unsigned(w);
-        if (!has_pred) cs.reset();  // chain (re)enters the image
-      }
-      uint32_t w8[WPL];
-#pragma unroll
-      for (int q = 0; q < WPL; ++q) w8[q] = inb[ad.at(q, rr, shift)];
-      uint32_t packed[WPL];
-      if (check && s < s_begin) continue;  // padding step: state stays INF
-#if RPD_AGG_REC == 3
-      chain_step_norm<WPL, G, NPAIR>(cs, w8, p1x2, p2x2 - p1x2, one, g, gmask, packed);
-#else
-      chain_step<WPL, G, NPAIR>(cs, w8, p1x2, p2x2, g, gmask, packed);
-#endif
-      if (TYPE == kDiag) {
-        if (unsigned(col) < unsigned(w) && s < s_end) {
-          const int vrow = dv > 0 ? s : h - 1 - s;
-          uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + size_t(vrow) * a.pitch +
-                                                      size_t(col) * (GE::WPP * 4));
-#pragma unroll
-          for (int q = 0; q < WPL; ++q) dst[q] = packed[q];
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < WPL; ++q) outb[ad.at(q, rr, 0)] = packed[q];
+  // Segmented chains (H / V jobs with J.nseg > 1).  The stages of a chain
+  // group are cut into nseg ranges [m0, m1), one CTA each.  Segment j > 0
+  // starts `warm_stages` before m0 from the restart state and stores nothing
+  // there; the recurrence forgets its start state within a few dozen steps
+  // on textured costs (BASELINE scenes: every chain within 64 steps at the
+  // cut), so its state at m0 - 1 (the guess) normally equals the true one.
+  // The outputs from m0 on depend only on that state and the raw costs, so
+  // they are exact whenever the guess equals the true state, which segment
+  // j - 1 publishes when it ends.  Segment j compares the two and, on any
+  // difference in a valid chain, reruns [m0, m1) from the true state,
+  // overwriting its outputs (uniform cost runs do not forget their start).
+  int seg = 0, nseg = 1;
+  if constexpr (TYPE != kDiag) {
+    nseg = J.nseg;
+    seg = cta_seg;
+  }
+  const int m0 = nseg > 1 ? int((long long)nstage * seg / nseg) : 0;
+  const int m1 = nseg > 1 ? int((long long)nstage * (seg + 1) / nseg) : nstage;
+  const int slot = J.slot0 + cta * (nseg - 1) + seg - 1;  // boundary (seg-1 | seg)
+  const int tid = int(threadIdx.x);
+
+  uint32_t seq = 0;  // stages consumed by this CTA (ring slot / mbarrier parity)
+  int ra = max(0, m0 - a.warm_stages);
+#pragma unroll 1
+  for (int pass = 0;; ++pass) {
+    const int rb = m1;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kDepth && ra + i < rb; ++i) {
+        const uint32_t sl = (seq + i) % kDepth;
+        mbar_expect_tx(&full[sl], stage_bytes(ra + i));
+        tile_ops(ra + i, true, in_ring + sl * GE::STAGE_IN, &full[sl]);
       }
     }
-    if (TYPE != kDiag) fence_async_smem();  // output-tile writes -> async proxy
-    __syncthreads();                         // tile consumed, output tile written
+#pragma unroll 1
+    for (int st = ra; st < rb; ++st, ++seq) {
+      const uint32_t sl = seq % kDepth;
+      mbar_wait(&full[sl], (seq / kDepth) & 1u);
+      const uint32_t* inb = in_ring + sl * GE::STAGE_IN;
+      uint32_t* outb = out_ring + (seq % kOutDepth) * GE::STAGE;
+      const bool store = st >= m0;
+      const int s0 = stage_base + st * R;
+      // only the first tile of a backward H/V scan holds padding steps
+      const bool check = TYPE != kDiag && s0 < s_begin;
+#pragma unroll(kStepUnroll)
+      for (int r = 0; r < R; ++r) {
+        const int s = s0 + r;
+        const int rr = (TYPE != kDiag && backward) ? R - 1 - r : r;
+        int shift = 0, col = 0;
+        if (TYPE == kDiag) {
+          const int cbase = kbase + du * s;
+          shift = (cbase * GE::WPP) & 3;
+          col = cbase + t;
+          const bool has_pred = s > 0 && unsigned(col - du) < unsigned(w);
+          if (!has_pred) cs.reset();  // chain (re)enters the image
+        }
+        uint32_t w8[WPL];
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) w8[q] = inb[ad.at(q, rr, shift)];
+        uint32_t packed[WPL];
+        if (check && s < s_begin) continue;  // padding step (outside the image): state stays
+#if RPD_AGG_REC == 3
+        chain_step_norm<WPL, G, NPAIR>(cs, w8, p1x2, p2x2 - p1x2, one, g, gmask, packed);
+#else
+        chain_step<WPL, G, NPAIR>(cs, w8, p1x2, p2x2, g, gmask, packed);
+#endif
+        if (TYPE == kDiag) {
+          if (unsigned(col) < unsigned(w) && s < s_end) {
+            const int vrow = dv > 0 ? s : h - 1 - s;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + size_t(vrow) * a.pitch +
+                                                        size_t(col) * (GE::WPP * 4));
+#pragma unroll
+            for (int q = 0; q < WPL; ++q) dst[q] = packed[q];
+          }
+        } else if (store) {
+#pragma unroll
+          for (int q = 0; q < WPL; ++q) outb[ad.at(q, rr, 0)] = packed[q];
+        }
+      }
+      if constexpr (TYPE != kDiag) {
+        if (seg > 0 && pass == 0 && st + 1 == m0) {
+          // the warm-up guess of the state after stage m0 - 1
+          uint32_t* gs = a.seg_state + size_t(slot) * 2 * a.seg_words + a.seg_words;
+#pragma unroll
+          for (int q = 0; q < NPAIR; ++q) __stcg(gs + q * GE::THREADS + tid, cs.prev[q]);
+        }
+      }
+      if (TYPE != kDiag && store) fence_async_smem();  // output-tile writes -> async proxy
+      __syncthreads();                                  // tile consumed, output tile written
+      if (threadIdx.x == 0) {
+        if (TYPE != kDiag && store) {
+          tile_ops(st, false, outb, nullptr);
+          tma_commit();
+        }
+        if (st + kDepth < rb) {
+          mbar_expect_tx(&full[sl], stage_bytes(st + kDepth));
+          tile_ops(st + kDepth, true, in_ring + sl * GE::STAGE_IN, &full[sl]);
+        }
+        if (TYPE != kDiag && store) tma_wait_read<kOutDepth - 1>();  // the next output buffer is free again
+      }
+      __syncthreads();
+    }
+    if constexpr (TYPE == kDiag) break;
+    if (!(seg > 0 && pass == 0)) break;
+    // Wait for the predecessor's true state after stage m0 - 1 (a lower
+    // logical block: it started before this one, so it makes progress).
     if (threadIdx.x == 0) {
-      if (TYPE != kDiag) {
-        tile_ops(st, false, outb, nullptr);
-        tma_commit();
+      const uint32_t* f = a.seg_flag + slot;
+      uint32_t v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) break;
+        __nanosleep(64);
       }
-      if (st + kDepth < nstage) {
-        mbar_expect_tx(&full[slot], stage_bytes(st + kDepth));
-        tile_ops(st + kDepth, true, in_ring + slot * GE::STAGE_IN, &full[slot]);
-      }
-      if (TYPE != kDiag) tma_wait_read<kOutDepth - 1>();  // the next output buffer is free again
+      a.seg_flag[slot] = 0u;  // consumed; the next launch's producer sets it again
     }
     __syncthreads();
+    const uint32_t* ts = a.seg_state + size_t(slot) * 2 * a.seg_words;
+    const bool valid = c0 + t < J.nchains;
+    bool diff = false;
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q)
+      diff |= __ldcg(ts + q * GE::THREADS + tid) != __ldcg(ts + a.seg_words + q * GE::THREADS + tid);
+    if (!__syncthreads_or(valid && diff)) break;
+    if (threadIdx.x == 0) atomicAdd(a.reruns, 1ull);
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) cs.prev[q] = __ldcg(ts + q * GE::THREADS + tid);
+    if (threadIdx.x == 0) tma_wait_all();  // own stores complete before rewriting them
+    __syncthreads();
+    ra = m0;
+  }
+  if constexpr (TYPE != kDiag) {
+    if (seg < nseg - 1) {
+      // publish this segment's (true) final state for segment seg + 1
+      uint32_t* ts = a.seg_state + size_t(slot + 1) * 2 * a.seg_words;
+#pragma unroll
+      for (int q = 0; q < NPAIR; ++q) __stcg(ts + q * GE::THREADS + tid, cs.prev[q]);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.seg_flag + slot + 1), "r"(1u)
+                     : "memory");
+    }
   }
   if (TYPE != kDiag && threadIdx.x == 0) tma_wait_all();
 }
@@ -564,30 +651,43 @@ __global__ void __launch_bounds__(Geo<WPL, G>::THREADS)
   uint32_t* in_ring = dsm + pad_words;                // kDepth * STAGE_IN
   uint32_t* out_ring = in_ring + kDepth * GE::STAGE_IN;  // kOutDepth * STAGE
   __shared__ __align__(8) uint64_t full[kDepth];
-  int jidx = 0;
-#pragma unroll 1
-  while (jidx + 1 < a.njobs && int(blockIdx.x) >= a.job[jidx + 1].block0) ++jidx;
-  const TmaJob& J = a.job[jidx];
-  const int cta = int(blockIdx.x) - J.block0;
+  __shared__ int s_block;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kDepth; ++i) mbar_init(&full[i], 1);
     fence_async_smem();
+    // Segmented chains wait on lower logical blocks: hand out logical block
+    // indices in start order (the last CTA rearms the counter for the next
+    // launch on this workspace).
+    int b = int(blockIdx.x);
+    if (a.ticket) {
+      b = int(atomicAdd(a.ticket, 1u));
+      if (b == int(gridDim.x) - 1) atomicExch(a.ticket, 0u);
+    }
+    s_block = b;
   }
   __syncthreads();
+  const int blk = s_block;
+  int jidx = 0;
+#pragma unroll 1
+  while (jidx + 1 < a.njobs && blk >= a.job[jidx + 1].block0) ++jidx;
+  const TmaJob& J = a.job[jidx];
+  const int cta = (blk - J.block0) / J.nseg;
+  const int cta_seg = (blk - J.block0) % J.nseg;
   unsigned long long t0 = 0;
   if (a.dbg == 100 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   if (J.type == kHoriz)
-    agg_body<kHoriz, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
+    agg_body<kHoriz, WPL, G, NPAIR>(a, J, cta, cta_seg, in_ring, out_ring, full);
   else if (J.type == kVert)
-    agg_body<kVert, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
+    agg_body<kVert, WPL, G, NPAIR>(a, J, cta, cta_seg, in_ring, out_ring, full);
   else
-    agg_body<kDiag, WPL, G, NPAIR>(a, J, cta, in_ring, out_ring, full);
+    agg_body<kDiag, WPL, G, NPAIR>(a, J, cta, 0, in_ring, out_ring, full);
   if (a.dbg == 100 && threadIdx.x == 0) {  // RPD_TMA_DBG=100: per-CTA timeline
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    printf("AGGTR %d %d %d %d %u %llu %llu\n", WPL, int(blockIdx.x), jidx, J.type, smid, t0, t1);
+    printf("AGGTR %d %d %d %d %d %d %d %u %llu %llu\n", WPL, G, blk, jidx, J.type, cta_seg, J.nseg,
+           smid, t0, t1);
   }
 }
 
@@ -598,6 +698,7 @@ struct KernelInfo {
   int smem;
   int threads;
   int R, wpp, row, cwf, cwl, nch, dcwf, dcwl;
+  int npair;
 };
 
 template <int WPL, int G, int NPAIR>
@@ -606,7 +707,7 @@ KernelInfo info() {
   return KernelInfo{k_aggregate_tma<WPL, G, NPAIR>,
                     (kDepth * GE::STAGE_IN + kOutDepth * GE::STAGE) * 4 + 1024,
                     GE::THREADS, GE::R, GE::WPP, GE::ROW, GE::CWF, GE::CWL, GE::NCH,
-                    GE::DROW < 256 ? GE::DROW : 256, GE::DCWL};
+                    GE::DROW < 256 ? GE::DROW : 256, GE::DCWL, NPAIR};
 }
 
 KernelInfo pick(int wpl, int G, int levels) {
@@ -619,7 +720,7 @@ KernelInfo pick(int wpl, int G, int levels) {
 #define RPD_TMA_GN(W_, G_) \
   if (wpl == W_ && G == G_) return info<W_, G_, 2 * W_>();
   RPD_TMA_G1(1) RPD_TMA_G1(2) RPD_TMA_G1(3) RPD_TMA_G1(4) RPD_TMA_G1(5) RPD_TMA_G1(6)
-  RPD_TMA_G1(7) RPD_TMA_G1(8) RPD_TMA_G1(9)
+  RPD_TMA_G1(7) RPD_TMA_G1(8) RPD_TMA_G1(9) RPD_TMA_G1(17)
   RPD_TMA_GN(2, 2) RPD_TMA_GN(3, 2) RPD_TMA_GN(4, 2)
   RPD_TMA_GN(2, 4) RPD_TMA_GN(3, 4) RPD_TMA_GN(4, 4)
   RPD_TMA_GN(2, 8) RPD_TMA_GN(3, 8) RPD_TMA_GN(4, 8)
@@ -662,6 +763,7 @@ CUtensorMap make_map(void* base, int words_per_row, int rows, int depth, size_t 
 }  // namespace
 
 bool sgm_tma_supported(const SgmLayout& L) {
+  if (L.G == 1 && L.wpl == kWplG1Max) return true;
   return (L.G == 1 || L.G == 2 || L.G == 4 || L.G == 8) && L.wpl >= 1 && L.wpl <= 9 &&
          (L.G == 1 || L.wpl >= 2);
 }
@@ -698,7 +800,30 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
   args.path_vl = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwl, R);
   args.path_df = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwf, 1);
   args.path_dl = make_map(paths, words_row, L.h, 2 * paths_n, L.pitch, ki.cwl, 1);
-  int blocks = 0;
+#ifndef RPD_AGG_WARM
+#define RPD_AGG_WARM 64  // warm-up steps of a chain segment (multiple of R)
+#endif
+#ifndef RPD_AGG_SPLIT
+#define RPD_AGG_SPLIT 1  // 0: never segment chains
+#endif
+  // H / V chains longer than the longest diagonal (min(W, H) steps) are cut
+  // into segments of at most that length (plus the warm-up), so no job type
+  // sets the serial makespan alone.
+  const int lmin = std::min(L.w, L.h);
+  int split = RPD_AGG_SPLIT, warm = RPD_AGG_WARM;
+  if (const char* e = debug_knob("RPD_AGG_SPLIT")) split = std::atoi(e);  // checked build only
+  if (const char* e = debug_knob("RPD_AGG_WARM")) warm = std::atoi(e);
+  auto nseg_for = [&](int len) {
+    // multi-lane chains (G > 1) already fill the SMs: segmenting them measured slower
+    if (!split || lmin <= 0 || (L.G > 1 && split == 1)) return 1;
+    // split > 1: force that many segments (A/B experiments, checked build)
+    const int n = split > 1 ? split : std::min({8, cdiv(len, lmin), len / (3 * warm)});
+    return std::max(n, 1);
+  };
+  args.warm_stages = warm / R;
+  args.seg_words = ki.npair * ki.threads;
+  int nslots = 0;
+  int blocks = 0, nonseg_blocks = 0;
   const char* dbg = debug_knob("RPD_TMA_TYPES");  // debugging: bitmask of job types to run
   const int type_mask = dbg ? std::atoi(dbg) : 7;
 #ifndef RPD_AGG_ORDER
@@ -729,9 +854,34 @@ void launch_aggregate_tma(rpd_ctx* ctx, const SgmLayout& L, uint8_t* vol_lr, uin
         J.nchains = L.w + L.h - 1;
         J.kmin = J.du > 0 ? -(L.h - 1) : 0;
       }
+      J.nseg = J.type == kHoriz ? nseg_for(L.w) : (J.type == kVert ? nseg_for(L.h) : 1);
+      J.slot0 = nslots;
       J.block0 = blocks;
-      blocks += cdiv(J.nchains, kNC);
+      nslots += cdiv(J.nchains, kNC) * (J.nseg - 1);
+      blocks += cdiv(J.nchains, kNC) * J.nseg;
+      nonseg_blocks += cdiv(J.nchains, kNC);
     }
+  if (nslots > 0) {
+    args.seg_state = ctx->ws.get<uint32_t>("agg_seg_state", size_t(nslots) * 2 * args.seg_words);
+    unsigned* flags = ctx->ws.get<unsigned>("agg_seg_flags", size_t(nslots) + 1);
+    // consumers rearm their flags and the last CTA the ticket: zero once per buffer
+    if (ctx->agg_flags_zeroed != flags || ctx->agg_flags_words < nslots + 1) {
+      RPD_CK(cudaMemsetAsync(flags, 0, (size_t(nslots) + 1) * sizeof(unsigned), ctx->stream));
+      ctx->agg_flags_zeroed = flags;
+      ctx->agg_flags_words = nslots + 1;
+    }
+    args.ticket = flags;
+    args.seg_flag = flags + 1;
+  }
+  {
+    unsigned long long* rr = ctx->ws.get<unsigned long long>("agg_reruns", 1);
+    if (rr != ctx->agg_reruns) {
+      RPD_CK(cudaMemsetAsync(rr, 0, sizeof(unsigned long long), ctx->stream));
+      ctx->agg_reruns = rr;
+    }
+  }
+  args.reruns = ctx->agg_reruns;
+  ctx->agg_segmented_ctas = blocks - nonseg_blocks;
   RPD_CK(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ki.smem));
   ki.fn<<<blocks, ki.threads, ki.smem, ctx->stream>>>(args);
   RPD_LAUNCH_CHECK();

@@ -14,7 +14,7 @@ v, rep = sys.argv[1], sys.argv[2]
 try:
     d = json.loads(open(f"gpurun_out/ab_{v}_{rep}.log").read().strip().splitlines()[-1])
     s = d["stage_ms"]
-    print(f"{v:10s} {d['value']:8.1f} serial {d['value_serial']:7.1f} e2e {d['e2e']['value']:7.1f} " +
+    print(f"{v:10s} {d["value"]:8.1f} agg {d["roofline"]["agg_ms_per_frame"]:.4f} serial {d['value_serial']:7.1f} e2e {d['e2e']['value']:7.1f} " +
           " ".join(f"{k[:6]}={x:.3f}" for k, x in s.items()))
 except Exception as e:
     print(v, "failed", e)
