@@ -191,7 +191,14 @@ struct AssignArgs {
   int* orphan_count;
   int* inexact;
   int force_walk;  // checked build only (RPD_SLIC_FORCE_WALK): exercise the brute-force path
+  uint32_t b_magic;  // floor(2^32 / B) + 1: x / B == umulhi(x, b_magic) for 0 <= x < 2^16 (0: divide)
 };
+
+// Bucket index of a non-negative coordinate (tile-uniform values: one
+// multiply-high instead of an integer division per thread).
+__device__ __forceinline__ int bucket_of(const AssignArgs& a, int x) {
+  return a.b_magic ? int(__umulhi(uint32_t(x), a.b_magic)) : x / a.B;
+}
 
 // assign_pixels, segmentation.cpp:30-57 (windowed part) for one pixel by
 // scanning every centre; used when a tile's candidate list or a bucket
@@ -227,11 +234,15 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 #endif
 constexpr int kTileU = 32, kTileV = RPD_ASSIGN_TILEV, kMaxTileCenters = 192;
 constexpr int kRowCap = RPD_ASSIGN_ROWCAP;  // candidate records per tile row (more: per-pixel bucket walk)
-constexpr int kAssignThreads = 256;
-#ifndef RPD_ASSIGN_MINB
-#define RPD_ASSIGN_MINB 6  // resident CTAs per SM the register budget targets
+#ifndef RPD_ASSIGN_THREADS
+#define RPD_ASSIGN_THREADS 256
 #endif
-constexpr int kRowsPerWarp = kTileV / (kAssignThreads / 32);  // a warp owns rows w, w+8, ...
+constexpr int kAssignThreads = RPD_ASSIGN_THREADS;
+constexpr int kAssignWarps = kAssignThreads / 32;
+#ifndef RPD_ASSIGN_MINB
+#define RPD_ASSIGN_MINB (6 * 256 / RPD_ASSIGN_THREADS)  // resident CTAs per SM the register budget targets
+#endif
+constexpr int kRowsPerWarp = kTileV / kAssignWarps;  // a warp owns rows w, w + kAssignWarps, ...
 
 template <bool SUMS>
 __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
@@ -251,17 +262,17 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   float xf[kRowsPerWarp];
 #pragma unroll
   for (int q = 0; q < kRowsPerWarp; ++q) {
-    const int v = v0 + wid + 8 * q;
+    const int v = v0 + wid + kAssignWarps * q;
     xf[q] = (u < a.w && v < a.h) ? a.vals[size_t(v) * a.w + u] : 0.0f;
   }
   if (threadIdx.x < kTileV) s_rowcnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_cnt = 0;
   const bool walk_all = a.force_walk || *a.ovf != 0;  // a bucket overflowed this round
   // bucket range of the tile +- win
-  const int bx0 = u0 - win < 0 ? 0 : (u0 - win) / a.B;
-  const int by0 = v0 - win < 0 ? 0 : (v0 - win) / a.B;
-  const int nbxr = min(a.nbx - 1, (u0 + kTileU - 1 + win) / a.B) - bx0 + 1;
-  const int nbyr = min(a.nby - 1, (v0 + kTileV - 1 + win) / a.B) - by0 + 1;
+  const int bx0 = u0 - win < 0 ? 0 : bucket_of(a, u0 - win);
+  const int by0 = v0 - win < 0 ? 0 : bucket_of(a, v0 - win);
+  const int nbxr = min(a.nbx - 1, bucket_of(a, u0 + kTileU - 1 + win)) - bx0 + 1;
+  const int nbyr = min(a.nby - 1, bucket_of(a, v0 + kTileV - 1 + win)) - by0 + 1;
   __syncthreads();
   if (!walk_all) {
     // one (bucket, slot) item per thread; keep the centres whose window
@@ -312,7 +323,7 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   }
 #pragma unroll
   for (int q = 0; q < kRowsPerWarp; ++q) {
-    const int ty = wid + 8 * q;
+    const int ty = wid + kAssignWarps * q;
     const int v = v0 + ty;  // uniform across the warp
     const bool in = u < a.w && v < a.h;
     const size_t p = size_t(v) * a.w + u;
@@ -358,10 +369,11 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
       run_add_value(s.sx, key, key > 0, xf[q], ri, a.inexact);
       // a run is a contiguous pixel segment of one row: count and coordinate
       // sums follow from its bounds
+      // (32-bit: cnt <= 32 and coordinates < 2^26)
       const int cnt = ri.end - tx + 1;
-      const long long su = (long long)cnt * u + (long long)cnt * (cnt - 1) / 2;
-      const long long sv = (long long)cnt * v;
       if (ri.head) {
+        const unsigned su = unsigned(cnt * u + ((cnt * (cnt - 1)) >> 1));
+        const unsigned sv = unsigned(cnt * v);
         atomicAdd(&s.n[key], cnt);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
@@ -782,7 +794,9 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
 
   AssignArgs aa{vals, h, w, K, c, nullptr, nullptr, grid.rec, B, nbx, nby, win, sw, labels,
                 orphan_list, orphan_count, inexact,
-                debug_knob("RPD_SLIC_FORCE_WALK") != nullptr ? 1 : 0};
+                debug_knob("RPD_SLIC_FORCE_WALK") != nullptr ? 1 : 0, 0u};
+  if (B >= 2 && w + win + kTileU < 65536 && h + win + kTileV < 65536)
+    aa.b_magic = uint32_t((1ull << 32) / unsigned(B) + 1ull);
   const dim3 tgrid(cdiv(w, kTileU), cdiv(h, kTileV));
   const int cblocks = cdiv(std::max(K, nb), 256);
   int round = 0;
