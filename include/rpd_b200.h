@@ -10,7 +10,13 @@
  * Cost volumes use the reference layout (v*W+u)*(d_max+1)+d (sgm.hpp:19).
  *
  * All host pointers are caller-owned.  The library owns only the device
- * workspaces inside an rpd_ctx.  A context is single-threaded: one per
+ * workspaces inside an rpd_ctx.  Device-resident data: the raster arguments
+ * and outputs of rpd_detect / rpd_detect_u8 / rpd_detect_fetch, the
+ * evaluation metrics (rpd_pep, rpd_rmse, rpd_pixel_metrics,
+ * rpd_instance_metrics), the reprojections and the image_io transforms may
+ * also point to device memory of the context's GPU (unified addressing; the
+ * staging copies become device-to-device), so a frame's outputs can be
+ * evaluated or reprojected without a host round trip.  A context is single-threaded: one per
  * (host thread, device); concurrent contexts are fine (sgm/pipeline are
  * reentrant in the reference, rpd_cli.cpp:293-302).
  *

@@ -222,27 +222,47 @@ _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
 
 
+def _on_device(a) -> bool:
+    """A CUDA tensor (torch): the C-ABI takes device memory of the context's
+    GPU wherever it takes a host buffer (abi_util.hpp: cudaMemcpyDefault)."""
+    return getattr(a, "is_cuda", False) and hasattr(a, "data_ptr")
+
+
+def _dev(a, dtype: str):
+    if str(a.dtype) != "torch." + dtype or not a.is_contiguous():
+        raise InvalidArgument(f"device arrays must be contiguous {dtype}")
+    return a
+
+
 def _ptr(a):
-    return None if a is None else a.ctypes.data_as(C.c_void_p)
+    if a is None:
+        return None
+    if _on_device(a):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
 
 
 def _f32(a):
-    return np.ascontiguousarray(a, dtype=np.float32)
+    return _dev(a, "float32") if _on_device(a) else np.ascontiguousarray(a, dtype=np.float32)
 
 
 def _f64(a):
-    return np.ascontiguousarray(a, dtype=np.float64)
+    return _dev(a, "float64") if _on_device(a) else np.ascontiguousarray(a, dtype=np.float64)
 
 
 def _i32(a):
-    return np.ascontiguousarray(a, dtype=np.int32)
+    return _dev(a, "int32") if _on_device(a) else np.ascontiguousarray(a, dtype=np.int32)
 
 
 def _fp(a):
+    if a is not None and _on_device(a):
+        return C.cast(a.data_ptr(), C.POINTER(C.c_float))
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_float))
 
 
 def _ip(a):
+    if a is not None and _on_device(a):
+        return C.cast(a.data_ptr(), C.POINTER(C.c_int32))
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
 
 

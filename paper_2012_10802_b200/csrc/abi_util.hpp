@@ -43,17 +43,20 @@ inline void check_dims(int h, int w) {
   if (h <= 0 || w <= 0) throw InvalidArg("image dimensions must be positive");
 }
 
+// Buffer arguments of the C-ABI are host memory (pageable or pinned) or
+// device memory of the context's GPU: the staging copies use
+// cudaMemcpyDefault (unified addressing picks host<->device or
+// device<->device), so device-resident data — e.g. a frame's outputs fetched
+// into device buffers — is evaluated without a host round trip.
 template <typename T>
 T* upload(rpd_ctx* ctx, const char* name, const T* host, size_t count) {
   T* d = ctx->ws.get<T>(name, count);
-  if (count)
-    RPD_CK(cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream));
+  if (count) RPD_CK(cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyDefault, ctx->stream));
   return d;
 }
 
 inline void download(rpd_ctx* ctx, void* host, const void* dev, size_t bytes) {
-  if (bytes)
-    RPD_CK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (bytes) RPD_CK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDefault, ctx->stream));
   RPD_CK(cudaStreamSynchronize(ctx->stream));
 }
 

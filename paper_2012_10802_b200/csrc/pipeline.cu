@@ -343,8 +343,10 @@ void run_frame(rpd_ctx* ctx, int h, int w, bool u8, const rpd_config& c, FrameBu
 void fetch(rpd_ctx* ctx, const FrameBuffers& f, int h, int w, rpd_detect_out* out) {
   cudaStream_t st = ctx->stream;
   const size_t n = size_t(h) * w;
+  // cudaMemcpyDefault: an output may be host memory or device memory of this
+  // GPU (device-resident consumers take a device-to-device copy)
   auto d2h = [&](void* dst, const void* src, size_t bytes) {
-    if (dst && bytes) RPD_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    if (dst && bytes) RPD_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
   };
   d2h(out->d0, f.d0, sizeof(float) * n);
   d2h(out->d1, f.d1, sizeof(float) * n);
@@ -360,7 +362,7 @@ void fetch(rpd_ctx* ctx, const FrameBuffers& f, int h, int w, rpd_detect_out* ou
   if (out->centers && out->centers_cap > 0 && count > 0) {
     const int m = std::min(out->centers_cap, count);
     RPD_CK(cudaMemcpyAsync(out->centers, f.sp.centers, sizeof(double) * 3 * size_t(m),
-                           cudaMemcpyDeviceToHost, st));
+                           cudaMemcpyDefault, st));
     RPD_CK(cudaStreamSynchronize(st));
   }
   out->sp_count = count;
@@ -409,8 +411,8 @@ rpd_status rpd_detect(rpd_ctx* ctx, const float* left, const float* right, int h
     const size_t n = size_t(h) * w;
     float* l = ctx->ws.get<float>("pl_left", n);
     float* r = ctx->ws.get<float>("pl_right", n);
-    RPD_CK(cudaMemcpyAsync(l, left, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
-    RPD_CK(cudaMemcpyAsync(r, right, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(l, left, sizeof(float) * n, cudaMemcpyDefault, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(r, right, sizeof(float) * n, cudaMemcpyDefault, ctx->stream));
     FrameBuffers f;
     run_frame(ctx, h, w, false, *cfg, f);
     fetch(ctx, f, h, w, out);
@@ -424,8 +426,8 @@ rpd_status rpd_detect_u8(rpd_ctx* ctx, const uint8_t* left, const uint8_t* right
     const size_t n = size_t(h) * w;
     uint8_t* l = ctx->ws.get<uint8_t>("pl_left8", n);
     uint8_t* r = ctx->ws.get<uint8_t>("pl_right8", n);
-    RPD_CK(cudaMemcpyAsync(l, left, n, cudaMemcpyHostToDevice, ctx->stream));
-    RPD_CK(cudaMemcpyAsync(r, right, n, cudaMemcpyHostToDevice, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(l, left, n, cudaMemcpyDefault, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(r, right, n, cudaMemcpyDefault, ctx->stream));
     FrameBuffers f;
     run_frame(ctx, h, w, true, *cfg, f);
     fetch(ctx, f, h, w, out);
@@ -479,8 +481,8 @@ rpd_status rpd_detect_async_host_u8(rpd_ctx* ctx, const uint8_t* left, const uin
     uint8_t* l = ctx->ws.get<uint8_t>("pl_left8", n);
     uint8_t* r = ctx->ws.get<uint8_t>("pl_right8", n);
     // asynchronous (DMA) when the host buffers are pinned (rpd_host_alloc)
-    RPD_CK(cudaMemcpyAsync(l, left, n, cudaMemcpyHostToDevice, ctx->stream));
-    RPD_CK(cudaMemcpyAsync(r, right, n, cudaMemcpyHostToDevice, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(l, left, n, cudaMemcpyDefault, ctx->stream));
+    RPD_CK(cudaMemcpyAsync(r, right, n, cudaMemcpyDefault, ctx->stream));
     PipelineState& ps = state(ctx);
     run_frame(ctx, h, w, true, *cfg, ps.last);
     ps.have_last = true;

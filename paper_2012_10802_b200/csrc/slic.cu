@@ -220,14 +220,14 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 }
 
 // Tiled assign_pixels with the next update_centers' sums fused in.  A CTA owns
-// a 32x8 pixel tile; the centres of every bucket that can reach the tile are
+// a 32 x kTileV pixel tile; the centres of every bucket that can reach the tile are
 // staged once in shared memory, each pixel keeps the lexicographic minimum
 // (dist, k) of the centres whose window holds it (== ascending-k strict `<`),
 // and — when SUMS — the pixel's (1, u, v, value) is added to its label's sums
 // with warp run aggregation (a warp is one tile row).  Pixels without a window
 // are left for the fallback kernel, which adds their sums itself.
 #ifndef RPD_ASSIGN_TILEV
-#define RPD_ASSIGN_TILEV 32
+#define RPD_ASSIGN_TILEV 24  // tile rows (3 per warp; 24 vs 32: SLIC 0.409 -> 0.395 ms serial)
 #endif
 #ifndef RPD_ASSIGN_ROWCAP
 #define RPD_ASSIGN_ROWCAP 24
@@ -243,6 +243,7 @@ constexpr int kAssignWarps = kAssignThreads / 32;
 #define RPD_ASSIGN_MINB (6 * 256 / RPD_ASSIGN_THREADS)  // resident CTAs per SM the register budget targets
 #endif
 constexpr int kRowsPerWarp = kTileV / kAssignWarps;  // a warp owns rows w, w + kAssignWarps, ...
+static_assert(kTileV % kAssignWarps == 0, "whole tile rows per warp");
 
 template <bool SUMS>
 __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     const int v = v0 + wid + kAssignWarps * q;
     xf[q] = (u < a.w && v < a.h) ? a.vals[size_t(v) * a.w + u] : 0.0f;
   }
-  if (threadIdx.x < kTileV) s_rowcnt[threadIdx.x] = 0;
+  for (int r = threadIdx.x; r < kTileV; r += blockDim.x) s_rowcnt[r] = 0;
   if (threadIdx.x == 0) s_cnt = 0;
   const bool walk_all = a.force_walk || *a.ovf != 0;  // a bucket overflowed this round
   // bucket range of the tile +- win
@@ -299,11 +300,11 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   if (nc <= kMaxTileCenters) {
     // distribute the candidates over the rows they reach, with the row's
     // (v - cv)^2 precomputed (the reference's dv * dv, segmentation.cpp:48)
-    // one (candidate, row) item per thread: lane = tile row, so a warp's
-    // counter atomics never collide and every thread has work
-    static_assert(kTileV == 32, "item decomposition assumes 32 tile rows");
+    // one (candidate, row) item per thread, consecutive threads on
+    // consecutive rows (a warp's counter atomics rarely collide); every
+    // thread has work
     for (int t = threadIdx.x; t < nc * kTileV; t += blockDim.x) {
-      const int i = t >> 5, r = t & 31;
+      const int i = t / kTileV, r = t - i * kTileV;
       const int icv = s_icv[i];
       if (r < max(icv - win, v0) - v0 || r > min(icv + win, v0 + kTileV - 1) - v0) continue;
       const double2 cuv = s_cd[2 * i];
@@ -317,8 +318,10 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   }
   __syncthreads();
   if (nc <= kMaxTileCenters) {  // a row list overflowed: per-pixel bucket walk for the tile
-    static_assert(kTileV <= 32, "one lane per tile row");
-    const bool over = __any_sync(0xFFFFFFFFu, tx < kTileV && s_rowcnt[tx] > kRowCap);
+    bool ov = false;
+#pragma unroll
+    for (int r0 = 0; r0 < kTileV; r0 += 32) ov |= r0 + tx < kTileV && s_rowcnt[r0 + tx] > kRowCap;
+    const bool over = __any_sync(0xFFFFFFFFu, ov);
     if (over) nc = kMaxTileCenters + 1;
   }
 #pragma unroll
