@@ -1,7 +1,7 @@
 #!/bin/bash
 # Cost attribution in the concurrent regime: bench with RPD_SKIP_STAGES masks.
 for m in "$@"; do
-  RPD_SKIP_STAGES=$m timeout 120 python bench.py --steps 20 --warmup 5 --no-cpu-baseline \
+  RPD_SKIP_STAGES=$m timeout 120 python bench.py --lib paper_2012_10802_b200/_lib_dbg/librpd_b200.so --no-extras --steps 20 --warmup 5 --no-cpu-baseline \
     > gpurun_out/sk_$m.log 2>&1
 done
 for m in "$@"; do
