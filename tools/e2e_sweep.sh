@@ -1,0 +1,8 @@
+#!/bin/bash
+# e2e frames/s vs host threads / outputs
+for et in 16 24 32; do
+  timeout 150 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-extras --e2e-threads $et > gpurun_out/e2e_$et.log 2>&1
+  tail -1 gpurun_out/e2e_$et.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('threads $et', d['value'], d['e2e']['value'])"
+done
+timeout 150 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-extras --e2e-outputs labels > gpurun_out/e2e_l.log 2>&1
+tail -1 gpurun_out/e2e_l.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('labels only', d['value'], d['e2e']['value'])"
