@@ -133,29 +133,107 @@ struct CenterGrid {
   CRec* rec;      // nb * kBucketCap
 };
 
-// update_centers tail (segmentation.cpp:88-92) of the previous assignment's
-// sums when `finalize`, then lround positions (assign_pixels' window centres,
-// :38-41) and the bucket insert.  Also zeroes the orphan counter of the round.
+// Nearest-centre fallback of one orphan pixel (segmentation.cpp:59-71), one
+// warp: lane-strided scan of every centre, then the lexicographic (d, k)
+// minimum across the warp; lane 0 writes the label (and the sums).
+template <bool SUMS>
+__device__ __forceinline__ void fallback_pixel(int p, int w, const Centers& c, int K,
+                                               int32_t* __restrict__ labels,
+                                               const float* __restrict__ vals, CenterSums& s,
+                                               int* __restrict__ inexact) {
+  const int lane = threadIdx.x & 31;
+  const int u = p % w, v = p / w;
+  double best = __longlong_as_double(0x7FF0000000000000ll);
+  int bk = -1;
+  for (int k = lane; k < K; k += 32) {
+    const double du = double(u) - c.cu[k], dv = double(v) - c.cv[k];
+    const double d = du * du + dv * dv;
+    if (d < best) {
+      best = d;
+      bk = k;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+    const int ok = __shfl_xor_sync(0xFFFFFFFFu, bk, off);
+    if (ok >= 0 && (bk < 0 || ob < best || (ob == best && ok < bk))) {
+      best = ob;
+      bk = ok;
+    }
+  }
+  if (lane == 0 && bk >= 0) {
+    labels[p] = bk + 1;
+    if (SUMS) {
+      int bad = 0;
+      const int l = bk + 1;
+      atomicAdd(&s.n[l], 1);
+      red_add_acc(&s.sx[l], to_fixed(vals[p], &bad));
+      if (bad) atomicOr(inexact, 1);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[l]), (unsigned long long)u);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[l]), (unsigned long long)v);
+    }
+  }
+}
+
+// One SLIC round's centre step:
+//  1. the previous assignment's orphans (pixels no window covers) take their
+//     nearest centre and add their sums (assign_pixels' fallback,
+//     segmentation.cpp:59-71), when there are any;
+//  2. update_centers' tail (segmentation.cpp:88-92) of the previous
+//     assignment's sums when `finalize`, the lround window centres
+//     (:38-41) and the bucket insert for this round's assignment.
+struct Orphans {
+  const int* list;
+  int* count;
+  const float* vals;
+  int32_t* labels;
+  int w;
+  int* inexact;
+  unsigned* done;  // blocks done with the orphans (the last one finalises)
+};
+
 __global__ void k_centers(Centers c, int K, CenterSums s, int finalize, CenterGrid g, int cur,
-                          int* __restrict__ orphan_count) {
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nthreads = gridDim.x * blockDim.x;
+                          Orphans o) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  int nthreads = gridDim.x * blockDim.x;
+  const int norph = *o.count;  // written by the previous round's assignment
+  if (norph > 0) {
+    // (rare) orphans first; the LAST block to finish them then runs the
+    // whole centre step alone, so every orphan's sums are in before any
+    // centre is finalised (no co-residency needed)
+    __shared__ bool s_last;
+    const int nwarps = nthreads >> 5;
+    for (int i = tid >> 5; i < norph; i += nwarps)
+      fallback_pixel<true>(o.list[i], o.w, c, K, o.labels, o.vals, s, o.inexact);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(o.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) *o.done = 0u;  // rearmed for the next round
+    tid = threadIdx.x;
+    nthreads = blockDim.x;
+  }
   const int nb = g.nbx * g.nby;
   int* cnt_next = g.count[cur ^ 1];
   for (int b = tid; b < nb; b += nthreads) cnt_next[b] = 0;
   if (tid == 0) {
     *g.ovf[cur ^ 1] = 0;
-    *orphan_count = 0;
+    *o.count = 0;  // every block has read it (the count-0 path rewrites 0)
   }
   for (int k = tid; k < K; k += nthreads) {
     if (finalize) {
+      // L2 loads: with orphans, other blocks of this launch added to the sums
       const int l = k + 1;
-      const int n = s.n[l];
+      const int n = __ldcg(s.n + l);
       if (n > 0) {
         const double dn = double(n);
-        c.cu[k] = double(s.su[l]) / dn;
-        c.cv[k] = double(s.sv[l]) / dn;
-        c.val[k] = fixed_to_double(acc_value(s.sx[l])) / dn;
+        c.cu[k] = double(__ldcg(s.su + l)) / dn;
+        c.cv[k] = double(__ldcg(s.sv + l)) / dn;
+        const AccSum sx{__ldcg(&s.sx[l].a0), __ldcg(&s.sx[l].a1), __ldcg(&s.sx[l].a2), 0ll};
+        c.val[k] = fixed_to_double(acc_value(sx)) / dn;
       }
       s.n[l] = 0;
       s.su[l] = 0;
@@ -385,50 +463,15 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   }
 }
 
-// Nearest-centre fallback, segmentation.cpp:59-71 (one warp per pixel).
-template <bool SUMS>
+// Nearest-centre fallback of the last round's orphans (the earlier rounds'
+// run inside the next k_centers), one warp per pixel.
 __global__ void k_assign_fallback(int w, Centers c, int K, int32_t* __restrict__ labels,
-                                  const int* __restrict__ list, const int* __restrict__ count,
-                                  const float* __restrict__ vals, CenterSums s,
-                                  int* __restrict__ inexact) {
-  const int lane = threadIdx.x & 31;
+                                  const int* __restrict__ list, const int* __restrict__ count) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int n = *count;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-    const int p = list[i];
-    const int u = p % w, v = p / w;
-    double best = __longlong_as_double(0x7FF0000000000000ll);
-    int bk = -1;
-    for (int k = lane; k < K; k += 32) {
-      const double du = double(u) - c.cu[k], dv = double(v) - c.cv[k];
-      const double d = du * du + dv * dv;
-      if (d < best) {
-        best = d;
-        bk = k;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
-      const int ok = __shfl_xor_sync(0xFFFFFFFFu, bk, off);
-      if (ok >= 0 && (bk < 0 || ob < best || (ob == best && ok < bk))) {
-        best = ob;
-        bk = ok;
-      }
-    }
-    if (lane == 0 && bk >= 0) {
-      labels[p] = bk + 1;
-      if (SUMS) {
-        int bad = 0;
-        const int l = bk + 1;
-        atomicAdd(&s.n[l], 1);
-        red_add_acc(&s.sx[l], to_fixed(vals[p], &bad));
-        if (bad) atomicOr(inexact, 1);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[l]), (unsigned long long)u);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[l]), (unsigned long long)v);
-      }
-    }
-  }
+  CenterSums none{};
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps)
+    fallback_pixel<false>(list[i], w, c, K, labels, nullptr, none, nullptr);
 }
 
 // Per-label sums of (u, v, value, n) with warp run pre-aggregation.  `valid`
@@ -781,8 +824,10 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   CenterGrid grid{B, nbx, nby, {gridbuf, gridbuf + nb}, {gridbuf + 2 * nb, gridbuf + 2 * nb + 1},
                   ctx->ws.get<CRec>("slic_recs", size_t(nb) * kBucketCap)};
   int* orphan_list = ctx->ws.get<int>("slic_orphans", n);
-  int* orphan_count = ctx->ws.get<int>("slic_orphan_count", 2);
+  int* orphan_count = ctx->ws.get<int>("slic_orphan_count", 3);
   int* inexact = orphan_count + 1;
+  unsigned* orph_done = reinterpret_cast<unsigned*>(orphan_count + 2);
+  const Orphans orph{orphan_list, orphan_count, vals, labels, w, inexact, orph_done};
 
   k_values_or_zero<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(d2, n, vals);
   RPD_LAUNCH_CHECK();
@@ -790,7 +835,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_LAUNCH_CHECK();
   k_zero_sums<<<cdiv(K + 1, 256), 256, 0, st>>>(s, K + 1);
   RPD_LAUNCH_CHECK();
-  RPD_CK(cudaMemsetAsync(orphan_count, 0, 2 * sizeof(int), st));
+  RPD_CK(cudaMemsetAsync(orphan_count, 0, 3 * sizeof(int), st));
   // round 0's bucket counts and overflow flag start at zero
   RPD_CK(cudaMemsetAsync(gridbuf, 0, sizeof(int) * nb, st));
   RPD_CK(cudaMemsetAsync(grid.ovf[0], 0, sizeof(int), st));
@@ -807,7 +852,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   // assignment that accumulates the sums the next round needs.
   auto assign = [&](bool finalize, bool sums) {
     const int cur = round++ & 1;
-    k_centers<<<cblocks, 256, 0, st>>>(c, K, s, finalize ? 1 : 0, grid, cur, orphan_count);
+    k_centers<<<cblocks, 256, 0, st>>>(c, K, s, finalize ? 1 : 0, grid, cur, orph);
     RPD_LAUNCH_CHECK();
     aa.bcount = grid.count[cur];
     aa.ovf = grid.ovf[cur];
@@ -816,13 +861,10 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
     else
       k_assign_tile<false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
     RPD_LAUNCH_CHECK();
-    if (sums)
-      k_assign_fallback<true><<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list,
-                                                                  orphan_count, vals, s, inexact);
-    else
-      k_assign_fallback<false><<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list,
-                                                                   orphan_count, vals, s, inexact);
-    RPD_LAUNCH_CHECK();
+    if (!sums) {  // the last round: no k_centers follows to take its orphans
+      k_assign_fallback<<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list, orphan_count);
+      RPD_LAUNCH_CHECK();
+    }
   };
   auto update = [&]() {
     k_label_sums<<<gblocks, 256, 0, st>>>(vals, labels, h, w, K, false, true, s, inexact);
