@@ -23,6 +23,9 @@
 
 #include "sgm.cuh"
 
+// TileAddr::kStride is unused by the chunked layouts
+#pragma nv_diag_suppress 177
+
 namespace rpdg {
 
 namespace {
