@@ -309,10 +309,18 @@ struct ThresholdResult {  // segmentation.hpp:48-55
   double t_r = 0.0, t_s = 0.0, mu1 = 0.0, mu2 = 0.0, excluded_fraction = 0.0;
   bool degenerate = false;
 };
+// SLIC keeps at most its nu * nv seeds (segmentation.cpp:181-184): the
+// capacity of the centre records of slic() / detect_potholes_pipeline().
+inline int slic_seed_count(int h, int w, int p) {
+  if (h <= 0 || w <= 0 || p <= 0) return 1;
+  const int nu = std::max(1, int(std::lround(std::sqrt(double(p) * w / h))));
+  const int nv = std::max(1, int(std::lround(double(p) / nu)));
+  return std::max(1, std::min(h * w, nu * nv));
+}
 inline SuperpixelMap slic(const DisparityMap& d2, int p, double compactness, int iterations) {
   SuperpixelMap sp;
   sp.labels = LabelMap(d2.rows(), d2.cols());
-  const int cap = std::max(1, std::min(d2.rows() * d2.cols(), 4 * std::max(p, 1) + 64));
+  const int cap = slic_seed_count(d2.rows(), d2.cols(), p);
   std::vector<rpd_center> c(static_cast<size_t>(cap));
   int32_t count = 0;
   detail::check(rpd_slic(detail::ctx(), d2.ptr(), d2.rows(), d2.cols(), p, compactness,
@@ -612,7 +620,8 @@ inline DetectResult detect_potholes_pipeline(const GrayImage& left, const GrayIm
   r.d0 = r.d1 = r.d2 = r.d3 = DisparityMap(h, w);
   r.labels = LabelMap(h, w);
   r.superpixels.labels = LabelMap(h, w);
-  std::vector<rpd_center> centers(size_t(std::max(1, h * w)));
+  const int cap = slic_seed_count(h, w, cfg.superpixels);
+  std::vector<rpd_center> centers(size_t(cap), rpd_center{});
   rpd_detect_out out{};
   out.d0 = r.d0.ptr();
   out.d1 = r.d1.ptr();
@@ -625,7 +634,7 @@ inline DetectResult detect_potholes_pipeline(const GrayImage& left, const GrayIm
   detail::check(rpd_detect(detail::ctx(), left.ptr(), right.ptr(), h, w, &cfg, &out));
   r.superpixels.count = out.sp_count;
   r.superpixels.spacing = out.sp_spacing;
-  for (int k = 0; k < out.sp_count; ++k)
+  for (int k = 0; k < std::min(out.sp_count, cap); ++k)
     r.superpixels.centers.push_back({centers[size_t(k)].cu, centers[size_t(k)].cv,
                                      centers[size_t(k)].value});
   r.fit = RoadFit{{out.fit.model.a0, out.fit.model.a1, out.fit.model.phi}, out.fit.e0min,

@@ -15,6 +15,7 @@ class to the CPU oracle (oracle/_build/librpd_oracle.so) as the checker.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import dataclasses
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -220,6 +221,15 @@ _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
+
+
+def slic_seed_count(h: int, w: int, p: int) -> int:
+    """SLIC keeps at most its nu * nv seeds (segmentation.cpp:181-184)."""
+    if h <= 0 or w <= 0 or p <= 0:
+        return 1
+    nu = max(1, int(math.floor(math.sqrt(p * w / h) + 0.5)))
+    nv = max(1, int(math.floor(p / nu + 0.5)))
+    return max(1, min(h * w, nu * nv))
 
 
 def _on_device(a) -> bool:
@@ -514,7 +524,7 @@ class Context:
                 for k in ("d0", "d1", "d2", "d3")}
         bufs["labels"] = np.empty((h, w), np.int32) if "labels" in want else None
         bufs["sp_labels"] = np.empty((h, w), np.int32) if "sp_labels" in want else None
-        cap = h * w if "centers" in want else 0
+        cap = slic_seed_count(h, w, cfg.superpixels) if "centers" in want else 0
         centers = (Center * max(cap, 1))() if cap else None
         out = DetectOut()
         for k in ("d0", "d1", "d2", "d3"):
@@ -527,7 +537,7 @@ class Context:
         self._check(fn(self.handle, _ptr(left), _ptr(right), h, w, C.byref(cfg), C.byref(out)))
         cent = None
         if centers is not None:
-            cent = np.array([(c.cu, c.cv, c.value) for c in centers[:out.sp_count]],
+            cent = np.array([(c.cu, c.cv, c.value) for c in centers[:min(out.sp_count, cap)]],
                             dtype=np.float64).reshape(-1, 3)
         return DetectResult(
             d0=bufs["d0"], d1=bufs["d1"], d2=bufs["d2"], d3=bufs["d3"],
@@ -764,7 +774,7 @@ class Context:
         d2 = _f32(d2)
         h, w = d2.shape
         labels = np.empty((h, w), np.int32)
-        cap = max(1, min(h * w, 4 * max(p, 1) + 64))
+        cap = slic_seed_count(h, w, p)
         centers = (Center * cap)()
         count = C.c_int32(0)
         spacing = C.c_double(0)

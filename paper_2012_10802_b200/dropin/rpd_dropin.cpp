@@ -14,6 +14,7 @@
 // Status codes map back onto the reference's exception types.  The header-
 // only functions of perspective.hpp / evaluation.hpp stay the reference's.
 
+#include <cmath>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -331,20 +332,30 @@ PointCloud load_ply(const std::string& path) {
   return cloud;
 }
 
+// SLIC keeps at most its nu * nv seeds (segmentation.cpp:181-184): the
+// capacity of the centre records.
+int slic_seed_count(int h, int w, int p) {
+  if (h <= 0 || w <= 0 || p <= 0) return 1;
+  const int nu = std::max(1, int(std::lround(std::sqrt(double(p) * w / h))));
+  const int nv = std::max(1, int(std::lround(double(p) / nu)));
+  return std::max(1, std::min(h * w, nu * nv));
+}
+
 // ---- segmentation.hpp --------------------------------------------------------
 SuperpixelMap slic(const DisparityMap& d2, int p, double compactness, int iterations) {
   const int h = int(d2.rows()), w = int(d2.cols());
   SuperpixelMap sp;
   sp.labels = LabelMap(h, w);
-  std::vector<rpd_center> cs(size_t(std::max(1, h * w)));
+  std::vector<rpd_center> cs(size_t(slic_seed_count(h, w, p)));
   int32_t count = 0;
   double spacing = 0.0;
   check(rpd_slic(ctx(), d2.data(), h, w, p, compactness, iterations, ptr(sp.labels), cs.data(),
                  int(cs.size()), &count, &spacing));
   sp.count = count;
   sp.spacing = spacing;
-  sp.centers.resize(size_t(count));
-  for (int k = 0; k < count; ++k)
+  const int nc = std::min(count, int(cs.size()));
+  sp.centers.resize(size_t(nc));
+  for (int k = 0; k < nc; ++k)
     sp.centers[size_t(k)] = {cs[size_t(k)].cu, cs[size_t(k)].cv, cs[size_t(k)].value};
   return sp;
 }
@@ -428,7 +439,7 @@ DetectResult detect_potholes_pipeline(const GrayImage& left, const GrayImage& ri
   r.d3 = DisparityMap(h, w);
   r.labels = LabelMap(h, w);
   r.superpixels.labels = LabelMap(h, w);
-  std::vector<rpd_center> cs(size_t(std::max(1, h * w)));
+  std::vector<rpd_center> cs(size_t(slic_seed_count(h, w, config.superpixels)));
   rpd_detect_out o{};
   o.d0 = ptr(r.d0);
   o.d1 = ptr(r.d1);
@@ -444,8 +455,9 @@ DetectResult detect_potholes_pipeline(const GrayImage& left, const GrayImage& ri
   check(st);
   r.superpixels.count = o.sp_count;
   r.superpixels.spacing = o.sp_spacing;
-  r.superpixels.centers.resize(size_t(o.sp_count));
-  for (int k = 0; k < o.sp_count; ++k)
+  const int nc = std::min(o.sp_count, int(cs.size()));
+  r.superpixels.centers.resize(size_t(nc));
+  for (int k = 0; k < nc; ++k)
     r.superpixels.centers[size_t(k)] = {cs[size_t(k)].cu, cs[size_t(k)].cv, cs[size_t(k)].value};
   r.fit.model = {o.fit.model.a0, o.fit.model.a1, o.fit.model.phi};
   r.fit.e0min = o.fit.e0min;
