@@ -518,6 +518,16 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
   const int slot = J.slot0 + cta * (nseg - 1) + seg - 1;  // boundary (seg-1 | seg)
   const int tid = int(threadIdx.x);
 
+  // diagonal results are stored by the threads: byte offset of this lane's
+  // pixel of the current step, advanced by one (row, column) step at a time
+  long long doff = 0, dstep = 0;
+  if constexpr (TYPE == kDiag) {
+    const int s = stage_base;
+    doff = (long long)(dv > 0 ? s : h - 1 - s) * (long long)a.pitch +
+           (long long)(kbase + du * s + t) * (GE::WPP * 4);
+    dstep = (dv > 0 ? (long long)a.pitch : -(long long)a.pitch) + (long long)du * (GE::WPP * 4);
+  }
+
   uint32_t seq = 0;  // stages consumed by this CTA (ring slot / mbarrier parity)
   int ra = max(0, m0 - a.warm_stages);
 #pragma unroll 1
@@ -564,12 +574,11 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
 #endif
         if (TYPE == kDiag) {
           if (unsigned(col) < unsigned(w) && s < s_end) {
-            const int vrow = dv > 0 ? s : h - 1 - s;
-            uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + size_t(vrow) * a.pitch +
-                                                        size_t(col) * (GE::WPP * 4));
+            uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + doff);
 #pragma unroll
             for (int q = 0; q < WPL; ++q) dst[q] = packed[q];
           }
+          doff += dstep;
         } else if (store) {
 #pragma unroll
           for (int q = 0; q < WPL; ++q) outb[ad.at(q, rr, 0)] = packed[q];
