@@ -522,7 +522,8 @@ def gpu_arm(args, rank, world, local):
     tf = ROOT / "profiles" / "agg_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+            # per config: both aggregation launches of one frame (ncu)
+            traffic = json.loads(tf.read_text())["configs"][str(c)]["bytes_per_frame"]
         except Exception:
             traffic = None
     ops_agg = 2.0 * cfg.sgm_paths * 9.0 * sum(agg_cells)  # OPS_agg
