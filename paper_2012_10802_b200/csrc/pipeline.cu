@@ -263,9 +263,10 @@ void enqueue_frame_body(rpd_ctx* ctx, FrameBuffers& f, int h, int w, bool u8,
     record_stage(ctx, 7);
     return;
   }
-  f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations);
-  if (dup & 2) f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations);
-  pool_superpixels_dev(ctx, f.d2, f.sp.labels, h, w, f.sp.k_seeds, f.d3);
+  // slic + pool_superpixels (the pooling shares slic's final label pass)
+  f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations, f.d3);
+  if (dup & 2)
+    f.sp = slic_dev(ctx, f.d2, h, w, c.superpixels, c.compactness, c.slic_iterations, f.d3);
   record_stage(ctx, 6);
   if (skip & 4) {
     record_stage(ctx, 7);

@@ -23,8 +23,10 @@ struct SlicOut {
 };
 
 // slic, segmentation.cpp:170-229.  d2 device float H*W.
+// d3 != nullptr: pool_superpixels (segmentation.cpp:231-249) of d2 over the
+// result as well, fused into slic's final update_centers pass.
 SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double compactness,
-                 int iterations);
+                 int iterations, float* d3 = nullptr);
 
 // pool_superpixels, segmentation.cpp:231-249.  count_dev or count_host gives
 // the label range [0, count].

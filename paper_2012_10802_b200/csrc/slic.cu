@@ -476,19 +476,27 @@ __global__ void k_assign_fallback(int w, Centers c, int K, int32_t* __restrict__
 
 // Per-label sums of (u, v, value, n) with warp run pre-aggregation.  `valid`
 // restricts to valid pixels (pooling); vals may be the raw d2 then.
+// nvalid != nullptr (the pipeline's final update fused with pool_superpixels):
+// vals is the raw D2, an invalid value adds 0 (values_or_zero) and each
+// label's valid pixels are counted into nvalid — its value sum is then also
+// pool_superpixels' sum of valid D2 (segmentation.cpp:236-241).
 __global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __restrict__ labels,
                              int h, int w, int max_label, bool valid_only, bool coords,
-                             CenterSums s, int* __restrict__ inexact) {
+                             CenterSums s, int* __restrict__ inexact,
+                             int* __restrict__ nvalid = nullptr) {
   const long long n = (long long)h * w;
   const long long base = (long long)blockIdx.x * blockDim.x;
   for (long long p0 = base; p0 < n; p0 += (long long)gridDim.x * blockDim.x) {
     const long long p = p0 + threadIdx.x;
     int key = -1;
     float x = 0.0f;
+    bool valid = false;
     if (p < n) {
       const int l = labels[p];
       x = vals[p];
-      if (l >= 0 && l <= max_label && (!valid_only || x != kInvalid)) key = l;
+      valid = x != kInvalid;
+      if (nvalid && !valid) x = 0.0f;
+      if (l >= 0 && l <= max_label && (!valid_only || valid)) key = l;
     }
     // (v, u) of this lane from one division per warp
     const long long pw = p0 + (threadIdx.x & ~31u);
@@ -503,11 +511,19 @@ __global__ void k_label_sums(const float* __restrict__ vals, const int32_t* __re
     const int cnt = ri.end - int(threadIdx.x & 31) + 1;
     const long long su = (long long)cnt * u + (long long)cnt * (cnt - 1) / 2;
     const long long sv = (long long)cnt * v;
+    unsigned vmask = 0u;
+    if (nvalid) vmask = __ballot_sync(0xFFFFFFFFu, valid && key >= 0);
     if (ri.head) {
       atomicAdd(&s.n[key], cnt);
       if (coords) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[key]), (unsigned long long)su);
         atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[key]), (unsigned long long)sv);
+      }
+      if (nvalid) {  // valid lanes of the run [lane, end]
+        const int lane = int(threadIdx.x & 31);
+        const unsigned run = (ri.end == 31 ? 0xFFFFFFFFu : ((2u << ri.end) - 1u)) & ~((1u << lane) - 1u);
+        const int nv = __popc(vmask & run);
+        if (nv) atomicAdd(&nvalid[key], nv);
       }
     }
   }
@@ -763,10 +779,11 @@ __global__ void k_centers_out(Centers c, const CenterSums s, const int* __restri
 
 // pool_superpixels tail: D3(p) = float(sum / n) of its label or invalid.
 // Pooled value per label (pool_superpixels, segmentation.cpp:236-246), once per label.
-__global__ void k_pool_values(CenterSums s, int max_label, float* __restrict__ val) {
+__global__ void k_pool_values(CenterSums s, int max_label, float* __restrict__ val,
+                              const int* __restrict__ nvalid = nullptr) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l > max_label) return;
-  const int c = s.n[l];
+  const int c = nvalid ? nvalid[l] : s.n[l];
   val[l] = c > 0 ? float(fixed_to_double(acc_value(s.sx[l])) / double(c)) : kInvalid;
 }
 
@@ -793,7 +810,8 @@ static void scan_flags(rpd_ctx* ctx, const int* flags, int* pos, long long n, co
   RPD_LAUNCH_CHECK();
 }
 
-SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, int iterations) {
+SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, int iterations,
+                 float* d3) {
   if (p < 4) throw InvalidArg("slic: p must be >= 4");
   if ((long long)p > (long long)w * h) throw InvalidArg("slic: p exceeds pixel count");
   cudaStream_t st = ctx->stream;
@@ -921,7 +939,23 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_CK(cudaMemsetAsync(c.cu, 0, sizeof(double) * K, st));
   RPD_CK(cudaMemsetAsync(c.cv, 0, sizeof(double) * K, st));
   RPD_CK(cudaMemsetAsync(c.val, 0, sizeof(double) * K, st));
-  update();
+  if (d3) {
+    // one label pass for update_centers and pool_superpixels: the same value
+    // sums (invalid D2 adds 0 to both), the pooled mean over the valid count
+    int* nvalid = ctx->ws.get<int>("slic_nvalid", K + 1);
+    RPD_CK(cudaMemsetAsync(nvalid, 0, sizeof(int) * (K + 1), st));
+    k_label_sums<<<gblocks, 256, 0, st>>>(d2, labels, h, w, K, false, true, s, inexact, nvalid);
+    RPD_LAUNCH_CHECK();
+    float* pval = ctx->ws.get<float>("pool_val", K + 1);
+    k_pool_values<<<cdiv(K + 1, 256), 256, 0, st>>>(s, K, pval, nvalid);
+    RPD_LAUNCH_CHECK();
+    k_pool_write<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(labels, pval, n, K, d3);
+    RPD_LAUNCH_CHECK();
+    k_center_finalize<<<cdiv(K, 256), 256, 0, st>>>(s, c, K);
+    RPD_LAUNCH_CHECK();
+  } else {
+    update();
+  }
   double* cout = ctx->ws.get<double>("slic_centers_out", 3 * size_t(K));
   k_centers_out<<<cdiv(K, 128), 128, 0, st>>>(c, s, count, K, cout);
   RPD_LAUNCH_CHECK();
