@@ -392,25 +392,24 @@ __device__ __forceinline__ Acc128 to_fixed(float x, int* inexact) {
 
 // Warp run sum of `x` (per contiguous key run, see run_info) added to the
 // run's AccSum by its head lane.  Fast path when every participating value is
-// 0 or has an exponent field in [110, 140] (2^-17 <= |x| < 2^14): then x * 2^40
-// is an exact int64 below 2^54 and a run of <= 32 of them stays below 2^59, so
-// the run is summed in one 64-bit word and lands in the accumulator as
-// s * 2^60 (a1 and a2 words; its a0 part is zero).  Otherwise the 128-bit
-// fixed-point path.  Both give the same exact total.
+// 0 or has an exponent field in [117, 140] (2^-10 <= |x| < 2^14): such values
+// are multiples of 2^-33 below 2^14, so every partial sum of <= 32 of them is
+// a multiple of 2^-33 below 2^19 — 52 significant bits — and the run is summed
+// EXACTLY in double (one DADD per step); the head converts it to the integer
+// s = sum * 2^40 (< 2^59) that lands in the accumulator as s * 2^60 (a1 and
+// a2 words; its a0 part is zero).  Otherwise the 128-bit fixed-point path.
+// Both give the same exact total.
 __device__ __forceinline__ void run_add_value(AccSum* sx, int key, bool active, float x,
                                               const RunInfo& ri, int* inexact) {
   const uint32_t b = __float_as_uint(x);
   const int e = int((b >> 23) & 0xFFu);
   const bool zero = !active || (b << 1) == 0u;
-  const bool fast = zero || (e >= 110 && e <= 140);
+  const bool fast = zero || (e >= 117 && e <= 140);
   if (__all_sync(0xFFFFFFFFu, fast)) {
-    long long v = 0;
-    if (!zero) {
-      v = (long long)((b & 0x7FFFFFu) | 0x800000u) << (e - 110);
-      if (b >> 31) v = -v;
-    }
-    v = run_sum(v, ri);
+    double d = zero ? 0.0 : double(x);
+    d = run_sum(d, ri);
     if (ri.head) {
+      const long long v = __double2ll_rz(d * 1099511627776.0);  // exact: d * 2^40
       const unsigned long long a1 = ((unsigned long long)v << 60) >> 32;
       if (a1) atomicAdd(&sx[key].a1, a1);
       atomicAdd(reinterpret_cast<unsigned long long*>(&sx[key].a2), (unsigned long long)(v >> 4));
