@@ -168,11 +168,7 @@ long long reproject_impl(rpd_ctx* ctx, const float* d1, const int32_t* labels, i
   const int blocks = int(std::min<long long>((n + 255) / 256, ctx->sm_count * 16));
   k_reproj_flags<<<blocks, 256, 0, st>>>(dd, dl, label, n, flags);
   RPD_LAUNCH_CHECK();
-  size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flags, pos, int(n), st);
-  void* tmp = ctx->ws.get<uint8_t>("rp_cub", tmp_bytes);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flags, pos, int(n), st);
-  RPD_LAUNCH_CHECK();
+  scan_exclusive_i32(ctx, flags, pos, n);
   k_reproj_scatter<<<blocks, 256, 0, st>>>(dd, flags, pos, w, n, rig, cap, dout, count);
   RPD_LAUNCH_CHECK();
   long long hc = 0;

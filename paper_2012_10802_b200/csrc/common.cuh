@@ -236,6 +236,9 @@ struct rpd_ctx {
   int last_agg_kernel = 0;  // rpdg::AggImpl of the last aggregation
   void* agg_flags_zeroed = nullptr;  // segmented aggregation: flag buffer known to be zero
   int agg_flags_words = 0;
+  void* scan_zeroed = nullptr;          // scan descriptors known to be zero (scan.cu)
+  long long scan_zeroed_tiles = 0;
+  void* scan_ctl_zeroed = nullptr;
   int agg_segmented_ctas = 0;                  // last aggregation launch
   unsigned long long* agg_reruns = nullptr;    // device counter (workspace)
 };
@@ -252,5 +255,7 @@ void pipeline_forget(rpd_ctx* ctx);           // releases captured graphs
 // Records `ev` on ctx->stream; inside a stream capture it becomes an external
 // event-record node so the event is really recorded on every graph replay.
 void record_event(rpd_ctx* ctx, cudaEvent_t ev);
+// out[i] = in[0] + ... + in[i-1] on ctx->stream, one launch (scan.cu).
+void scan_exclusive_i32(rpd_ctx* ctx, const int* in, int* out, long long n);
 
 }  // namespace rpdg

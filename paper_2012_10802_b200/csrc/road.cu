@@ -217,11 +217,7 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
   int* total = ctx->ws.get<int>("so_total", 1);
   k_sample_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(d1, h, w, r, flags);
   RPD_LAUNCH_CHECK();
-  size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flags, pos, int(n), st);
-  void* tmp = ctx->ws.get<uint8_t>("so_cub", tmp_bytes);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flags, pos, int(n), st);
-  RPD_LAUNCH_CHECK();
+  scan_exclusive_i32(ctx, flags, pos, n);
   k_sample_scatter<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(flags, pos, n, list, total);
   RPD_LAUNCH_CHECK();
   const long long gmax = std::min<long long>(cap, n);

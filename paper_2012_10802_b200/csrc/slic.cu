@@ -802,12 +802,8 @@ __global__ void k_pool_write(const int32_t* __restrict__ labels, const float* __
 
 }  // namespace
 
-static void scan_flags(rpd_ctx* ctx, const int* flags, int* pos, long long n, const char* tag) {
-  size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flags, pos, int(n), ctx->stream);
-  void* tmp = ctx->ws.get<uint8_t>(std::string("cub_scan_") + tag, tmp_bytes);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flags, pos, int(n), ctx->stream);
-  RPD_LAUNCH_CHECK();
+static void scan_flags(rpd_ctx* ctx, const int* flags, int* pos, long long n, const char*) {
+  scan_exclusive_i32(ctx, flags, pos, n);
 }
 
 SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, int iterations,
