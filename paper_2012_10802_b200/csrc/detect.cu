@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include "ccl.cuh"
+#include "scan.cuh"
 
 namespace rpdg {
 
@@ -397,18 +398,18 @@ __global__ void __launch_bounds__(kThrThreads) k_threshold(const __grid_constant
 // ------------------------------------------------------------ labelling ----
 // Elementwise passes take four pixels per thread (one 16-byte access per
 // array; workspace buffers are 256-byte aligned), launched with ew4_blocks(n).
-__global__ void k_root_flags(const int* __restrict__ parent, const unsigned char* __restrict__ keep,
-                             long long n, int* __restrict__ flags) {
-  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
-  if (p0 + 3 < n) {
-    const int4 r = *reinterpret_cast<const int4*>(parent + p0);
-    const uchar4 k = keep ? *reinterpret_cast<const uchar4*>(keep + p0) : make_uchar4(1, 1, 1, 1);
-    *reinterpret_cast<int4*>(flags + p0) =
-        make_int4(r.x == p0 && k.x, r.y == p0 + 1 && k.y, r.z == p0 + 2 && k.z, r.w == p0 + 3 && k.w);
-    return;
+// Root flag of pixel p (a kept component's representative): parent[p] == p.
+struct RootFlagIn {
+  const int* parent;
+  const unsigned char* keep;  // nullptr: every component
+  __device__ __forceinline__ void load8(long long base, long long n, int (&f)[8]) const {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long p = base + k;
+      f[k] = p < n && parent[p] == p && (!keep || keep[p]) ? 1 : 0;
+    }
   }
-  for (long long p = p0; p < min(n, p0 + 4); ++p) flags[p] = (parent[p] == p && (!keep || keep[p])) ? 1 : 0;
-}
+};
 
 __global__ void k_root_relabel(const int* __restrict__ parent,
                                const unsigned char* __restrict__ keep,
@@ -423,10 +424,6 @@ __global__ void k_root_relabel(const int* __restrict__ parent,
   for (long long p = p0; p < min(n, p0 + 4); ++p) out[p] = lab(parent[p]);
 }
 
-__global__ void k_total_from_scan(const int* __restrict__ flags, const int* __restrict__ pos,
-                                  long long n, int* __restrict__ total) {
-  *total = n > 0 ? pos[n - 1] + flags[n - 1] : 0;
-}
 
 __global__ void k_detect_mask(const float* __restrict__ d3, long long n,
                               const rpd_threshold* __restrict__ thr, int32_t* __restrict__ mask) {
@@ -505,9 +502,6 @@ __global__ void k_detect_keep(const int* __restrict__ parent, const int* __restr
 
 }  // namespace
 
-static void scan_flags_d(rpd_ctx* ctx, const int* flags, int* pos, long long n, const char*) {
-  scan_exclusive_i32(ctx, flags, pos, n);
-}
 
 namespace {
 __global__ void k_hist_init(long long* meta) {
@@ -657,12 +651,9 @@ void connected_components_dev(rpd_ctx* ctx, const int32_t* mask, int h, int w, i
   cudaStream_t st = ctx->stream;
   const long long n = (long long)h * w;
   int* parent = ctx->ws.get<int>("ccl_parent", n);
-  int* flags = ctx->ws.get<int>("ccl_flags", n);
   int* pos = ctx->ws.get<int>("ccl_pos", n);
   uf_label(SameMask{mask}, h, w, connectivity == 4 ? 0 : 1, parent, ctx->sm_count, st);
-  k_root_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, nullptr, n, flags);
-  RPD_LAUNCH_CHECK();
-  scan_flags_d(ctx, flags, pos, n, "ccl");
+  scan_exclusive(ctx, RootFlagIn{parent, nullptr}, pos, n);
   k_root_relabel<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, nullptr, pos, n, out);
   RPD_LAUNCH_CHECK();
 }
@@ -680,7 +671,6 @@ void detect_potholes_dev(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels
   unsigned char* border = ctx->ws.get<unsigned char>("det_border", n);
   unsigned char* keep = ctx->ws.get<unsigned char>("det_keep", n);
   int* nsp = ctx->ws.get<int>("det_nsp", n);
-  int* flags = ctx->ws.get<int>("det_flags", n);
   int* pos = ctx->ws.get<int>("det_pos", n);
   unsigned long long tsize = 1024;
   while (tsize < 2ull * (unsigned long long)n) tsize <<= 1;
@@ -700,15 +690,9 @@ void detect_potholes_dev(rpd_ctx* ctx, const float* d3, const int32_t* sp_labels
   k_detect_keep<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, area, border, nsp, n, min_area, min_superpixels,
                                          keep);
   RPD_LAUNCH_CHECK();
-  k_root_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, keep, n, flags);
-  RPD_LAUNCH_CHECK();
-  scan_flags_d(ctx, flags, pos, n, "det");
+  scan_exclusive(ctx, RootFlagIn{parent, keep}, pos, n, n_out);
   k_root_relabel<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(parent, keep, pos, n, out);
   RPD_LAUNCH_CHECK();
-  if (n_out) {
-    k_total_from_scan<<<1, 1, 0, st>>>(flags, pos, n, n_out);
-    RPD_LAUNCH_CHECK();
-  }
 }
 
 }  // namespace rpdg

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "road.cuh"
+#include "scan.cuh"
 
 
 namespace rpdg {
@@ -138,48 +139,42 @@ struct RoiPred {
   int u0, v0, u1, v1;
 };
 
-__global__ void k_sample_flags(const float* __restrict__ d1, int h, int w, RoiPred r,
-                               int* __restrict__ flags) {
+
+// Sample flag of pixel p (road_geometry.cpp:112-117): in the ROI and a valid
+// disparity.  load8 feeds the scan; the scatter re-evaluates it.
+struct SampleFlagIn {
+  const float* d1;
+  int w;
+  RoiPred r;
+  __device__ __forceinline__ int at(int u, int v, long long p) const {
+    return (u >= r.u0 && u < r.u1 && v >= r.v0 && v < r.v1 && d1[p] != kInvalid) ? 1 : 0;
+  }
+  __device__ __forceinline__ void load8(long long base, long long n, int (&f)[8]) const {
+    int v = int(base / w), u = int(base - (long long)v * w);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      f[k] = base + k < n ? at(u, v, base + k) : 0;
+      if (++u == w) {
+        u = 0;
+        ++v;
+      }
+    }
+  }
+};
+
+__global__ void k_sample_scatter(const SampleFlagIn in, const int* __restrict__ pos, long long n,
+                                 int* __restrict__ list) {
   // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
-  const long long n = (long long)h * w;
   const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
   if (p0 >= n) return;
-  int v = int(p0 / w), u = int(p0 - (long long)v * w);
-  int f[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const long long p = p0 + k;
-    f[k] = (p < n && u >= r.u0 && u < r.u1 && v >= r.v0 && v < r.v1 && d1[p] != kInvalid) ? 1 : 0;
-    if (++u == w) {
+  int v = int(p0 / in.w), u = int(p0 - (long long)v * in.w);
+  for (long long p = p0; p < min(n, p0 + 4); ++p) {
+    if (in.at(u, v, p)) list[pos[p]] = int(p);
+    if (++u == in.w) {
       u = 0;
       ++v;
     }
   }
-  if (p0 + 3 < n) {
-    *reinterpret_cast<int4*>(flags + p0) = make_int4(f[0], f[1], f[2], f[3]);
-  } else {
-    for (int k = 0; p0 + k < n; ++k) flags[p0 + k] = f[k];
-  }
-}
-
-__global__ void k_sample_scatter(const int* __restrict__ flags, const int* __restrict__ pos,
-                                 long long n, int* __restrict__ list, int* __restrict__ total) {
-  // four pixels per thread (launched with max(1, cdiv(n, 1024)) blocks of 256)
-  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
-  if (p0 + 3 < n) {
-    const int4 f = *reinterpret_cast<const int4*>(flags + p0);
-    if (f.x | f.y | f.z | f.w) {
-      const int4 q = *reinterpret_cast<const int4*>(pos + p0);
-      if (f.x) list[q.x] = int(p0);
-      if (f.y) list[q.y] = int(p0 + 1);
-      if (f.z) list[q.z] = int(p0 + 2);
-      if (f.w) list[q.w] = int(p0 + 3);
-    }
-  } else {
-    for (long long p = p0; p < n; ++p)
-      if (flags[p]) list[pos[p]] = int(p);
-  }
-  if (p0 <= n - 1 && n - 1 < p0 + 4) *total = pos[n - 1] + flags[n - 1];
 }
 
 // road_geometry.cpp:119-133: k = min(n, cap); obs_i = valid[floor(i*n/k)].
@@ -211,14 +206,13 @@ void sample_observations_dev(rpd_ctx* ctx, const float* d1, int h, int w, const 
   }
   cudaStream_t st = ctx->stream;
   const long long n = (long long)h * w;
-  int* flags = ctx->ws.get<int>("so_flags", n);
   int* pos = ctx->ws.get<int>("so_pos", n);
   int* list = ctx->ws.get<int>("so_list", n);
   int* total = ctx->ws.get<int>("so_total", 1);
-  k_sample_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(d1, h, w, r, flags);
-  RPD_LAUNCH_CHECK();
-  scan_exclusive_i32(ctx, flags, pos, n);
-  k_sample_scatter<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(flags, pos, n, list, total);
+  // flags -> scan (+ total) -> scatter, the flags evaluated in place
+  const SampleFlagIn in{d1, w, r};
+  scan_exclusive(ctx, in, pos, n, total);
+  k_sample_scatter<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(in, pos, n, list);
   RPD_LAUNCH_CHECK();
   const long long gmax = std::min<long long>(cap, n);
   k_sample_gather<<<std::max(1, cdiv(gmax, 256)), 256, 0, st>>>(

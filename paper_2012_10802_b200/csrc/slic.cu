@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include "ccl.cuh"
+#include "scan.cuh"
 
 namespace rpdg {
 
@@ -326,7 +327,7 @@ static_assert(kTileV % kAssignWarps == 0, "whole tile rows per warp");
 template <bool SUMS>
 __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
-  __shared__ int s_cnt, s_nrows, s_rs[8], s_rb[9];
+  __shared__ int s_cnt;
   __shared__ int s_rowcnt[kTileV];
   // candidate c: s_cd[2c] = (cu, cv), s_cd[2c+1] = (val, icu | k << 32)
   __shared__ double2 s_cd[2 * kMaxTileCenters];
@@ -729,18 +730,16 @@ __global__ void k_label_minidx(const int32_t* __restrict__ labels, long long n,
   }
 }
 
-__global__ void k_first_flags(const int32_t* __restrict__ labels, const int* __restrict__ minidx,
-                              long long n, int* __restrict__ flags) {
-  const long long p0 = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
-  if (p0 + 3 < n) {
-    const int4 l = *reinterpret_cast<const int4*>(labels + p0);
-    const int q = int(p0);
-    *reinterpret_cast<int4*>(flags + p0) =
-        make_int4(minidx[l.x] == q, minidx[l.y] == q + 1, minidx[l.z] == q + 2, minidx[l.w] == q + 3);
-    return;
+// First-appearance flag of pixel p: the label's minimum raster index is p.
+struct FirstFlagIn {
+  const int32_t* labels;
+  const int* minidx;
+  __device__ __forceinline__ void load8(long long base, long long n, int (&f)[8]) const {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      f[k] = base + k < n ? (minidx[labels[base + k]] == int(base + k) ? 1 : 0) : 0;
   }
-  for (long long p = p0; p < min(n, p0 + 4); ++p) flags[p] = minidx[labels[p]] == int(p) ? 1 : 0;
-}
+};
 
 __global__ void k_relabel(int32_t* __restrict__ labels, const int* __restrict__ minidx,
                           const int* __restrict__ rank, long long n) {
@@ -755,10 +754,6 @@ __global__ void k_relabel(int32_t* __restrict__ labels, const int* __restrict__ 
   for (long long p = p0; p < min(n, p0 + 4); ++p) labels[p] = rank[minidx[labels[p]]] + 1;
 }
 
-__global__ void k_count_from_scan(const int* __restrict__ flags, const int* __restrict__ pos,
-                                  long long n, int* __restrict__ count) {
-  *count = pos[n - 1] + flags[n - 1];
-}
 
 __global__ void k_fill_int(int* p, int v, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -924,11 +919,8 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   RPD_LAUNCH_CHECK();
   k_label_minidx<<<gblocks, 256, 0, st>>>(labels, n, minidx);
   RPD_LAUNCH_CHECK();
-  k_first_flags<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(labels, minidx, n, flags);
-  RPD_LAUNCH_CHECK();
-  scan_flags(ctx, flags, pos, n, "first");
-  k_count_from_scan<<<1, 1, 0, st>>>(flags, pos, n, count);
-  RPD_LAUNCH_CHECK();
+  // first-appearance flags evaluated inside the scan; its total is the count
+  scan_exclusive(ctx, FirstFlagIn{labels, minidx}, pos, n, count);
   k_relabel<<<std::max(1, cdiv(n, 1024)), 256, 0, st>>>(labels, minidx, pos, n);
   RPD_LAUNCH_CHECK();
   // final update_centers over the compacted labels (centres start at zero)
