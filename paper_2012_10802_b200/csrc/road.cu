@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "road.cuh"
+#include "sincos_table.cuh"
 #include "scan.cuh"
 
 
@@ -71,39 +72,48 @@ __constant__ double c_sin_hi[kTaylorTerms] = {1.0, -0.16666666666666666, 0.00833
 __constant__ double c_sin_lo[kTaylorTerms] = {0.0, -9.25185853854297e-18, 1.1564823173178714e-19, -1.7209558293420705e-22, -1.858393274046472e-22, 1.448814070935912e-24, 1.2585294588752098e-26, -7.03872877733453e-30, 1.6508842730861433e-31, -2.2141894119604265e-34, -1.3643503830087908e-36, 8.843177655482344e-40, -1.9330404233703465e-42, -1.4303150396787322e-45, 1.0498015412959506e-47, -5.586290567888806e-51, -6.09957445788454e-54, -3.202295548645562e-57};
 __constant__ double c_cos_hi[kTaylorTerms] = {1.0, -0.5, 0.041666666666666664, -0.001388888888888889, 2.48015873015873e-05, -2.755731922398589e-07, 2.08767569878681e-09, -1.1470745597729725e-11, 4.779477332387385e-14, -1.5619206968586225e-16, 4.110317623312165e-19, -8.896791392450574e-22, 1.6117375710961184e-24, -2.4795962632247976e-27, 3.279889237069838e-30, -3.7699876288159054e-33, 3.8003907548547434e-36, -3.387157535521162e-39};
 __constant__ double c_cos_lo[kTaylorTerms] = {0.0, 0.0, 2.3129646346357427e-18, 5.300543954373577e-20, 2.1511947866775882e-23, -2.3767714622250297e-23, -1.20734505911326e-25, -2.0655512752830745e-28, 4.399205485834081e-31, -1.1910679660273754e-32, 1.4412973378659527e-36, 7.911402614872376e-38, -3.6846573564509766e-41, 1.2953730964765229e-43, 1.5117542744029879e-46, -2.5870347832750324e-49, 1.7457158024652518e-52, -5.09056148151085e-56};
-// sin/cos of a_k = k/64 as double-double (generated offline with 60-digit
-// decimal arithmetic).
-constexpr int kSinTabHalf = 48;  // a_k = k/64, k in [-48, 48]
-__device__ const double c_tab_sin_hi[97] = {-0.6816387600233341, -0.6701233804731629, -0.6584443999105676, -0.6466046695911524, -0.6346070800152693, -0.6224545602223437, -0.6101500770757914, -0.5976966345387015, -0.5850972729404622, -0.5723550682345072, -0.5594731312473669, -0.5464546069192036, -0.5333026735360201, -0.520020541953727, -0.5066114548142574, -0.49307868575392305, -0.479425538604203, -0.46565534658516017, -0.4517714714916838, -0.4377773028727551, -0.42367625720393803, -0.40947177705329507, -0.39516733024093426, -0.38076640899239017, -0.36627252908604757, -0.3516892289948141, -0.33702006902225307, -0.3222686304333866, -0.30743851458038085, -0.29253334202332754, -0.2775567516463363, -0.2625123997691533, -0.24740395925452294, -0.23223511861151147, -0.21700958109501015, -0.2017310638016388, -0.18640329676226988, -0.17103002203139503, -0.15561499277355603, -0.1401619723470637, -0.12467473338522769, -0.10915705687532236, -0.09361273123551289, -0.07804555138996731, -0.0624593178423802, -0.04685783574813424, -0.03124491398532608, -0.015624364224883372, 0.0, 0.015624364224883372, 0.03124491398532608, 0.04685783574813424, 0.0624593178423802, 0.07804555138996731, 0.09361273123551289, 0.10915705687532236, 0.12467473338522769, 0.1401619723470637, 0.15561499277355603, 0.17103002203139503, 0.18640329676226988, 0.2017310638016388, 0.21700958109501015, 0.23223511861151147, 0.24740395925452294, 0.2625123997691533, 0.2775567516463363, 0.29253334202332754, 0.30743851458038085, 0.3222686304333866, 0.33702006902225307, 0.3516892289948141, 0.36627252908604757, 0.38076640899239017, 0.39516733024093426, 0.40947177705329507, 0.42367625720393803, 0.4377773028727551, 0.4517714714916838, 0.46565534658516017, 0.479425538604203, 0.49307868575392305, 0.5066114548142574, 0.520020541953727, 0.5333026735360201, 0.5464546069192036, 0.5594731312473669, 0.5723550682345072, 0.5850972729404622, 0.5976966345387015, 0.6101500770757914, 0.6224545602223437, 0.6346070800152693, 0.6466046695911524, 0.6584443999105676, 0.6701233804731629, 0.6816387600233341};
-__device__ const double c_tab_sin_lo[97] = {-4.410467313197903e-17, -6.183536725574959e-18, 3.7736386700306717e-17, -4.567647714393289e-19, 3.4568582392624965e-17, 6.049035765709707e-18, 1.479826990758988e-17, -5.450323593054385e-17, 5.4883972461161805e-17, -2.6575872357215316e-17, -1.575565514488728e-17, -8.399754840929507e-18, -5.129318115032044e-17, 3.983266745698455e-17, 3.269413423618168e-17, -5.605083973871755e-18, 5.103969860556013e-18, -1.459870391051426e-17, 8.234073942098903e-18, -7.64345629962023e-18, 2.331800700068871e-17, 5.679403000091266e-18, 1.9613487871414228e-17, -2.1372528646211374e-17, 9.938814562106524e-18, 2.5616208736069942e-17, -1.0312279860787216e-17, -2.093773358126606e-17, -1.1004366442765296e-19, -7.516944930327352e-18, -1.7674070262791822e-17, 2.2534597527902125e-17, 7.53102495590706e-18, 8.318080852687206e-18, -1.1170071073364376e-17, -5.587232815460113e-18, -2.3493796901281573e-18, 9.954774726452923e-18, -8.886053372342288e-18, 9.946847113883478e-18, 2.925947496057858e-18, -6.6284699502736666e-18, -1.4628632005878733e-18, 5.449443782005793e-18, 2.040259504585711e-18, 2.3419368365610254e-18, 1.562781562225433e-18, 1.2650937552759816e-19, 0.0, -1.2650937552759816e-19, -1.562781562225433e-18, -2.3419368365610254e-18, -2.040259504585711e-18, -5.449443782005793e-18, 1.4628632005878733e-18, 6.6284699502736666e-18, -2.925947496057858e-18, -9.946847113883478e-18, 8.886053372342288e-18, -9.954774726452923e-18, 2.3493796901281573e-18, 5.587232815460113e-18, 1.1170071073364376e-17, -8.318080852687206e-18, -7.53102495590706e-18, -2.2534597527902125e-17, 1.7674070262791822e-17, 7.516944930327352e-18, 1.1004366442765296e-19, 2.093773358126606e-17, 1.0312279860787216e-17, -2.5616208736069942e-17, -9.938814562106524e-18, 2.1372528646211374e-17, -1.9613487871414228e-17, -5.679403000091266e-18, -2.331800700068871e-17, 7.64345629962023e-18, -8.234073942098903e-18, 1.459870391051426e-17, -5.103969860556013e-18, 5.605083973871755e-18, -3.269413423618168e-17, -3.983266745698455e-17, 5.129318115032044e-17, 8.399754840929507e-18, 1.575565514488728e-17, 2.6575872357215316e-17, -5.4883972461161805e-17, 5.450323593054385e-17, -1.479826990758988e-17, -6.049035765709707e-18, -3.4568582392624965e-17, 4.567647714393289e-19, -3.7736386700306717e-17, 6.183536725574959e-18, 4.410467313197903e-17};
-__device__ const double c_tab_cos_hi[97] = {0.7316888688738209, 0.7422497254585013, 0.7526293724180665, 0.7628252757105762, 0.7728349461524715, 0.7826559400262728, 0.7922858596771786, 0.8017223540984184, 0.8109631195052179, 0.820005899897234, 0.8288484876093257, 0.8374887238505236, 0.8459244992310679, 0.8541537542773854, 0.8621744799348805, 0.8699847180584174, 0.8775825618903728, 0.8849661565261433, 0.8921336993669944, 0.8990834405601384, 0.9058136834259364, 0.9123227848721178, 0.9186091557949183, 0.924671261467036, 0.9305076219123143, 0.9361168122670553, 0.9414974631278811, 0.9466482608860534, 0.9515679480481722, 0.9562553235431753, 0.9607092430155619, 0.964928619104771, 0.9689124217106447, 0.9726596782449127, 0.9761694738686353, 0.9794409517155483, 0.9824733131012553, 0.9852658177182139, 0.9878177838164719, 0.9901285883701071, 0.992197667229329, 0.9940245152582091, 0.9956086864580017, 0.9969497940760287, 0.9980475107000991, 0.9989015683384429, 0.9995117584851364, 0.9998779321710066, 1.0, 0.9998779321710066, 0.9995117584851364, 0.9989015683384429, 0.9980475107000991, 0.9969497940760287, 0.9956086864580017, 0.9940245152582091, 0.992197667229329, 0.9901285883701071, 0.9878177838164719, 0.9852658177182139, 0.9824733131012553, 0.9794409517155483, 0.9761694738686353, 0.9726596782449127, 0.9689124217106447, 0.964928619104771, 0.9607092430155619, 0.9562553235431753, 0.9515679480481722, 0.9466482608860534, 0.9414974631278811, 0.9361168122670553, 0.9305076219123143, 0.924671261467036, 0.9186091557949183, 0.9123227848721178, 0.9058136834259364, 0.8990834405601384, 0.8921336993669944, 0.8849661565261433, 0.8775825618903728, 0.8699847180584174, 0.8621744799348805, 0.8541537542773854, 0.8459244992310679, 0.8374887238505236, 0.8288484876093257, 0.820005899897234, 0.8109631195052179, 0.8017223540984184, 0.7922858596771786, 0.7826559400262728, 0.7728349461524715, 0.7628252757105762, 0.7526293724180665, 0.7422497254585013, 0.7316888688738209};
-__device__ const double c_tab_cos_lo[97] = {-1.0475824306512768e-17, -1.2339303604869521e-17, -1.2970993013150526e-17, 1.6672995021546628e-17, 4.231014921891023e-17, -1.474071641211487e-17, -2.9049779312834576e-17, 4.0134533311087014e-17, -3.091333486122179e-17, -3.912431748209128e-17, 1.1163935406617444e-17, 4.3337026043948396e-17, 1.549506647350329e-17, 5.420565102675286e-18, 4.4132427578105805e-18, 1.657385110740923e-17, -4.2623149864279997e-17, -7.690557775987357e-18, 2.3160655211380166e-17, 9.076951775075616e-18, 4.2864666490805214e-17, 2.6349040211413332e-17, -4.0564150104514996e-17, 5.5444125388034563e-17, 4.488760003328074e-18, -5.2350302039683216e-17, -4.8523830236797095e-18, -3.911683334934152e-17, -3.8614834675674123e-17, -3.148450868841629e-17, -2.807827063516729e-17, -3.0345542681018625e-18, 5.071436662403936e-17, 2.3920264546490165e-17, -7.850690609285027e-18, 1.3108769521526758e-17, -3.919920375420088e-17, -4.925721262944555e-17, 4.91917302237681e-17, -4.589906353553811e-18, 4.754870575189364e-17, 1.3287985046260087e-17, 3.312922430932991e-17, -1.2467075728553626e-17, 3.3232291674141346e-17, -2.1425557800399754e-17, -3.418806487972947e-17, 3.216122229972341e-17, 0.0, 3.216122229972341e-17, -3.418806487972947e-17, -2.1425557800399754e-17, 3.3232291674141346e-17, -1.2467075728553626e-17, 3.312922430932991e-17, 1.3287985046260087e-17, 4.754870575189364e-17, -4.589906353553811e-18, 4.91917302237681e-17, -4.925721262944555e-17, -3.919920375420088e-17, 1.3108769521526758e-17, -7.850690609285027e-18, 2.3920264546490165e-17, 5.071436662403936e-17, -3.0345542681018625e-18, -2.807827063516729e-17, -3.148450868841629e-17, -3.8614834675674123e-17, -3.911683334934152e-17, -4.8523830236797095e-18, -5.2350302039683216e-17, 4.488760003328074e-18, 5.5444125388034563e-17, -4.0564150104514996e-17, 2.6349040211413332e-17, 4.2864666490805214e-17, 9.076951775075616e-18, 2.3160655211380166e-17, -7.690557775987357e-18, -4.2623149864279997e-17, 1.657385110740923e-17, 4.4132427578105805e-18, 5.420565102675286e-18, 1.549506647350329e-17, 4.3337026043948396e-17, 1.1163935406617444e-17, -3.912431748209128e-17, -3.091333486122179e-17, 4.0134533311087014e-17, -2.9049779312834576e-17, -1.474071641211487e-17, 4.231014921891023e-17, 1.6672995021546628e-17, -1.2970993013150526e-17, -1.2339303604869521e-17, -1.0475824306512768e-17};
 }  // namespace
 
 // Correctly rounded sin/cos (with overwhelming probability).  Fast path for
-// the roll angles (|x| <= 0.75): x = a_k + r with a_k = k/64 (r exact by
-// Sterbenz, |r| <= 1/128), an 8-term double-double Taylor series for r and the
-// addition formulas with tabulated double-double sin/cos(a_k).  Otherwise:
-// reduction by pi/2 and an 18-term series.
+// the roll angles (|x| <= 0.75): x = a_k + r with a_k = k/256 (r exact,
+// |r| <= 2^-9).  sin(r) = r - r^3/6 + O(r^5) and cos(r) = 1 - r^2/2 + O(r^4):
+// the leading terms in double-double from the exact r^2 = p + e (two_prod),
+// the tails (< 2^-38 |r| and < 2^-40) in double, so sin/cos(r) are
+// double-doubles good to ~2^-90 relative; the addition formulas with
+// tabulated double-double sin/cos(a_k) (sincos_table.cuh) combine them.  A
+// short dependent chain: the roll search's latency (tree batches, final
+// probes) is dominated by this function.  Otherwise: reduction by pi/2 and an
+// 18-term double-double series.
 __device__ void dd_sincos(double x, double* s_out, double* c_out) {
   if (fabs(x) <= 0.75) {
-    const double kf = rint(x * 64.0);
-    const double r = x - kf * 0.015625;
-    const DD rr = {r, 0.0};
-    const DD x2 = dd_mul(rr, rr);
-    DD ps = {c_sin_hi[7], c_sin_lo[7]};
-    DD pc = {c_cos_hi[7], c_cos_lo[7]};
-#pragma unroll
-    for (int n = 6; n >= 0; --n) {
-      ps = dd_add(dd_mul(ps, x2), DD{c_sin_hi[n], c_sin_lo[n]});
-      pc = dd_add(dd_mul(pc, x2), DD{c_cos_hi[n], c_cos_lo[n]});
+    if (x == 0.0) {  // keeps the sign of zero
+      *s_out = x;
+      *c_out = 1.0;
+      return;
     }
-    const DD sr = dd_mul(ps, rr), cr = pc;
-    const int idx = int(kf) + kSinTabHalf;
-    const DD sa = {c_tab_sin_hi[idx], c_tab_sin_lo[idx]};
-    const DD ca = {c_tab_cos_hi[idx], c_tab_cos_lo[idx]};
+    const double kf = rint(x * 256.0);
+    const double r = x - kf * 0.00390625;  // exact
+    const double p = r * r;
+    const double e = __fma_rn(r, r, -p);  // r^2 = p + e exactly
+    // sin(r) = r - r * (r^2/3!) + r * p * S, S = r^2/5! - r^4/7! + r^6/9!: the
+    // r^3 term in double-double from the exact r^2, the rest (< 2^-38 |r|) in
+    // double
+    const DD d6 = dd_mul(DD{p, e}, DD{0.16666666666666666, 9.25185853854297e-18});
+    const DD t3 = dd_mul(d6, DD{r, 0.0});
+    const double S =
+        p * (0.008333333333333333 + p * (-0.0001984126984126984 + p * 2.7557319223985893e-06));
+    const DD sr = dd_add(dd_add(DD{r, 0.0}, DD{-t3.hi, -t3.lo}), DD{(r * p) * S, 0.0});
+    // cos(r) = 1 - (p + e)/2 + Q, Q = r^4/4! - r^6/6! + r^8/8!
+    const double Q = (p * p) * (0.041666666666666664 +
+                                p * (-0.001388888888888889 + p * 2.48015873015873e-05));
+    const DD c0 = two_sum(1.0, -0.5 * p);
+    const DD cr = quick_two_sum(c0.hi, c0.lo + (Q - 0.5 * e));
+    const int idx = int(kf) + kSinTab256Half;
+    const DD sa = {c_t256_sin_hi[idx], c_t256_sin_lo[idx]};
+    const DD ca = {c_t256_cos_hi[idx], c_t256_cos_lo[idx]};
     const DD sx = dd_add(dd_mul(sa, cr), dd_mul(ca, sr));
-    const DD cx = dd_add(dd_mul(ca, cr), DD{-dd_mul(sa, sr).hi, -dd_mul(sa, sr).lo});
+    const DD m = dd_mul(sa, sr);
+    const DD cx = dd_add(dd_mul(ca, cr), DD{-m.hi, -m.lo});
     *s_out = sx.hi;
     *c_out = cx.hi;
     return;
@@ -605,6 +615,7 @@ __device__ bool fit_line_final(FitState& F, const Moments& M, double phi, double
                                unsigned long long mask, LineFitD& out) {
   DD A0, A1;
   if (!line_coef(M, c, s, A0, A1)) return false;
+  fit_tr(F, 13);
   const double a0 = A0.hi, a1 = A1.hi;
   double acc[1] = {0.0};
   for (int m = 0; m < F.rows; ++m) {
@@ -716,9 +727,12 @@ __device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, 
     br = dd_lt(f1, f2);
     node = 2 * node + (br ? 1 : 0);
   }
+  fit_tr(F, 10);
   phi = 0.5 * (st.a + st.b);
   dd_sincos(phi, &sphi, &cphi);
+  fit_tr(F, 11);
   __syncthreads();  // the table is free for the next search
+  fit_tr(F, 12);
   return true;
 }
 
