@@ -244,6 +244,11 @@ rpd_status rpd_debug_guard_selftest(rpd_ctx* ctx, size_t bytes);
  * rounded with overwhelming probability) for n angles. */
 rpd_status rpd_debug_sincos(rpd_ctx* ctx, const double* x, int n, double* s, double* c);
 
+/* Test hook: the device's single-pass exclusive prefix sum (scan.cuh, the
+ * ordered-compaction primitive of sample_observations, the SLIC and CCL
+ * numbering): out[i] = in[0] + ... + in[i-1], *total = sum of all n. */
+rpd_status rpd_debug_scan(rpd_ctx* ctx, const int32_t* in, int64_t n, int32_t* out, int32_t* total);
+
 /* Parity extension: runs the production match_pair SGM path and materialises
  * its intermediates in the reference float layout (v*W+u)*(d_max+1)+d:
  * census_cost_volume, aggregate_costs of it and of swap_reference(it), and the

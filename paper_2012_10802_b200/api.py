@@ -386,6 +386,7 @@ _EXT_SIGS = {  # extensions of the product library (streaming, measurement)
     "rpd_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "rpd_ctx_stats": (C.c_int, [_vp, C.POINTER(Stats)]),
     "rpd_debug_sincos": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+    "rpd_debug_scan": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),
     "rpd_debug_guard_check": (C.c_int, [_vp, C.POINTER(C.c_longlong), C.c_char_p, C.c_int]),
     "rpd_debug_guard_selftest": (C.c_int, [_vp, C.c_size_t]),
 }
@@ -579,6 +580,15 @@ class Context:
         c = np.empty_like(x)
         self._check(self.dll.rpd_debug_sincos(self.handle, _ptr(x), x.shape[0], _ptr(s), _ptr(c)))
         return s, c
+
+    def debug_scan(self, flags):
+        """(exclusive prefix sums, total) of int32 flags on the device (scan.cuh)."""
+        a = np.ascontiguousarray(flags, dtype=np.int32)
+        out = np.empty_like(a)
+        tot = C.c_int32(0)
+        self._check(self.dll.rpd_debug_scan(self.handle, _ptr(a), a.shape[0], _ptr(out),
+                                            C.byref(tot)))
+        return out, tot.value
 
     def guard_check(self):
         """(corrupted guard bytes, first buffer) — checked build only (-1 otherwise)."""

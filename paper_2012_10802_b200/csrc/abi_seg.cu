@@ -4,6 +4,7 @@
 // result back.
 #include <vector>
 
+#include "scan.cuh"
 #include "abi_util.hpp"
 #include "road.cuh"
 #include "seg.cuh"
@@ -247,6 +248,22 @@ rpd_status rpd_debug_sincos(rpd_ctx* ctx, const double* x, int n, double* s, dou
     sincos_probe_dev(dx, n, ds, dc, ctx->stream);
     download(ctx, s, ds, sizeof(double) * size_t(n));
     download(ctx, c, dc, sizeof(double) * size_t(n));
+  });
+}
+
+rpd_status rpd_debug_scan(rpd_ctx* ctx, const int32_t* in, int64_t n, int32_t* out,
+                          int32_t* total) {
+  return guard(ctx, [&] {
+    if (n < 0) throw InvalidArg("scan: n < 0");
+    int* dtot = ctx->ws.get<int>("abi_dbg_scan_total", 1);
+    RPD_CK(cudaMemsetAsync(dtot, 0, sizeof(int), ctx->stream));
+    if (n > 0) {
+      const int* din = upload(ctx, "abi_dbg_scan_in", in, size_t(n));
+      int* dout = ctx->ws.get<int>("abi_dbg_scan_out", size_t(n));
+      scan_exclusive(ctx, ScanArrayIn{din}, dout, n, dtot);
+      download(ctx, out, dout, sizeof(int) * size_t(n));
+    }
+    download(ctx, total, dtot, sizeof(int));
   });
 }
 
