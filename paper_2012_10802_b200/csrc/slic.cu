@@ -311,6 +311,10 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 #ifndef RPD_ASSIGN_ROWCAP
 #define RPD_ASSIGN_ROWCAP 24
 #endif
+#ifndef RPD_ASSIGN_UNROLL
+#define RPD_ASSIGN_UNROLL 1  // candidate loop unroll (0: the compiler's choice; 1 measured best)
+#endif
+constexpr int kAssignUnroll = RPD_ASSIGN_UNROLL > 0 ? RPD_ASSIGN_UNROLL : 1;
 constexpr int kTileU = 32, kTileV = RPD_ASSIGN_TILEV, kMaxTileCenters = 192;
 constexpr int kRowCap = RPD_ASSIGN_ROWCAP;  // candidate records per tile row (more: per-pixel bucket walk)
 #ifndef RPD_ASSIGN_THREADS
@@ -416,6 +420,9 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
       const double du0 = double(u), sw = a.sw;
       const int nr = s_rowcnt[ty];
       const unsigned span = 2u * unsigned(win);
+#if RPD_ASSIGN_UNROLL > 0
+#pragma unroll kAssignUnroll
+#endif
       for (int j = 0; j < nr; ++j) {
         const double2 cd = s_rec[ty][2 * j];      // cu, (v - cv)^2
         const double2 vk = s_rec[ty][2 * j + 1];  // val, icu | k << 32
