@@ -31,6 +31,19 @@
 #include "scan.cuh"
 
 
+// k_fit's code size: with both input kinds' copies of the fit inlined it was
+// ~44 k SASS instructions (~700 KB); one copy is 22 k.  Out-of-line helpers
+// (RPD_FIT_NOINLINE_ON) shrink it to 11 k and the serial fit, but measured
+// slower in the concurrent regime.
+#ifndef RPD_FIT_NOINLINE_ON
+#define RPD_FIT_NOINLINE_ON 0  // 1: 10.9 k instead of 22.4 k instructions, fit 0.111 -> 0.096 ms serial, but -1 % frames/s
+#endif
+#if RPD_FIT_NOINLINE_ON
+#define RPD_FIT_NOINLINE __noinline__
+#else
+#define RPD_FIT_NOINLINE
+#endif
+
 namespace rpdg {
 
 // ------------------------------------------------ double-double sin/cos ----
@@ -84,7 +97,7 @@ __constant__ double c_cos_lo[kTaylorTerms] = {0.0, 0.0, 2.3129646346357427e-18, 
 // short dependent chain: the roll search's latency (tree batches, final
 // probes) is dominated by this function.  Otherwise: reduction by pi/2 and an
 // 18-term double-double series.
-__device__ void dd_sincos(double x, double* s_out, double* c_out) {
+__device__ RPD_FIT_NOINLINE void dd_sincos(double x, double* s_out, double* c_out) {
   if (fabs(x) <= 0.75) {
     if (x == 0.0) {  // keeps the sign of zero
       *s_out = x;
@@ -398,7 +411,7 @@ __device__ __forceinline__ void fit_get(const FitState& F, int m, double& d, dou
 // call parity: a CTA rewrites a slot only after every CTA has published the
 // following call, i.e. finished reading this one.
 template <int NV, bool DDV>
-__device__ void grid_sum(FitState& F, double (&x)[NV]) {
+__device__ RPD_FIT_NOINLINE void grid_sum(FitState& F, double (&x)[NV]) {
   static_assert(NV <= kMaxNV && (!DDV || NV % 2 == 0), "values");
   // Every step below runs element by element (one double, or one
   // double-double when DDV): the per-element trees are those of the
@@ -533,7 +546,7 @@ __device__ void grid_sum(FitState& F, double (&x)[NV]) {
 }
 
 // Moments of the elements whose row bit is set in `mask` (this lane's rows).
-__device__ Moments fit_moments(FitState& F, unsigned long long mask) {
+__device__ RPD_FIT_NOINLINE Moments fit_moments(FitState& F, unsigned long long mask) {
   DD acc[kNMom];
 #pragma unroll
   for (int q = 0; q < kNMom; ++q) acc[q] = DD{0.0, 0.0};
@@ -586,7 +599,7 @@ __device__ __forceinline__ bool line_sums(const Moments& M, double c, double s, 
   const double scale = nT2.hi < 1.0 ? 1.0 : nT2.hi;
   return !(fabs(o.det.hi) < 1e-12 * scale);
 }
-__device__ bool line_energy(const Moments& M, double c, double s, DD& e) {
+__device__ RPD_FIT_NOINLINE bool line_energy(const Moments& M, double c, double s, DD& e) {
   LineSums L;
   if (!line_sums(M, c, s, L)) return false;
   const DD D1 = M.m[2];
@@ -596,7 +609,7 @@ __device__ bool line_energy(const Moments& M, double c, double s, DD& e) {
   e = dd_sub(M.m[8], dd_div(q, L.det));
   return true;
 }
-__device__ bool line_coef(const Moments& M, double c, double s, DD& a0, DD& a1) {
+__device__ RPD_FIT_NOINLINE bool line_coef(const Moments& M, double c, double s, DD& a0, DD& a1) {
   LineSums L;
   if (!line_sums(M, c, s, L)) return false;
   const DD D1 = M.m[2];
@@ -736,10 +749,10 @@ __device__ bool fit_golden(FitState& F, const Moments& M, double lo, double hi, 
   return true;
 }
 
-template <bool COMPACT>
-__device__ void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok) {
+// The fit after staging (one copy for both input kinds: the kernel's code
+// size is what the instruction caches of the SMs it shares see).
+__device__ RPD_FIT_NOINLINE void fit_run(FitState& F, const FitKParams& P, FitOut& res, bool& ok) {
   const FitRequest& R = P.r;
-  fit_stage<COMPACT>(F, R);
   fit_tr(F, 1);
   const unsigned long long all = F.rows >= 64 ? ~0ull : ((1ull << F.rows) - 1ull);
   const Moments M = fit_moments(F, all);
@@ -813,9 +826,10 @@ __global__ void __launch_bounds__(kFitThreads, RPD_FIT_MINB * 64 / kFitThreads) 
   }
   if (ok) {
     if (R.compact)
-      fit_run<true>(F, P, res, ok);
+      fit_stage<true>(F, R);
     else
-      fit_run<false>(F, P, res, ok);
+      fit_stage<false>(F, R);
+    fit_run(F, P, res, ok);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (!ok && !failed_before) set_status(P.status, RPD_EDEGENERATE, R.where);

@@ -43,7 +43,10 @@ constexpr int kDepth = RPD_AGG_DEPTH;  // input ring depth (stages)
 #define RPD_AGG_RBASE 4      // steps per stage for <= 32 words per pixel
 #endif
 #ifndef RPD_AGG_UNROLL
-#define RPD_AGG_UNROLL 4     // unrolled steps of the inner loop (code size vs ILP)
+#define RPD_AGG_UNROLL 2     // unrolled steps of the inner loop, multi-lane chains (code size vs ILP)
+#endif
+#ifndef RPD_AGG_UNROLL_G1
+#define RPD_AGG_UNROLL_G1 2  // the same, one-lane chains
 #endif
 #ifndef RPD_AGG_REC
 // recurrence form: 0 = 2x add-min + min, 1 = min3 + add-min, 2 = min3 + add + min3,
@@ -59,7 +62,7 @@ constexpr int kRBase = RPD_AGG_RBASE;
 #define RPD_AGG_RBASE_G1 4  // steps per stage of the one-lane-per-chain kernels
 #endif
 constexpr int kRBaseG1 = RPD_AGG_RBASE_G1;
-constexpr int kStepUnroll = RPD_AGG_UNROLL;
+constexpr int kStepUnroll = RPD_AGG_UNROLL, kStepUnrollG1 = RPD_AGG_UNROLL_G1;
 constexpr uint32_t kInf2 = 0x7FFF7FFFu;
 
 enum JobType : int { kHoriz = 0, kVert = 1, kDiag = 2 };
@@ -550,7 +553,7 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
       const int s0 = stage_base + st * R;
       // only the first tile of a backward H/V scan holds padding steps
       const bool check = TYPE != kDiag && s0 < s_begin;
-#pragma unroll(kStepUnroll)
+#pragma unroll(G == 1 ? kStepUnrollG1 : kStepUnroll)
       for (int r = 0; r < R; ++r) {
         const int s = s0 + r;
         const int rr = (TYPE != kDiag && backward) ? R - 1 - r : r;
