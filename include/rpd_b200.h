@@ -221,6 +221,12 @@ typedef struct rpd_stats {
                                    after the first (long H / V chains are cut) */
   int64_t agg_segment_reruns;   /* cumulative: segments whose warm-up state differed from
                                    the predecessor's and that were recomputed */
+  int64_t slic_tiles_assigned;  /* cumulative: assignment tiles evaluated by the SLIC rounds
+                                   after the first (incremental rounds) */
+  int64_t slic_tiles_skipped;   /* cumulative: tiles of those rounds that no moved centre
+                                   reached and that kept their labels */
+  int64_t slic_centres_moved;   /* checked build only (0 otherwise): cumulative count of
+                                   centres that moved in those rounds */
 } rpd_stats;
 #define RPD_AGG_NONE 0
 #define RPD_AGG_F32 1    /* generic float kernels (non-integral penalties, other directions) */

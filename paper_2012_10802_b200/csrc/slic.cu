@@ -194,8 +194,39 @@ struct Orphans {
   unsigned* done;  // blocks done with the orphans (the last one finalises)
 };
 
+// Incremental rounds (RPD_SLIC_INCREMENTAL).  A pixel's assignment depends
+// only on its value and on the centres whose window holds it, so a tile that
+// no MOVED centre's window reaches — neither the window of the previous round
+// nor this round's — keeps every label, and the assignment skips it.  A centre
+// moved when (cu, cv, value) differ bitwise from the previous round.  The
+// per-label sums then persist across rounds and the assignment applies only
+// the changed pixels (- old label, + new label): all sums are exact integers,
+// so the totals are those of a full pass.  Orphans (pixels no window covers)
+// take the nearest of ALL centres: a round that follows one with orphans
+// marks every tile.
+//   flags[b][t]: tile t must be re-assigned in the round using buffer b;
+//   flags[b][ntx * nty]: every tile must.  Double-buffered like the grid counts.
+struct TileDirty {
+  int* flags[2];
+  int ntx, nty;
+  int tile_u, tile_v;
+  int w, h, win;
+  unsigned long long* moved_dbg;  // checked build: moved-centre count
+};
+
+__device__ __forceinline__ void mark_window(const TileDirty& td, int* __restrict__ flags, int iu,
+                                            int iv) {
+  const int u0 = max(iu - td.win, 0), u1 = min(iu + td.win, td.w - 1);
+  const int v0 = max(iv - td.win, 0), v1 = min(iv + td.win, td.h - 1);
+  if (u0 > u1 || v0 > v1) return;
+  for (int ty = v0 / td.tile_v; ty <= v1 / td.tile_v; ++ty)
+    for (int tx = u0 / td.tile_u; tx <= u1 / td.tile_u; ++tx) flags[ty * td.ntx + tx] = 1;
+}
+
+// finalize: 0 = seeds as they are (round 0); 1 = update_centers' tail, the sums
+// are kept (incremental rounds); 2 = the tail, then the sums are zeroed.
 __global__ void k_centers(Centers c, int K, CenterSums s, int finalize, CenterGrid g, int cur,
-                          Orphans o) {
+                          Orphans o, TileDirty td) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nthreads = gridDim.x * blockDim.x;
   const int norph = *o.count;  // written by the previous round's assignment
@@ -220,9 +251,15 @@ __global__ void k_centers(Centers c, int K, CenterSums s, int finalize, CenterGr
   const int nb = g.nbx * g.nby;
   int* cnt_next = g.count[cur ^ 1];
   for (int b = tid; b < nb; b += nthreads) cnt_next[b] = 0;
+  const int ntiles = td.ntx * td.nty;
+  if (td.flags[0]) {
+    int* dirty_next = td.flags[cur ^ 1];
+    for (int t = tid; t <= ntiles; t += nthreads) dirty_next[t] = 0;
+  }
   if (tid == 0) {
     *g.ovf[cur ^ 1] = 0;
     *o.count = 0;  // every block has read it (the count-0 path rewrites 0)
+    if (td.flags[0] && norph > 0) td.flags[cur][ntiles] = 1;
   }
   for (int k = tid; k < K; k += nthreads) {
     if (finalize) {
@@ -231,15 +268,32 @@ __global__ void k_centers(Centers c, int K, CenterSums s, int finalize, CenterGr
       const int n = __ldcg(s.n + l);
       if (n > 0) {
         const double dn = double(n);
-        c.cu[k] = double(__ldcg(s.su + l)) / dn;
-        c.cv[k] = double(__ldcg(s.sv + l)) / dn;
+        const double ncu = double(__ldcg(s.su + l)) / dn;
+        const double ncv = double(__ldcg(s.sv + l)) / dn;
         const AccSum sx{__ldcg(&s.sx[l].a0), __ldcg(&s.sx[l].a1), __ldcg(&s.sx[l].a2), 0ll};
-        c.val[k] = fixed_to_double(acc_value(sx)) / dn;
+        const double nval = fixed_to_double(acc_value(sx)) / dn;
+        if (td.flags[0]) {
+          const bool moved = __double_as_longlong(ncu) != __double_as_longlong(c.cu[k]) ||
+                             __double_as_longlong(ncv) != __double_as_longlong(c.cv[k]) ||
+                             __double_as_longlong(nval) != __double_as_longlong(c.val[k]);
+          if (moved) {
+#ifdef RPD_DEBUG_KNOBS
+            if (td.moved_dbg) atomicAdd(td.moved_dbg, 1ull);
+#endif
+            mark_window(td, td.flags[cur], c.icu[k], c.icv[k]);  // the window it leaves
+            mark_window(td, td.flags[cur], int(lround(ncu)), int(lround(ncv)));
+          }
+        }
+        c.cu[k] = ncu;
+        c.cv[k] = ncv;
+        c.val[k] = nval;
       }
-      s.n[l] = 0;
-      s.su[l] = 0;
-      s.sv[l] = 0;
-      s.sx[l] = AccSum{0ull, 0ull, 0ll, 0ll};
+      if (finalize == 2) {
+        s.n[l] = 0;
+        s.su[l] = 0;
+        s.sv[l] = 0;
+        s.sx[l] = AccSum{0ull, 0ull, 0ll, 0ll};
+      }
     }
     const double cu = c.cu[k], cv = c.cv[k];
     const int iu = int(lround(cu)), iv = int(lround(cv));
@@ -271,6 +325,8 @@ struct AssignArgs {
   int* inexact;
   int force_walk;  // checked build only (RPD_SLIC_FORCE_WALK): exercise the brute-force path
   uint32_t b_magic;  // floor(2^32 / B) + 1: x / B == umulhi(x, b_magic) for 0 <= x < 2^16 (0: divide)
+  const int* dirty;  // this round's tile flags (TileDirty), SKIP kernels only
+  unsigned long long* tiles;  // {assigned, skipped} counters of the SKIP kernels (rpd_stats)
 };
 
 // Bucket index of a non-negative coordinate (tile-uniform values: one
@@ -328,9 +384,36 @@ constexpr int kAssignWarps = kAssignThreads / 32;
 constexpr int kRowsPerWarp = kTileV / kAssignWarps;  // a warp owns rows w, w + kAssignWarps, ...
 static_assert(kTileV % kAssignWarps == 0, "whole tile rows per warp");
 
-template <bool SUMS>
+// One pixel's (1, u, v, value) added to (sign = 1) or taken from (sign = -1)
+// label l's exact sums: the incremental rounds' changed pixels.
+__device__ __forceinline__ void delta_pixel(const CenterSums& s, int l, int sign, int u, int v,
+                                            float x, int* __restrict__ inexact) {
+  int bad = 0;
+  Acc128 ax = to_fixed(x, &bad);
+  if (bad) atomicOr(inexact, 1);
+  if (sign < 0) {
+    ax.lo = ~ax.lo + 1ull;
+    ax.hi = ~ax.hi + (ax.lo == 0 ? 1 : 0);
+  }
+  atomicAdd(&s.n[l], sign);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&s.su[l]), (unsigned long long)(long long)(sign * u));
+  atomicAdd(reinterpret_cast<unsigned long long*>(&s.sv[l]), (unsigned long long)(long long)(sign * v));
+  red_add_acc(&s.sx[l], ax);
+}
+
+// SUMS: 0 = labels only (the last round), 1 = every pixel adds to its label's
+// sums (round 0, and every round of the non-incremental build), 2 = the sums
+// persist: only a pixel whose label changed moves its terms (see TileDirty).
+// SKIP: tiles no moved centre reaches return at once.
+template <int SUMS, bool SKIP>
 __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
+  if (SKIP) {
+    const int ntiles = gridDim.x * gridDim.y;
+    const bool dirty = (a.dirty[blockIdx.y * gridDim.x + blockIdx.x] | a.dirty[ntiles]) != 0;
+    if (threadIdx.x == 0) atomicAdd(a.tiles + (dirty ? 0 : 1), 1ull);
+    if (!dirty) return;
+  }
   __shared__ int s_cnt;
   __shared__ int s_rowcnt[kTileV];
   // candidate c: s_cd[2c] = (cu, cv), s_cd[2c+1] = (val, icu | k << 32)
@@ -348,6 +431,14 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   for (int q = 0; q < kRowsPerWarp; ++q) {
     const int v = v0 + wid + kAssignWarps * q;
     xf[q] = (u < a.w && v < a.h) ? a.vals[size_t(v) * a.w + u] : 0.0f;
+  }
+  int oldl[kRowsPerWarp];
+  if (SUMS == 2) {
+#pragma unroll
+    for (int q = 0; q < kRowsPerWarp; ++q) {
+      const int v = v0 + wid + kAssignWarps * q;
+      oldl[q] = (u < a.w && v < a.h) ? a.labels[size_t(v) * a.w + u] : 0;
+    }
   }
   for (int r = threadIdx.x; r < kTileV; r += blockDim.x) s_rowcnt[r] = 0;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -442,17 +533,27 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     if (in) {
       if (nc > kMaxTileCenters)
         bk = assign_walk(a, u, v, x);  // pathological centre pile-up: per-pixel bucket walk
+      label = bk + 1;
       if (bk < 0) {
-        a.labels[p] = 0;
         const int slot = atomicAdd(a.orphan_count, 1);
         a.orphan_list[slot] = int(p);
-        label = 0;
+      }
+      if (SUMS == 2) {
+        // persistent sums: a changed pixel leaves its old label and joins the
+        // new one (an orphan joins through the fallback, like every round)
+        if (label != oldl[q]) {
+#ifdef RPD_DEBUG_KNOBS
+          if (a.tiles) atomicAdd(a.tiles + 2, 1ull << 32);  // changed pixels in the high word
+#endif
+          a.labels[p] = label;
+          if (oldl[q] > 0) delta_pixel(s, oldl[q], -1, u, v, xf[q], a.inexact);
+          if (label > 0) delta_pixel(s, label, 1, u, v, xf[q], a.inexact);
+        }
       } else {
-        a.labels[p] = bk + 1;
-        label = bk + 1;
+        a.labels[p] = label;
       }
     }
-    if (SUMS) {
+    if (SUMS == 1) {
       const int key = label > 0 ? label : -1;
       const RunInfo ri = run_info(key);
       run_add_value(s.sx, key, key > 0, xf[q], ri, a.inexact);
@@ -858,24 +959,61 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
 
   AssignArgs aa{vals, h, w, K, c, nullptr, nullptr, grid.rec, B, nbx, nby, win, sw, labels,
                 orphan_list, orphan_count, inexact,
-                debug_knob("RPD_SLIC_FORCE_WALK") != nullptr ? 1 : 0, 0u};
+                debug_knob("RPD_SLIC_FORCE_WALK") != nullptr ? 1 : 0, 0u, nullptr, nullptr};
   if (B >= 2 && w + win + kTileU < 65536 && h + win + kTileV < 65536)
     aa.b_magic = uint32_t((1ull << 32) / unsigned(B) + 1ull);
   const dim3 tgrid(cdiv(w, kTileU), cdiv(h, kTileV));
   const int cblocks = cdiv(std::max(K, nb), 256);
+#ifndef RPD_SLIC_INCREMENTAL
+// 0: every round assigns and sums every pixel; 1: persistent sums (changed
+// pixels only) and clean-tile skipping; 2: persistent sums without skipping
+#define RPD_SLIC_INCREMENTAL 2
+#endif
+  int inc_mode = RPD_SLIC_INCREMENTAL;
+  if (const char* e = debug_knob("RPD_SLIC_INCREMENTAL")) inc_mode = std::atoi(e);
+  const bool incremental = inc_mode != 0, skip = inc_mode == 1;
+  TileDirty td{{nullptr, nullptr}, int(tgrid.x), int(tgrid.y), kTileU, kTileV, w, h, win, nullptr};
+  if (skip) {
+    const size_t ntiles = size_t(tgrid.x) * tgrid.y;
+    int* dirty = ctx->ws.get<int>("slic_tile_dirty", 2 * (ntiles + 1));
+    td.flags[0] = dirty;
+    td.flags[1] = dirty + ntiles + 1;
+    // round 1 marks buffer 1 (cleared by round 0's centre kernel); buffer 0 is
+    // cleared by round 1's
+    unsigned long long* tiles = ctx->ws.get<unsigned long long>("slic_tile_counts", 3);
+    if (tiles != ctx->slic_tiles) {
+      RPD_CK(cudaMemsetAsync(tiles, 0, 3 * sizeof(unsigned long long), st));
+      ctx->slic_tiles = tiles;
+    }
+    aa.tiles = tiles;
+    td.moved_dbg = tiles + 2;
+  }
   int round = 0;
   // One round = centre grid (finalising the previous round's sums first) +
   // assignment that accumulates the sums the next round needs.
   auto assign = [&](bool finalize, bool sums) {
-    const int cur = round++ & 1;
-    k_centers<<<cblocks, 256, 0, st>>>(c, K, s, finalize ? 1 : 0, grid, cur, orph);
+    const int cur = round & 1;
+    const bool first = round == 0;
+    ++round;
+    // incremental: the sums persist until the last round's centre step
+    const int fin = !finalize ? 0 : (incremental && sums ? 1 : 2);
+    k_centers<<<cblocks, 256, 0, st>>>(c, K, s, fin, grid, cur, orph, td);
     RPD_LAUNCH_CHECK();
     aa.bcount = grid.count[cur];
     aa.ovf = grid.ovf[cur];
-    if (sums)
-      k_assign_tile<true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
-    else
-      k_assign_tile<false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+    aa.dirty = td.flags[cur];
+    if (skip && !first) {
+      if (sums)
+        k_assign_tile<2, true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+      else
+        k_assign_tile<0, true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+    } else if (incremental && !first && sums) {
+      k_assign_tile<2, false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+    } else if (sums) {
+      k_assign_tile<1, false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+    } else {
+      k_assign_tile<0, false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+    }
     RPD_LAUNCH_CHECK();
     if (!sums) {  // the last round: no k_centers follows to take its orphans
       k_assign_fallback<<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list, orphan_count);
