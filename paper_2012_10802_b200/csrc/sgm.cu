@@ -1048,14 +1048,23 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
           "l"(a.path[vol][r] + off), "r"(bytes), "r"(wta_smem_addr(&bar))
           : "memory");
   }
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WTA_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-      "@!p bra WTA_WAIT_%=;\n"
-      "}\n" ::"r"(wta_smem_addr(&bar))
-      : "memory");
+#ifndef RPD_WTA_WAIT_ONE
+#define RPD_WTA_WAIT_ONE 1  // 1: one thread polls the mbarrier, the others block at the CTA barrier
+#endif
+  // One thread observes the completion (acquire) and the CTA barrier orders
+  // every thread's reads after it; the other warps wait at the barrier
+  // without issuing instructions (all threads polling cost 17 % of the
+  // kernel's issued instructions).
+  if (!RPD_WTA_WAIT_ONE || threadIdx.x == 0)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WTA_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra WTA_WAIT_%=;\n"
+        "}\n" ::"r"(wta_smem_addr(&bar))
+        : "memory");
+  if (RPD_WTA_WAIT_ONE) __syncthreads();
   const int t = threadIdx.x;
   if (t >= npx) return;
   // exact per-level sums over the P paths, two levels per u16x2 word
