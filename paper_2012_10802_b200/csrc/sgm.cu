@@ -1040,6 +1040,20 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
                  "r"(bytes * P)
                  : "memory");
     const size_t off = size_t(row) * a.pitch + size_t(u0) * (NW * 4);
+#ifndef RPD_WTA_L2_HINT
+#define RPD_WTA_L2_HINT 1  // 1: the path tiles are loaded evict_first (read once)
+#endif
+#if RPD_WTA_L2_HINT
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              wta_smem_addr(tile + r * (TP * NW))),
+          "l"(a.path[vol][r] + off), "r"(bytes), "r"(wta_smem_addr(&bar)), "l"(pol)
+          : "memory");
+#else
 #pragma unroll
     for (int r = 0; r < P; ++r)
       asm volatile(
@@ -1047,6 +1061,7 @@ __global__ void __launch_bounds__(WtaGeo<NW>::TP) k_wta_bulk(const __grid_consta
               wta_smem_addr(tile + r * (TP * NW))),
           "l"(a.path[vol][r] + off), "r"(bytes), "r"(wta_smem_addr(&bar))
           : "memory");
+#endif
   }
 #ifndef RPD_WTA_WAIT_ONE
 #define RPD_WTA_WAIT_ONE 1  // 1: one thread polls the mbarrier, the others block at the CTA barrier
@@ -1206,8 +1221,12 @@ bool launch_wta_bulk(const WtaBulkArgs& wa, int paths, int h, int w, cudaStream_
                          : paths == 4 ? wta_bulk_pick<4>(nw, wa.levels)
                                       : WtaBulkInfo{};
   if (!ki.fn) return false;
-  RPD_CK(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ki.smem));
-  ki.fn<<<dim3(cdiv(w, ki.tp), h, 2), ki.tp, ki.smem, st>>>(wa);
+#ifndef RPD_WTA_SMEM_MIN
+#define RPD_WTA_SMEM_MIN 0  // experiment: request at least this much shared memory per CTA (caps CTAs/SM)
+#endif
+  const int wsmem = std::max(ki.smem, RPD_WTA_SMEM_MIN);
+  RPD_CK(cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem));
+  ki.fn<<<dim3(cdiv(w, ki.tp), h, 2), ki.tp, wsmem, st>>>(wa);
   RPD_LAUNCH_CHECK();
   return true;
 }

@@ -126,22 +126,58 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+#ifndef RPD_AGG_L2_HINTS
+// L2 eviction hints of the aggregation's bulk copies: bit 0 = cost tiles are
+// loaded evict_last (each is read by all 2P jobs of the launch), bit 1 = path
+// tiles are stored evict_first (written once, read once by the WTA much later),
+// bit 2 = the diagonal jobs' direct stores are streaming stores
+#define RPD_AGG_L2_HINTS 1
+#endif
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
                                             uint64_t* bar) {
+#if RPD_AGG_L2_HINTS & 1
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar)),
+      "l"(l2_policy_evict_last())
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z,
                                              const void* src) {
+#if RPD_AGG_L2_HINTS & 2
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(x), "r"(y), "r"(z), "r"(smem_addr(src)), "l"(l2_policy_evict_first())
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
           reinterpret_cast<uint64_t>(map)),
       "r"(x), "r"(y), "r"(z), "r"(smem_addr(src))
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;"); }
@@ -579,7 +615,13 @@ __device__ __forceinline__ void agg_body(const TmaArgs& a, const TmaJob& J, int 
           if (unsigned(col) < unsigned(w) && s < s_end) {
             uint32_t* dst = reinterpret_cast<uint32_t*>(pbase + doff);
 #pragma unroll
-            for (int q = 0; q < WPL; ++q) dst[q] = packed[q];
+            for (int q = 0; q < WPL; ++q) {
+#if RPD_AGG_L2_HINTS & 4
+              __stcs(dst + q, packed[q]);  // streaming: read once by the WTA, much later
+#else
+              dst[q] = packed[q];
+#endif
+            }
           }
           doff += dstep;
         } else if (store) {
