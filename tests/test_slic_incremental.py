@@ -96,6 +96,8 @@ def test_partly_moving_raster_skips_some_tiles(dbg, oracle):
     skipped = after.slic_tiles_skipped - before.slic_tiles_skipped
     assigned = after.slic_tiles_assigned - before.slic_tiles_assigned
     assert skipped > 0 and assigned > skipped
+    n, who = dbg.guard_check()  # the tile flag / counter buffers of the skipping mode included
+    assert n == 0, f"{n} guard bytes overwritten (first: {who})"
 
 
 ORPHAN_CASES = blocky_cases()[:48]  # orphans before the last round in 3 of these (test_slic_orphans)
