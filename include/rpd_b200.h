@@ -227,6 +227,8 @@ typedef struct rpd_stats {
                                    reached and that kept their labels */
   int64_t slic_centres_moved;   /* checked build only (0 otherwise): cumulative count of
                                    centres that moved in those rounds */
+  int64_t slic_pixels_changed;  /* checked build only (0 otherwise): cumulative count of
+                                   pixels whose label changed in those rounds */
 } rpd_stats;
 #define RPD_AGG_NONE 0
 #define RPD_AGG_F32 1    /* generic float kernels (non-integral penalties, other directions) */

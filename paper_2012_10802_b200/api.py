@@ -362,7 +362,8 @@ class Stats(C.Structure):
                 ("sgm_agg_alg_bytes", C.c_double * 2), ("sgm_cells", C.c_double * 2),
                 ("last_agg_kernel", C.c_int32), ("agg_segmented_ctas", C.c_int32),
                 ("agg_segment_reruns", C.c_int64), ("slic_tiles_assigned", C.c_int64),
-                ("slic_tiles_skipped", C.c_int64), ("slic_centres_moved", C.c_int64)]
+                ("slic_tiles_skipped", C.c_int64), ("slic_centres_moved", C.c_int64),
+                ("slic_pixels_changed", C.c_int64)]
 
 
 AGG_KERNELS = {0: "none", 1: "f32", 2: "u8_tma", 3: "u8"}  # RPD_AGG_*

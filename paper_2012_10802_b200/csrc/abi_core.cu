@@ -170,11 +170,12 @@ rpd_status rpd_ctx_stats(rpd_ctx* ctx, rpd_stats* out) {
       s.agg_segment_reruns = (int64_t)n;
     }
     if (ctx->slic_tiles) {
-      unsigned long long n[3] = {0, 0, 0};
+      unsigned long long n[4] = {0, 0, 0, 0};
       RPD_CK(cudaMemcpy(n, ctx->slic_tiles, sizeof(n), cudaMemcpyDeviceToHost));
       s.slic_tiles_assigned = (int64_t)n[0];
       s.slic_tiles_skipped = (int64_t)n[1];
       s.slic_centres_moved = (int64_t)n[2];
+      s.slic_pixels_changed = (int64_t)n[3];
     }
     s.sgm_passes = ctx->profile ? ctx->agg_pass : 0;
     for (int i = 0; i < s.sgm_passes; ++i) {

@@ -241,7 +241,7 @@ struct rpd_ctx {
   void* scan_ctl_zeroed = nullptr;
   int agg_segmented_ctas = 0;                  // last aggregation launch
   unsigned long long* agg_reruns = nullptr;    // device counter (workspace)
-  unsigned long long* slic_tiles = nullptr;    // device counters {assigned, skipped} (workspace)
+  unsigned long long* slic_tiles = nullptr;    // device counters {tiles assigned, skipped, centres moved, pixels changed}
 };
 
 namespace rpdg {

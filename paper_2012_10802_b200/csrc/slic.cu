@@ -326,7 +326,7 @@ struct AssignArgs {
   int force_walk;  // checked build only (RPD_SLIC_FORCE_WALK): exercise the brute-force path
   uint32_t b_magic;  // floor(2^32 / B) + 1: x / B == umulhi(x, b_magic) for 0 <= x < 2^16 (0: divide)
   const int* dirty;  // this round's tile flags (TileDirty), SKIP kernels only
-  unsigned long long* tiles;  // {assigned, skipped} counters of the SKIP kernels (rpd_stats)
+  unsigned long long* tiles;  // {assigned, skipped, moved centres, changed pixels} counters (rpd_stats)
 };
 
 // Bucket index of a non-negative coordinate (tile-uniform values: one
@@ -383,6 +383,7 @@ constexpr int kAssignWarps = kAssignThreads / 32;
 #endif
 constexpr int kRowsPerWarp = kTileV / kAssignWarps;  // a warp owns rows w, w + kAssignWarps, ...
 static_assert(kTileV % kAssignWarps == 0, "whole tile rows per warp");
+static_assert(kTileV <= 256, "a candidate's tile-row range is packed into two bytes");
 
 // One pixel's (1, u, v, value) added to (sign = 1) or taken from (sign = -1)
 // label l's exact sums: the incremental rounds' changed pixels.
@@ -418,27 +419,28 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   __shared__ int s_rowcnt[kTileV];
   // candidate c: s_cd[2c] = (cu, cv), s_cd[2c+1] = (val, icu | k << 32)
   __shared__ double2 s_cd[2 * kMaxTileCenters];
-  __shared__ int s_icv[kMaxTileCenters];
+  __shared__ int s_icv[kMaxTileCenters];  // first | last << 8 tile row of the candidate's window
   // per tile row, the candidates whose window reaches it: {cu, (v - cv)^2}, {val, icu | k << 32}
   __shared__ double2 s_rec[kTileV][2 * kRowCap];
   const int tx = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
   const int u = u0 + tx;
   const int win = a.win;
-  // pixel values first (their loads overlap the candidate fill)
+  // pixel values first (their loads overlap the candidate fill); one 32-bit
+  // pixel index per thread, advanced by a row stride (H * W < 2^31: the orphan
+  // list holds int indices)
+  const bool uin = u < a.w;
+  const int p0 = (v0 + wid) * a.w + u;
+  const int pstride = kAssignWarps * a.w;
   float xf[kRowsPerWarp];
 #pragma unroll
-  for (int q = 0; q < kRowsPerWarp; ++q) {
-    const int v = v0 + wid + kAssignWarps * q;
-    xf[q] = (u < a.w && v < a.h) ? a.vals[size_t(v) * a.w + u] : 0.0f;
-  }
+  for (int q = 0; q < kRowsPerWarp; ++q)
+    xf[q] = (uin && v0 + wid + kAssignWarps * q < a.h) ? a.vals[p0 + q * pstride] : 0.0f;
   int oldl[kRowsPerWarp];
   if (SUMS == 2) {
 #pragma unroll
-    for (int q = 0; q < kRowsPerWarp; ++q) {
-      const int v = v0 + wid + kAssignWarps * q;
-      oldl[q] = (u < a.w && v < a.h) ? a.labels[size_t(v) * a.w + u] : 0;
-    }
+    for (int q = 0; q < kRowsPerWarp; ++q)
+      oldl[q] = (uin && v0 + wid + kAssignWarps * q < a.h) ? a.labels[p0 + q * pstride] : 0;
   }
   for (int r = threadIdx.x; r < kTileV; r += blockDim.x) s_rowcnt[r] = 0;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -466,7 +468,8 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
       s_cd[2 * slotc] = rec->cuv;
       s_cd[2 * slotc + 1] = make_double2(
           rec->val.x, __longlong_as_double((long long)(uint32_t(ik.x) | (uint64_t(uint32_t(ik.z)) << 32))));
-      s_icv[slotc] = ik.y;
+      // tile rows the centre's window reaches (dv <= win: never empty)
+      s_icv[slotc] = (max(ik.y - win, v0) - v0) | ((min(ik.y + win, v0 + kTileV - 1) - v0) << 8);
     }
   }
   __syncthreads();
@@ -479,8 +482,8 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     // thread has work
     for (int t = threadIdx.x; t < nc * kTileV; t += blockDim.x) {
       const int i = t / kTileV, r = t - i * kTileV;
-      const int icv = s_icv[i];
-      if (r < max(icv - win, v0) - v0 || r > min(icv + win, v0 + kTileV - 1) - v0) continue;
+      const int rows = s_icv[i];
+      if (r < (rows & 255) || r > (rows >> 8)) continue;
       const double2 cuv = s_cd[2 * i];
       const int slot = atomicAdd(&s_rowcnt[r], 1);
       if (slot < kRowCap) {
@@ -502,8 +505,8 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   for (int q = 0; q < kRowsPerWarp; ++q) {
     const int ty = wid + kAssignWarps * q;
     const int v = v0 + ty;  // uniform across the warp
-    const bool in = u < a.w && v < a.h;
-    const size_t p = size_t(v) * a.w + u;
+    const bool in = uin && v < a.h;
+    const int p = p0 + q * pstride;
     const double x = double(xf[q]);
     double best = __longlong_as_double(0x7FF0000000000000ll);
     int bk = -1;
@@ -536,14 +539,14 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
       label = bk + 1;
       if (bk < 0) {
         const int slot = atomicAdd(a.orphan_count, 1);
-        a.orphan_list[slot] = int(p);
+        a.orphan_list[slot] = p;
       }
       if (SUMS == 2) {
         // persistent sums: a changed pixel leaves its old label and joins the
         // new one (an orphan joins through the fallback, like every round)
         if (label != oldl[q]) {
 #ifdef RPD_DEBUG_KNOBS
-          if (a.tiles) atomicAdd(a.tiles + 2, 1ull << 32);  // changed pixels in the high word
+          if (a.tiles) atomicAdd(a.tiles + 3, 1ull);  // changed pixels
 #endif
           a.labels[p] = label;
           if (oldl[q] > 0) delta_pixel(s, oldl[q], -1, u, v, xf[q], a.inexact);
@@ -913,6 +916,7 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
                  float* d3) {
   if (p < 4) throw InvalidArg("slic: p must be >= 4");
   if ((long long)p > (long long)w * h) throw InvalidArg("slic: p exceeds pixel count");
+  if ((long long)w * h >= (1ll << 31)) throw InvalidArg("slic: more than 2^31 - 1 pixels");
   cudaStream_t st = ctx->stream;
   const long long n = (long long)h * w;
   const int gblocks = int(std::max<long long>(1, std::min<long long>((n + 255) / 256,
@@ -980,9 +984,9 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
     td.flags[1] = dirty + ntiles + 1;
     // round 1 marks buffer 1 (cleared by round 0's centre kernel); buffer 0 is
     // cleared by round 1's
-    unsigned long long* tiles = ctx->ws.get<unsigned long long>("slic_tile_counts", 3);
+    unsigned long long* tiles = ctx->ws.get<unsigned long long>("slic_tile_counts", 4);
     if (tiles != ctx->slic_tiles) {
-      RPD_CK(cudaMemsetAsync(tiles, 0, 3 * sizeof(unsigned long long), st));
+      RPD_CK(cudaMemsetAsync(tiles, 0, 4 * sizeof(unsigned long long), st));
       ctx->slic_tiles = tiles;
     }
     aa.tiles = tiles;

@@ -96,6 +96,10 @@ def test_partly_moving_raster_skips_some_tiles(dbg, oracle):
     skipped = after.slic_tiles_skipped - before.slic_tiles_skipped
     assigned = after.slic_tiles_assigned - before.slic_tiles_assigned
     assert skipped > 0 and assigned > skipped
+    # checked-build counters: some centres moved and some pixels changed label, far from all
+    moved = after.slic_centres_moved - before.slic_centres_moved
+    changed = after.slic_pixels_changed - before.slic_pixels_changed
+    assert 0 < moved < 10 * 200 and 0 < changed < h * w
     n, who = dbg.guard_check()  # the tile flag / counter buffers of the skipping mode included
     assert n == 0, f"{n} guard bytes overwritten (first: {who})"
 
