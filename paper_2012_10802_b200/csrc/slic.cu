@@ -362,7 +362,15 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 // with warp run aggregation (a warp is one tile row).  Pixels without a window
 // are left for the fallback kernel, which adds their sums itself.
 #ifndef RPD_ASSIGN_TILEV
-#define RPD_ASSIGN_TILEV 24  // tile rows (3 per warp; 24 vs 32: SLIC 0.409 -> 0.395 ms serial)
+// tile rows of large rasters (5 per warp): the staging is shared by more
+// pixels, config 5 +1.3 % frames/s over 24 rows (32 / 40 rows equal, 48 rows
+// lose it again through their shared memory)
+#define RPD_ASSIGN_TILEV 40
+#endif
+#ifndef RPD_ASSIGN_TILEV_SMALL
+// tile rows of rasters with few tiles (3 per warp): config 1's 240 x 320 is
+// 2.5 % faster with the extra CTAs
+#define RPD_ASSIGN_TILEV_SMALL 24
 #endif
 #ifndef RPD_ASSIGN_ROWCAP
 #define RPD_ASSIGN_ROWCAP 24
@@ -371,7 +379,8 @@ __device__ __forceinline__ int assign_walk(const AssignArgs& a, int u, int v, do
 #define RPD_ASSIGN_UNROLL 1  // candidate loop unroll (0: the compiler's choice; 1 measured best)
 #endif
 constexpr int kAssignUnroll = RPD_ASSIGN_UNROLL > 0 ? RPD_ASSIGN_UNROLL : 1;
-constexpr int kTileU = 32, kTileV = RPD_ASSIGN_TILEV, kMaxTileCenters = 192;
+constexpr int kTileU = 32, kTileVLarge = RPD_ASSIGN_TILEV, kTileVSmall = RPD_ASSIGN_TILEV_SMALL,
+              kMaxTileCenters = 192;
 constexpr int kRowCap = RPD_ASSIGN_ROWCAP;  // candidate records per tile row (more: per-pixel bucket walk)
 #ifndef RPD_ASSIGN_THREADS
 #define RPD_ASSIGN_THREADS 256
@@ -381,9 +390,11 @@ constexpr int kAssignWarps = kAssignThreads / 32;
 #ifndef RPD_ASSIGN_MINB
 #define RPD_ASSIGN_MINB (6 * 256 / RPD_ASSIGN_THREADS)  // resident CTAs per SM the register budget targets
 #endif
-constexpr int kRowsPerWarp = kTileV / kAssignWarps;  // a warp owns rows w, w + kAssignWarps, ...
-static_assert(kTileV % kAssignWarps == 0, "whole tile rows per warp");
-static_assert(kTileV <= 256, "a candidate's tile-row range is packed into two bytes");
+// a warp owns rows w, w + kAssignWarps, ...
+static_assert(kTileVLarge % kAssignWarps == 0 && kTileVSmall % kAssignWarps == 0,
+              "whole tile rows per warp");
+static_assert(kTileVLarge <= 256 && kTileVSmall <= 256,
+              "a candidate's tile-row range is packed into two bytes");
 
 // One pixel's (1, u, v, value) added to (sign = 1) or taken from (sign = -1)
 // label l's exact sums: the incremental rounds' changed pixels.
@@ -406,9 +417,10 @@ __device__ __forceinline__ void delta_pixel(const CenterSums& s, int l, int sign
 // sums (round 0, and every round of the non-incremental build), 2 = the sums
 // persist: only a pixel whose label changed moves its terms (see TileDirty).
 // SKIP: tiles no moved centre reaches return at once.
-template <int SUMS, bool SKIP>
+template <int SUMS, bool SKIP, int kTileV>
 __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
     k_assign_tile(const __grid_constant__ AssignArgs a, CenterSums s) {
+  constexpr int kRowsPerWarp = kTileV / kAssignWarps;
   if (SKIP) {
     const int ntiles = gridDim.x * gridDim.y;
     const bool dirty = (a.dirty[blockIdx.y * gridDim.x + blockIdx.x] | a.dirty[ntiles]) != 0;
@@ -964,6 +976,10 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
   AssignArgs aa{vals, h, w, K, c, nullptr, nullptr, grid.rec, B, nbx, nby, win, sw, labels,
                 orphan_list, orphan_count, inexact,
                 debug_knob("RPD_SLIC_FORCE_WALK") != nullptr ? 1 : 0, 0u, nullptr, nullptr};
+  // tile height: the large tile when it still gives every SM several CTAs
+  bool large_tiles = cdiv(w, kTileU) * cdiv(h, kTileVLarge) >= 3 * ctx->sm_count;
+  if (const char* e = debug_knob("RPD_SLIC_LARGE_TILES")) large_tiles = std::atoi(e) != 0;  // tests
+  const int kTileV = large_tiles ? kTileVLarge : kTileVSmall;
   if (B >= 2 && w + win + kTileU < 65536 && h + win + kTileV < 65536)
     aa.b_magic = uint32_t((1ull << 32) / unsigned(B) + 1ull);
   const dim3 tgrid(cdiv(w, kTileU), cdiv(h, kTileV));
@@ -1006,18 +1022,25 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
     aa.bcount = grid.count[cur];
     aa.ovf = grid.ovf[cur];
     aa.dirty = td.flags[cur];
-    if (skip && !first) {
-      if (sums)
-        k_assign_tile<2, true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
-      else
-        k_assign_tile<0, true><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
-    } else if (incremental && !first && sums) {
-      k_assign_tile<2, false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
-    } else if (sums) {
-      k_assign_tile<1, false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
-    } else {
-      k_assign_tile<0, false><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
-    }
+    auto launch = [&](auto tv) {
+      constexpr int TV = decltype(tv)::value;
+      if (skip && !first) {
+        if (sums)
+          k_assign_tile<2, true, TV><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+        else
+          k_assign_tile<0, true, TV><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+      } else if (incremental && !first && sums) {
+        k_assign_tile<2, false, TV><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+      } else if (sums) {
+        k_assign_tile<1, false, TV><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+      } else {
+        k_assign_tile<0, false, TV><<<tgrid, kAssignThreads, 0, st>>>(aa, s);
+      }
+    };
+    if (large_tiles)
+      launch(std::integral_constant<int, kTileVLarge>{});
+    else
+      launch(std::integral_constant<int, kTileVSmall>{});
     RPD_LAUNCH_CHECK();
     if (!sums) {  // the last round: no k_centers follows to take its orphans
       k_assign_fallback<<<ctx->sm_count, 256, 0, st>>>(w, c, K, labels, orphan_list, orphan_count);

@@ -33,12 +33,15 @@ def dbg():
     return Library(str(DBG_LIB)).context(0)
 
 
-def slic_mode(ctx, mode, d2, p, comp, it):
+def slic_mode(ctx, mode, d2, p, comp, it, large=None):
     os.environ["RPD_SLIC_INCREMENTAL"] = str(mode)
+    if large is not None:  # tile height: the large-raster kernels on a small raster, or the reverse
+        os.environ["RPD_SLIC_LARGE_TILES"] = str(int(large))
     try:
         return ctx.slic(d2, p, comp, it)
     finally:
         del os.environ["RPD_SLIC_INCREMENTAL"]
+        os.environ.pop("RPD_SLIC_LARGE_TILES", None)
 
 
 def same(a, b):
@@ -64,6 +67,7 @@ def test_modes_equal_oracle_noisy(dbg, oracle, h, w, p, it):
     ref = oracle.slic(d2, p, 8.0, it)
     for mode in MODES:
         same(slic_mode(dbg, mode, d2, p, 8.0, it), ref)
+        same(slic_mode(dbg, mode, d2, p, 8.0, it, large=True), ref)
 
 
 def test_flat_raster_converges_and_skips_tiles(dbg, oracle):
@@ -73,7 +77,7 @@ def test_flat_raster_converges_and_skips_tiles(dbg, oracle):
     d2[:, w // 2:] = 3.0
     ref = oracle.slic(d2, 120, 8.0, 10)
     before = dbg.stats()
-    same(slic_mode(dbg, 1, d2, 120, 8.0, 10), ref)
+    same(slic_mode(dbg, 1, d2, 120, 8.0, 10, large=False), ref)
     after = dbg.stats()
     assigned = after.slic_tiles_assigned - before.slic_tiles_assigned
     skipped = after.slic_tiles_skipped - before.slic_tiles_skipped
@@ -91,7 +95,7 @@ def test_partly_moving_raster_skips_some_tiles(dbg, oracle):
     d2[:, : w // 2] = 1.0
     ref = oracle.slic(d2, 200, 8.0, 10)
     before = dbg.stats()
-    same(slic_mode(dbg, 1, d2, 200, 8.0, 10), ref)
+    same(slic_mode(dbg, 1, d2, 200, 8.0, 10, large=True), ref)
     after = dbg.stats()
     skipped = after.slic_tiles_skipped - before.slic_tiles_skipped
     assigned = after.slic_tiles_assigned - before.slic_tiles_assigned
@@ -113,6 +117,21 @@ def test_orphan_rounds_all_modes(dbg, oracle, i):
     ref = oracle.slic(d2, p, comp, 10)
     for mode in MODES:
         same(slic_mode(dbg, mode, d2, p, comp, 10), ref)
+    same(slic_mode(dbg, 2, d2, p, comp, 10, large=True), ref)  # 40-row tiles (large rasters)
+    same(slic_mode(dbg, 1, d2, p, comp, 10, large=True), ref)
+
+
+@pytest.mark.parametrize("large", [False, True])
+def test_brute_force_walk_with_persistent_sums(dbg, oracle, large):
+    # the per-pixel scan of every centre (bucket / tile overflow path) under both tile heights
+    d2 = noisy(120, 170, 11)
+    ref = oracle.slic(d2, 150, 8.0, 5)
+    os.environ["RPD_SLIC_FORCE_WALK"] = "1"
+    try:
+        for mode in MODES:
+            same(slic_mode(dbg, mode, d2, 150, 8.0, 5, large=large), ref)
+    finally:
+        del os.environ["RPD_SLIC_FORCE_WALK"]
 
 
 def test_product_ignores_the_knob(gpu, oracle):
