@@ -93,6 +93,10 @@ def parse(argv=None):
     ap.add_argument("--e2e-outputs", default="labels,d1,d2",
                     help="outputs copied back per e2e call (rpd_detect_out fields)")
     ap.add_argument("--e2e-threads", type=int, default=0, help="0 = --streams")
+    ap.add_argument("--e2e-contexts", type=int, default=0,
+                    help="pipeline contexts of the e2e run (0 = max(--streams, e2e threads)); more "
+                         "contexts than threads: each thread streams several frames "
+                         "(rpd_detect_async_host_u8 + rpd_detect_fetch)")
     return ap.parse_args(argv)
 
 
@@ -462,7 +466,7 @@ def gpu_arm(args, rank, world, local):
     # rpd_detect_fetch: D2H of the outputs), so a many-GPU box with few host
     # cores per rank is not measured as a host-thread limit.
     ET = args.e2e_threads or min(S, max(1, (os.cpu_count() or 1) // world))
-    NE = max(S, ET)
+    NE = args.e2e_contexts or max(S, ET)
     ectxs = ctxs[:NE] + [lib.context(local) for _ in range(max(0, NE - S))]
     outs = [make_out() for _ in ectxs]
     lhp = [left_h[i].data_ptr() for i in range(P)]

@@ -1000,7 +1000,13 @@ __device__ __forceinline__ uint32_t wta_smem_addr(const void* p) {
 
 template <int NW>
 struct WtaGeo {
-  static constexpr int TP = NW <= 9 ? 128 : 64;                 // pixels per CTA
+#ifndef RPD_WTA_TP_SMALL
+#define RPD_WTA_TP_SMALL 128  // pixels per CTA, <= 9 words per pixel
+#endif
+#ifndef RPD_WTA_TP_BIG
+#define RPD_WTA_TP_BIG 64     // pixels per CTA, wider layouts
+#endif
+  static constexpr int TP = NW <= 9 ? RPD_WTA_TP_SMALL : RPD_WTA_TP_BIG;  // pixels per CTA
   static constexpr int V = NW % 4 == 0 ? 4 : (NW % 2 == 0 ? 2 : 1);  // words per LDS
   static constexpr int NP = 2 * NW;                              // u16x2 level pairs
 };
