@@ -38,6 +38,20 @@ def test_config_parity(gpu, oracle_results, case):
     compare_detect(a, b)
 
 
+def test_ragged_large_frame(gpu, oracle_lib):
+    """A config-2 style scene at 701 x 1003: every tiled kernel meets ragged
+    edges in both directions (the 32 x 40 SLIC tiles of large rasters, the
+    aggregation's 32-chain blocks, the WTA's 128-pixel row tiles)."""
+    from paper_2012_10802_b200.synth import scene_params
+    prm = scene_params(2, 7)
+    prm.width, prm.height = 1003, 701
+    sc = make_scene(2, 7, prm)
+    assert sc.left.shape == (701, 1003)
+    a = gpu.detect(sc.left, sc.right, pipeline_config(gpu.lib, 2))
+    b = oracle_lib.context().detect(sc.left, sc.right, pipeline_config(oracle_lib, 2))
+    compare_detect(a, b)
+
+
 def test_streaming_matches_single_calls(gpu, cuda_lib):
     from paper_2012_10802_b200.shard import StreamingRunner, summarize
 
