@@ -928,7 +928,9 @@ SlicOut slic_dev(rpd_ctx* ctx, const float* d2, int h, int w, int p, double m, i
                  float* d3) {
   if (p < 4) throw InvalidArg("slic: p must be >= 4");
   if ((long long)p > (long long)w * h) throw InvalidArg("slic: p exceeds pixel count");
-  if ((long long)w * h >= (1ll << 31)) throw InvalidArg("slic: more than 2^31 - 1 pixels");
+  // 32-bit pixel indices, also for the rows of a ragged last tile
+  if ((long long)(w + kTileU) * (h + kTileVLarge) >= (1ll << 31))
+    throw InvalidArg("slic: more than 2^31 - 1 pixels");
   cudaStream_t st = ctx->stream;
   const long long n = (long long)h * w;
   const int gblocks = int(std::max<long long>(1, std::min<long long>((n + 255) / 256,
