@@ -433,7 +433,9 @@ __global__ void __launch_bounds__(kAssignThreads, RPD_ASSIGN_MINB)
   __shared__ double2 s_cd[2 * kMaxTileCenters];
   __shared__ int s_icv[kMaxTileCenters];  // first | last << 8 tile row of the candidate's window
   // per tile row, the candidates whose window reaches it: {cu, (v - cv)^2}, {val, icu | k << 32}
-  __shared__ double2 s_rec[kTileV][2 * kRowCap];
+  // (+1: rows start 4 banks apart; an unpadded row pitch of 768 bytes put every row of the
+  // distribution step on the same banks, 79 % of its store wavefronts were conflicts)
+  __shared__ double2 s_rec[kTileV][2 * kRowCap + 1];
   const int tx = threadIdx.x % 32, wid = threadIdx.x / 32;
   const int u0 = blockIdx.x * kTileU, v0 = blockIdx.y * kTileV;
   const int u = u0 + tx;
